@@ -1,0 +1,318 @@
+/*
+ * laivg.h — C ABI of the B200-native lookahead IVF retrieval path
+ * (paper_2502_20969_b200/liblaivg.so).
+ *
+ * The reference (`laiv`, /root/reference/proj/core) is a C++20 library; this
+ * ABI is what its hot-path functions bind to when they are re-pointed at the
+ * GPU (see INTEGRATION.md for the C++ shim a maintainer adds). Each entry point
+ * cites the reference interface it replaces as file:line under
+ * /root/reference/proj/core/.
+ *
+ * Conventions
+ *  - Every function returns int status: LAIVG_OK (0) or a negative code whose
+ *    class mirrors the reference exception type (std::invalid_argument,
+ *    std::runtime_error, std::logic_error); laivg_last_error() gives the
+ *    message (thread-local). Nothing throws across the ABI.
+ *  - Plain pointers and sizes only. Host pointers unless a name says `dev`.
+ *  - Store layout = the LAIX list-major order (ivf.cpp:373-388): vecs[N][D]
+ *    f32, ids[N] u64, list_off[nc+1] u64; list c is rows
+ *    [list_off[c], list_off[c+1]). cluster_bytes(c) = |c|*(4D+8) (ivf.cpp:23).
+ *  - Scores follow vectorstore.cpp:93-115: per-candidate accumulation in
+ *    fp64 rounded to fp32; L2 reports sqrt. Coarse ranking uses unrounded
+ *    fp64 (squared L2). Total order: score by metric orientation, then
+ *    ascending id (vectorstore.hpp:34-39).
+ *  - Threading: a laivg_index is immutable and shareable by all contexts; a
+ *    laivg_ctx (one GPU + its cluster cache) is driven by one host thread.
+ *  - There is no CPU fallback for the device path: a missing/unusable GPU
+ *    makes laivg_ctx_create fail with LAIVG_ECUDA.
+ */
+#ifndef LAIVG_H
+#define LAIVG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status ------------------------------------------------------------ */
+#define LAIVG_OK 0
+#define LAIVG_EINVAL (-1)   /* std::invalid_argument */
+#define LAIVG_ERUNTIME (-2) /* std::runtime_error   */
+#define LAIVG_ELOGIC (-3)   /* std::logic_error     */
+#define LAIVG_ECUDA (-4)    /* CUDA runtime failure (no reference analogue) */
+
+#define LAIVG_METRIC_IP 0 /* vectorstore.hpp:18 Metric::InnerProduct */
+#define LAIVG_METRIC_L2 1 /* vectorstore.hpp:18 Metric::L2           */
+
+#define LAIVG_TAG_PREFETCHED 0 /* tiered.hpp:17 Residency::Prefetched */
+#define LAIVG_TAG_CACHED 1     /* tiered.hpp:17 Residency::Cached     */
+
+#define LAIVG_CHAN_SIMULATED 0 /* tiered.hpp:65 ChannelMode::SimulatedClock */
+#define LAIVG_CHAN_MEASURED 1  /* tiered.hpp:65 ChannelMode::Measured       */
+#define LAIVG_CHAN_DEVICE 2    /* new: async H2D on a copy stream, event-timed */
+
+const char* laivg_last_error(void);
+/* ABI version (major << 16 | minor). */
+uint32_t laivg_version(void);
+
+/* ---- pinned host memory -------------------------------------------------- */
+/* Portable pinned allocation (cudaHostAllocPortable) so every device shares
+ * one host datastore slab. */
+int laivg_host_alloc(uint64_t bytes, void** out);
+int laivg_host_free(void* p);
+
+/* ---- index: IvfIndex + EmbeddingMatrix (ivf.hpp:26-50, vectorstore.hpp:50-83)
+ * centroids[nc*d] are copied. With LAIVG_INDEX_BORROW the store arrays are
+ * borrowed (caller keeps them alive and ideally allocated them with
+ * laivg_host_alloc); otherwise they are copied into a library-owned pinned
+ * slab. Validation mirrors the reference constructors: d > 0, finite
+ * components (vectorstore.cpp:66-85) unless LAIVG_INDEX_TRUST is set,
+ * monotone list_off. */
+#define LAIVG_INDEX_BORROW 1u
+#define LAIVG_INDEX_TRUST 2u
+typedef struct laivg_index laivg_index;
+int laivg_index_create(const float* centroids, uint32_t nc, uint32_t d,
+                       int metric, const float* vecs, const uint64_t* ids,
+                       const uint64_t* list_off, uint32_t flags,
+                       laivg_index** out);
+void laivg_index_destroy(laivg_index* ix);
+uint32_t laivg_index_num_clusters(const laivg_index* ix);
+uint32_t laivg_index_dim(const laivg_index* ix);
+int laivg_index_metric(const laivg_index* ix);
+uint64_t laivg_index_total_vectors(const laivg_index* ix);
+/* ivf.hpp:40 IvfIndex::cluster_bytes */
+uint64_t laivg_index_cluster_bytes(const laivg_index* ix, uint32_t c);
+/* ivf.hpp:41 IvfIndex::total_payload_bytes */
+uint64_t laivg_index_total_payload_bytes(const laivg_index* ix);
+
+/* ---- device context: one GPU, its cluster cache (TieredStore), streams --- */
+typedef struct {
+  int device;              /* CUDA ordinal */
+  uint64_t capacity_bytes; /* TieredStore capacity (tiered.hpp:24), reference
+                              byte accounting n*(4D+8) */
+  uint32_t miss_threads;   /* host threads scanning cache misses; 0 = all cores */
+  uint32_t max_batch;      /* max queries per batched call; 0 = 256 */
+  uint32_t max_probe;      /* max L per call; 0 = nc */
+  uint32_t acc_fp64;       /* 1 (default): scan accumulates in fp64 as the
+                              reference does; 0: fp32 FMA accumulation */
+  uint32_t reserved[8];
+} laivg_opts;
+void laivg_opts_default(laivg_opts* o);
+typedef struct laivg_ctx laivg_ctx;
+int laivg_ctx_create(const laivg_index* ix, const laivg_opts* opts,
+                     laivg_ctx** out);
+void laivg_ctx_destroy(laivg_ctx* ctx);
+/* Waits for all device work of the context. */
+int laivg_ctx_sync(laivg_ctx* ctx);
+
+/* ---- coarse quantizer (ivf.cpp:269-299) ---------------------------------- */
+/* Full ranking of all nc clusters for each of nq queries Q[nq*d]:
+ * order_out[nq*nc]. scores_out (nullable) receives the fp64 scores indexed by
+ * cluster id [nq*nc]. Replaces rank_clusters (ivf.hpp:68-69). */
+int laivg_rank_clusters(laivg_ctx* ctx, const float* Q, uint32_t nq,
+                        uint32_t* order_out, double* scores_out);
+/* First min(max(L,0), nc) clusters per query: probe_out[nq*Lp] where
+ * Lp = min(max(L,0), nc) is written to *lp_out. Replaces coarse_probe
+ * (ivf.hpp:72-73). */
+int laivg_coarse_probe(laivg_ctx* ctx, const float* Q, uint32_t nq, int L,
+                       uint32_t* probe_out, uint32_t* lp_out);
+
+/* ---- fine search ----------------------------------------------------------
+ * Results: ids_out[nq*k], scores_out[nq*k], count_out[nq] (= min(k,
+ * candidates)), best-first. Resident clusters are scanned on the GPU, the rest
+ * by the host miss path; the merged result equals the monolithic search
+ * whatever the residency (tiered.hpp:120-124). */
+/* search_clusters (ivf.hpp:85-87) for one query over an explicit cluster
+ * list. */
+int laivg_search_clusters(laivg_ctx* ctx, const float* q,
+                          const uint32_t* clusters, uint32_t n, int k,
+                          uint64_t* ids_out, float* scores_out,
+                          uint32_t* count_out);
+/* ivf_search (ivf.hpp:90-91) for nq queries. */
+int laivg_ivf_search(laivg_ctx* ctx, const float* Q, uint32_t nq, int L,
+                     int k, uint64_t* ids_out, float* scores_out,
+                     uint32_t* count_out);
+
+/* ---- tiered store = the GPU cluster cache (tiered.hpp:22-56) ------------- */
+uint64_t laivg_store_capacity_bytes(const laivg_ctx* ctx);
+uint64_t laivg_store_used_bytes(const laivg_ctx* ctx);
+uint64_t laivg_store_free_bytes(const laivg_ctx* ctx);
+int laivg_store_contains(const laivg_ctx* ctx, uint32_t c); /* 1/0 */
+uint32_t laivg_store_resident_count(const laivg_ctx* ctx);
+/* Resident clusters ascending by id (std::map order): clusters_out[n],
+ * tags_out[n] (nullable), bytes_out[n] (nullable); returns count via *n_out
+ * (buffers must hold resident_count entries). */
+int laivg_store_resident(const laivg_ctx* ctx, uint32_t* clusters_out,
+                         uint8_t* tags_out, uint64_t* bytes_out,
+                         uint32_t* n_out);
+/* TieredStore::insert (tiered.cpp:15-24): makes cluster c resident with its
+ * payload copied into the device cache (synchronously). Throws-equivalents:
+ * LAIVG_ELOGIC already resident, LAIVG_ERUNTIME capacity exceeded. */
+int laivg_store_insert(laivg_ctx* ctx, uint32_t c, int tag);
+/* TieredStore::evict (tiered.cpp:26-36); *bytes_out = freed bytes. */
+int laivg_store_evict(laivg_ctx* ctx, uint32_t c, uint64_t* bytes_out);
+int laivg_store_retag_all(laivg_ctx* ctx, int tag);     /* tiered.cpp:38-42 */
+int laivg_store_clear(laivg_ctx* ctx);                  /* tiered.cpp:44-47 */
+uint64_t laivg_store_bytes_with_tag(const laivg_ctx* ctx, int tag);
+uint64_t laivg_store_recompute_used_bytes(const laivg_ctx* ctx);
+/* Compacts the device slab (paper: consolidate GPU memory after a batch). */
+int laivg_store_compact(laivg_ctx* ctx);
+
+/* ---- lookahead prefetch (tiered.hpp:97-117) ----------------------------- */
+/* plan_prefetch (tiered.cpp:67-84) against the context's store: walks the
+ * full ranking of q_in (GPU coarse), skips resident clusters, takes a cluster
+ * if its bytes fit the remaining budget, else skips and continues.
+ * plan_out / skipped_out must hold nc entries. */
+int laivg_plan_prefetch(laivg_ctx* ctx, const float* q_in,
+                        uint64_t budget_bytes, uint32_t* plan_out,
+                        uint32_t* nplan_out, uint64_t* planned_bytes_out,
+                        uint32_t* skipped_out, uint32_t* nskipped_out);
+
+typedef struct {
+  double bandwidth_bytes_per_s; /* tiered.hpp:69 */
+  int mode;                     /* LAIVG_CHAN_* */
+} laivg_channel;
+
+typedef struct {
+  double t_p;          /* seconds: transfer time (Device: copy-stream events;
+                          Simulated: bytes/B; Measured: host wall clock) */
+  uint64_t bytes;      /* tiered.hpp:80 */
+  double overshoot_s;  /* max(0, t_p - window) (tiered.cpp:134); Device mode:
+                          measured copy end minus window end, >= 0 */
+  uint32_t n_transferred;
+  double window_s;     /* measured duration of the generation-window kernel */
+  double h2d_gbps;     /* achieved host->device GB/s of this transfer */
+} laivg_transfer_report;
+
+/* execute_prefetch (tiered.cpp:86-136): inserts the planned clusters
+ * (Prefetched) and copies their payload into the device cache. In
+ * LAIVG_CHAN_DEVICE mode the copies run on the context's copy stream while a
+ * timed generation-window kernel of overlap_window_s seconds occupies the
+ * compute stream; the call returns when both have finished.
+ * transferred_out (nullable) receives the transferred clusters in order. */
+int laivg_execute_prefetch(laivg_ctx* ctx, const uint32_t* plan, uint32_t n,
+                           const laivg_channel* chan, double overlap_window_s,
+                           uint32_t* transferred_out,
+                           laivg_transfer_report* rep);
+/* incremental_prefetch (tiered.cpp:138-146). */
+int laivg_incremental_prefetch(laivg_ctx* ctx, const float* q_round,
+                               uint64_t budget_bytes,
+                               const laivg_channel* chan,
+                               double overlap_window_s,
+                               uint32_t* transferred_out,
+                               laivg_transfer_report* rep);
+/* Runs only the generation-window kernel (seconds) on the compute stream and
+ * returns its measured duration. */
+int laivg_window(laivg_ctx* ctx, double seconds, double* measured_s);
+
+/* ---- hybrid search (tiered.cpp:148-198) ---------------------------------- */
+typedef struct {
+  double bandwidth_bytes_per_s; /* budget.hpp:14 */
+  double t_cc;                  /* budget.hpp:15 */
+  double t_gc;                  /* budget.hpp:16 */
+  int parallel_slots;           /* budget.hpp:17 */
+} laivg_cost_model;
+
+typedef struct {
+  /* Reference HybridTiming (tiered.hpp:84-88), now measured: */
+  double t_g; /* GPU side: coarse + scan + merge, device events (s) */
+  double t_c; /* host miss scan wall time (s) */
+  double t_2; /* whole retrieval, call entry to merged result (s) */
+  /* Modeled per the reference cost model (tiered.cpp:190-196): */
+  double model_t_g, model_t_c, model_t_2;
+  double t_coarse; /* device: coarse scores + selection (s) */
+  double t_scan;   /* device: list scan + block/grid merge (s) */
+  uint64_t scanned_vectors; /* vectors scanned on the GPU */
+  uint64_t scanned_bytes;   /* reference bytes: n*(4D+8) over fast lists */
+} laivg_hybrid_timing;
+
+/* hybrid_search for one query. fast_out / slow_out (nullable, L entries)
+ * receive the probe split by residency in probe order. */
+int laivg_hybrid_search(laivg_ctx* ctx, const float* q_out, int L, int k,
+                        const laivg_cost_model* cost, uint64_t* ids_out,
+                        float* scores_out, uint32_t* count_out,
+                        uint32_t* fast_out, uint32_t* nfast_out,
+                        uint32_t* slow_out, uint32_t* nslow_out,
+                        double* hit_rate_out, laivg_hybrid_timing* timing);
+
+/* coverage (tiered.cpp:200-211). */
+int laivg_coverage(laivg_ctx* ctx, const float* q_in, const float* q_out,
+                   int L, double* out);
+
+/* ---- device-resident query staging (benchmark path: inputs already in HBM)
+ * Upload nq queries once; laivg_hybrid_search_staged then reads query i from
+ * HBM instead of copying it from the host. */
+int laivg_stage_queries(laivg_ctx* ctx, const float* Q, uint32_t nq);
+int laivg_hybrid_search_staged(laivg_ctx* ctx, uint32_t qi, int L, int k,
+                               uint64_t* ids_out, float* scores_out,
+                               uint32_t* count_out, uint32_t* nfast_out,
+                               laivg_hybrid_timing* timing);
+
+/* ---- schedulers (sched.cpp) ---------------------------------------------- */
+/* group_microbatches (sched.cpp:39-70): order_out[n] holds the queries batch
+ * by batch, batch_off_out[nb+1] the CSR offsets; *nb_out = #batches. */
+int laivg_group_microbatches(const float* queries, uint64_t n, uint32_t d,
+                             uint64_t m, uint64_t* order_out,
+                             uint64_t* batch_off_out, uint32_t* nb_out);
+/* chunk_microbatches (sched.cpp:72-85) */
+int laivg_chunk_microbatches(uint64_t n, uint64_t m, uint64_t* order_out,
+                             uint64_t* batch_off_out, uint32_t* nb_out);
+/* assign_cache_aware (sched.cpp:87-144). Batches in CSR form; resident is
+ * [nw][nc] bytes (1 = worker caches the cluster). Probe unions come from the
+ * context's GPU coarse quantizer. */
+int laivg_assign_cache_aware(laivg_ctx* ctx, const uint64_t* batch_off,
+                             const uint64_t* members, uint32_t nb,
+                             const uint8_t* resident, uint32_t nw,
+                             const float* queries, uint64_t nq, int L,
+                             uint32_t* assignment_out);
+/* assign_round_robin (sched.cpp:146-155) */
+int laivg_assign_round_robin(uint64_t nb, uint64_t nw, uint32_t* out);
+/* assignment_overlap (sched.cpp:157-168) */
+int laivg_assignment_overlap(laivg_ctx* ctx, const uint64_t* batch_off,
+                             const uint64_t* members, uint32_t nb,
+                             const uint8_t* resident, uint32_t nw,
+                             const uint32_t* assignment, const float* queries,
+                             uint64_t nq, int L, uint64_t* out);
+/* split_budget (sched.cpp:170-192) */
+int laivg_split_budget(uint64_t total, const uint64_t* batch, uint64_t n,
+                       uint64_t* out);
+
+/* ---- hotness cache policy (cache.hpp:28-56) ------------------------------ */
+typedef struct laivg_hotness laivg_hotness;
+int laivg_hotness_create(float h_init, float h_inc, float decay,
+                         double cache_fraction, laivg_hotness** out);
+void laivg_hotness_destroy(laivg_hotness* h);
+int laivg_hotness_on_fetch(laivg_hotness* h, uint32_t c);          /* cache.cpp:27 */
+int laivg_hotness_end_of_round(laivg_hotness* h, const uint32_t* used,
+                               uint32_t n);                       /* cache.cpp:31 */
+/* evict_to_fraction (cache.cpp:40-66) on the context's store; evicted_out
+ * (nullable, resident_count entries) receives the evicted ids in order. */
+int laivg_hotness_evict_to_fraction(laivg_hotness* h, laivg_ctx* ctx,
+                                    uint32_t* evicted_out, uint32_t* n_out);
+/* hotness of c, or -1 when untracked */
+float laivg_hotness_get(const laivg_hotness* h, uint32_t c);
+int laivg_hotness_forget(laivg_hotness* h, uint32_t c);
+int laivg_hotness_clear(laivg_hotness* h);
+
+/* ---- synthetic workload (the generator of SURVEY §8d; not on the path) ---
+ * Planted clusters: centroids mu_j = normalize(g), members
+ * x = normalize(mu_j + spread*g), balanced lists, ids j*n_j+i, list-major.
+ * Deterministic from (seed, j, i, dim) and bit-identical across thread
+ * counts. vecs must hold n_total*d floats. */
+int laivg_synth_centroids(uint64_t seed, uint32_t nc, uint32_t d,
+                          float* centroids_out);
+int laivg_synth_lists(uint64_t seed, const float* centroids, uint32_t nc,
+                      uint32_t d, uint64_t per_list, float spread,
+                      uint32_t c_begin, uint32_t c_end, float* vecs_out,
+                      uint64_t* ids_out, int threads);
+/* q_in = normalize(x_r + 0.01 g) for uniform rows r; q_out =
+ * normalize(q_in + sigma g) (trace.cpp:203-220 pattern). */
+int laivg_synth_queries(uint64_t seed, const float* vecs, uint64_t n_rows,
+                        uint32_t d, uint32_t nq, float sigma, float* q_in_out,
+                        float* q_out_out, uint64_t* rows_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LAIVG_H */

@@ -1,0 +1,1302 @@
+// ctx.cu — device context (one GPU + its cluster cache) and the C ABI of
+// include/laivg.h. Host orchestration only; kernels live in kernels.cu and the
+// CPU side (miss scan, planner, schedulers, hotness, synth) in host.cpp.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <thread>
+#include <unordered_set>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/laivg.h"
+#include "host.hpp"
+#include "kernels.cuh"
+
+namespace laivg {
+namespace {
+
+thread_local std::string g_err;
+
+#define CK(x)                                                                   \
+  do {                                                                          \
+    cudaError_t e_ = (x);                                                       \
+    if (e_ != cudaSuccess) {                                                    \
+      throw ::laivg::CudaError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    }                                                                           \
+  } while (0)
+
+using Clock = std::chrono::steady_clock;
+double secs(Clock::time_point a, Clock::time_point b) {
+  return std::chrono::duration<double>(b - a).count();
+}
+
+template <class T>
+T* dev_alloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  return static_cast<T*>(p);
+}
+template <class T>
+T* pin_alloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  CK(cudaHostAlloc(&p, n * sizeof(T), cudaHostAllocPortable));
+  return static_cast<T*>(p);
+}
+
+// First-fit allocator over the device slab, in vectors.
+class SlabAlloc {
+ public:
+  void reset(uint64_t total) {
+    total_ = total;
+    free_.clear();
+    if (total) free_[0] = total;
+  }
+  bool alloc(uint64_t n, uint64_t& off) {
+    if (n == 0) {
+      off = 0;
+      return true;
+    }
+    for (auto it = free_.begin(); it != free_.end(); ++it) {
+      if (it->second >= n) {
+        off = it->first;
+        const uint64_t rest = it->second - n;
+        free_.erase(it);
+        if (rest) free_[off + n] = rest;
+        return true;
+      }
+    }
+    return false;
+  }
+  void release(uint64_t off, uint64_t n) {
+    if (n == 0) return;
+    auto it = free_.emplace(off, n).first;
+    auto nx = std::next(it);
+    if (nx != free_.end() && it->first + it->second == nx->first) {
+      it->second += nx->second;
+      free_.erase(nx);
+    }
+    if (it != free_.begin()) {
+      auto pv = std::prev(it);
+      if (pv->first + pv->second == it->first) {
+        pv->second += it->second;
+        free_.erase(it);
+      }
+    }
+  }
+  uint64_t free_total() const {
+    uint64_t s = 0;
+    for (auto& [o, n] : free_) s += n;
+    return s;
+  }
+
+ private:
+  uint64_t total_ = 0;
+  std::map<uint64_t, uint64_t> free_;
+};
+
+struct Resident {
+  int tag;
+  uint64_t bytes;
+};
+
+} // namespace
+
+// ============================================================================
+// context
+// ============================================================================
+struct Ctx {
+  const Index* ix = nullptr;
+  int dev = 0;
+  int sms = 148;
+  bool acc_fp64 = true;
+  cudaStream_t comp = nullptr, copy = nullptr, aux = nullptr;
+
+  // static device data
+  float* d_cen = nullptr;
+  uint64_t* d_list_off = nullptr;
+  uint64_t* d_ids = nullptr;
+
+  // cluster cache (TieredStore, tiered.hpp:22-56)
+  uint64_t capacity = 0, used = 0;
+  std::map<uint32_t, Resident> resident;
+  std::vector<int64_t> h_res;  // slab vector offset per cluster, -1 if absent
+  int64_t* d_res = nullptr;
+  bool res_dirty = true;
+  int64_t* res_stage[2] = {nullptr, nullptr};
+  cudaEvent_t res_ev[2] = {nullptr, nullptr};
+  int res_slot = 0;
+  float* d_slab = nullptr;
+  uint64_t slab_vecs = 0;
+  SlabAlloc alloc;
+  float* d_tmp = nullptr;       // one-list bounce buffer for compaction
+  uint64_t tmp_vecs = 0;
+
+  // scratch
+  uint32_t max_batch = 256, max_probe = 0;
+  float* d_Q = nullptr;
+  double* d_scores = nullptr;
+  uint32_t* d_order = nullptr;
+  FastTable ft{};
+  ScanOut so{};
+  int part_cap = 0; // partial top-k rows available (CTAs x queries)
+  float* h_Q = nullptr;
+  uint32_t* h_order = nullptr;
+  float* h_out_s = nullptr;
+  uint64_t* h_out_id = nullptr;
+  uint32_t* h_out_cnt = nullptr;
+  uint32_t* h_fcount = nullptr;
+  float* d_staged = nullptr;
+  uint32_t n_staged = 0;
+  std::vector<float> staged_host;
+
+  // events
+  cudaEvent_t ev_a, ev_b, ev_p, ev_s, ev_c, ev_probe, ev_base, ev_win, ev_cp0,
+      ev_cp1, ev_copy_tail, ev_comp_tail;
+
+  std::unique_ptr<ThreadPool> pool;
+
+  ~Ctx();
+  void init(const Index* index, const laivg_opts& o);
+
+  // ---- residency -----------------------------------------------------------
+  void commit_res(cudaStream_t st) {
+    if (!res_dirty) return;
+    const int s = res_slot;
+    res_slot ^= 1;
+    CK(cudaEventSynchronize(res_ev[s]));
+    std::memcpy(res_stage[s], h_res.data(), h_res.size() * sizeof(int64_t));
+    CK(cudaMemcpyAsync(d_res, res_stage[s], h_res.size() * sizeof(int64_t),
+                       cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(res_ev[s], st));
+    res_dirty = false;
+  }
+  // Copy-stream work issued after this point is ordered after all compute
+  // work issued so far (scans may still read slab regions being reused).
+  void copy_after_comp() {
+    CK(cudaEventRecord(ev_comp_tail, comp));
+    CK(cudaStreamWaitEvent(copy, ev_comp_tail, 0));
+  }
+  void compact();
+  // TieredStore::insert + payload upload on the copy stream (no sync).
+  void insert_async(uint32_t c, int tag);
+  uint64_t evict(uint32_t c);
+  void clear_store();
+
+  // ---- search --------------------------------------------------------------
+  void coarse(const float* dQ, uint32_t nq, uint32_t n_out, cudaStream_t st);
+  struct Result {
+    std::vector<Scored> top;
+    std::vector<uint32_t> fast, slow;
+    double t_g = 0, t_c = 0, t_2 = 0, t_coarse = 0, t_scan = 0;
+    uint64_t vecs_gpu = 0, bytes_gpu = 0;
+  };
+  // One query: dq on device, hq on host (miss path). With `explicit_probe`
+  // the probe is those clusters (search_clusters), otherwise the coarse
+  // quantizer picks min(L, nc) of them (hybrid/ivf search).
+  Result search(const float* dq, const float* hq, int L, int k,
+                const std::vector<uint32_t>* explicit_probe);
+};
+
+Ctx::~Ctx() {
+  if (comp) cudaStreamSynchronize(comp);
+  if (copy) cudaStreamSynchronize(copy);
+  if (aux) cudaStreamSynchronize(aux);
+  for (void* p : {(void*)d_cen, (void*)d_list_off, (void*)d_ids, (void*)d_res,
+                  (void*)d_slab, (void*)d_tmp, (void*)d_Q, (void*)d_scores,
+                  (void*)d_order, (void*)ft.slab, (void*)ft.row, (void*)ft.len,
+                  (void*)ft.cluster, (void*)ft.pre, (void*)ft.count,
+                  (void*)so.part_s, (void*)so.part_id, (void*)so.ticket,
+                  (void*)so.out_s, (void*)so.out_id, (void*)so.out_count,
+                  (void*)d_staged}) {
+    if (p) cudaFree(p);
+  }
+  for (void* p : {(void*)res_stage[0], (void*)res_stage[1], (void*)h_Q,
+                  (void*)h_order, (void*)h_out_s, (void*)h_out_id,
+                  (void*)h_out_cnt, (void*)h_fcount}) {
+    if (p) cudaFreeHost(p);
+  }
+  for (cudaEvent_t e : {ev_a, ev_b, ev_p, ev_s, ev_c, ev_probe, ev_base, ev_win,
+                        ev_cp0, ev_cp1, ev_copy_tail, ev_comp_tail, res_ev[0],
+                        res_ev[1]}) {
+    if (e) cudaEventDestroy(e);
+  }
+  if (comp) cudaStreamDestroy(comp);
+  if (copy) cudaStreamDestroy(copy);
+  if (aux) cudaStreamDestroy(aux);
+}
+
+void Ctx::init(const Index* index, const laivg_opts& o) {
+  ix = index;
+  dev = o.device;
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (dev < 0 || dev >= ndev) {
+    throw CudaError("device ordinal " + std::to_string(dev) + " not present (" +
+                    std::to_string(ndev) + " devices)");
+  }
+  CK(cudaSetDevice(dev));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10) {
+    throw CudaError(std::string("device is ") + prop.name +
+                    " (sm_" + std::to_string(prop.major) + std::to_string(prop.minor) +
+                    "); this build targets sm_100a");
+  }
+  sms = prop.multiProcessorCount;
+  acc_fp64 = o.acc_fp64 != 0;
+  if (ix->nc > kMaxSortNc) {
+    throw std::invalid_argument("device coarse ranking supports up to " +
+                                std::to_string(kMaxSortNc) + " clusters");
+  }
+  CK(cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&ev_a, &ev_b, &ev_p, &ev_s, &ev_c, &ev_probe, &ev_base,
+                         &ev_win, &ev_cp0, &ev_cp1, &ev_copy_tail, &ev_comp_tail,
+                         &res_ev[0], &res_ev[1]}) {
+    CK(cudaEventCreate(e));
+  }
+  CK(cudaEventRecord(ev_copy_tail, copy));
+  CK(cudaEventRecord(res_ev[0], copy));
+  CK(cudaEventRecord(res_ev[1], copy));
+
+  const uint32_t nc = ix->nc, d = ix->d;
+  d_cen = dev_alloc<float>(size_t(nc) * d);
+  CK(cudaMemcpy(d_cen, ix->centroids.data(), size_t(nc) * d * sizeof(float),
+                cudaMemcpyHostToDevice));
+  d_list_off = dev_alloc<uint64_t>(nc + 1);
+  CK(cudaMemcpy(d_list_off, ix->list_off.data(), (nc + 1) * sizeof(uint64_t),
+                cudaMemcpyHostToDevice));
+  d_ids = dev_alloc<uint64_t>(ix->total());
+  if (ix->total()) {
+    CK(cudaMemcpy(d_ids, ix->ids, ix->total() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  }
+
+  capacity = o.capacity_bytes;
+  h_res.assign(nc, -1);
+  d_res = dev_alloc<int64_t>(nc);
+  res_stage[0] = pin_alloc<int64_t>(nc);
+  res_stage[1] = pin_alloc<int64_t>(nc);
+  slab_vecs = capacity / ix->member_bytes();
+  d_slab = dev_alloc<float>(slab_vecs * d);
+  alloc.reset(slab_vecs);
+  uint64_t maxlen = 1;
+  for (uint32_t c = 0; c < nc; ++c) maxlen = std::max(maxlen, ix->list_len(c));
+  tmp_vecs = maxlen;
+
+  max_batch = o.max_batch ? o.max_batch : 256;
+  max_probe = o.max_probe ? std::min(o.max_probe, nc) : nc;
+  if (max_probe == 0) max_probe = 1;
+  d_Q = dev_alloc<float>(size_t(max_batch) * d);
+  d_scores = dev_alloc<double>(size_t(max_batch) * nc);
+  d_order = dev_alloc<uint32_t>(size_t(max_batch) * std::max(nc, 1u));
+  ft.stride = max_probe;
+  ft.slab = dev_alloc<int64_t>(size_t(max_batch) * max_probe);
+  ft.row = dev_alloc<uint64_t>(size_t(max_batch) * max_probe);
+  ft.len = dev_alloc<uint32_t>(size_t(max_batch) * max_probe);
+  ft.cluster = dev_alloc<uint32_t>(size_t(max_batch) * max_probe);
+  ft.pre = dev_alloc<uint64_t>(size_t(max_batch) * (max_probe + 1));
+  ft.count = dev_alloc<uint32_t>(max_batch);
+  part_cap = std::max<int>(2 * sms, int(max_batch)) + 2 * sms;
+  so.part_s = dev_alloc<float>(size_t(part_cap) * kMaxK);
+  so.part_id = dev_alloc<uint64_t>(size_t(part_cap) * kMaxK);
+  so.ticket = dev_alloc<unsigned>(max_batch);
+  CK(cudaMemset(so.ticket, 0, max_batch * sizeof(unsigned)));
+  so.out_s = dev_alloc<float>(size_t(max_batch) * kMaxK);
+  so.out_id = dev_alloc<uint64_t>(size_t(max_batch) * kMaxK);
+  so.out_count = dev_alloc<uint32_t>(max_batch);
+  h_Q = pin_alloc<float>(size_t(max_batch) * d);
+  h_order = pin_alloc<uint32_t>(size_t(max_batch) * std::max(nc, 1u));
+  h_out_s = pin_alloc<float>(size_t(max_batch) * kMaxK);
+  h_out_id = pin_alloc<uint64_t>(size_t(max_batch) * kMaxK);
+  h_out_cnt = pin_alloc<uint32_t>(max_batch);
+  h_fcount = pin_alloc<uint32_t>(max_batch);
+
+  unsigned threads = o.miss_threads;
+  if (threads == 0) threads = std::max(1u, std::thread::hardware_concurrency());
+  pool = std::make_unique<ThreadPool>(threads - 1);
+  CK(cudaDeviceSynchronize());
+}
+
+void Ctx::compact() {
+  // Slide every resident list down to the lowest free offset (slab order),
+  // through a bounce buffer so source and destination never overlap.
+  copy_after_comp();
+  std::vector<std::pair<int64_t, uint32_t>> by_off;
+  for (auto& [c, r] : resident) by_off.emplace_back(h_res[c], c);
+  std::sort(by_off.begin(), by_off.end());
+  const uint32_t d = ix->d;
+  if (!d_tmp) d_tmp = dev_alloc<float>(tmp_vecs * d);
+  uint64_t cursor = 0;
+  for (auto& [off, c] : by_off) {
+    const uint64_t n = ix->list_len(c);
+    if (uint64_t(off) != cursor && n) {
+      CK(cudaMemcpyAsync(d_tmp, d_slab + uint64_t(off) * d, n * d * sizeof(float),
+                         cudaMemcpyDeviceToDevice, copy));
+      CK(cudaMemcpyAsync(d_slab + cursor * d, d_tmp, n * d * sizeof(float),
+                         cudaMemcpyDeviceToDevice, copy));
+    }
+    h_res[c] = int64_t(cursor);
+    cursor += n;
+  }
+  alloc.reset(slab_vecs);
+  uint64_t dummy;
+  if (cursor) alloc.alloc(cursor, dummy);
+  res_dirty = true;
+}
+
+void Ctx::insert_async(uint32_t c, int tag) {
+  if (c >= ix->nc) throw std::invalid_argument("unknown cluster id " + std::to_string(c));
+  if (resident.count(c)) {
+    throw std::logic_error("cluster " + std::to_string(c) + " is already resident");
+  }
+  const uint64_t bytes = ix->cluster_bytes(c);
+  if (used + bytes > capacity) {
+    throw std::runtime_error("fast tier capacity exceeded inserting cluster " +
+                             std::to_string(c));
+  }
+  const uint64_t n = ix->list_len(c);
+  uint64_t off = 0;
+  if (!alloc.alloc(n, off)) {
+    compact();
+    if (!alloc.alloc(n, off)) {
+      throw std::runtime_error("device cache slab exhausted inserting cluster " +
+                               std::to_string(c));
+    }
+  }
+  if (n) {
+    const uint32_t d = ix->d;
+    CK(cudaMemcpyAsync(d_slab + off * d, ix->vecs + ix->list_off[c] * d,
+                       n * d * sizeof(float), cudaMemcpyHostToDevice, copy));
+  }
+  resident[c] = {tag, bytes};
+  used += bytes;
+  h_res[c] = int64_t(off);
+  res_dirty = true;
+}
+
+uint64_t Ctx::evict(uint32_t c) {
+  auto it = resident.find(c);
+  if (it == resident.end()) {
+    throw std::logic_error("evicting non-resident cluster " + std::to_string(c));
+  }
+  const uint64_t bytes = it->second.bytes;
+  used -= bytes;
+  alloc.release(uint64_t(h_res[c]), ix->list_len(c));
+  h_res[c] = -1;
+  res_dirty = true;
+  resident.erase(it);
+  return bytes;
+}
+
+void Ctx::clear_store() {
+  resident.clear();
+  used = 0;
+  std::fill(h_res.begin(), h_res.end(), -1);
+  alloc.reset(slab_vecs);
+  res_dirty = true;
+}
+
+void Ctx::coarse(const float* dQ, uint32_t nq, uint32_t n_out, cudaStream_t st) {
+  launch_coarse_scores(dQ, nq, d_cen, ix->nc, ix->d, ix->metric, d_scores, st);
+  launch_select(d_scores, nq, ix->nc, ix->metric, n_out, d_order, st);
+}
+
+Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
+                        const std::vector<uint32_t>* explicit_probe) {
+  if (k < 1) throw std::invalid_argument("k must be >= 1");
+  if (k > kMaxK) {
+    throw std::invalid_argument("k = " + std::to_string(k) +
+                                " exceeds the device top-k limit " + std::to_string(kMaxK));
+  }
+  const auto t0 = Clock::now();
+  Result r;
+  uint32_t lp;
+  if (explicit_probe) {
+    for (uint32_t c : *explicit_probe) {
+      if (c >= ix->nc) throw std::invalid_argument("unknown cluster id " + std::to_string(c));
+    }
+    lp = uint32_t(explicit_probe->size());
+  } else {
+    lp = uint32_t(std::min<int64_t>(std::max(L, 0), ix->nc));
+  }
+  if (lp > max_probe) {
+    throw std::invalid_argument("probe of " + std::to_string(lp) +
+                                " clusters exceeds the context's max_probe " +
+                                std::to_string(max_probe));
+  }
+  // Retrieval is ordered after every prefetch copy issued so far, then sees
+  // the residency table of the host store state.
+  CK(cudaStreamWaitEvent(comp, ev_copy_tail, 0));
+  commit_res(comp);
+  CK(cudaEventRecord(ev_a, comp));
+  if (explicit_probe) {
+    if (lp) {
+      std::memcpy(h_order, explicit_probe->data(), lp * sizeof(uint32_t));
+      CK(cudaMemcpyAsync(d_order, h_order, lp * sizeof(uint32_t), cudaMemcpyHostToDevice, comp));
+    }
+  } else {
+    coarse(dq, 1, lp, comp);
+  }
+  CK(cudaEventRecord(ev_b, comp));
+  if (!explicit_probe && lp) {
+    CK(cudaStreamWaitEvent(aux, ev_b, 0));
+    CK(cudaMemcpyAsync(h_order, d_order, lp * sizeof(uint32_t), cudaMemcpyDeviceToHost, aux));
+    CK(cudaEventRecord(ev_probe, aux));
+  }
+  launch_partition(d_order, 1, lp, d_res, d_list_off, ft, comp);
+  CK(cudaEventRecord(ev_p, comp));
+  launch_scan(dq, 1, ix->d, ix->metric, k, ft, d_slab, d_ids, so,
+              std::min(scan_grid_x(1, sms), part_cap), acc_fp64, comp);
+  CK(cudaEventRecord(ev_s, comp));
+  CK(cudaMemcpyAsync(h_out_s, so.out_s, k * sizeof(float), cudaMemcpyDeviceToHost, comp));
+  CK(cudaMemcpyAsync(h_out_id, so.out_id, k * sizeof(uint64_t), cudaMemcpyDeviceToHost, comp));
+  CK(cudaMemcpyAsync(h_out_cnt, so.out_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, comp));
+  CK(cudaMemcpyAsync(h_fcount, ft.count, sizeof(uint32_t), cudaMemcpyDeviceToHost, comp));
+  CK(cudaEventRecord(ev_c, comp));
+
+  // Host: split the probe by residency (tiered.cpp:155-161) and scan the
+  // misses while the GPU scans the hits.
+  if (!explicit_probe && lp) CK(cudaEventSynchronize(ev_probe));
+  for (uint32_t i = 0; i < lp; ++i) {
+    const uint32_t c = h_order[i];
+    (h_res[c] >= 0 ? r.fast : r.slow).push_back(c);
+  }
+  std::vector<Scored> miss;
+  if (!r.slow.empty()) {
+    const auto tc = Clock::now();
+    miss = miss_scan(*ix, hq, r.slow, k, *pool);
+    r.t_c = secs(tc, Clock::now());
+  }
+  CK(cudaEventSynchronize(ev_c));
+  if (*h_fcount != r.fast.size()) {
+    throw std::runtime_error("device residency table disagrees with the store");
+  }
+  std::vector<Scored> gpu(*h_out_cnt);
+  for (uint32_t i = 0; i < *h_out_cnt; ++i) gpu[i] = {h_out_s[i], h_out_id[i]};
+  r.top = merge_topk(ix->metric, gpu, miss, k);
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, ev_a, ev_s));
+  r.t_g = ms * 1e-3;
+  CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
+  r.t_coarse = ms * 1e-3;
+  CK(cudaEventElapsedTime(&ms, ev_p, ev_s));
+  r.t_scan = ms * 1e-3;
+  for (uint32_t c : r.fast) {
+    r.vecs_gpu += ix->list_len(c);
+    r.bytes_gpu += ix->cluster_bytes(c);
+  }
+  r.t_2 = secs(t0, Clock::now());
+  return r;
+}
+
+} // namespace laivg
+
+// ============================================================================
+// C ABI
+// ============================================================================
+using laivg::Ctx;
+using laivg::Index;
+using laivg::Clock;
+
+struct laivg_index {
+  Index ix;
+};
+struct laivg_ctx {
+  Ctx c;
+};
+struct laivg_hotness {
+  laivg::Hotness h;
+};
+
+namespace {
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return LAIVG_OK;
+  } catch (const laivg::CudaError& e) {
+    laivg::g_err = e.what();
+    return LAIVG_ECUDA;
+  } catch (const std::invalid_argument& e) {
+    laivg::g_err = e.what();
+    return LAIVG_EINVAL;
+  } catch (const std::logic_error& e) {
+    laivg::g_err = e.what();
+    return LAIVG_ELOGIC;
+  } catch (const std::runtime_error& e) {
+    laivg::g_err = e.what();
+    return LAIVG_ERUNTIME;
+  } catch (const std::exception& e) {
+    laivg::g_err = e.what();
+    return LAIVG_ERUNTIME;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw std::invalid_argument(std::string(what) + " is null");
+}
+
+void set_ctx_device(const laivg_ctx* ctx) {
+  need(ctx, "ctx");
+  CK(cudaSetDevice(ctx->c.dev));
+}
+
+void fill_timing(laivg_hybrid_timing* t, const Ctx::Result& r,
+                 const laivg_cost_model* cost) {
+  if (!t) return;
+  t->t_g = r.t_g;
+  t->t_c = r.t_c;
+  t->t_2 = r.t_2;
+  t->t_coarse = r.t_coarse;
+  t->t_scan = r.t_scan;
+  t->scanned_vectors = r.vecs_gpu;
+  t->scanned_bytes = r.bytes_gpu;
+  if (cost) { // tiered.cpp:190-196
+    const double miss = double(r.slow.size());
+    t->model_t_c = std::ceil(miss / cost->parallel_slots) * cost->t_cc;
+    t->model_t_g = double(r.fast.size()) * cost->t_gc;
+    t->model_t_2 = std::max(t->model_t_c, t->model_t_g);
+  } else {
+    t->model_t_c = t->model_t_g = t->model_t_2 = 0.0;
+  }
+}
+
+void write_top(const std::vector<laivg::Scored>& top, int k, uint64_t* ids,
+               float* scores, uint32_t* count) {
+  for (size_t i = 0; i < top.size(); ++i) {
+    ids[i] = top[i].id;
+    scores[i] = top[i].s;
+  }
+  for (size_t i = top.size(); i < size_t(k); ++i) {
+    ids[i] = ~0ull;
+    scores[i] = std::nanf("");
+  }
+  if (count) *count = uint32_t(top.size());
+}
+
+void stage_query(Ctx& c, const float* q) {
+  need(q, "query");
+  std::memcpy(c.h_Q, q, c.ix->d * sizeof(float));
+  CK(cudaMemcpyAsync(c.d_Q, c.h_Q, c.ix->d * sizeof(float), cudaMemcpyHostToDevice, c.comp));
+}
+
+} // namespace
+
+extern "C" {
+
+const char* laivg_last_error(void) { return laivg::g_err.c_str(); }
+uint32_t laivg_version(void) { return (1u << 16) | 0u; }
+
+int laivg_host_alloc(uint64_t bytes, void** out) {
+  return guard([&] {
+    need(out, "out");
+    CK(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable));
+  });
+}
+int laivg_host_free(void* p) {
+  return guard([&] {
+    if (p) CK(cudaFreeHost(p));
+  });
+}
+
+// ---- index -----------------------------------------------------------------
+int laivg_index_create(const float* centroids, uint32_t nc, uint32_t d, int metric,
+                       const float* vecs, const uint64_t* ids, const uint64_t* list_off,
+                       uint32_t flags, laivg_index** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = nullptr;
+    if (d == 0) throw std::invalid_argument("matrix has no dimension set");
+    if (metric != LAIVG_METRIC_IP && metric != LAIVG_METRIC_L2) {
+      throw std::invalid_argument("bad metric");
+    }
+    need(list_off, "list_off");
+    if (nc) need(centroids, "centroids");
+    auto h = std::make_unique<laivg_index>();
+    Index& ix = h->ix;
+    ix.nc = nc;
+    ix.d = d;
+    ix.metric = metric;
+    ix.centroids.assign(centroids, centroids + size_t(nc) * d);
+    ix.list_off.assign(list_off, list_off + nc + 1);
+    if (ix.list_off[0] != 0) throw std::invalid_argument("list_off[0] must be 0");
+    for (uint32_t c = 0; c < nc; ++c) {
+      if (ix.list_off[c + 1] < ix.list_off[c]) {
+        throw std::invalid_argument("list_off must be non-decreasing");
+      }
+    }
+    const uint64_t n = ix.list_off[nc];
+    if (n) {
+      need(vecs, "vecs");
+      need(ids, "ids");
+    }
+    if (!(flags & LAIVG_INDEX_TRUST)) { // vectorstore.cpp:66-85
+      for (size_t i = 0; i < ix.centroids.size(); ++i) {
+        if (!std::isfinite(ix.centroids[i])) {
+          throw std::invalid_argument("non-finite component in centroid " +
+                                      std::to_string(i / d));
+        }
+      }
+      for (uint64_t i = 0; i < n * d; ++i) {
+        if (!std::isfinite(vecs[i])) {
+          throw std::invalid_argument("non-finite component in row for id " +
+                                      std::to_string(ids[i / d]));
+        }
+      }
+      std::unordered_set<uint64_t> seen;
+      seen.reserve(n);
+      for (uint64_t i = 0; i < n; ++i) {
+        if (!seen.insert(ids[i]).second) {
+          throw std::invalid_argument("duplicate id " + std::to_string(ids[i]));
+        }
+      }
+    }
+    if (flags & LAIVG_INDEX_BORROW) {
+      ix.vecs = vecs;
+      ix.ids = ids;
+    } else {
+      const size_t vb = size_t(n) * d * sizeof(float), ib = size_t(n) * sizeof(uint64_t);
+      // Pinned when a driver is present; pageable host memory otherwise (the
+      // index itself is host data -- only the device context needs a GPU).
+      void* blk = nullptr;
+      if (cudaHostAlloc(&blk, vb + ib + 16, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        blk = std::aligned_alloc(64, ((vb + ib + 16) + 63) & ~size_t(63));
+        if (!blk) throw std::runtime_error("host allocation failed");
+        ix.owned_pageable = true;
+      }
+      ix.owned_block = blk;
+      float* v = static_cast<float*>(blk);
+      uint64_t* id = reinterpret_cast<uint64_t*>(static_cast<char*>(blk) + ((vb + 15) & ~size_t(15)));
+      if (n) {
+        std::memcpy(v, vecs, vb);
+        std::memcpy(id, ids, ib);
+      }
+      ix.vecs = v;
+      ix.ids = id;
+    }
+    *out = h.release();
+  });
+}
+
+void laivg_index_destroy(laivg_index* ix) {
+  if (!ix) return;
+  if (ix->ix.owned_block) {
+    if (ix->ix.owned_pageable) std::free(ix->ix.owned_block);
+    else cudaFreeHost(ix->ix.owned_block);
+  }
+  delete ix;
+}
+uint32_t laivg_index_num_clusters(const laivg_index* ix) { return ix ? ix->ix.nc : 0; }
+uint32_t laivg_index_dim(const laivg_index* ix) { return ix ? ix->ix.d : 0; }
+int laivg_index_metric(const laivg_index* ix) { return ix ? ix->ix.metric : -1; }
+uint64_t laivg_index_total_vectors(const laivg_index* ix) { return ix ? ix->ix.total() : 0; }
+uint64_t laivg_index_cluster_bytes(const laivg_index* ix, uint32_t c) {
+  return (ix && c < ix->ix.nc) ? ix->ix.cluster_bytes(c) : 0;
+}
+uint64_t laivg_index_total_payload_bytes(const laivg_index* ix) {
+  return ix ? ix->ix.total() * ix->ix.member_bytes() : 0;
+}
+
+// ---- context ---------------------------------------------------------------
+void laivg_opts_default(laivg_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->acc_fp64 = 1;
+}
+
+int laivg_ctx_create(const laivg_index* ix, const laivg_opts* opts, laivg_ctx** out) {
+  return guard([&] {
+    need(ix, "index");
+    need(out, "out");
+    *out = nullptr;
+    laivg_opts o;
+    if (opts) o = *opts;
+    else laivg_opts_default(&o);
+    auto h = std::make_unique<laivg_ctx>();
+    h->c.init(&ix->ix, o);
+    *out = h.release();
+  });
+}
+
+void laivg_ctx_destroy(laivg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->c.dev);
+  delete ctx;
+}
+
+int laivg_ctx_sync(laivg_ctx* ctx) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    CK(cudaStreamSynchronize(ctx->c.copy));
+    CK(cudaStreamSynchronize(ctx->c.aux));
+    CK(cudaStreamSynchronize(ctx->c.comp));
+  });
+}
+
+// ---- coarse ----------------------------------------------------------------
+namespace {
+void coarse_batch(Ctx& c, const float* Q, uint32_t nq, uint32_t n_out,
+                  uint32_t* order_out, double* scores_out) {
+  need(Q, "queries");
+  const uint32_t d = c.ix->d, nc = c.ix->nc;
+  for (uint32_t q0 = 0; q0 < nq; q0 += c.max_batch) {
+    const uint32_t b = std::min(c.max_batch, nq - q0);
+    std::memcpy(c.h_Q, Q + size_t(q0) * d, size_t(b) * d * sizeof(float));
+    CK(cudaMemcpyAsync(c.d_Q, c.h_Q, size_t(b) * d * sizeof(float), cudaMemcpyHostToDevice, c.comp));
+    c.coarse(c.d_Q, b, n_out, c.comp);
+    if (n_out) {
+      CK(cudaMemcpyAsync(c.h_order, c.d_order, size_t(b) * n_out * sizeof(uint32_t),
+                         cudaMemcpyDeviceToHost, c.comp));
+    }
+    if (scores_out) {
+      CK(cudaMemcpyAsync(scores_out + size_t(q0) * nc, c.d_scores, size_t(b) * nc * sizeof(double),
+                         cudaMemcpyDeviceToHost, c.comp));
+    }
+    CK(cudaStreamSynchronize(c.comp));
+    if (n_out) std::memcpy(order_out + size_t(q0) * n_out, c.h_order, size_t(b) * n_out * sizeof(uint32_t));
+  }
+}
+} // namespace
+
+int laivg_rank_clusters(laivg_ctx* ctx, const float* Q, uint32_t nq, uint32_t* order_out,
+                        double* scores_out) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    need(order_out, "order_out");
+    coarse_batch(ctx->c, Q, nq, ctx->c.ix->nc, order_out, scores_out);
+  });
+}
+
+int laivg_coarse_probe(laivg_ctx* ctx, const float* Q, uint32_t nq, int L, uint32_t* probe_out,
+                       uint32_t* lp_out) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    const uint32_t lp = uint32_t(std::min<int64_t>(std::max(L, 0), ctx->c.ix->nc));
+    if (lp_out) *lp_out = lp;
+    if (lp) need(probe_out, "probe_out");
+    coarse_batch(ctx->c, Q, nq, lp, probe_out, nullptr);
+  });
+}
+
+// ---- fine search -------------------------------------------------------------
+int laivg_search_clusters(laivg_ctx* ctx, const float* q, const uint32_t* clusters, uint32_t n,
+                          int k, uint64_t* ids_out, float* scores_out, uint32_t* count_out) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    if (k < 1) throw std::invalid_argument("k must be >= 1");
+    need(ids_out, "ids_out");
+    need(scores_out, "scores_out");
+    if (n) need(clusters, "clusters");
+    Ctx& c = ctx->c;
+    stage_query(c, q);
+    std::vector<uint32_t> probe(clusters, clusters + n);
+    auto r = c.search(c.d_Q, q, 0, k, &probe);
+    write_top(r.top, k, ids_out, scores_out, count_out);
+  });
+}
+
+int laivg_ivf_search(laivg_ctx* ctx, const float* Q, uint32_t nq, int L, int k, uint64_t* ids_out,
+                     float* scores_out, uint32_t* count_out) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    if (k < 1) throw std::invalid_argument("k must be >= 1");
+    need(ids_out, "ids_out");
+    need(scores_out, "scores_out");
+    Ctx& c = ctx->c;
+    for (uint32_t i = 0; i < nq; ++i) {
+      const float* q = Q + size_t(i) * c.ix->d;
+      stage_query(c, q);
+      auto r = c.search(c.d_Q, q, L, k, nullptr);
+      write_top(r.top, k, ids_out + size_t(i) * k, scores_out + size_t(i) * k,
+                count_out ? count_out + i : nullptr);
+    }
+  });
+}
+
+// ---- store -------------------------------------------------------------------
+uint64_t laivg_store_capacity_bytes(const laivg_ctx* ctx) { return ctx ? ctx->c.capacity : 0; }
+uint64_t laivg_store_used_bytes(const laivg_ctx* ctx) { return ctx ? ctx->c.used : 0; }
+uint64_t laivg_store_free_bytes(const laivg_ctx* ctx) {
+  return ctx ? ctx->c.capacity - ctx->c.used : 0;
+}
+int laivg_store_contains(const laivg_ctx* ctx, uint32_t c) {
+  return ctx && ctx->c.resident.count(c) ? 1 : 0;
+}
+uint32_t laivg_store_resident_count(const laivg_ctx* ctx) {
+  return ctx ? uint32_t(ctx->c.resident.size()) : 0;
+}
+int laivg_store_resident(const laivg_ctx* ctx, uint32_t* clusters_out, uint8_t* tags_out,
+                         uint64_t* bytes_out, uint32_t* n_out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    uint32_t i = 0;
+    for (auto& [c, r] : ctx->c.resident) {
+      if (clusters_out) clusters_out[i] = c;
+      if (tags_out) tags_out[i] = uint8_t(r.tag);
+      if (bytes_out) bytes_out[i] = r.bytes;
+      ++i;
+    }
+    if (n_out) *n_out = i;
+  });
+}
+int laivg_store_insert(laivg_ctx* ctx, uint32_t c, int tag) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    Ctx& x = ctx->c;
+    x.copy_after_comp();
+    x.insert_async(c, tag);
+    x.commit_res(x.copy);
+    CK(cudaEventRecord(x.ev_copy_tail, x.copy));
+    CK(cudaStreamSynchronize(x.copy));
+  });
+}
+int laivg_store_evict(laivg_ctx* ctx, uint32_t c, uint64_t* bytes_out) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    const uint64_t b = ctx->c.evict(c);
+    if (bytes_out) *bytes_out = b;
+  });
+}
+int laivg_store_retag_all(laivg_ctx* ctx, int tag) {
+  return guard([&] {
+    need(ctx, "ctx");
+    for (auto& [c, r] : ctx->c.resident) r.tag = tag;
+  });
+}
+int laivg_store_clear(laivg_ctx* ctx) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    ctx->c.clear_store();
+  });
+}
+uint64_t laivg_store_bytes_with_tag(const laivg_ctx* ctx, int tag) {
+  uint64_t s = 0;
+  if (ctx) {
+    for (auto& [c, r] : ctx->c.resident) {
+      if (r.tag == tag) s += r.bytes;
+    }
+  }
+  return s;
+}
+uint64_t laivg_store_recompute_used_bytes(const laivg_ctx* ctx) {
+  uint64_t s = 0;
+  if (ctx) {
+    for (auto& [c, r] : ctx->c.resident) s += r.bytes;
+  }
+  return s;
+}
+int laivg_store_compact(laivg_ctx* ctx) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    Ctx& x = ctx->c;
+    x.compact();
+    x.commit_res(x.copy);
+    CK(cudaEventRecord(x.ev_copy_tail, x.copy));
+    CK(cudaStreamSynchronize(x.copy));
+  });
+}
+
+// ---- prefetch ------------------------------------------------------------------
+int laivg_plan_prefetch(laivg_ctx* ctx, const float* q_in, uint64_t budget_bytes,
+                        uint32_t* plan_out, uint32_t* nplan_out, uint64_t* planned_bytes_out,
+                        uint32_t* skipped_out, uint32_t* nskipped_out) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    Ctx& x = ctx->c;
+    std::vector<uint32_t> order(x.ix->nc);
+    coarse_batch(x, q_in, 1, x.ix->nc, order.data(), nullptr);
+    std::vector<uint32_t> plan, skipped;
+    uint64_t planned = 0;
+    laivg::plan_walk(*x.ix, order.data(), [&](uint32_t c) { return x.h_res[c] >= 0; },
+                     budget_bytes, plan, planned, skipped);
+    if (plan_out) std::copy(plan.begin(), plan.end(), plan_out);
+    if (skipped_out) std::copy(skipped.begin(), skipped.end(), skipped_out);
+    if (nplan_out) *nplan_out = uint32_t(plan.size());
+    if (nskipped_out) *nskipped_out = uint32_t(skipped.size());
+    if (planned_bytes_out) *planned_bytes_out = planned;
+  });
+}
+
+int laivg_execute_prefetch(laivg_ctx* ctx, const uint32_t* plan, uint32_t n,
+                           const laivg_channel* chan, double overlap_window_s,
+                           uint32_t* transferred_out, laivg_transfer_report* rep) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    need(chan, "chan");
+    if (n) need(plan, "plan");
+    Ctx& x = ctx->c;
+    laivg_transfer_report r{};
+    const int mode = chan->mode;
+    if (mode != LAIVG_CHAN_SIMULATED && mode != LAIVG_CHAN_MEASURED && mode != LAIVG_CHAN_DEVICE) {
+      throw std::invalid_argument("bad channel mode");
+    }
+    if (mode == LAIVG_CHAN_SIMULATED && !(chan->bandwidth_bytes_per_s > 0)) {
+      throw std::invalid_argument("bandwidth must be positive");
+    }
+    uint64_t bytes = 0;
+    const auto w0 = Clock::now();
+    CK(cudaEventRecord(x.ev_base, x.comp));
+    CK(cudaStreamWaitEvent(x.copy, x.ev_base, 0));
+    const bool win = mode == LAIVG_CHAN_DEVICE && overlap_window_s > 0;
+    if (win) laivg::launch_window(uint64_t(overlap_window_s * 1e9), x.sms, x.comp);
+    CK(cudaEventRecord(x.ev_win, x.comp));
+    CK(cudaEventRecord(x.ev_cp0, x.copy));
+    uint32_t done = 0;
+    try {
+      for (uint32_t i = 0; i < n; ++i) {
+        x.insert_async(plan[i], LAIVG_TAG_PREFETCHED);
+        bytes += x.ix->cluster_bytes(plan[i]);
+        if (transferred_out) transferred_out[i] = plan[i];
+        ++done;
+      }
+    } catch (...) {
+      // Reference semantics: clusters inserted before the failure stay.
+      x.commit_res(x.copy);
+      CK(cudaEventRecord(x.ev_copy_tail, x.copy));
+      CK(cudaStreamSynchronize(x.copy));
+      CK(cudaStreamSynchronize(x.comp));
+      throw;
+    }
+    x.commit_res(x.copy);
+    CK(cudaEventRecord(x.ev_cp1, x.copy));
+    CK(cudaEventRecord(x.ev_copy_tail, x.copy));
+    CK(cudaEventSynchronize(x.ev_cp1));
+    CK(cudaEventSynchronize(x.ev_win));
+    const double wall = std::chrono::duration<double>(Clock::now() - w0).count();
+    float ms_cp = 0, ms_win = 0, ms_end = 0;
+    CK(cudaEventElapsedTime(&ms_cp, x.ev_cp0, x.ev_cp1));
+    CK(cudaEventElapsedTime(&ms_win, x.ev_base, x.ev_win));
+    CK(cudaEventElapsedTime(&ms_end, x.ev_base, x.ev_cp1));
+    r.bytes = bytes;
+    r.n_transferred = done;
+    r.window_s = win ? ms_win * 1e-3 : 0.0;
+    r.h2d_gbps = ms_cp > 0 ? double(bytes) / (ms_cp * 1e-3) / 1e9 : 0.0;
+    if (mode == LAIVG_CHAN_SIMULATED) {
+      r.t_p = double(bytes) / chan->bandwidth_bytes_per_s; // tiered.cpp:131
+      r.overshoot_s = std::max(0.0, r.t_p - overlap_window_s);
+    } else if (mode == LAIVG_CHAN_MEASURED) {
+      r.t_p = wall;
+      r.overshoot_s = std::max(0.0, r.t_p - overlap_window_s);
+    } else {
+      r.t_p = ms_cp * 1e-3;
+      // exposed transfer: copy end past window end (both from ev_base)
+      r.overshoot_s = std::max(0.0, double(ms_end - (win ? ms_win : 0.0f)) * 1e-3);
+    }
+    if (rep) *rep = r;
+  });
+}
+
+int laivg_incremental_prefetch(laivg_ctx* ctx, const float* q_round, uint64_t budget_bytes,
+                               const laivg_channel* chan, double overlap_window_s,
+                               uint32_t* transferred_out, laivg_transfer_report* rep) {
+  return guard([&] {
+    need(ctx, "ctx");
+    std::vector<uint32_t> plan(ctx->c.ix->nc), skipped(ctx->c.ix->nc);
+    uint32_t np = 0, ns = 0;
+    uint64_t pb = 0;
+    int rc = laivg_plan_prefetch(ctx, q_round, budget_bytes, plan.data(), &np, &pb,
+                                 skipped.data(), &ns);
+    if (rc) throw std::runtime_error(laivg::g_err);
+    rc = laivg_execute_prefetch(ctx, plan.data(), np, chan, overlap_window_s, transferred_out, rep);
+    if (rc == LAIVG_ELOGIC) throw std::logic_error(laivg::g_err);
+    if (rc == LAIVG_ECUDA) throw laivg::CudaError(laivg::g_err);
+    if (rc == LAIVG_EINVAL) throw std::invalid_argument(laivg::g_err);
+    if (rc) throw std::runtime_error(laivg::g_err);
+  });
+}
+
+int laivg_window(laivg_ctx* ctx, double seconds, double* measured_s) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    Ctx& x = ctx->c;
+    CK(cudaEventRecord(x.ev_base, x.comp));
+    if (seconds > 0) laivg::launch_window(uint64_t(seconds * 1e9), x.sms, x.comp);
+    CK(cudaEventRecord(x.ev_win, x.comp));
+    CK(cudaEventSynchronize(x.ev_win));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, x.ev_base, x.ev_win));
+    if (measured_s) *measured_s = ms * 1e-3;
+  });
+}
+
+// ---- hybrid ----------------------------------------------------------------------
+int laivg_hybrid_search(laivg_ctx* ctx, const float* q_out, int L, int k,
+                        const laivg_cost_model* cost, uint64_t* ids_out, float* scores_out,
+                        uint32_t* count_out, uint32_t* fast_out, uint32_t* nfast_out,
+                        uint32_t* slow_out, uint32_t* nslow_out, double* hit_rate_out,
+                        laivg_hybrid_timing* timing) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    if (k < 1) throw std::invalid_argument("k must be >= 1");
+    need(ids_out, "ids_out");
+    need(scores_out, "scores_out");
+    Ctx& c = ctx->c;
+    stage_query(c, q_out);
+    auto r = c.search(c.d_Q, q_out, L, k, nullptr);
+    write_top(r.top, k, ids_out, scores_out, count_out);
+    if (fast_out) std::copy(r.fast.begin(), r.fast.end(), fast_out);
+    if (slow_out) std::copy(r.slow.begin(), r.slow.end(), slow_out);
+    if (nfast_out) *nfast_out = uint32_t(r.fast.size());
+    if (nslow_out) *nslow_out = uint32_t(r.slow.size());
+    const size_t probed = r.fast.size() + r.slow.size();
+    if (hit_rate_out) *hit_rate_out = probed ? double(r.fast.size()) / double(probed) : 0.0;
+    fill_timing(timing, r, cost);
+  });
+}
+
+int laivg_coverage(laivg_ctx* ctx, const float* q_in, const float* q_out, int L, double* out) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    need(q_in, "q_in");
+    need(q_out, "q_out");
+    need(out, "out");
+    Ctx& c = ctx->c;
+    const uint32_t d = c.ix->d;
+    const uint32_t lp = uint32_t(std::min<int64_t>(std::max(L, 0), c.ix->nc));
+    if (lp == 0) {
+      *out = 0.0;
+      return;
+    }
+    std::vector<float> Q(size_t(2) * d);
+    std::memcpy(Q.data(), q_in, d * sizeof(float));
+    std::memcpy(Q.data() + d, q_out, d * sizeof(float));
+    std::vector<uint32_t> probe(size_t(2) * lp);
+    coarse_batch(c, Q.data(), 2, lp, probe.data(), nullptr);
+    std::unordered_set<uint32_t> in(probe.begin(), probe.begin() + lp);
+    size_t overlap = 0;
+    for (uint32_t i = 0; i < lp; ++i) overlap += in.count(probe[lp + i]);
+    *out = double(overlap) / double(lp);
+  });
+}
+
+int laivg_stage_queries(laivg_ctx* ctx, const float* Q, uint32_t nq) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    need(Q, "queries");
+    Ctx& c = ctx->c;
+    if (c.d_staged) {
+      CK(cudaFree(c.d_staged));
+      c.d_staged = nullptr;
+    }
+    const size_t n = size_t(nq) * c.ix->d;
+    c.d_staged = laivg::dev_alloc<float>(n);
+    CK(cudaMemcpy(c.d_staged, Q, n * sizeof(float), cudaMemcpyHostToDevice));
+    c.staged_host.assign(Q, Q + n);
+    c.n_staged = nq;
+  });
+}
+
+int laivg_hybrid_search_staged(laivg_ctx* ctx, uint32_t qi, int L, int k, uint64_t* ids_out,
+                               float* scores_out, uint32_t* count_out, uint32_t* nfast_out,
+                               laivg_hybrid_timing* timing) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    Ctx& c = ctx->c;
+    if (qi >= c.n_staged) throw std::invalid_argument("staged query index out of range");
+    const size_t off = size_t(qi) * c.ix->d;
+    auto r = c.search(c.d_staged + off, c.staged_host.data() + off, L, k, nullptr);
+    if (ids_out && scores_out) write_top(r.top, k, ids_out, scores_out, count_out);
+    if (nfast_out) *nfast_out = uint32_t(r.fast.size());
+    fill_timing(timing, r, nullptr);
+  });
+}
+
+// ---- schedulers ----------------------------------------------------------------
+int laivg_group_microbatches(const float* queries, uint64_t n, uint32_t d, uint64_t m,
+                             uint64_t* order_out, uint64_t* batch_off_out, uint32_t* nb_out) {
+  return guard([&] {
+    if (n) need(queries, "queries");
+    std::vector<uint64_t> order, off;
+    static laivg::ThreadPool pool(std::max(1u, std::thread::hardware_concurrency()) - 1);
+    laivg::group_microbatches(queries, n, d, m, order, off, &pool);
+    std::copy(order.begin(), order.end(), order_out);
+    std::copy(off.begin(), off.end(), batch_off_out);
+    if (nb_out) *nb_out = uint32_t(off.size() - 1);
+  });
+}
+
+int laivg_chunk_microbatches(uint64_t n, uint64_t m, uint64_t* order_out, uint64_t* batch_off_out,
+                             uint32_t* nb_out) {
+  return guard([&] {
+    if (m < 1) throw std::invalid_argument("micro-batch size must be >= 1");
+    uint32_t nb = 0;
+    batch_off_out[0] = 0;
+    for (uint64_t i = 0; i < n; i += m) {
+      for (uint64_t j = i; j < std::min(i + m, n); ++j) order_out[j] = j;
+      batch_off_out[++nb] = std::min(i + m, n);
+    }
+    if (nb_out) *nb_out = nb;
+  });
+}
+
+namespace {
+// overlap[b][w] = |probe union of batch b  ∩  resident set of worker w|
+// (sched.cpp:15-35, 99-108); probes from the GPU coarse quantizer.
+std::vector<uint64_t> overlap_matrix(Ctx& c, const uint64_t* off, const uint64_t* mem,
+                                     uint32_t nb, const uint8_t* resident, uint32_t nw,
+                                     const float* queries, uint64_t nq, int L) {
+  const uint32_t nc = c.ix->nc;
+  const uint32_t lp = uint32_t(std::min<int64_t>(std::max(L, 0), nc));
+  std::vector<uint32_t> probe(size_t(nq) * lp);
+  if (lp && nq) coarse_batch(c, queries, uint32_t(nq), lp, probe.data(), nullptr);
+  std::vector<uint64_t> ov(size_t(nb) * nw, 0);
+  std::vector<uint8_t> mark(nc);
+  for (uint32_t b = 0; b < nb; ++b) {
+    std::fill(mark.begin(), mark.end(), 0);
+    for (uint64_t i = off[b]; i < off[b + 1]; ++i) {
+      if (mem[i] >= nq) throw std::out_of_range("query index out of range");
+      for (uint32_t j = 0; j < lp; ++j) mark[probe[size_t(mem[i]) * lp + j]] = 1;
+    }
+    for (uint32_t w = 0; w < nw; ++w) {
+      uint64_t s = 0;
+      const uint8_t* r = resident + size_t(w) * nc;
+      for (uint32_t x = 0; x < nc; ++x) s += mark[x] & (r[x] != 0);
+      ov[size_t(b) * nw + w] = s;
+    }
+  }
+  return ov;
+}
+} // namespace
+
+int laivg_assign_cache_aware(laivg_ctx* ctx, const uint64_t* batch_off, const uint64_t* members,
+                             uint32_t nb, const uint8_t* resident, uint32_t nw,
+                             const float* queries, uint64_t nq, int L, uint32_t* assignment_out) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    if (nw == 0) throw std::invalid_argument("need at least one worker");
+    auto ov = overlap_matrix(ctx->c, batch_off, members, nb, resident, nw, queries, nq, L);
+    auto a = laivg::greedy_assign(ov, nb, nw);
+    std::copy(a.begin(), a.end(), assignment_out);
+  });
+}
+
+int laivg_assign_round_robin(uint64_t nb, uint64_t nw, uint32_t* out) {
+  return guard([&] {
+    if (nw == 0) throw std::invalid_argument("need at least one worker");
+    for (uint64_t b = 0; b < nb; ++b) out[b] = uint32_t(b % nw);
+  });
+}
+
+int laivg_assignment_overlap(laivg_ctx* ctx, const uint64_t* batch_off, const uint64_t* members,
+                             uint32_t nb, const uint8_t* resident, uint32_t nw,
+                             const uint32_t* assignment, const float* queries, uint64_t nq, int L,
+                             uint64_t* out) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    auto ov = overlap_matrix(ctx->c, batch_off, members, nb, resident, nw, queries, nq, L);
+    uint64_t s = 0;
+    for (uint32_t b = 0; b < nb; ++b) {
+      if (assignment[b] >= nw) throw std::out_of_range("assignment out of range");
+      s += ov[size_t(b) * nw + assignment[b]];
+    }
+    *out = s;
+  });
+}
+
+int laivg_split_budget(uint64_t total, const uint64_t* batch, uint64_t n, uint64_t* out) {
+  return guard([&] {
+    auto s = laivg::split_budget(total, batch, n);
+    std::copy(s.begin(), s.end(), out);
+  });
+}
+
+// ---- hotness ---------------------------------------------------------------------
+int laivg_hotness_create(float h_init, float h_inc, float decay, double cache_fraction,
+                         laivg_hotness** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = new laivg_hotness{laivg::Hotness(h_init, h_inc, decay, cache_fraction)};
+  });
+}
+void laivg_hotness_destroy(laivg_hotness* h) { delete h; }
+int laivg_hotness_on_fetch(laivg_hotness* h, uint32_t c) {
+  return guard([&] {
+    need(h, "hotness");
+    h->h.on_fetch(c);
+  });
+}
+int laivg_hotness_end_of_round(laivg_hotness* h, const uint32_t* used, uint32_t n) {
+  return guard([&] {
+    need(h, "hotness");
+    std::unordered_set<uint32_t> u;
+    if (n) u.insert(used, used + n);
+    h->h.end_of_round(u);
+  });
+}
+int laivg_hotness_evict_to_fraction(laivg_hotness* h, laivg_ctx* ctx, uint32_t* evicted_out,
+                                    uint32_t* n_out) {
+  return guard([&] {
+    need(h, "hotness");
+    set_ctx_device(ctx);
+    Ctx& x = ctx->c;
+    for (auto& [c, r] : x.resident) r.tag = LAIVG_TAG_CACHED; // cache.cpp:41
+    const auto budget = uint64_t(h->h.fraction() * double(x.capacity));
+    std::vector<uint32_t> ids;
+    for (auto& [c, r] : x.resident) ids.push_back(c);
+    uint32_t n = 0;
+    for (uint32_t c : h->h.eviction_order(ids)) {
+      if (x.used <= budget) break;
+      x.evict(c);
+      h->h.forget(c);
+      if (evicted_out) evicted_out[n] = c;
+      ++n;
+    }
+    if (n_out) *n_out = n;
+  });
+}
+float laivg_hotness_get(const laivg_hotness* h, uint32_t c) {
+  return h && h->h.tracked(c) ? h->h.get(c) : -1.0f;
+}
+int laivg_hotness_forget(laivg_hotness* h, uint32_t c) {
+  return guard([&] {
+    need(h, "hotness");
+    h->h.forget(c);
+  });
+}
+int laivg_hotness_clear(laivg_hotness* h) {
+  return guard([&] {
+    need(h, "hotness");
+    h->h.clear();
+  });
+}
+
+// ---- synthetic workload -------------------------------------------------------------
+int laivg_synth_centroids(uint64_t seed, uint32_t nc, uint32_t d, float* centroids_out) {
+  return guard([&] {
+    need(centroids_out, "centroids_out");
+    laivg::synth_centroids(seed, nc, d, centroids_out);
+  });
+}
+int laivg_synth_lists(uint64_t seed, const float* centroids, uint32_t nc, uint32_t d,
+                      uint64_t per_list, float spread, uint32_t c_begin, uint32_t c_end,
+                      float* vecs_out, uint64_t* ids_out, int threads) {
+  return guard([&] {
+    need(centroids, "centroids");
+    if (c_end > nc || c_begin > c_end) throw std::invalid_argument("bad cluster range");
+    if (threads <= 0) threads = int(std::max(1u, std::thread::hardware_concurrency()));
+    laivg::synth_lists(seed, centroids, d, per_list, spread, c_begin, c_end, vecs_out,
+                       ids_out, threads);
+  });
+}
+int laivg_synth_queries(uint64_t seed, const float* vecs, uint64_t n_rows, uint32_t d, uint32_t nq,
+                        float sigma, float* q_in_out, float* q_out_out, uint64_t* rows_out) {
+  return guard([&] {
+    need(vecs, "vecs");
+    if (n_rows == 0) throw std::invalid_argument("no rows");
+    laivg::synth_queries(seed, vecs, n_rows, d, nq, sigma, q_in_out, q_out_out, rows_out);
+  });
+}
+
+} // extern "C"

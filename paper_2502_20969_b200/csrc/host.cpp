@@ -1,0 +1,428 @@
+// host.cpp — CPU side of the retrieval path (see host.hpp).
+// Built with -ffp-contract=off: every fp64 add/mul rounds separately, as the
+// reference's scalar loops do (vectorstore.cpp:93-108).
+#include "host.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+namespace laivg {
+
+// ==========================================================================
+// ThreadPool
+// ==========================================================================
+ThreadPool::ThreadPool(unsigned n) {
+  for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this, i] { loop(i + 1); });
+}
+
+ThreadPool::~ThreadPool() {
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    stop_ = true;
+  }
+  cv_.notify_all();
+  for (auto& t : workers_) t.join();
+}
+
+void ThreadPool::loop(unsigned wid) {
+  uint64_t seen = 0;
+  for (;;) {
+    const std::function<void(size_t, unsigned)>* job;
+    size_t n;
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+      job = job_;
+      n = n_;
+      if (job == nullptr) continue; // woke after that job already finished
+      ++active_;
+    }
+    for (size_t i; (i = next_.fetch_add(1)) < n;) (*job)(i, wid);
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      if (--active_ == 0) done_cv_.notify_all();
+    }
+  }
+}
+
+void ThreadPool::parallel_for(size_t n,
+                              const std::function<void(size_t, unsigned)>& fn) {
+  if (n == 0) return;
+  if (workers_.empty() || n == 1) {
+    for (size_t i = 0; i < n; ++i) fn(i, 0);
+    return;
+  }
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    job_ = &fn;
+    n_ = n;
+    next_ = 0;
+    ++gen_;
+  }
+  cv_.notify_all();
+  for (size_t i; (i = next_.fetch_add(1)) < n;) fn(i, 0);
+  std::unique_lock<std::mutex> lk(mu_);
+  done_cv_.wait(lk, [&] { return active_ == 0 && next_ >= n; });
+  job_ = nullptr;
+}
+
+// ==========================================================================
+// miss scan
+// ==========================================================================
+namespace {
+
+// fp64 dot / squared L2 over fp32 inputs, 16 partial sums (vectorised).
+__attribute__((target_clones("arch=sapphirerapids", "default")))
+double dot_f64(const float* a, const float* b, uint32_t d) {
+  double acc[16] = {0};
+  uint32_t j = 0;
+  for (; j + 16 <= d; j += 16) {
+    for (int t = 0; t < 16; ++t) {
+      acc[t] += static_cast<double>(a[j + t]) * static_cast<double>(b[j + t]);
+    }
+  }
+  for (int t = 0; t < 8; ++t) acc[t] += acc[t + 8];
+  for (int t = 0; t < 4; ++t) acc[t] += acc[t + 4];
+  double s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  for (; j < d; ++j) s += static_cast<double>(a[j]) * static_cast<double>(b[j]);
+  return s;
+}
+
+__attribute__((target_clones("arch=sapphirerapids", "default")))
+double l2sq_f64(const float* a, const float* b, uint32_t d) {
+  double acc[16] = {0};
+  uint32_t j = 0;
+  for (; j + 16 <= d; j += 16) {
+    for (int t = 0; t < 16; ++t) {
+      const double x = static_cast<double>(a[j + t]) - static_cast<double>(b[j + t]);
+      acc[t] += x * x;
+    }
+  }
+  for (int t = 0; t < 8; ++t) acc[t] += acc[t + 8];
+  for (int t = 0; t < 4; ++t) acc[t] += acc[t + 4];
+  double s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  for (; j < d; ++j) {
+    const double x = static_cast<double>(a[j]) - static_cast<double>(b[j]);
+    s += x * x;
+  }
+  return s;
+}
+
+// Sorted best-first list of at most k entries.
+struct TopList {
+  int metric;
+  int k;
+  std::vector<Scored> e;
+  void push(const Scored& c) {
+    if (static_cast<int>(e.size()) == k && !ranks_before(metric, c, e.back())) return;
+    auto it = std::upper_bound(e.begin(), e.end(), c, [this](const Scored& a, const Scored& b) {
+      return ranks_before(metric, a, b);
+    });
+    e.insert(it, c);
+    if (static_cast<int>(e.size()) > k) e.pop_back();
+  }
+};
+
+constexpr uint64_t kMissChunk = 1024; // vectors per miss-scan task
+
+} // namespace
+
+std::vector<Scored> miss_scan(const Index& ix, const float* q,
+                              const std::vector<uint32_t>& lists, int k,
+                              ThreadPool& pool) {
+  struct Task {
+    uint64_t r0, r1;
+  };
+  std::vector<Task> tasks;
+  for (uint32_t c : lists) {
+    for (uint64_t r = ix.list_off[c]; r < ix.list_off[c + 1]; r += kMissChunk) {
+      tasks.push_back({r, std::min(r + kMissChunk, ix.list_off[c + 1])});
+    }
+  }
+  std::vector<TopList> per(pool.size(), TopList{ix.metric, k, {}});
+  const uint32_t d = ix.d;
+  pool.parallel_for(tasks.size(), [&](size_t t, unsigned wid) {
+    TopList& tl = per[wid];
+    for (uint64_t r = tasks[t].r0; r < tasks[t].r1; ++r) {
+      const float* x = ix.vecs + r * d;
+      float s;
+      if (ix.metric == kMetricIP) {
+        s = static_cast<float>(dot_f64(q, x, d));
+      } else {
+        s = static_cast<float>(std::sqrt(l2sq_f64(q, x, d)));
+      }
+      tl.push({s, ix.ids[r]});
+    }
+  });
+  TopList all{ix.metric, k, {}};
+  for (auto& tl : per) {
+    for (const auto& e : tl.e) all.push(e);
+  }
+  return std::move(all.e);
+}
+
+std::vector<Scored> merge_topk(int metric, const std::vector<Scored>& a,
+                               const std::vector<Scored>& b, int k) {
+  std::vector<Scored> out;
+  out.reserve(std::min<size_t>(a.size() + b.size(), static_cast<size_t>(k)));
+  size_t i = 0, j = 0;
+  while (static_cast<int>(out.size()) < k && (i < a.size() || j < b.size())) {
+    if (j >= b.size() || (i < a.size() && ranks_before(metric, a[i], b[j]))) {
+      out.push_back(a[i++]);
+    } else {
+      out.push_back(b[j++]);
+    }
+  }
+  return out;
+}
+
+// ==========================================================================
+// planner (tiered.cpp:67-84)
+// ==========================================================================
+void plan_walk(const Index& ix, const uint32_t* order,
+               const std::function<bool(uint32_t)>& resident, uint64_t budget,
+               std::vector<uint32_t>& plan, uint64_t& planned,
+               std::vector<uint32_t>& skipped) {
+  plan.clear();
+  skipped.clear();
+  planned = 0;
+  uint64_t remaining = budget;
+  for (uint32_t i = 0; i < ix.nc; ++i) {
+    const uint32_t c = order[i];
+    if (resident(c)) continue;
+    const uint64_t b = ix.cluster_bytes(c);
+    if (b <= remaining) {
+      plan.push_back(c);
+      planned += b;
+      remaining -= b;
+    } else {
+      skipped.push_back(c);
+    }
+  }
+}
+
+// ==========================================================================
+// schedulers (sched.cpp)
+// ==========================================================================
+namespace {
+double l2sq_serial(const float* a, const float* b, uint32_t d) {
+  double acc = 0.0;
+  for (uint32_t j = 0; j < d; ++j) {
+    const double t = static_cast<double>(a[j]) - static_cast<double>(b[j]);
+    acc += t * t;
+  }
+  return acc;
+}
+} // namespace
+
+void group_microbatches(const float* q, uint64_t n, uint32_t d, uint64_t m,
+                        std::vector<uint64_t>& order,
+                        std::vector<uint64_t>& off, ThreadPool* pool) {
+  if (m < 1) throw std::invalid_argument("micro-batch size must be >= 1");
+  // Pairwise fp64 L2^2 with the reference's serial accumulation (the
+  // distance is symmetric bit for bit: (a-b)^2 == (b-a)^2), rows in parallel.
+  std::vector<double> dist(n * n, 0.0);
+  auto row = [&](size_t i, unsigned) {
+    for (uint64_t j = i + 1; j < n; ++j) dist[i * n + j] = l2sq_serial(q + i * d, q + j * d, d);
+  };
+  if (pool) pool->parallel_for(n, row);
+  else for (size_t i = 0; i < n; ++i) row(i, 0);
+  order.clear();
+  off.assign(1, 0);
+  std::vector<char> assigned(n, 0);
+  std::vector<std::pair<double, uint64_t>> cand;
+  for (uint64_t seed = 0; seed < n; ++seed) {
+    if (assigned[seed]) continue;
+    order.push_back(seed);
+    assigned[seed] = 1;
+    cand.clear();
+    for (uint64_t j = seed + 1; j < n; ++j) {
+      if (!assigned[j]) cand.emplace_back(dist[seed * n + j], j);
+    }
+    const size_t take = std::min<size_t>(m - 1, cand.size());
+    std::partial_sort(cand.begin(), cand.begin() + take, cand.end());
+    for (size_t t = 0; t < take; ++t) {
+      order.push_back(cand[t].second);
+      assigned[cand[t].second] = 1;
+    }
+    off.push_back(order.size());
+  }
+}
+
+std::vector<uint32_t> greedy_assign(const std::vector<uint64_t>& overlap,
+                                    uint32_t nb, uint32_t nw) {
+  if (nw == 0) throw std::invalid_argument("need at least one worker");
+  const uint64_t cap = (uint64_t(nb) + nw - 1) / nw;
+  std::vector<uint32_t> a(nb, 0);
+  std::vector<char> placed(nb, 0);
+  std::vector<uint64_t> load(nw, 0);
+  for (uint32_t step = 0; step < nb; ++step) {
+    uint32_t bb = nb, bw = nw;
+    uint64_t best = 0;
+    bool found = false;
+    for (uint32_t b = 0; b < nb; ++b) {
+      if (placed[b]) continue;
+      for (uint32_t w = 0; w < nw; ++w) {
+        if (load[w] >= cap) continue;
+        const uint64_t o = overlap[uint64_t(b) * nw + w];
+        const bool better =
+            !found || o > best ||
+            (o == best && (b < bb || (b == bb && (load[w] < load[bw] ||
+                                                  (load[w] == load[bw] && w < bw)))));
+        if (better) {
+          found = true;
+          bb = b;
+          bw = w;
+          best = o;
+        }
+      }
+    }
+    a[bb] = bw;
+    placed[bb] = 1;
+    ++load[bw];
+  }
+  return a;
+}
+
+std::vector<uint64_t> split_budget(uint64_t total, const uint64_t* batch,
+                                   uint64_t n) {
+  if (n == 0) throw std::invalid_argument("cannot split a budget over an empty batch");
+  const uint64_t base = total / n, rem = total % n;
+  std::vector<size_t> by_id(n);
+  std::iota(by_id.begin(), by_id.end(), size_t{0});
+  std::stable_sort(by_id.begin(), by_id.end(),
+                   [&](size_t a, size_t b) { return batch[a] < batch[b]; });
+  std::vector<uint64_t> out(n, base);
+  for (uint64_t r = 0; r < rem; ++r) out[by_id[r]] += 1;
+  return out;
+}
+
+// ==========================================================================
+// hotness (cache.cpp)
+// ==========================================================================
+Hotness::Hotness(float h_init, float h_inc, float decay, double fraction)
+    : h_init_(h_init), h_inc_(h_inc), decay_(decay), fraction_(fraction) {
+  if (h_init <= 0.0f || h_inc <= 0.0f) {
+    throw std::invalid_argument("h_init and h_inc must be positive");
+  }
+  if (decay <= 1.0f) throw std::invalid_argument("decay factor must exceed 1");
+  if (fraction <= 0.0 || fraction > 1.0) {
+    throw std::invalid_argument("cache_fraction must be in (0, 1]");
+  }
+}
+
+void Hotness::end_of_round(const std::unordered_set<uint32_t>& used) {
+  for (auto& [c, h] : h_) {
+    float v = h / decay_;
+    if (used.count(c)) v = v + h_inc_;
+    h = v;
+  }
+}
+
+std::vector<uint32_t> Hotness::eviction_order(const std::vector<uint32_t>& resident) const {
+  std::vector<uint32_t> o(resident);
+  std::sort(o.begin(), o.end(), [this](uint32_t a, uint32_t b) {
+    const auto ia = h_.find(a), ib = h_.find(b);
+    const float ha = ia == h_.end() ? 0.0f : ia->second;
+    const float hb = ib == h_.end() ? 0.0f : ib->second;
+    if (ha != hb) return ha < hb;
+    return a < b;
+  });
+  return o;
+}
+
+// ==========================================================================
+// synthetic workload
+// ==========================================================================
+namespace {
+inline uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+// Approximately standard normal: Irwin-Hall sum of four 16-bit uniforms,
+// scaled to unit variance. Exact integer + IEEE arithmetic only, so the
+// stream is identical on every platform.
+inline double gauss(uint64_t key) {
+  const uint64_t h = mix64(key);
+  const double s = double(h & 0xffff) + double((h >> 16) & 0xffff) +
+                   double((h >> 32) & 0xffff) + double(h >> 48);
+  // each term uniform on {0..65535}: mean 32767.5, var (65536^2-1)/12
+  return (s - 4.0 * 32767.5) * (1.7320508075688772 / 65536.0);
+}
+inline uint64_t stream(uint64_t seed, uint64_t a, uint64_t b) {
+  return mix64(mix64(seed ^ 0x6c61697667ull) + a * 0x100000001b3ull + b);
+}
+void normalize_into(const double* v, uint32_t d, float* out) {
+  double ss = 0.0;
+  for (uint32_t t = 0; t < d; ++t) ss += v[t] * v[t];
+  const double n = std::sqrt(ss);
+  for (uint32_t t = 0; t < d; ++t) out[t] = static_cast<float>(n > 0.0 ? v[t] / n : v[t]);
+}
+} // namespace
+
+void synth_centroids(uint64_t seed, uint32_t nc, uint32_t d, float* out) {
+  std::vector<double> v(d);
+  for (uint32_t j = 0; j < nc; ++j) {
+    const uint64_t s = stream(seed, 1, j);
+    for (uint32_t t = 0; t < d; ++t) v[t] = gauss(s * 0x9e3779b97f4a7c15ull + t);
+    normalize_into(v.data(), d, out + uint64_t(j) * d);
+  }
+}
+
+void synth_lists(uint64_t seed, const float* centroids, uint32_t d,
+                 uint64_t per_list, float spread, uint32_t c_begin,
+                 uint32_t c_end, float* vecs, uint64_t* ids, int threads) {
+  const uint32_t n = c_end - c_begin;
+  auto work = [&](uint32_t lo, uint32_t hi) {
+    std::vector<double> v(d);
+    for (uint32_t j = lo; j < hi; ++j) {
+      const float* mu = centroids + uint64_t(j) * d;
+      for (uint64_t i = 0; i < per_list; ++i) {
+        const uint64_t row = uint64_t(j - c_begin) * per_list + i;
+        const uint64_t s = stream(seed, 2 + (uint64_t(j) << 32), i);
+        for (uint32_t t = 0; t < d; ++t) {
+          v[t] = static_cast<double>(mu[t]) +
+                 static_cast<double>(spread) * gauss(s * 0x9e3779b97f4a7c15ull + t);
+        }
+        normalize_into(v.data(), d, vecs + row * d);
+        ids[row] = uint64_t(j) * per_list + i;
+      }
+    }
+  };
+  const int nt = std::max(1, threads);
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t) {
+    const uint32_t lo = c_begin + uint32_t(uint64_t(n) * t / nt);
+    const uint32_t hi = c_begin + uint32_t(uint64_t(n) * (t + 1) / nt);
+    pool.emplace_back(work, lo, hi);
+  }
+  for (auto& t : pool) t.join();
+}
+
+void synth_queries(uint64_t seed, const float* vecs, uint64_t n_rows,
+                   uint32_t d, uint32_t nq, float sigma, float* q_in,
+                   float* q_out, uint64_t* rows) {
+  std::vector<double> v(d);
+  for (uint32_t i = 0; i < nq; ++i) {
+    const uint64_t r = mix64(stream(seed, 3, i)) % n_rows;
+    rows[i] = r;
+    const uint64_t s1 = stream(seed, 4, i), s2 = stream(seed, 5, i);
+    for (uint32_t t = 0; t < d; ++t) {
+      v[t] = static_cast<double>(vecs[r * d + t]) + 0.01 * gauss(s1 * 0x9e3779b97f4a7c15ull + t);
+    }
+    normalize_into(v.data(), d, q_in + uint64_t(i) * d);
+    for (uint32_t t = 0; t < d; ++t) {
+      v[t] = static_cast<double>(q_in[uint64_t(i) * d + t]) +
+             static_cast<double>(sigma) * gauss(s2 * 0x9e3779b97f4a7c15ull + t);
+    }
+    normalize_into(v.data(), d, q_out + uint64_t(i) * d);
+  }
+}
+
+} // namespace laivg

@@ -1,0 +1,58 @@
+// kernels.cuh — launch interface of the sm_100a kernels (kernels.cu).
+// Host orchestration (ctx.cu) calls these; nothing here is part of the C ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace laivg {
+
+constexpr int kMaxK = 256;           // device top-k limit (8 entries per lane)
+constexpr uint32_t kMaxSortNc = 16384; // on-chip full ranking limit
+
+// Per-query fast-list table produced by partition_kernel and consumed by the
+// scan: entry f of query q lives at [q * stride + f].
+struct FastTable {
+  int64_t* slab;      // device-cache vector offset of the list
+  uint64_t* row;      // host-store row offset of the list (id table index)
+  uint32_t* len;      // list length (vectors)
+  uint32_t* cluster;  // cluster id (for the host)
+  uint64_t* pre;      // exclusive prefix of len, stride + 1 entries per query
+  uint32_t* count;    // number of fast lists per query
+  uint32_t stride;
+};
+
+struct ScanOut {
+  float* part_s;      // [nq][grid][k] per-CTA partial top-k
+  uint64_t* part_id;
+  unsigned* ticket;   // [nq] last-CTA-done counters (self-resetting)
+  float* out_s;       // [nq][k]
+  uint64_t* out_id;   // [nq][k]
+  uint32_t* out_count;// [nq]
+};
+
+// Coarse: fp64 scores[nq][nc] of Q[nq][d] against centroids[nc][d]
+// (dot for IP, squared L2 for L2; ivf.cpp:276-280).
+void launch_coarse_scores(const float* Q, uint32_t nq, const float* centroids,
+                          uint32_t nc, uint32_t d, int metric, double* scores,
+                          cudaStream_t st);
+// Full on-chip ranking of each query's scores, best-first with ascending
+// cluster id on ties (ivf.cpp:282-289); writes the first n_out entries of
+// each ranking to order[q * n_out + i]. nc <= kMaxSortNc.
+void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
+                   uint32_t n_out, uint32_t* order, cudaStream_t st);
+// Splits each query's probe (probe[q * lp + i], i < lp) by residency
+// (res_off[c] >= 0) preserving probe order; fills the fast table.
+void launch_partition(const uint32_t* probe, uint32_t nq, uint32_t lp,
+                      const int64_t* res_off, const uint64_t* list_off,
+                      FastTable ft, cudaStream_t st);
+// Scans the fast lists of nq queries (queries at Q[q * d]) and leaves the
+// best-k (score, id) per query in out. grid_x CTAs per query.
+void launch_scan(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
+                 const FastTable& ft, const float* slab_vecs,
+                 const uint64_t* ids_all, const ScanOut& out, int grid_x,
+                 bool acc_fp64, cudaStream_t st);
+int scan_grid_x(uint32_t nq, int num_sms);
+// Generation-window stand-in: one CTA per SM spins on %globaltimer for ns.
+void launch_window(uint64_t ns, int num_sms, cudaStream_t st);
+
+} // namespace laivg
