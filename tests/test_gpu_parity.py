@@ -118,7 +118,7 @@ def test_k_range(orc, laiv, k):
 
 def test_edge_cases(orc, laiv):
     cen, vecs, ids, off, qi, qo, _ = planted_data()
-    ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric.IP)
+    ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric.InnerProduct)
     dev = laiv.Device(ix, BIG)
     set_residency(dev, np.ones(64, np.uint8))
     # L = 0 / negative: empty probe, empty result

@@ -176,7 +176,7 @@ def test_window_kernel(laiv):
 def test_device_prefetch_overlap_planted(laiv):
     # lookahead: the copy of the planned lists hides behind the window
     cen, vecs, ids, off, qi, qo, _ = planted_data()
-    ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric.IP)
+    ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric.InnerProduct)
     dev = laiv.Device(ix, 64 * 300 * (4 * 768 + 8))
     chan = laiv.TransferChannel(50e9, laiv.ChannelMode.Device)
     plan = laiv.plan_prefetch(dev, qi[0], 16 * 300 * (4 * 768 + 8))
