@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""bench.py — lookahead IVF retrieval on B200 (BASELINE.json metric).
+
+Workload (default `--config c2`, BASELINE.json configs[1]): synthetic
+IVF-Flat 10M x 768 fp32 (4096 balanced lists of 2442 planted-cluster members,
+SURVEY §8d generator), nprobe 128, k 10, inner product, single-query
+lookahead prefetch on one B200.
+
+One step = one query round of the TeleRAG pipeline (pipeline.cpp:357-441):
+  1. the device cache (TieredStore, capacity 10% of the datastore) starts
+     empty (cache off, pipeline.cpp:466-473);
+  2. plan_prefetch from the pre-retrieval embedding q_in (GPU coarse ranking +
+     host greedy walk) under budget = min(B_link * window, capacity)
+     (calibrate_budget rule, budget.cpp:159-182);
+  3. execute_prefetch: the planned IVF lists stream host->HBM on the copy
+     stream while the generation-window kernel occupies the compute stream;
+  4. hybrid_search for q_out: GPU coarse + list scan over the resident probed
+     lists, host scan of the misses, merge.
+
+Reported metric: retrieval queries/s and p50 retrieval latency, where the
+retrieval latency of a query = exposed prefetch (copy end past window end)
++ the hybrid search. `value` uses queries staged in HBM; `e2e` the host-buffer
+C-ABI call (query H2D and result D2H inside). The window itself is simulated
+LLM time, reported separately (`pipeline_ms_per_step`).
+
+`--impl reference` times the reference's own CPU search (laiv::ivf_search from
+oracle/_ref/libref.so, built from the reference sources) on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[1]
+    "c2": dict(workload="synthetic IVF-Flat 10M x 768 fp32, 4096 lists, nprobe=128, k=10, "
+                        "single-query lookahead prefetch on 1 x B200",
+               n_lists=4096, per_list=2442, d=768, nprobe=128, k=10, window_s=0.15,
+               cache_frac=0.10),
+    # BASELINE.json configs[0] shape (1M x 768, 1024 lists, nprobe 32)
+    "c1": dict(workload="synthetic IVF-Flat 1M x 768 fp32, 1024 lists, nprobe=32, k=10, batch=1",
+               n_lists=1024, per_list=977, d=768, nprobe=32, k=10, window_s=0.02,
+               cache_frac=0.10),
+    "small": dict(workload="synthetic IVF-Flat 100K x 768 fp32, 256 lists, nprobe=16, k=10",
+                  n_lists=256, per_list=400, d=768, nprobe=16, k=10, window_s=0.005,
+                  cache_frac=0.25),
+}
+SEED, QSEED, SPREAD = 0, 1, 0.05
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# --------------------------------------------------------------------------
+# datastore
+# --------------------------------------------------------------------------
+def make_datastore(cfg, world, rank, pinned=True):
+    """Planted-cluster list-major datastore. One process: pinned allocation.
+    Several ranks: rank 0 fills a /dev/shm file that every rank maps and pins
+    (one host copy shared by all GPUs)."""
+    from paper_2502_20969_b200 import laiv
+
+    nc, per, d = cfg["n_lists"], cfg["per_list"], cfg["d"]
+    n = nc * per
+    cen = laiv.synth_centroids(SEED, nc, d)
+    t0 = time.time()
+    if world == 1:
+        vecs = laiv.pinned_empty((n, d), np.float32) if pinned else np.empty((n, d), np.float32)
+        ids = np.empty(n, np.uint64)
+        laiv.synth_lists(SEED, cen, per, SPREAD, vecs=vecs, ids=ids)
+    else:
+        import torch.distributed as dist
+
+        path = f"/dev/shm/laivg_{nc}x{per}x{d}_s{SEED}.bin"
+        if rank == 0:
+            mm = np.memmap(path, np.float32, "w+", shape=(n, d))
+            ids = np.empty(n, np.uint64)
+            laiv.synth_lists(SEED, cen, per, SPREAD, vecs=mm, ids=ids)
+            mm.flush()
+            del mm
+        dist.barrier()
+        vecs = np.memmap(path, np.float32, "r+", shape=(n, d))
+        ids = np.arange(n, dtype=np.uint64)  # synth ids are j*per+i == row index
+        if pinned:
+            laiv._lib.check(laiv.lib().laivg_host_register(vecs.ctypes.data, vecs.nbytes))
+    off = np.arange(0, n + 1, per, dtype=np.uint64)
+    log(f"[bench] datastore {n}x{d} ({n * (4 * d + 8) / 1e9:.1f} GB) in {time.time() - t0:.1f}s")
+    return cen, vecs, ids, off
+
+
+def calibrate_sigma(laiv, dev, vecs, L, target=0.8, nq=32):
+    """Largest q_out perturbation whose mean coverage at nprobe >= target
+    (coverage in [0.6, 0.95]; acceptance.cpp:219-223)."""
+    best = None
+    for sigma in (0.002, 0.004, 0.006, 0.008, 0.010, 0.012, 0.015, 0.02, 0.03):
+        qi, qo, _ = laiv.synth_queries(QSEED + 1000, vecs, nq, sigma)
+        cov = float(np.mean([laiv.coverage(dev, a, b, L) for a, b in zip(qi, qo)]))
+        if cov >= target:
+            best = (sigma, cov)
+        else:
+            break
+    return best if best else (0.002, None)
+
+
+# --------------------------------------------------------------------------
+# clocks (nvidia-smi during the timed region)
+# --------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.proc = None
+        self.lines = []
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                smax.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------------
+# reference CPU arm
+# --------------------------------------------------------------------------
+def reference_index(cen, vecs, ids, off, metric):
+    from oracle.oracle import RefLib
+
+    t0 = time.time()
+    ri = RefLib().index(cen, vecs, ids, off, metric)
+    log(f"[bench] reference index built in {time.time() - t0:.1f}s")
+    return ri
+
+
+def cpu_baseline(ri, q_out, L, k, threads, sample):
+    """The reference laiv::ivf_search on `threads` host threads over `sample`
+    queries; returns q/s, p50 latency and the results."""
+    t0 = time.perf_counter()
+    ids, sc, lat = ri.search_many(q_out[:sample], L, k, threads)
+    wall = time.perf_counter() - t0
+    return dict(qps=sample / wall, p50_ms=float(np.median(lat) * 1e3), wall_s=wall,
+                ids=ids, scores=sc)
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0  # the reference arm is one host process on rank 0
+    from paper_2502_20969_b200 import laiv
+
+    cen, vecs, ids, off = make_datastore(cfg, 1, 0, pinned=False)
+    metric = 0 if args.metric == "ip" else 1
+    sigma = args.sigma or 0.006
+    qi, qo, _ = laiv.synth_queries(QSEED, vecs, 4096, sigma)
+    ri = reference_index(cen, vecs, ids, off, metric)
+    threads = os.cpu_count() or 1
+    per_step = threads
+    L, k = cfg["nprobe"], cfg["k"]
+    qpos = 0
+    for _ in range(args.warmup):
+        ri.search_many(qo[qpos:qpos + per_step], L, k, threads)
+        qpos += per_step
+    lats = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _, _, lat = ri.search_many(qo[qpos:qpos + per_step], L, k, threads)
+        lats.extend(lat.tolist())
+        qpos += per_step
+    wall = time.perf_counter() - t0
+    qps = args.steps * per_step / wall
+    line = {
+        "impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64-accumulate/f32", "data": "synthetic",
+        "p50_latency_ms": float(np.median(lats) * 1e3),
+        "config": config_block(cfg, args, sigma),
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"{per_step} queries per step (one per host thread), "
+                                   f"laiv::ivf_search from oracle/_ref/libref.so"},
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+METRIC = "IVF retrieval queries/sec and p50 retrieval latency (prefetch-overlapped)"
+
+
+def config_block(cfg, args, sigma):
+    return {"workload": cfg["workload"], "n_vectors": cfg["n_lists"] * cfg["per_list"],
+            "dim": cfg["d"], "n_lists": cfg["n_lists"], "nprobe": cfg["nprobe"], "k": cfg["k"],
+            "metric": args.metric, "batch": 1, "window_s": args.window,
+            "cache_fraction_of_lists": cfg["cache_frac"], "q_out_sigma": sigma,
+            "l2_flush": "not needed: each query scans up to ~1 GB of lists > 126 MB L2, "
+                        "and every step re-fetches its lists into a cleared cache"}
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+def run_ours(args, cfg):
+    from paper_2502_20969_b200 import laiv
+
+    rank, world, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cen, vecs, ids, off = make_datastore(cfg, world, rank)
+    metric = laiv.Metric.InnerProduct if args.metric == "ip" else laiv.Metric.L2
+    ix = laiv.IvfIndex(cen, vecs, ids, off, metric, borrow=True, trust=True)
+    member = 4 * cfg["d"] + 8
+    capacity = int(cfg["cache_frac"] * cfg["n_lists"]) * cfg["per_list"] * member
+    dev = laiv.Device(ix, capacity, device=local if world > 1 else 0)
+    L, k = cfg["nprobe"], cfg["k"]
+
+    # link bandwidth for the calibrate_budget rule, measured on this box
+    probe_plan = laiv.plan_prefetch(dev, cen[0], min(capacity, 64 * cfg["per_list"] * member))
+    rep = laiv.execute_prefetch(dev, probe_plan, laiv.TransferChannel(1, laiv.ChannelMode.Device))
+    dev.store.clear()
+    b_link = rep.h2d_gbps * 1e9
+    budget = int(min(b_link * args.window, capacity))
+    sigma, cov = (args.sigma, None) if args.sigma else calibrate_sigma(laiv, dev, vecs, L)
+    nq_total = (args.warmup + args.steps) * world + 8
+    qi, qo, _ = laiv.synth_queries(QSEED, vecs, nq_total, sigma)
+    mine = np.arange(rank, nq_total, world)[: args.warmup + args.steps]
+    dev.stage_queries(qo[mine])
+    chan = laiv.TransferChannel(b_link, laiv.ChannelMode.Device)
+    log(f"[bench] rank {rank}: B_link {b_link / 1e9:.1f} GB/s, budget {budget / 1e9:.2f} GB, "
+        f"sigma {sigma} (coverage {cov}), capacity {capacity / 1e9:.2f} GB")
+
+    def step(j, rec):
+        qidx = mine[j]
+        dev.store.clear()
+        t0 = time.perf_counter()
+        plan = laiv.plan_prefetch(dev, qi[qidx], budget)
+        rp = laiv.execute_prefetch(dev, plan, chan, args.window)
+        t1 = time.perf_counter()
+        got_ids, got_sc, nfast, tm = dev.hybrid_search_staged(j, L, k)  # value path
+        t2 = time.perf_counter()
+        res, tm2 = laiv.hybrid_search(dev, qo[qidx], L, k)                 # e2e path
+        t3 = time.perf_counter()
+        if rec is not None:
+            nvec = sum(cfg["per_list"] for _ in plan.clusters)
+            rec.append(dict(
+                exposed=rp.overshoot_s, t_p=rp.t_p, window=rp.window_s, h2d_gbps=rp.h2d_gbps,
+                lat_value=rp.overshoot_s + tm.t_2, lat_e2e=rp.overshoot_s + (t3 - t2),
+                t_scan=tm.t_scan, t_coarse=tm.t_coarse, t_g=tm.t_g, t_c=tm.t_c,
+                bytes=tm.scanned_bytes, hit=nfast / L, plan_s=t1 - t0,
+                h2d_bytes=2 * 4 * cfg["d"] + nvec * 4 * cfg["d"] + cfg["n_lists"] * 8,
+                d2h_bytes=cfg["n_lists"] * 4 + L * 4 + k * 12 + 8,
+                same=bool(np.array_equal(got_ids, res.topk.ids))))
+
+    for j in range(args.warmup):
+        step(j, None)
+    if dist:
+        dist.barrier()
+    dev.sync()
+    clocks = ClockSampler(local if world > 1 else 0)
+    launches0 = laiv.lib().laivg_kernel_launches()
+    rec = []
+    t0 = time.perf_counter()
+    for j in range(args.warmup, args.warmup + args.steps):
+        step(j, rec)
+    dev.sync()
+    wall = time.perf_counter() - t0
+    launches = laiv.lib().laivg_kernel_launches() - launches0
+    clk = clocks.stop()
+
+    lat_v = np.array([r["lat_value"] for r in rec])
+    lat_e = np.array([r["lat_e2e"] for r in rec])
+    sum_v, sum_e = float(lat_v.sum()), float(lat_e.sum())
+    if dist:
+        import torch
+
+        t = torch.tensor([sum_v, sum_e, wall], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sum_v, sum_e, wall = (float(x) for x in t.tolist())
+    n_total = args.steps * world
+    bytes_scan = sum(r["bytes"] for r in rec)
+    t_scan = sum(r["t_scan"] for r in rec)
+    peak, peak_kind = measured_peaks()
+    achieved = bytes_scan / t_scan / 1e9 if t_scan > 0 else 0.0
+    exposed = np.array([r["exposed"] for r in rec])
+    t_p = np.array([r["t_p"] for r in rec])
+    line = {
+        "metric": METRIC, "value": n_total / sum_v, "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum_v / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 data, f64 accumulate", "data": "synthetic (planted clusters, SURVEY §8d)",
+        "p50_latency_ms": float(np.median(lat_v) * 1e3),
+        "p99_latency_ms": float(np.percentile(lat_v, 99) * 1e3),
+        "pipeline_ms_per_step": wall / args.steps * 1e3,
+        "config": config_block(cfg, args, sigma),
+        "roofline": {"kernel": "scan_kernel", "bound": "hbm", "achieved": achieved,
+                     "peak": peak, "peak_kind": f"{peak_kind} copy (MEASURED_PEAKS.json hbm_gbs)",
+                     "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None,
+                     "algorithmic_bytes_per_launch": bytes_scan / max(len(rec), 1),
+                     "avg_launch_ms": t_scan / max(len(rec), 1) * 1e3},
+        "prefetch": {"h2d_gbps": float(np.mean([r["h2d_gbps"] for r in rec])),
+                     "b_link_gbps": b_link / 1e9, "budget_gb": budget / 1e9,
+                     "hidden_frac": float(1.0 - exposed.sum() / t_p.sum()) if t_p.sum() else 1.0,
+                     "exposed_ms_mean": float(exposed.mean() * 1e3),
+                     "hit_rate": float(np.mean([r["hit"] for r in rec]))},
+        "breakdown_ms": {k_: float(np.mean([r[k_] for r in rec]) * 1e3)
+                         for k_ in ("t_coarse", "t_scan", "t_g", "t_c", "plan_s")},
+        "e2e": {"value": n_total / sum_e, "unit": "queries/s",
+                "p50_latency_ms": float(np.median(lat_e) * 1e3),
+                "h2d_bytes_per_step": int(np.mean([r["h2d_bytes"] for r in rec])),
+                "d2h_bytes_per_step": int(np.mean([r["d2h_bytes"] for r in rec]))},
+        "value_e2e_results_identical": all(r["same"] for r in rec),
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        ri = reference_index(cen, np.asarray(vecs), ids, off, int(metric))
+        threads = os.cpu_count() or 1
+        sample = args.cpu_sample
+        cb = cpu_baseline(ri, qo[mine[args.warmup:]].repeat(1, axis=0), L, k, threads,
+                          min(sample, len(mine) - args.warmup))
+        # parity of the timed queries with the reference on the same inputs
+        eq = 0
+        for j in range(min(sample, len(mine) - args.warmup)):
+            got_ids, got_sc, _, _ = dev.hybrid_search_staged(args.warmup + j, L, k)
+            eq += bool(np.array_equal(got_ids, cb["ids"][j]) and
+                       np.array_equal(got_sc, cb["scores"][j]))
+        line["cpu_baseline"] = {"value": cb["qps"], "unit": "queries/s", "cores": threads,
+                                "kind": "reference",
+                                "p50_latency_ms": cb["p50_ms"],
+                                "sample": f"{min(sample, len(mine) - args.warmup)} of the timed "
+                                          f"q_out queries, laiv::ivf_search (oracle/_ref) one "
+                                          f"query per host thread"}
+        line["parity_vs_reference"] = {"queries": min(sample, len(mine) - args.warmup),
+                                       "bit_identical": eq}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--metric", default="ip", choices=["ip", "l2"])
+    ap.add_argument("--window", type=float, default=None)
+    ap.add_argument("--sigma", type=float, default=None)
+    ap.add_argument("--cpu-sample", type=int, default=16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.window is None:
+        args.window = cfg["window_s"]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

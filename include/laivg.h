@@ -61,6 +61,12 @@ uint32_t laivg_version(void);
  * one host datastore slab. */
 int laivg_host_alloc(uint64_t bytes, void** out);
 int laivg_host_free(void* p);
+/* Pins an existing host range (cudaHostRegister, portable) so a datastore
+ * mapped from shared memory can be shared by several processes/devices. */
+int laivg_host_register(void* p, uint64_t bytes);
+int laivg_host_unregister(void* p);
+/* Number of kernels this library has launched (all contexts). */
+uint64_t laivg_kernel_launches(void);
 
 /* ---- index: IvfIndex + EmbeddingMatrix (ivf.hpp:26-50, vectorstore.hpp:50-83)
  * centroids[nc*d] are copied. With LAIVG_INDEX_BORROW the store arrays are

@@ -278,7 +278,8 @@ class RefLib:
         L.ref_cache_used.restype = u64
         L.ref_cache_used.argtypes = [vp]
         L.ref_cache_contains.argtypes = [vp, u32]
-        L.ref_search_many.argtypes = [vp, i32, C.c_void_p, u64, i32, i32, i32, _u64p, _f32p]
+        L.ref_search_many.argtypes = [vp, i32, C.c_void_p, u64, i32, i32, i32, _u64p, _f32p,
+                                      C.c_void_p]
 
     @staticmethod
     def available(path: str | None = None) -> bool:
@@ -426,11 +427,15 @@ class RefIndex:
         return out[: len(batches)].copy()
 
     def search_many(self, Q, L, k, threads, mode=0):
+        """Reference ivf_search (mode 0) / hybrid_search with an empty store
+        (mode 1) over nq queries on `threads` host threads; returns ids,
+        scores and per-query latency (s)."""
         Q = _c(Q, np.float32)
         nq = Q.shape[0]
         ids = np.zeros((nq, k), np.uint64)
         sc = np.zeros((nq, k), np.float32)
+        lat = np.zeros(nq, np.float64)
         self.lib.check(self.lib.L.ref_search_many(self.h, mode, Q.ctypes.data, nq, int(L),
                                                   int(k), int(threads), ids.reshape(-1),
-                                                  sc.reshape(-1)))
-        return ids, sc
+                                                  sc.reshape(-1), lat.ctypes.data))
+        return ids, sc, lat

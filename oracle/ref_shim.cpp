@@ -9,6 +9,7 @@
 // Every entry point returns >= 0 on success, -1 on a reference exception
 // (message via ref_last_error()).
 #include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <set>
@@ -368,7 +369,8 @@ int ref_cache_contains(void* cv, uint32_t c) {
 // (tiered.cpp:148). Queries are claimed from a shared counter by `threads`
 // host threads (ivf.hpp:25: concurrent searches are safe).
 int ref_search_many(void* hv, int mode, const float* Q, uint64_t nq, int L,
-                    int k, int threads, uint64_t* ids, float* scores) {
+                    int k, int threads, uint64_t* ids, float* scores,
+                    double* latency_s) {
   auto* h = static_cast<RefIndex*>(hv);
   std::atomic<uint64_t> next{0};
   std::atomic<int> failed{0};
@@ -378,6 +380,7 @@ int ref_search_many(void* hv, int mode, const float* Q, uint64_t nq, int L,
       const uint64_t i = next.fetch_add(1);
       if (i >= nq) return;
       try {
+        const auto t0 = std::chrono::steady_clock::now();
         laiv::TopK t;
         const std::span<const float> q(Q + i * h->ix.dim(), h->ix.dim());
         if (mode == 0) {
@@ -388,6 +391,10 @@ int ref_search_many(void* hv, int mode, const float* Q, uint64_t nq, int L,
         for (size_t j = 0; j < t.entries.size(); ++j) {
           ids[i * k + j] = t.entries[j].id;
           scores[i * k + j] = t.entries[j].score;
+        }
+        if (latency_s) {
+          latency_s[i] = std::chrono::duration<double>(
+                             std::chrono::steady_clock::now() - t0).count();
         }
       } catch (const std::exception& e) {
         failed = 1;

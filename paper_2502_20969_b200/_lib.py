@@ -59,6 +59,9 @@ SIGNATURES = {
     "laivg_version": (u32, []),
     "laivg_host_alloc": (i32, [u64, P(vp)]),
     "laivg_host_free": (i32, [vp]),
+    "laivg_host_register": (i32, [vp, u64]),
+    "laivg_host_unregister": (i32, [vp]),
+    "laivg_kernel_launches": (u64, []),
     "laivg_index_create": (i32, [vp, u32, u32, i32, vp, vp, vp, u32, P(vp)]),
     "laivg_index_destroy": (None, [vp]),
     "laivg_index_num_clusters": (u32, [vp]),

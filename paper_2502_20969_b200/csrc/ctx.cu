@@ -609,6 +609,19 @@ int laivg_host_free(void* p) {
     if (p) CK(cudaFreeHost(p));
   });
 }
+int laivg_host_register(void* p, uint64_t bytes) {
+  return guard([&] {
+    need(p, "pointer");
+    CK(cudaHostRegister(p, bytes, cudaHostRegisterPortable));
+  });
+}
+int laivg_host_unregister(void* p) {
+  return guard([&] {
+    need(p, "pointer");
+    CK(cudaHostUnregister(p));
+  });
+}
+uint64_t laivg_kernel_launches(void) { return laivg::launch_counter().load(); }
 
 // ---- index -----------------------------------------------------------------
 int laivg_index_create(const float* centroids, uint32_t nc, uint32_t d, int metric,

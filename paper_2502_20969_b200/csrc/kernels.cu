@@ -608,6 +608,7 @@ void launch_scan_t(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
     attr_set = true;
   }
   fn<<<dim3(gx, nq), kScanThreads, smem, st>>>(Q, d, metric, k, ft, slab, ids, out);
+  launch_counter()++;
 }
 
 template <typename ACC, int NCH>
@@ -625,6 +626,10 @@ void launch_scan_k(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
 // ==========================================================================
 // launchers
 // ==========================================================================
+std::atomic<uint64_t>& launch_counter() {
+  static std::atomic<uint64_t> n{0};
+  return n;
+}
 void launch_coarse_scores(const float* Q, uint32_t nq, const float* centroids,
                           uint32_t nc, uint32_t d, int metric, double* scores,
                           cudaStream_t st) {
@@ -638,6 +643,7 @@ void launch_coarse_scores(const float* Q, uint32_t nq, const float* centroids,
     }
     coarse_scores_kernel<8><<<dim3((nc + warps - 1) / warps, (nq + 7) / 8), block, smem, st>>>(
         Q, nq, centroids, nc, d, metric, scores);
+    launch_counter()++;
   } else {
     const size_t smem = size_t(d) * sizeof(float);
     if (smem > 48 * 1024) {
@@ -646,6 +652,7 @@ void launch_coarse_scores(const float* Q, uint32_t nq, const float* centroids,
     }
     coarse_scores_kernel<1><<<dim3((nc + warps - 1) / warps, nq), block, smem, st>>>(
         Q, nq, centroids, nc, d, metric, scores);
+    launch_counter()++;
   }
 }
 
@@ -662,12 +669,14 @@ void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
   }
   const int threads = p2 >= 2048 ? 1024 : (p2 >= 64 ? int(p2 / 2) : 32);
   select_kernel<<<nq, threads, smem, st>>>(scores, nc, metric, p2, n_out, order);
+  launch_counter()++;
 }
 
 void launch_partition(const uint32_t* probe, uint32_t nq, uint32_t lp,
                       const int64_t* res_off, const uint64_t* list_off,
                       FastTable ft, cudaStream_t st) {
   partition_kernel<<<nq, 256, 0, st>>>(probe, lp, res_off, list_off, ft);
+  launch_counter()++;
 }
 
 int scan_grid_x(uint32_t nq, int num_sms) {
@@ -692,6 +701,7 @@ void launch_scan(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
 
 void launch_window(uint64_t ns, int num_sms, cudaStream_t st) {
   window_kernel<<<num_sms, 32, 0, st>>>(ns);
+  launch_counter()++;
 }
 
 } // namespace laivg

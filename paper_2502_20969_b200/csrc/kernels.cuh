@@ -1,10 +1,15 @@
 // kernels.cuh — launch interface of the sm_100a kernels (kernels.cu).
 // Host orchestration (ctx.cu) calls these; nothing here is part of the C ABI.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace laivg {
+
+// Every kernel launch of this library increments this (evidence for the
+// bench's gpu_launches).
+std::atomic<uint64_t>& launch_counter();
 
 constexpr int kMaxK = 256;           // device top-k limit (8 entries per lane)
 constexpr uint32_t kMaxSortNc = 16384; // on-chip full ranking limit
