@@ -276,7 +276,8 @@ def run_ours(args, cfg):
     ix = laiv.IvfIndex(cen, vecs, ids, off, metric, borrow=True, trust=True)
     member = 4 * cfg["d"] + 8
     capacity = int(cfg["cache_frac"] * cfg["n_lists"]) * cfg["per_list"] * member
-    dev = laiv.Device(ix, capacity, device=local if world > 1 else 0)
+    dev = laiv.Device(ix, capacity, device=local if world > 1 else 0,
+                      acc_fp64=args.acc == "fp64")
     L, k = cfg["nprobe"], cfg["k"]
 
     # link bandwidth for the calibrate_budget rule, measured on this box
@@ -352,7 +353,7 @@ def run_ours(args, cfg):
         "metric": METRIC, "value": n_total / sum_v, "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum_v / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32 data, f64 accumulate", "data": "synthetic (planted clusters, SURVEY §8d)",
+        "dtype": f"f32 data, {args.acc} accumulate", "data": "synthetic (planted clusters, SURVEY §8d)",
         "p50_latency_ms": float(np.median(lat_v) * 1e3),
         "p99_latency_ms": float(np.percentile(lat_v, 99) * 1e3),
         "pipeline_ms_per_step": wall / args.steps * 1e3,
@@ -417,6 +418,8 @@ def main():
     ap.add_argument("--sigma", type=float, default=None)
     ap.add_argument("--cpu-sample", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--acc", default="fp64", choices=["fp64", "fp32"],
+                    help="scan accumulation: fp64 as the reference (default) or fp32 FMA")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.window is None:
