@@ -100,9 +100,12 @@ typedef struct {
   uint32_t miss_threads;   /* host threads scanning cache misses; 0 = all cores */
   uint32_t max_batch;      /* max queries per batched call; 0 = 256 */
   uint32_t max_probe;      /* max L per call; 0 = nc */
-  uint32_t acc_fp64;       /* 1 (default): scan accumulates in fp64 as the
-                              reference does; 0: fp32 FMA accumulation */
-  uint32_t reserved[8];
+  uint32_t acc_fp64;       /* 0 (default): fp32 FMA accumulation, survivors
+                              re-scored with the reference's fp64 arithmetic;
+                              1: every candidate accumulated in fp64 */
+  uint32_t scan_impl;      /* 0 (default): TMA bulk-copy staged scan;
+                              1: direct 128-bit register loads */
+  uint32_t reserved[7];
 } laivg_opts;
 void laivg_opts_default(laivg_opts* o);
 typedef struct laivg_ctx laivg_ctx;

@@ -30,7 +30,7 @@ P = C.POINTER
 class Opts(C.Structure):
     _fields_ = [("device", i32), ("capacity_bytes", u64), ("miss_threads", u32),
                 ("max_batch", u32), ("max_probe", u32), ("acc_fp64", u32),
-                ("reserved", u32 * 8)]
+                ("scan_impl", u32), ("reserved", u32 * 7)]
 
 
 class Channel(C.Structure):

@@ -117,7 +117,8 @@ struct Ctx {
   const Index* ix = nullptr;
   int dev = 0;
   int sms = 148;
-  bool acc_fp64 = true;
+  bool acc_fp64 = false;
+  ScanImpl scan_impl = ScanImpl::kTma;
   cudaStream_t comp = nullptr, copy = nullptr, aux = nullptr;
 
   // static device data
@@ -214,7 +215,7 @@ Ctx::~Ctx() {
                   (void*)d_slab, (void*)d_tmp, (void*)d_Q, (void*)d_scores,
                   (void*)d_order, (void*)ft.slab, (void*)ft.row, (void*)ft.len,
                   (void*)ft.cluster, (void*)ft.pre, (void*)ft.count,
-                  (void*)so.part_s, (void*)so.part_id, (void*)so.ticket,
+                  (void*)so.part_s, (void*)so.part_id, (void*)so.part_vi, (void*)so.ticket,
                   (void*)so.out_s, (void*)so.out_id, (void*)so.out_count,
                   (void*)d_staged}) {
     if (p) cudaFree(p);
@@ -253,6 +254,8 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   }
   sms = prop.multiProcessorCount;
   acc_fp64 = o.acc_fp64 != 0;
+  if (o.scan_impl > 1) throw std::invalid_argument("scan_impl must be 0 (TMA) or 1 (LDG)");
+  scan_impl = static_cast<ScanImpl>(o.scan_impl);
   if (ix->nc > kMaxSortNc) {
     throw std::invalid_argument("device coarse ranking supports up to " +
                                 std::to_string(kMaxSortNc) + " clusters");
@@ -309,6 +312,7 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   part_cap = std::max<int>(2 * sms, int(max_batch)) + 2 * sms;
   so.part_s = dev_alloc<float>(size_t(part_cap) * kMaxK);
   so.part_id = dev_alloc<uint64_t>(size_t(part_cap) * kMaxK);
+  so.part_vi = dev_alloc<uint32_t>(size_t(part_cap) * kMaxK);
   so.ticket = dev_alloc<unsigned>(max_batch);
   CK(cudaMemset(so.ticket, 0, max_batch * sizeof(unsigned)));
   so.out_s = dev_alloc<float>(size_t(max_batch) * kMaxK);
@@ -408,7 +412,8 @@ void Ctx::clear_store() {
 
 void Ctx::coarse(const float* dQ, uint32_t nq, uint32_t n_out, cudaStream_t st) {
   launch_coarse_scores(dQ, nq, d_cen, ix->nc, ix->d, ix->metric, d_scores, st);
-  launch_select(d_scores, nq, ix->nc, ix->metric, n_out, d_order, st);
+  launch_select(d_scores, nq, ix->nc, ix->metric, n_out, d_order, nullptr, nullptr, nullptr,
+                st);
 }
 
 Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
@@ -444,19 +449,22 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
       std::memcpy(h_order, explicit_probe->data(), lp * sizeof(uint32_t));
       CK(cudaMemcpyAsync(d_order, h_order, lp * sizeof(uint32_t), cudaMemcpyHostToDevice, comp));
     }
+    CK(cudaEventRecord(ev_b, comp));
+    launch_partition(d_order, 1, lp, d_res, d_list_off, ft, comp);
   } else {
-    coarse(dq, 1, lp, comp);
+    // coarse scores, then ranking + residency split fused in one CTA
+    launch_coarse_scores(dq, 1, d_cen, ix->nc, ix->d, ix->metric, d_scores, comp);
+    launch_select(d_scores, 1, ix->nc, ix->metric, lp, d_order, d_res, d_list_off, &ft, comp);
+    CK(cudaEventRecord(ev_b, comp));
+    if (lp) {
+      CK(cudaStreamWaitEvent(aux, ev_b, 0));
+      CK(cudaMemcpyAsync(h_order, d_order, lp * sizeof(uint32_t), cudaMemcpyDeviceToHost, aux));
+      CK(cudaEventRecord(ev_probe, aux));
+    }
   }
-  CK(cudaEventRecord(ev_b, comp));
-  if (!explicit_probe && lp) {
-    CK(cudaStreamWaitEvent(aux, ev_b, 0));
-    CK(cudaMemcpyAsync(h_order, d_order, lp * sizeof(uint32_t), cudaMemcpyDeviceToHost, aux));
-    CK(cudaEventRecord(ev_probe, aux));
-  }
-  launch_partition(d_order, 1, lp, d_res, d_list_off, ft, comp);
   CK(cudaEventRecord(ev_p, comp));
   launch_scan(dq, 1, ix->d, ix->metric, k, ft, d_slab, d_ids, so,
-              std::min(scan_grid_x(1, sms), part_cap), acc_fp64, comp);
+              std::min(scan_grid_x(1, sms, scan_impl), part_cap), acc_fp64, scan_impl, comp);
   CK(cudaEventRecord(ev_s, comp));
   CK(cudaMemcpyAsync(h_out_s, so.out_s, k * sizeof(float), cudaMemcpyDeviceToHost, comp));
   CK(cudaMemcpyAsync(h_out_id, so.out_id, k * sizeof(uint64_t), cudaMemcpyDeviceToHost, comp));
@@ -726,7 +734,8 @@ uint64_t laivg_index_total_payload_bytes(const laivg_index* ix) {
 void laivg_opts_default(laivg_opts* o) {
   if (!o) return;
   std::memset(o, 0, sizeof(*o));
-  o->acc_fp64 = 1;
+  o->acc_fp64 = 0;
+  o->scan_impl = 0;
 }
 
 int laivg_ctx_create(const laivg_index* ix, const laivg_opts* opts, laivg_ctx** out) {

@@ -1,13 +1,21 @@
 // kernels.cu — sm_100a kernels of the lookahead IVF retrieval path.
 //
 //   coarse_scores_kernel : query x centroid scores in fp64 (ivf.cpp:269-281)
-//   select_kernel        : full on-chip ranking, ascending cluster id on ties
-//                          (ivf.cpp:282-299)
-//   partition_kernel     : probe split by device-cache residency
-//                          (tiered.cpp:155-161), exclusive prefix of lengths
-//   scan_kernel          : IVF-Flat list scan over the resident probed lists,
-//                          per-warp register top-k, CTA merge, last-CTA grid
-//                          merge (ivf.cpp:301-343, tiered.cpp:172-185)
+//   select_kernel        : full on-chip ranking (register/shuffle/smem bitonic
+//                          sort), ascending cluster id on ties
+//                          (ivf.cpp:282-299), fused split of the probe by
+//                          device-cache residency (tiered.cpp:155-161)
+//   partition_kernel     : the same split for an explicit cluster list
+//                          (search_clusters, ivf.cpp:301-323)
+//   scan_tma_kernel      : IVF-Flat list scan. One producer warp streams
+//                          list tiles HBM -> shared memory with cp.async.bulk
+//                          (TMA) into an mbarrier ring; eight consumer warps
+//                          score vectors from shared memory, keep a register
+//                          top-k, merge per CTA, and the last CTA merges the
+//                          grid and re-scores the survivors exactly
+//                          (ivf.cpp:301-343, tiered.cpp:172-185)
+//   scan_ldg_kernel      : the same scan with direct 128-bit register loads
+//                          (rows that are not 16-byte aligned; A/B baseline)
 //   window_kernel        : %globaltimer spin standing in for LLM generation
 //
 // Reference semantics kept on device: per-term arithmetic of dot_d / l2_sq_d
@@ -16,9 +24,17 @@
 // score, sqrt for L2, and the (score, ascending id) total order with
 // -0.0 == +0.0 (vectorstore.hpp:34-39). Only the summation order differs
 // (parallel tree instead of a serial chain).
+//
+// Accumulation: the scan accumulates in fp32 (FMA) to stay HBM-bound and keeps
+// k + kRerankMargin survivors; the last CTA recomputes their scores with the
+// fp64 arithmetic above and re-ranks, so reported scores and the boundary
+// order are the reference's. acc_fp64 instead accumulates every candidate in
+// fp64 (no re-score needed).
+#include <algorithm>
 #include <cfloat>
 #include <cstdint>
 #include <cstdio>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -28,28 +44,22 @@ namespace {
 constexpr int kIP = 0;
 constexpr unsigned kFull = 0xffffffffu;
 
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
 // --------------------------------------------------------------------------
 // scoring terms
 // --------------------------------------------------------------------------
-template <typename ACC>
-__device__ __forceinline__ ACC term_ip(float q, float x, ACC acc);
-template <>
-__device__ __forceinline__ double term_ip<double>(float q, float x, double acc) {
-  return __fma_rn(static_cast<double>(q), static_cast<double>(x), acc);
+__device__ __forceinline__ double term_ip_d(double q, float x, double acc) {
+  return __fma_rn(q, static_cast<double>(x), acc); // exact product: == mul+add
 }
-template <>
-__device__ __forceinline__ float term_ip<float>(float q, float x, float acc) {
-  return __fmaf_rn(q, x, acc);
-}
-template <typename ACC>
-__device__ __forceinline__ ACC term_l2(float q, float x, ACC acc);
-template <>
-__device__ __forceinline__ double term_l2<double>(float q, float x, double acc) {
-  const double t = __dsub_rn(static_cast<double>(q), static_cast<double>(x));
+__device__ __forceinline__ double term_l2_d(double q, float x, double acc) {
+  const double t = __dsub_rn(q, static_cast<double>(x));
   return __dadd_rn(acc, __dmul_rn(t, t));
 }
-template <>
-__device__ __forceinline__ float term_l2<float>(float q, float x, float acc) {
+__device__ __forceinline__ float term_ip_f(float q, float x, float acc) {
+  return __fmaf_rn(q, x, acc);
+}
+__device__ __forceinline__ float term_l2_f(float q, float x, float acc) {
   const float t = q - x;
   return __fmaf_rn(t, t, acc);
 }
@@ -75,6 +85,86 @@ __device__ __forceinline__ float4 ldg_stream(const float4* p) {
   return r;
 }
 
+// Accumulates one float4 of a row into acc with the metric's term.
+template <bool kFp64>
+struct Acc4;
+template <>
+struct Acc4<true> {
+  __device__ __forceinline__ static void run(int metric, const double* q, float4 x,
+                                             double& a) {
+    if (metric == kIP) {
+      a = term_ip_d(q[0], x.x, a);
+      a = term_ip_d(q[1], x.y, a);
+      a = term_ip_d(q[2], x.z, a);
+      a = term_ip_d(q[3], x.w, a);
+    } else {
+      a = term_l2_d(q[0], x.x, a);
+      a = term_l2_d(q[1], x.y, a);
+      a = term_l2_d(q[2], x.z, a);
+      a = term_l2_d(q[3], x.w, a);
+    }
+  }
+};
+template <>
+struct Acc4<false> {
+  __device__ __forceinline__ static void run(int metric, const float* q, float4 x, float& a) {
+    if (metric == kIP) {
+      a = term_ip_f(q[0], x.x, a);
+      a = term_ip_f(q[1], x.y, a);
+      a = term_ip_f(q[2], x.z, a);
+      a = term_ip_f(q[3], x.w, a);
+    } else {
+      a = term_l2_f(q[0], x.x, a);
+      a = term_l2_f(q[1], x.y, a);
+      a = term_l2_f(q[2], x.z, a);
+      a = term_l2_f(q[3], x.w, a);
+    }
+  }
+};
+
+// --------------------------------------------------------------------------
+// mbarrier + bulk copy (TMA) primitives
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // --------------------------------------------------------------------------
 // total order (vectorstore.hpp:34-39)
 // --------------------------------------------------------------------------
@@ -87,12 +177,14 @@ __device__ __forceinline__ float sentinel_score(int metric) {
   return metric == kIP ? -INFINITY : INFINITY;
 }
 
-// Warp-resident sorted top-k: entry j = i * 32 + lane lives in slot i of that
-// lane. Entries j >= k are scratch.
+// Warp-resident sorted top-k with a payload (slab vector index, for the exact
+// re-score): entry j = i * 32 + lane lives in slot i of that lane. Entries
+// j >= k are scratch.
 template <int KPL>
 struct WarpTopK {
   float s[KPL];
   uint64_t id[KPL];
+  uint32_t vi[KPL];
   float worst_s;
   uint64_t worst_id;
 
@@ -101,6 +193,7 @@ struct WarpTopK {
     for (int i = 0; i < KPL; ++i) {
       s[i] = sentinel_score(metric);
       id[i] = ~0ull;
+      vi[i] = ~0u;
     }
     worst_s = sentinel_score(metric);
     worst_id = ~0ull;
@@ -121,13 +214,12 @@ struct WarpTopK {
   __device__ __forceinline__ bool may_enter(int metric, float cs) const {
     return metric == kIP ? cs >= worst_s : cs <= worst_s;
   }
-  __device__ __forceinline__ bool enters(int metric, float cs,
-                                         uint64_t cid) const {
+  __device__ __forceinline__ bool enters(int metric, float cs, uint64_t cid) const {
     return ranks_before(metric, cs, cid, worst_s, worst_id);
   }
 
   // Warp-uniform insertion of a candidate known to enter.
-  __device__ void insert(int metric, int k, float cs, uint64_t cid) {
+  __device__ void insert(int metric, int k, float cs, uint64_t cid, uint32_t cvi) {
     const int lane = threadIdx.x & 31;
     int pos = 0;
 #pragma unroll
@@ -138,20 +230,25 @@ struct WarpTopK {
     }
     float ps[KPL];
     uint64_t pid[KPL];
+    uint32_t pvi[KPL];
 #pragma unroll
     for (int i = 0; i < KPL; ++i) {
       float us = __shfl_up_sync(kFull, s[i], 1);
       uint64_t uid = __shfl_up_sync(kFull, id[i], 1);
+      uint32_t uvi = __shfl_up_sync(kFull, vi[i], 1);
       if (i > 0) {
         const float ts = __shfl_sync(kFull, s[i - 1], 31);
         const uint64_t tid = __shfl_sync(kFull, id[i - 1], 31);
+        const uint32_t tvi = __shfl_sync(kFull, vi[i - 1], 31);
         if (lane == 0) {
           us = ts;
           uid = tid;
+          uvi = tvi;
         }
       }
       ps[i] = us;
       pid[i] = uid;
+      pvi[i] = uvi;
     }
 #pragma unroll
     for (int i = 0; i < KPL; ++i) {
@@ -159,30 +256,37 @@ struct WarpTopK {
       if (j > pos) {
         s[i] = ps[i];
         id[i] = pid[i];
+        vi[i] = pvi[i];
       } else if (j == pos) {
         s[i] = cs;
         id[i] = cid;
+        vi[i] = cvi;
       }
     }
     refresh_worst(k);
   }
 
+  __device__ __forceinline__ void offer(int metric, int k, float cs, uint64_t cid,
+                                        uint32_t cvi) {
+    if (may_enter(metric, cs) && enters(metric, cs, cid)) insert(metric, k, cs, cid, cvi);
+  }
+
   // Merge a best-first list of n entries (sentinels allowed) from memory.
   // Stops at the first entry that cannot enter (the list is sorted).
   template <bool kCG>
-  __device__ void merge_list(int metric, int k, const float* ls,
-                             const uint64_t* lid, int n) {
+  __device__ void merge_list(int metric, int k, const float* ls, const uint64_t* lid,
+                             const uint32_t* lvi, int n) {
     for (int e = 0; e < n; ++e) {
       const float cs = kCG ? __ldcg(ls + e) : ls[e];
       if (!may_enter(metric, cs)) break;
-      const uint64_t cid = kCG ? __ldcg(reinterpret_cast<const unsigned long long*>(lid) + e)
-                               : lid[e];
+      const uint64_t cid =
+          kCG ? __ldcg(reinterpret_cast<const unsigned long long*>(lid) + e) : lid[e];
       if (!enters(metric, cs, cid)) break;
-      insert(metric, k, cs, cid);
+      insert(metric, k, cs, cid, kCG ? __ldcg(lvi + e) : lvi[e]);
     }
   }
 
-  __device__ void store(int k, float* ls, uint64_t* lid) const {
+  __device__ void store(int k, float* ls, uint64_t* lid, uint32_t* lvi) const {
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int i = 0; i < KPL; ++i) {
@@ -190,6 +294,7 @@ struct WarpTopK {
       if (j < k) {
         ls[j] = s[i];
         lid[j] = id[i];
+        lvi[j] = vi[i];
       }
     }
   }
@@ -225,17 +330,8 @@ __global__ void __launch_bounds__(256)
       for (int t = 0; t < QT; ++t) {
         if (t < nqt) {
           const float4 qq = reinterpret_cast<const float4*>(sq + t * d)[j];
-          if (metric == kIP) {
-            acc[t] = term_ip<double>(qq.x, x.x, acc[t]);
-            acc[t] = term_ip<double>(qq.y, x.y, acc[t]);
-            acc[t] = term_ip<double>(qq.z, x.z, acc[t]);
-            acc[t] = term_ip<double>(qq.w, x.w, acc[t]);
-          } else {
-            acc[t] = term_l2<double>(qq.x, x.x, acc[t]);
-            acc[t] = term_l2<double>(qq.y, x.y, acc[t]);
-            acc[t] = term_l2<double>(qq.z, x.z, acc[t]);
-            acc[t] = term_l2<double>(qq.w, x.w, acc[t]);
-          }
+          const double qd[4] = {qq.x, qq.y, qq.z, qq.w};
+          Acc4<true>::run(metric, qd, x, acc[t]);
         }
       }
     }
@@ -245,8 +341,8 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int t = 0; t < QT; ++t) {
         if (t < nqt) {
-          acc[t] = metric == kIP ? term_ip<double>(sq[t * d + j], x, acc[t])
-                                 : term_l2<double>(sq[t * d + j], x, acc[t]);
+          acc[t] = metric == kIP ? term_ip_d(sq[t * d + j], x, acc[t])
+                                 : term_l2_d(sq[t * d + j], x, acc[t]);
         }
       }
     }
@@ -261,86 +357,33 @@ __global__ void __launch_bounds__(256)
 }
 
 // --------------------------------------------------------------------------
-// selection: bitonic sort of (orderable key, cluster id) in shared memory
+// residency split of a probe held in memory (block-wide, any blockDim <= 1024)
 // --------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t order_key(double s, int metric) {
-  s = s + 0.0;                      // -0.0 -> +0.0: equal scores tie on id
-  if (metric == kIP) s = -s;        // descending -> ascending
-  const uint64_t b = static_cast<uint64_t>(__double_as_longlong(s));
-  return (b >> 63) ? ~b : (b | (1ull << 63));
-}
-
-__global__ void __launch_bounds__(1024)
-    select_kernel(const double* __restrict__ scores, uint32_t nc, int metric,
-                  uint32_t p2, uint32_t n_out, uint32_t* __restrict__ order) {
-  extern __shared__ uint64_t skey[];
-  uint32_t* sid = reinterpret_cast<uint32_t*>(skey + p2);
-  const uint32_t q = blockIdx.x;
-  const double* sc = scores + static_cast<uint64_t>(q) * nc;
-  for (uint32_t i = threadIdx.x; i < p2; i += blockDim.x) {
-    if (i < nc) {
-      skey[i] = order_key(sc[i], metric);
-      sid[i] = i;
-    } else {
-      skey[i] = ~0ull;
-      sid[i] = ~0u;
-    }
-  }
-  __syncthreads();
-  for (uint32_t kk = 2; kk <= p2; kk <<= 1) {
-    for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = threadIdx.x; i < p2; i += blockDim.x) {
-        const uint32_t l = i ^ j;
-        if (l > i) {
-          const uint64_t ka = skey[i], kb = skey[l];
-          const uint32_t ia = sid[i], ib = sid[l];
-          const bool a_gt_b = ka > kb || (ka == kb && ia > ib);
-          const bool up = (i & kk) == 0;
-          if (up == a_gt_b) {
-            skey[i] = kb;
-            skey[l] = ka;
-            sid[i] = ib;
-            sid[l] = ia;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  uint32_t* out = order + static_cast<uint64_t>(q) * n_out;
-  for (uint32_t i = threadIdx.x; i < n_out; i += blockDim.x) out[i] = sid[i];
-}
-
-// --------------------------------------------------------------------------
-// partition by residency (tiered.cpp:155-161) + exclusive prefix of lengths
-// --------------------------------------------------------------------------
-__global__ void __launch_bounds__(256)
-    partition_kernel(const uint32_t* __restrict__ probe, uint32_t lp,
-                     const int64_t* __restrict__ res_off,
-                     const uint64_t* __restrict__ list_off, FastTable ft) {
-  __shared__ uint32_t w_cnt[8];
-  __shared__ uint64_t w_len[8];
+__device__ void partition_block(const uint32_t* probe, uint32_t lp, const int64_t* res_off,
+                                const uint64_t* list_off, const FastTable& ft, uint32_t q) {
+  __shared__ uint32_t w_cnt[32];
+  __shared__ uint64_t w_len[32];
   __shared__ uint32_t base_cnt;
   __shared__ uint64_t base_len;
-  const uint32_t q = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = (blockDim.x + 31) >> 5;
   const uint64_t tb = static_cast<uint64_t>(q) * ft.stride;
+  uint64_t* pre = ft.pre + static_cast<uint64_t>(q) * (ft.stride + 1);
   if (threadIdx.x == 0) {
     base_cnt = 0;
     base_len = 0;
   }
   __syncthreads();
-  for (uint32_t t0 = 0; t0 < lp; t0 += 256) {
+  for (uint32_t t0 = 0; t0 < lp; t0 += blockDim.x) {
     const uint32_t i = t0 + threadIdx.x;
     uint32_t c = 0;
     int64_t so = -1;
     if (i < lp) {
-      c = probe[static_cast<uint64_t>(q) * lp + i];
+      c = probe[i];
       so = res_off[c];
     }
     const bool fast = so >= 0;
     const uint64_t len = fast ? list_off[c + 1] - list_off[c] : 0;
-    // warp inclusive scans
     uint32_t ic = fast ? 1u : 0u;
     uint64_t il = len;
 #pragma unroll
@@ -363,34 +406,265 @@ __global__ void __launch_bounds__(256)
       pc += w_cnt[w];
       pl += w_len[w];
     }
-    const uint32_t ex_c = pc + ic - (fast ? 1u : 0u);
-    const uint64_t ex_l = pl + il - len;
     if (fast) {
+      const uint32_t ex_c = pc + ic - 1u;
       ft.slab[tb + ex_c] = so;
       ft.row[tb + ex_c] = list_off[c];
       ft.len[tb + ex_c] = static_cast<uint32_t>(len);
       ft.cluster[tb + ex_c] = c;
-      ft.pre[static_cast<uint64_t>(q) * (ft.stride + 1) + ex_c] = ex_l;
+      pre[ex_c] = pl + il - len;
     }
     __syncthreads();
-    if (threadIdx.x == 255) {
-      base_cnt = pc + ic;
-      base_len = pl + il;
+    if (threadIdx.x == 0) {
+      uint32_t tc = base_cnt;
+      uint64_t tl = base_len;
+      for (int w = 0; w < nwarps; ++w) {
+        tc += w_cnt[w];
+        tl += w_len[w];
+      }
+      base_cnt = tc;
+      base_len = tl;
     }
     __syncthreads();
   }
   if (threadIdx.x == 0) {
     ft.count[q] = base_cnt;
-    ft.pre[static_cast<uint64_t>(q) * (ft.stride + 1) + base_cnt] = base_len;
+    pre[base_cnt] = base_len;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    partition_kernel(const uint32_t* __restrict__ probe, uint32_t lp,
+                     const int64_t* __restrict__ res_off,
+                     const uint64_t* __restrict__ list_off, FastTable ft) {
+  partition_block(probe + static_cast<uint64_t>(blockIdx.x) * lp, lp, res_off, list_off, ft,
+                  blockIdx.x);
+}
+
+// --------------------------------------------------------------------------
+// selection: block bitonic sort of (orderable key, cluster id); strides below
+// E stay in registers, below 32E use warp shuffles, the rest shared memory
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t order_key(double s, int metric) {
+  s = s + 0.0;                      // -0.0 -> +0.0: equal scores tie on id
+  if (metric == kIP) s = -s;        // descending -> ascending
+  const uint64_t b = static_cast<uint64_t>(__double_as_longlong(s));
+  return (b >> 63) ? ~b : (b | (1ull << 63));
+}
+
+__device__ __forceinline__ bool kv_gt(uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
+  return ka > kb || (ka == kb && va > vb);
+}
+
+// Compare-exchange stage with stride J < E inside one thread's registers.
+template <int E, int J>
+__device__ __forceinline__ void inthread_stage(uint64_t (&k)[E], uint32_t (&v)[E], uint32_t kk) {
+  if constexpr (J < E) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int p = e ^ J;
+      if (p > e) {
+        const uint32_t i = threadIdx.x * E + e;
+        const bool up = (i & kk) == 0;
+        if (kv_gt(k[e], v[e], k[p], v[p]) == up) {
+          const uint64_t tk = k[e];
+          k[e] = k[p];
+          k[p] = tk;
+          const uint32_t tv = v[e];
+          v[e] = v[p];
+          v[p] = tv;
+        }
+      }
+    }
+  }
+}
+
+template <int E>
+__device__ void block_bitonic_sort(uint64_t (&k)[E], uint32_t (&v)[E], uint64_t* sk,
+                                   uint32_t* sv, uint32_t n) {
+  const uint32_t t = threadIdx.x;
+  for (uint32_t kk = 2; kk <= n; kk <<= 1) {
+    for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+      if (j < static_cast<uint32_t>(E)) {
+        if (j == 1) inthread_stage<E, 1>(k, v, kk);
+        else if (j == 2) inthread_stage<E, 2>(k, v, kk);
+        else if (j == 4) inthread_stage<E, 4>(k, v, kk);
+        else inthread_stage<E, 8>(k, v, kk);
+      } else if (j < 32u * E) {
+        const int lm = static_cast<int>(j / E);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint64_t ok = __shfl_xor_sync(kFull, k[e], lm);
+          const uint32_t ov = __shfl_xor_sync(kFull, v[e], lm);
+          const uint32_t i = t * E + e;
+          const bool up = (i & kk) == 0, lower = (i & j) == 0;
+          const bool gt = kv_gt(k[e], v[e], ok, ov);
+          if (lower == up ? gt : !gt) {
+            k[e] = ok;
+            v[e] = ov;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          sk[t * E + e] = k[e];
+          sv[t * E + e] = v[e];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint32_t i = t * E + e, p = i ^ j;
+          const uint64_t ok = sk[p];
+          const uint32_t ov = sv[p];
+          const bool up = (i & kk) == 0, lower = (i & j) == 0;
+          const bool gt = kv_gt(k[e], v[e], ok, ov);
+          if (lower == up ? gt : !gt) {
+            k[e] = ok;
+            v[e] = ov;
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+}
+
+// One CTA per query; blockDim * E = p2 (power of two >= nc, >= 32).
+template <int E>
+__global__ void __launch_bounds__(1024)
+    select_kernel(const double* __restrict__ scores, uint32_t nc, int metric, uint32_t p2,
+                  uint32_t n_out, uint32_t* __restrict__ order, const int64_t* res_off,
+                  const uint64_t* list_off, FastTable ft, bool do_partition) {
+  extern __shared__ uint64_t sk[];
+  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + p2);
+  const uint32_t q = blockIdx.x;
+  const double* sc = scores + static_cast<uint64_t>(q) * nc;
+  uint64_t k[E];
+  uint32_t v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t i = threadIdx.x * E + e;
+    if (i < nc) {
+      k[e] = order_key(sc[i], metric);
+      v[e] = i;
+    } else {
+      k[e] = ~0ull;
+      v[e] = ~0u;
+    }
+  }
+  block_bitonic_sort<E>(k, v, sk, sv, p2);
+  uint32_t* out = order + static_cast<uint64_t>(q) * n_out;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t i = threadIdx.x * E + e;
+    if (i < n_out) out[i] = v[e];
+    sv[i] = v[e];
+  }
+  if (do_partition) {
+    __syncthreads();
+    partition_block(sv, n_out, res_off, list_off, ft, q);
   }
 }
 
 // --------------------------------------------------------------------------
-// list scan
+// shared scan epilogue: CTA merge, grid merge, exact re-score of survivors
 // --------------------------------------------------------------------------
-constexpr int kScanWarps = 8;
-constexpr int kScanThreads = kScanWarps * 32;
-constexpr int kU = 2; // vectors in flight per warp iteration
+struct MergeSmem {
+  float* s;
+  uint64_t* id;
+  uint32_t* vi;
+};
+
+// Exact fp64 score (vectorstore.cpp:93-115 arithmetic) of slab row `vi`.
+__device__ float exact_score(const float* __restrict__ slab, uint32_t vi, const float* sq,
+                             uint32_t d, int metric) {
+  const int lane = threadIdx.x & 31;
+  const float* row = slab + static_cast<uint64_t>(vi) * d;
+  double acc = 0.0;
+  for (uint32_t j = lane; j < d; j += 32) {
+    acc = metric == kIP ? term_ip_d(static_cast<double>(sq[j]), __ldg(row + j), acc)
+                        : term_l2_d(static_cast<double>(sq[j]), __ldg(row + j), acc);
+  }
+  acc = warp_sum(acc);
+  return finish_score<double>(metric, acc);
+}
+
+// Called by every thread of the CTA once the warps [first, first + nw) hold
+// their top-kk in registers.
+template <int KPL>
+__device__ void scan_epilogue(WarpTopK<KPL>& top, int metric, int k, int kk, bool rerank,
+                              MergeSmem m, const ScanOut& out, const float* sq,
+                              const float* __restrict__ slab, uint32_t d, uint64_t V,
+                              int first, int nw, bool* am_last) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t q = blockIdx.y;
+  const bool holder = warp >= first && warp < first + nw;
+  const int w = warp - first;
+  if (holder) top.store(kk, m.s + w * kk, m.id + w * kk, m.vi + w * kk);
+  __syncthreads();
+  const uint64_t part = (static_cast<uint64_t>(q) * gridDim.x + blockIdx.x) * kk;
+  if (warp == first) {
+    for (int o = 1; o < nw; ++o) {
+      top.template merge_list<false>(metric, kk, m.s + o * kk, m.id + o * kk, m.vi + o * kk, kk);
+    }
+    top.store(kk, out.part_s + part, out.part_id + part, out.part_vi + part);
+    __threadfence();
+    if (lane == 0) {
+      const unsigned t = atomicAdd(out.ticket + q, 1u);
+      *am_last = (t == gridDim.x - 1);
+    }
+  }
+  __syncthreads();
+  if (!*am_last) return;
+
+  // ---- grid merge in the last CTA ----
+  __threadfence();
+  const uint64_t pbase = static_cast<uint64_t>(q) * gridDim.x * kk;
+  if (holder) {
+    top.init(metric);
+    for (uint32_t g = w; g < gridDim.x; g += nw) {
+      top.template merge_list<true>(metric, kk, out.part_s + pbase + g * kk,
+                                    out.part_id + pbase + g * kk,
+                                    out.part_vi + pbase + g * kk, kk);
+    }
+    top.store(kk, m.s + w * kk, m.id + w * kk, m.vi + w * kk);
+  }
+  __syncthreads();
+  if (warp == first) {
+    for (int o = 1; o < nw; ++o) {
+      top.template merge_list<false>(metric, kk, m.s + o * kk, m.id + o * kk, m.vi + o * kk, kk);
+    }
+    top.store(kk, m.s, m.id, m.vi);
+  }
+  __syncthreads();
+  const int navail = static_cast<int>(V < static_cast<uint64_t>(kk) ? V : kk);
+  if (rerank) {
+    // exact fp64 re-score of the survivors, then re-rank on (score, id)
+    if (holder) {
+      for (int c = w; c < navail; c += nw) {
+        const float es = exact_score(slab, m.vi[c], sq, d, metric);
+        if (lane == 0) m.s[c] = es;
+      }
+    }
+    __syncthreads();
+    if (warp == first) {
+      top.init(metric);
+      for (int c = 0; c < navail; ++c) top.offer(metric, k, m.s[c], m.id[c], m.vi[c]);
+      top.store(k, m.s, m.id, m.vi);
+    }
+    __syncthreads();
+  }
+  if (warp == first) {
+    for (int j = lane; j < k; j += 32) {
+      out.out_s[static_cast<uint64_t>(q) * k + j] = m.s[j];
+      out.out_id[static_cast<uint64_t>(q) * k + j] = m.id[j];
+    }
+    if (lane == 0) {
+      out.out_count[q] = static_cast<uint32_t>(V < static_cast<uint64_t>(k) ? V : k);
+      out.ticket[q] = 0; // self-reset for the next launch / graph replay
+    }
+  }
+}
 
 // Cursor over a query's flattened fast-list vector space.
 struct Cursor {
@@ -399,19 +673,239 @@ struct Cursor {
   uint64_t o;
   int64_t slab;
   uint64_t row;
+  __device__ void load(const FastTable& ft, uint64_t tb) {
+    len = ft.len[tb + li];
+    slab = ft.slab[tb + li];
+    row = ft.row[tb + li];
+  }
+  // position at flattened index v (pre: exclusive prefix over nf lists)
+  __device__ void seek(const FastTable& ft, uint64_t tb, const uint64_t* pre, uint32_t nf,
+                       uint64_t v) {
+    uint32_t lo = 0, hi = nf - 1;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (pre[mid] <= v) lo = mid;
+      else hi = mid - 1;
+    }
+    li = lo;
+    load(ft, tb);
+    o = v - pre[lo];
+    while (o >= len) { // skip empty lists
+      ++li;
+      load(ft, tb);
+      o = 0;
+    }
+  }
+  // Move forward n vectors; only called when the target position exists.
+  __device__ void advance(const FastTable& ft, uint64_t tb, uint64_t n) {
+    o += n;
+    while (o >= len) {
+      o -= len;
+      ++li;
+      load(ft, tb);
+    }
+  }
 };
 
-template <typename ACC, int KPL, int NCH>
-__global__ void __launch_bounds__(kScanThreads, 2)
-    scan_kernel(const float* __restrict__ Q, uint32_t d, int metric, int k,
-                FastTable ft, const float* __restrict__ slab_vecs,
-                const uint64_t* __restrict__ ids_all, ScanOut out) {
-  extern __shared__ unsigned char smem_raw[];
-  float* sq = reinterpret_cast<float*>(smem_raw);                  // d floats
-  float* ms = sq + ((d + 3) & ~3u);                                // [W][k]
-  uint64_t* mid = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(ms + kScanWarps * k) + 7) & ~uintptr_t(7)); // [W][k]
+// --------------------------------------------------------------------------
+// TMA-staged scan
+// --------------------------------------------------------------------------
+constexpr int kConsumers = 8;
+constexpr int kTmaThreads = 32 * (kConsumers + 1);
+
+template <bool kFp64, int KPL, int NCH>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    scan_tma_kernel(const float* __restrict__ Q, uint32_t d, int metric, int k, int kk,
+                    FastTable ft, const float* __restrict__ slab,
+                    const uint64_t* __restrict__ ids_all, ScanOut out, uint32_t T, uint32_t S) {
+  using ACC = typename std::conditional<kFp64, double, float>::type;
+  extern __shared__ __align__(128) unsigned char smem[];
   __shared__ bool am_last;
+  const size_t stage_floats = static_cast<size_t>(T) * d;
+  float* stage = reinterpret_cast<float*>(smem);
+  size_t off = (static_cast<size_t>(S) * stage_floats * 4 + 127) & ~size_t(127);
+  const size_t merge_bytes = static_cast<size_t>(kConsumers) * kk * 16;
+  if (off < merge_bytes) off = (merge_bytes + 127) & ~size_t(127);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + off);
+  uint64_t* empty = full + S;
+  uint64_t* mrow = empty + S;                                 // [S][T]
+  uint32_t* mvi = reinterpret_cast<uint32_t*>(mrow + S * T);  // [S][T]
+  uint32_t* mn = mvi + S * T;                                 // [S]
+  float* sq = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(mn + S) + 15) & ~uintptr_t(15));
+
+  const uint32_t q = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* qv = Q + static_cast<uint64_t>(q) * d;
+  for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) sq[i] = qv[i];
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kConsumers);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const uint64_t tb = static_cast<uint64_t>(q) * ft.stride;
+  const uint64_t* pre = ft.pre + static_cast<uint64_t>(q) * (ft.stride + 1);
+  const uint32_t nf = ft.count[q];
+  const uint64_t V = pre[nf];
+  const uint64_t v0 = V * blockIdx.x / gridDim.x, v1 = V * (blockIdx.x + 1) / gridDim.x;
+  const uint32_t ntiles = static_cast<uint32_t>((v1 - v0 + T - 1) / T);
+
+  WarpTopK<KPL> top;
+  top.init(metric);
+
+  if (warp == 0) {
+    // ---------------- producer: one lane drives the bulk copies ----------
+    if (lane == 0 && ntiles) {
+      Cursor cur;
+      cur.seek(ft, tb, pre, nf, v0);
+      for (uint32_t i = 0; i < ntiles; ++i) {
+        const uint32_t s = i % S;
+        mbar_wait(empty + s, ((i / S) & 1u) ^ 1u);
+        const uint64_t tile0 = v0 + uint64_t(i) * T;
+        const uint32_t n = static_cast<uint32_t>(umin64(T, v1 - tile0));
+        // tile metadata first (published by the arrive), then the copies
+        uint32_t j = 0;
+        Cursor c2 = cur;
+        while (true) {
+          const uint32_t take = static_cast<uint32_t>(umin64(n - j, c2.len - c2.o));
+          for (uint32_t t = 0; t < take; ++t) {
+            mrow[s * T + j + t] = c2.row + c2.o + t;
+            mvi[s * T + j + t] = static_cast<uint32_t>(c2.slab + c2.o + t);
+          }
+          j += take;
+          if (j >= n) break;
+          c2.advance(ft, tb, take);
+        }
+        mn[s] = n;
+        mbar_arrive_expect_tx(full + s, n * d * 4u);
+        j = 0;
+        while (true) {
+          const uint32_t take = static_cast<uint32_t>(umin64(n - j, cur.len - cur.o));
+          bulk_g2s(stage + s * stage_floats + static_cast<size_t>(j) * d,
+                   slab + static_cast<uint64_t>(cur.slab + static_cast<int64_t>(cur.o)) * d,
+                   take * d * 4u, full + s);
+          j += take;
+          if (tile0 + j >= v1) break;
+          cur.advance(ft, tb, take);
+          if (j >= n) break;
+        }
+      }
+    }
+  } else {
+    // ---------------- consumers ----------------
+    const int cw = warp - 1;
+    float qf[NCH > 0 ? NCH * 4 : 1];
+    double qd[(NCH > 0 && kFp64) ? NCH * 4 : 1];
+    if constexpr (NCH > 0) {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const float4 t = reinterpret_cast<const float4*>(sq)[c * 32 + lane];
+        qf[4 * c + 0] = t.x;
+        qf[4 * c + 1] = t.y;
+        qf[4 * c + 2] = t.z;
+        qf[4 * c + 3] = t.w;
+        if constexpr (kFp64) {
+          qd[4 * c + 0] = t.x;
+          qd[4 * c + 1] = t.y;
+          qd[4 * c + 2] = t.z;
+          qd[4 * c + 3] = t.w;
+        }
+      }
+    }
+    for (uint32_t i = 0; i < ntiles; ++i) {
+      const uint32_t s = i % S;
+      mbar_wait(full + s, (i / S) & 1u);
+      const uint32_t n = mn[s];
+      const float* base = stage + s * stage_floats;
+      for (uint32_t j = cw; j < n; j += 2 * kConsumers) {
+        const uint32_t j2 = j + kConsumers;
+        const bool two = j2 < n;
+        const float4* r0 = reinterpret_cast<const float4*>(base + static_cast<size_t>(j) * d);
+        const float4* r1 =
+            reinterpret_cast<const float4*>(base + static_cast<size_t>(two ? j2 : j) * d);
+        ACC a0 = ACC(0), a1 = ACC(0);
+        if constexpr (NCH > 0) {
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) {
+            const float4 x0 = r0[c * 32 + lane];
+            const float4 x1 = r1[c * 32 + lane];
+            if constexpr (kFp64) {
+              Acc4<true>::run(metric, qd + 4 * c, x0, a0);
+              Acc4<true>::run(metric, qd + 4 * c, x1, a1);
+            } else {
+              Acc4<false>::run(metric, qf + 4 * c, x0, a0);
+              Acc4<false>::run(metric, qf + 4 * c, x1, a1);
+            }
+          }
+        } else {
+          const uint32_t d4 = d >> 2;
+          for (uint32_t j4 = lane; j4 < d4; j4 += 32) {
+            const float4 qq = reinterpret_cast<const float4*>(sq)[j4];
+            if constexpr (kFp64) {
+              const double q4[4] = {qq.x, qq.y, qq.z, qq.w};
+              Acc4<true>::run(metric, q4, r0[j4], a0);
+              Acc4<true>::run(metric, q4, r1[j4], a1);
+            } else {
+              const float q4[4] = {qq.x, qq.y, qq.z, qq.w};
+              Acc4<false>::run(metric, q4, r0[j4], a0);
+              Acc4<false>::run(metric, q4, r1[j4], a1);
+            }
+          }
+        }
+        a0 = warp_sum(a0);
+        a1 = warp_sum(a1);
+        const float s0 = finish_score<ACC>(metric, a0);
+        if (top.may_enter(metric, s0)) {
+          const uint64_t id0 = ids_all[mrow[s * T + j]];
+          if (top.enters(metric, s0, id0)) top.insert(metric, kk, s0, id0, mvi[s * T + j]);
+        }
+        if (two) {
+          const float s1 = finish_score<ACC>(metric, a1);
+          if (top.may_enter(metric, s1)) {
+            const uint64_t id1 = ids_all[mrow[s * T + j2]];
+            if (top.enters(metric, s1, id1)) top.insert(metric, kk, s1, id1, mvi[s * T + j2]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
+    }
+  }
+  __syncthreads(); // every tile consumed: the stage ring is free for merging
+
+  MergeSmem m;
+  m.s = reinterpret_cast<float*>(smem);
+  m.id = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(m.s + kConsumers * kk) + 7) & ~uintptr_t(7));
+  m.vi = reinterpret_cast<uint32_t*>(m.id + kConsumers * kk);
+  scan_epilogue<KPL>(top, metric, k, kk, !kFp64, m, out, sq, slab, d, V, 1, kConsumers,
+                     &am_last);
+}
+
+// --------------------------------------------------------------------------
+// LDG scan (direct 128-bit loads into registers)
+// --------------------------------------------------------------------------
+constexpr int kScanWarps = 8;
+constexpr int kScanThreads = kScanWarps * 32;
+constexpr int kU = 2; // vectors in flight per warp iteration
+
+template <bool kFp64, int KPL, int NCH>
+__global__ void __launch_bounds__(kScanThreads, 2)
+    scan_ldg_kernel(const float* __restrict__ Q, uint32_t d, int metric, int k, int kk,
+                    FastTable ft, const float* __restrict__ slab_vecs,
+                    const uint64_t* __restrict__ ids_all, ScanOut out) {
+  using ACC = typename std::conditional<kFp64, double, float>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ bool am_last;
+  float* sq = reinterpret_cast<float*>(smem_raw);
+  float* ms = sq + ((d + 3) & ~3u);
+  uint64_t* mid = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(ms + kScanWarps * kk) + 7) & ~uintptr_t(7));
+  uint32_t* mvi = reinterpret_cast<uint32_t*>(mid + kScanWarps * kk);
 
   const uint32_t q = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -431,37 +925,21 @@ __global__ void __launch_bounds__(kScanThreads, 2)
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kScanWarps + warp;
   const uint64_t v0 = V * gw / tw, v1 = V * (gw + 1) / tw;
 
-  // q slice in registers for the fixed-D fast path
-  float4 qr[NCH > 0 ? NCH : 1];
+  float qf[NCH > 0 ? NCH * 4 : 1];
   if constexpr (NCH > 0) {
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
-      qr[c] = reinterpret_cast<const float4*>(sq)[c * 32 + lane];
+      const float4 t = reinterpret_cast<const float4*>(sq)[c * 32 + lane];
+      qf[4 * c + 0] = t.x;
+      qf[4 * c + 1] = t.y;
+      qf[4 * c + 2] = t.z;
+      qf[4 * c + 3] = t.w;
     }
   }
 
   if (v0 < v1) {
-    // locate the list holding v0: last li with pre[li] <= v0
-    uint32_t lo = 0, hi = nf - 1;
-    while (lo < hi) {
-      const uint32_t mid_ = (lo + hi + 1) >> 1;
-      if (pre[mid_] <= v0) lo = mid_;
-      else hi = mid_ - 1;
-    }
     Cursor cur;
-    cur.li = lo;
-    cur.len = ft.len[tb + lo];
-    cur.o = v0 - pre[lo];
-    cur.slab = ft.slab[tb + lo];
-    cur.row = ft.row[tb + lo];
-    while (cur.o >= cur.len) { // skip empty lists
-      ++cur.li;
-      cur.len = ft.len[tb + cur.li];
-      cur.o = 0;
-      cur.slab = ft.slab[tb + cur.li];
-      cur.row = ft.row[tb + cur.li];
-    }
-
+    cur.seek(ft, tb, pre, nf, v0);
     for (uint64_t v = v0; v < v1; v += kU) {
       int64_t vec[kU];
       uint64_t rowi[kU];
@@ -471,16 +949,7 @@ __global__ void __launch_bounds__(kScanThreads, 2)
         valid[u] = v + u < v1;
         vec[u] = cur.slab + static_cast<int64_t>(cur.o);
         rowi[u] = cur.row + cur.o;
-        if (valid[u] && v + u + 1 < v1) {
-          ++cur.o;
-          while (cur.o >= cur.len) {
-            ++cur.li;
-            cur.len = ft.len[tb + cur.li];
-            cur.o = 0;
-            cur.slab = ft.slab[tb + cur.li];
-            cur.row = ft.row[tb + cur.li];
-          }
-        }
+        if (valid[u] && v + u + 1 < v1) cur.advance(ft, tb, 1);
       }
       ACC acc[kU];
 #pragma unroll
@@ -489,9 +958,9 @@ __global__ void __launch_bounds__(kScanThreads, 2)
         float4 x[kU][NCH];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-          const float4* p = reinterpret_cast<const float4*>(
-                                slab_vecs + static_cast<uint64_t>(vec[u]) * (NCH * 128)) +
-                            lane;
+          const float4* p =
+              reinterpret_cast<const float4*>(slab_vecs + static_cast<uint64_t>(vec[u]) * (NCH * 128)) +
+              lane;
 #pragma unroll
           for (int c = 0; c < NCH; ++c) {
             x[u][c] = valid[u] ? ldg_stream(p + c * 32) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -501,16 +970,11 @@ __global__ void __launch_bounds__(kScanThreads, 2)
         for (int u = 0; u < kU; ++u) {
 #pragma unroll
           for (int c = 0; c < NCH; ++c) {
-            if (metric == kIP) {
-              acc[u] = term_ip<ACC>(qr[c].x, x[u][c].x, acc[u]);
-              acc[u] = term_ip<ACC>(qr[c].y, x[u][c].y, acc[u]);
-              acc[u] = term_ip<ACC>(qr[c].z, x[u][c].z, acc[u]);
-              acc[u] = term_ip<ACC>(qr[c].w, x[u][c].w, acc[u]);
+            if constexpr (kFp64) {
+              const double q4[4] = {qf[4 * c], qf[4 * c + 1], qf[4 * c + 2], qf[4 * c + 3]};
+              Acc4<true>::run(metric, q4, x[u][c], acc[u]);
             } else {
-              acc[u] = term_l2<ACC>(qr[c].x, x[u][c].x, acc[u]);
-              acc[u] = term_l2<ACC>(qr[c].y, x[u][c].y, acc[u]);
-              acc[u] = term_l2<ACC>(qr[c].z, x[u][c].z, acc[u]);
-              acc[u] = term_l2<ACC>(qr[c].w, x[u][c].w, acc[u]);
+              Acc4<false>::run(metric, qf + 4 * c, x[u][c], acc[u]);
             }
           }
         }
@@ -521,8 +985,11 @@ __global__ void __launch_bounds__(kScanThreads, 2)
           const float* p = slab_vecs + static_cast<uint64_t>(vec[u]) * d;
           for (uint32_t j = lane; j < d; j += 32) {
             const float xv = __ldg(p + j);
-            acc[u] = metric == kIP ? term_ip<ACC>(sq[j], xv, acc[u])
-                                   : term_l2<ACC>(sq[j], xv, acc[u]);
+            if constexpr (kFp64) {
+              acc[u] = metric == kIP ? term_ip_d(sq[j], xv, acc[u]) : term_l2_d(sq[j], xv, acc[u]);
+            } else {
+              acc[u] = metric == kIP ? term_ip_f(sq[j], xv, acc[u]) : term_l2_f(sq[j], xv, acc[u]);
+            }
           }
         }
       }
@@ -533,51 +1000,16 @@ __global__ void __launch_bounds__(kScanThreads, 2)
         const float cs = finish_score<ACC>(metric, tot);
         if (top.may_enter(metric, cs)) {
           const uint64_t cid = ids_all[rowi[u]];
-          if (top.enters(metric, cs, cid)) top.insert(metric, k, cs, cid);
+          if (top.enters(metric, cs, cid)) {
+            top.insert(metric, kk, cs, cid, static_cast<uint32_t>(vec[u]));
+          }
         }
       }
     }
   }
-
-  // ---- CTA merge: warps -> smem -> warp 0 ----
-  top.store(k, ms + warp * k, mid + warp * k);
-  __syncthreads();
-  const uint64_t part = (static_cast<uint64_t>(q) * gridDim.x + blockIdx.x) * k;
-  if (warp == 0) {
-    for (int w = 1; w < kScanWarps; ++w) {
-      top.template merge_list<false>(metric, k, ms + w * k, mid + w * k, k);
-    }
-    top.store(k, out.part_s + part, out.part_id + part);
-    __threadfence();
-    if (lane == 0) {
-      const unsigned t = atomicAdd(out.ticket + q, 1u);
-      am_last = (t == gridDim.x - 1);
-    }
-  }
-  __syncthreads();
-  if (!am_last) return;
-
-  // ---- grid merge in the last CTA ----
-  __threadfence();
-  top.init(metric);
-  const uint64_t pbase = static_cast<uint64_t>(q) * gridDim.x * k;
-  for (uint32_t g = warp; g < gridDim.x; g += kScanWarps) {
-    top.template merge_list<true>(metric, k, out.part_s + pbase + g * k,
-                                  out.part_id + pbase + g * k, k);
-  }
-  top.store(k, ms + warp * k, mid + warp * k);
-  __syncthreads();
-  if (warp == 0) {
-    for (int w = 1; w < kScanWarps; ++w) {
-      top.template merge_list<false>(metric, k, ms + w * k, mid + w * k, k);
-    }
-    top.store(k, out.out_s + static_cast<uint64_t>(q) * k,
-              out.out_id + static_cast<uint64_t>(q) * k);
-    if (lane == 0) {
-      out.out_count[q] = static_cast<uint32_t>(V < static_cast<uint64_t>(k) ? V : k);
-      out.ticket[q] = 0; // self-reset for the next launch / graph replay
-    }
-  }
+  MergeSmem m{ms, mid, mvi};
+  scan_epilogue<KPL>(top, metric, k, kk, !kFp64, m, out, sq, slab_vecs, d, V, 0, kScanWarps,
+                     &am_last);
 }
 
 // --------------------------------------------------------------------------
@@ -595,30 +1027,73 @@ __global__ void window_kernel(uint64_t ns) {
   }
 }
 
-template <typename ACC, int KPL, int NCH>
-void launch_scan_t(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
-                   const FastTable& ft, const float* slab, const uint64_t* ids,
-                   const ScanOut& out, int gx, cudaStream_t st) {
-  const size_t smem = ((d + 3) & ~3u) * sizeof(float) +
-                      kScanWarps * k * (sizeof(float) + sizeof(uint64_t)) + 16;
-  auto fn = scan_kernel<ACC, KPL, NCH>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    attr_set = true;
+// --------------------------------------------------------------------------
+// launch plumbing
+// --------------------------------------------------------------------------
+struct TmaGeom {
+  uint32_t T, S;
+  size_t smem;
+};
+
+TmaGeom tma_geom(uint32_t d, int kk) {
+  const size_t row = size_t(d) * 4;
+  TmaGeom g;
+  g.T = static_cast<uint32_t>(std::max<size_t>(1, std::min<size_t>(32, 49152 / row)));
+  const size_t stage = g.T * row;
+  g.S = static_cast<uint32_t>(std::max<size_t>(2, std::min<size_t>(8, 196608 / stage)));
+  size_t off = (g.S * stage + 127) & ~size_t(127);
+  const size_t merge = size_t(kConsumers) * kk * 16;
+  if (off < merge) off = (merge + 127) & ~size_t(127);
+  off += g.S * 16 + g.S * g.T * 12 + g.S * 4 + 16;
+  off += row + 16;
+  g.smem = off;
+  return g;
+}
+
+template <bool kFp64, int KPL, int NCH>
+void launch_tma_t(const float* Q, uint32_t nq, uint32_t d, int metric, int k, int kk,
+                  const FastTable& ft, const float* slab, const uint64_t* ids,
+                  const ScanOut& out, int gx, cudaStream_t st) {
+  const TmaGeom g = tma_geom(d, kk);
+  auto fn = scan_tma_kernel<kFp64, KPL, NCH>;
+  static size_t attr = 0;
+  if (g.smem > attr) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.smem));
+    attr = g.smem;
   }
-  fn<<<dim3(gx, nq), kScanThreads, smem, st>>>(Q, d, metric, k, ft, slab, ids, out);
+  fn<<<dim3(gx, nq), kTmaThreads, g.smem, st>>>(Q, d, metric, k, kk, ft, slab, ids, out, g.T, g.S);
   launch_counter()++;
 }
 
-template <typename ACC, int NCH>
-void launch_scan_k(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
-                   const FastTable& ft, const float* slab, const uint64_t* ids,
-                   const ScanOut& out, int gx, cudaStream_t st) {
-  if (k <= 32) launch_scan_t<ACC, 1, NCH>(Q, nq, d, metric, k, ft, slab, ids, out, gx, st);
-  else if (k <= 64) launch_scan_t<ACC, 2, NCH>(Q, nq, d, metric, k, ft, slab, ids, out, gx, st);
-  else if (k <= 128) launch_scan_t<ACC, 4, NCH>(Q, nq, d, metric, k, ft, slab, ids, out, gx, st);
-  else launch_scan_t<ACC, 8, NCH>(Q, nq, d, metric, k, ft, slab, ids, out, gx, st);
+template <bool kFp64, int KPL, int NCH>
+void launch_ldg_t(const float* Q, uint32_t nq, uint32_t d, int metric, int k, int kk,
+                  const FastTable& ft, const float* slab, const uint64_t* ids,
+                  const ScanOut& out, int gx, cudaStream_t st) {
+  const size_t smem = ((d + 3) & ~3u) * sizeof(float) + size_t(kScanWarps) * kk * 16 + 16;
+  auto fn = scan_ldg_kernel<kFp64, KPL, NCH>;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = smem;
+  }
+  fn<<<dim3(gx, nq), kScanThreads, smem, st>>>(Q, d, metric, k, kk, ft, slab, ids, out);
+  launch_counter()++;
+}
+
+template <bool kFp64, int NCH>
+void dispatch_k(bool tma, const float* Q, uint32_t nq, uint32_t d, int metric, int k, int kk,
+                const FastTable& ft, const float* slab, const uint64_t* ids,
+                const ScanOut& out, int gx, cudaStream_t st) {
+#define LAIVG_SCAN(KPL)                                                                    \
+  do {                                                                                     \
+    if (tma) launch_tma_t<kFp64, KPL, NCH>(Q, nq, d, metric, k, kk, ft, slab, ids, out, gx, st); \
+    else launch_ldg_t<kFp64, KPL, NCH>(Q, nq, d, metric, k, kk, ft, slab, ids, out, gx, st);     \
+  } while (0)
+  if (kk <= 32) LAIVG_SCAN(1);
+  else if (kk <= 64) LAIVG_SCAN(2);
+  else if (kk <= 128) LAIVG_SCAN(4);
+  else LAIVG_SCAN(8);
+#undef LAIVG_SCAN
 }
 
 } // namespace
@@ -630,6 +1105,7 @@ std::atomic<uint64_t>& launch_counter() {
   static std::atomic<uint64_t> n{0};
   return n;
 }
+
 void launch_coarse_scores(const float* Q, uint32_t nq, const float* centroids,
                           uint32_t nc, uint32_t d, int metric, double* scores,
                           cudaStream_t st) {
@@ -643,7 +1119,6 @@ void launch_coarse_scores(const float* Q, uint32_t nq, const float* centroids,
     }
     coarse_scores_kernel<8><<<dim3((nc + warps - 1) / warps, (nq + 7) / 8), block, smem, st>>>(
         Q, nq, centroids, nc, d, metric, scores);
-    launch_counter()++;
   } else {
     const size_t smem = size_t(d) * sizeof(float);
     if (smem > 48 * 1024) {
@@ -652,23 +1127,35 @@ void launch_coarse_scores(const float* Q, uint32_t nq, const float* centroids,
     }
     coarse_scores_kernel<1><<<dim3((nc + warps - 1) / warps, nq), block, smem, st>>>(
         Q, nq, centroids, nc, d, metric, scores);
-    launch_counter()++;
   }
+  launch_counter()++;
 }
 
 void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
-                   uint32_t n_out, uint32_t* order, cudaStream_t st) {
-  uint32_t p2 = 1;
+                   uint32_t n_out, uint32_t* order, const int64_t* res_off,
+                   const uint64_t* list_off, const FastTable* ft, cudaStream_t st) {
+  uint32_t p2 = 32;
   while (p2 < nc) p2 <<= 1;
   const size_t smem = size_t(p2) * (sizeof(uint64_t) + sizeof(uint32_t));
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
-    attr = smem;
-  }
-  const int threads = p2 >= 2048 ? 1024 : (p2 >= 64 ? int(p2 / 2) : 32);
-  select_kernel<<<nq, threads, smem, st>>>(scores, nc, metric, p2, n_out, order);
+  const FastTable f = ft ? *ft : FastTable{};
+  const bool part = ft != nullptr;
+#define LAIVG_SELECT(E)                                                                     \
+  do {                                                                                      \
+    static size_t attr = 0;                                                                 \
+    if (smem > 48 * 1024 && smem > attr) {                                                  \
+      cudaFuncSetAttribute(select_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                           int(smem));                                                      \
+      attr = smem;                                                                          \
+    }                                                                                       \
+    select_kernel<E><<<nq, p2 / E, smem, st>>>(scores, nc, metric, p2, n_out, order, res_off, \
+                                               list_off, f, part);                          \
+  } while (0)
+  if (p2 <= 1024) LAIVG_SELECT(1);
+  else if (p2 == 2048) LAIVG_SELECT(2);
+  else if (p2 == 4096) LAIVG_SELECT(4);
+  else if (p2 == 8192) LAIVG_SELECT(8);
+  else LAIVG_SELECT(16);
+#undef LAIVG_SELECT
   launch_counter()++;
 }
 
@@ -679,23 +1166,30 @@ void launch_partition(const uint32_t* probe, uint32_t nq, uint32_t lp,
   launch_counter()++;
 }
 
-int scan_grid_x(uint32_t nq, int num_sms) {
-  const int ctas = 2 * num_sms; // 2 CTAs of 8 warps per SM
+int scan_grid_x(uint32_t nq, int num_sms, ScanImpl impl) {
+  const int ctas = impl == ScanImpl::kTma ? num_sms : 2 * num_sms;
   int gx = ctas / static_cast<int>(nq ? nq : 1);
   return gx < 1 ? 1 : gx;
+}
+
+int scan_kk(int k, bool acc_fp64) {
+  if (acc_fp64) return k;
+  return k + kRerankMargin < kMaxK ? k + kRerankMargin : kMaxK;
 }
 
 void launch_scan(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
                  const FastTable& ft, const float* slab_vecs,
                  const uint64_t* ids_all, const ScanOut& out, int grid_x,
-                 bool acc_fp64, cudaStream_t st) {
+                 bool acc_fp64, ScanImpl impl, cudaStream_t st) {
+  const int kk = scan_kk(k, acc_fp64);
+  const bool tma = impl == ScanImpl::kTma && (d % 4) == 0;
   const bool d768 = d == 768;
   if (acc_fp64) {
-    if (d768) launch_scan_k<double, 6>(Q, nq, d, metric, k, ft, slab_vecs, ids_all, out, grid_x, st);
-    else launch_scan_k<double, 0>(Q, nq, d, metric, k, ft, slab_vecs, ids_all, out, grid_x, st);
+    if (d768) dispatch_k<true, 6>(tma, Q, nq, d, metric, k, kk, ft, slab_vecs, ids_all, out, grid_x, st);
+    else dispatch_k<true, 0>(tma, Q, nq, d, metric, k, kk, ft, slab_vecs, ids_all, out, grid_x, st);
   } else {
-    if (d768) launch_scan_k<float, 6>(Q, nq, d, metric, k, ft, slab_vecs, ids_all, out, grid_x, st);
-    else launch_scan_k<float, 0>(Q, nq, d, metric, k, ft, slab_vecs, ids_all, out, grid_x, st);
+    if (d768) dispatch_k<false, 6>(tma, Q, nq, d, metric, k, kk, ft, slab_vecs, ids_all, out, grid_x, st);
+    else dispatch_k<false, 0>(tma, Q, nq, d, metric, k, kk, ft, slab_vecs, ids_all, out, grid_x, st);
   }
 }
 

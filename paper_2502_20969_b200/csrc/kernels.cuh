@@ -11,11 +11,12 @@ namespace laivg {
 // bench's gpu_launches).
 std::atomic<uint64_t>& launch_counter();
 
-constexpr int kMaxK = 256;           // device top-k limit (8 entries per lane)
+constexpr int kMaxK = 256;             // device top-k limit (8 entries per lane)
+constexpr int kRerankMargin = 16;      // extra fp32 survivors re-scored in fp64
 constexpr uint32_t kMaxSortNc = 16384; // on-chip full ranking limit
 
-// Per-query fast-list table produced by partition_kernel and consumed by the
-// scan: entry f of query q lives at [q * stride + f].
+// Per-query fast-list table produced by the partition step and consumed by
+// the scan: entry f of query q lives at [q * stride + f].
 struct FastTable {
   int64_t* slab;      // device-cache vector offset of the list
   uint64_t* row;      // host-store row offset of the list (id table index)
@@ -27,12 +28,18 @@ struct FastTable {
 };
 
 struct ScanOut {
-  float* part_s;      // [nq][grid][k] per-CTA partial top-k
+  float* part_s;      // [nq][grid][kk] per-CTA partial top-kk
   uint64_t* part_id;
+  uint32_t* part_vi;  // slab vector index of each partial entry (re-score)
   unsigned* ticket;   // [nq] last-CTA-done counters (self-resetting)
   float* out_s;       // [nq][k]
   uint64_t* out_id;   // [nq][k]
   uint32_t* out_count;// [nq]
+};
+
+enum class ScanImpl : int {
+  kTma = 0,      // cp.async.bulk (TMA) staged, warp-specialised (default)
+  kLdg = 1,      // direct 128-bit loads into registers
 };
 
 // Coarse: fp64 scores[nq][nc] of Q[nq][d] against centroids[nc][d]
@@ -42,9 +49,12 @@ void launch_coarse_scores(const float* Q, uint32_t nq, const float* centroids,
                           cudaStream_t st);
 // Full on-chip ranking of each query's scores, best-first with ascending
 // cluster id on ties (ivf.cpp:282-289); writes the first n_out entries of
-// each ranking to order[q * n_out + i]. nc <= kMaxSortNc.
+// each ranking to order[q * n_out + i]. nc <= kMaxSortNc. With `ft`, also
+// splits the first n_out entries by residency (fused partition).
 void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
-                   uint32_t n_out, uint32_t* order, cudaStream_t st);
+                   uint32_t n_out, uint32_t* order, const int64_t* res_off,
+                   const uint64_t* list_off, const FastTable* ft,
+                   cudaStream_t st);
 // Splits each query's probe (probe[q * lp + i], i < lp) by residency
 // (res_off[c] >= 0) preserving probe order; fills the fast table.
 void launch_partition(const uint32_t* probe, uint32_t nq, uint32_t lp,
@@ -55,8 +65,10 @@ void launch_partition(const uint32_t* probe, uint32_t nq, uint32_t lp,
 void launch_scan(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
                  const FastTable& ft, const float* slab_vecs,
                  const uint64_t* ids_all, const ScanOut& out, int grid_x,
-                 bool acc_fp64, cudaStream_t st);
-int scan_grid_x(uint32_t nq, int num_sms);
+                 bool acc_fp64, ScanImpl impl, cudaStream_t st);
+int scan_grid_x(uint32_t nq, int num_sms, ScanImpl impl);
+// Entries each per-CTA partial list holds for a given k (k + re-score margin).
+int scan_kk(int k, bool acc_fp64);
 // Generation-window stand-in: one CTA per SM spins on %globaltimer for ns.
 void launch_window(uint64_t ns, int num_sms, cudaStream_t st);
 

@@ -235,7 +235,7 @@ class Device:
 
     def __init__(self, ix: IvfIndex, capacity_bytes: int, device: int = 0,
                  miss_threads: int = 0, max_batch: int = 0, max_probe: int = 0,
-                 acc_fp64: bool = True):
+                 acc_fp64: bool = False, scan_impl: str = "tma"):
         L = lib()
         o = Opts()
         L.laivg_opts_default(C.byref(o))
@@ -245,6 +245,9 @@ class Device:
         o.max_batch = max_batch
         o.max_probe = max_probe
         o.acc_fp64 = 1 if acc_fp64 else 0
+        if scan_impl not in ("tma", "ldg"):
+            raise ValueError("scan_impl must be 'tma' or 'ldg'")
+        o.scan_impl = 0 if scan_impl == "tma" else 1
         h = C.c_void_p()
         check(L.laivg_ctx_create(ix.h, C.byref(o), C.byref(h)))
         self.h = h
