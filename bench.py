@@ -277,7 +277,7 @@ def run_ours(args, cfg):
     member = 4 * cfg["d"] + 8
     capacity = int(cfg["cache_frac"] * cfg["n_lists"]) * cfg["per_list"] * member
     dev = laiv.Device(ix, capacity, device=local if world > 1 else 0,
-                      acc_fp64=args.acc == "fp64")
+                      acc_fp64=args.acc == "fp64", scan_impl=args.scan)
     L, k = cfg["nprobe"], cfg["k"]
 
     # link bandwidth for the calibrate_budget rule, measured on this box
@@ -353,12 +353,12 @@ def run_ours(args, cfg):
         "metric": METRIC, "value": n_total / sum_v, "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum_v / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": f"f32 data, {args.acc} accumulate", "data": "synthetic (planted clusters, SURVEY §8d)",
+        "dtype": f"f32 data, {args.acc} accumulate" + (", fp64 re-score" if args.acc == "fp32" else ""), "data": "synthetic (planted clusters, SURVEY §8d)",
         "p50_latency_ms": float(np.median(lat_v) * 1e3),
         "p99_latency_ms": float(np.percentile(lat_v, 99) * 1e3),
         "pipeline_ms_per_step": wall / args.steps * 1e3,
         "config": config_block(cfg, args, sigma),
-        "roofline": {"kernel": "scan_kernel", "bound": "hbm", "achieved": achieved,
+        "roofline": {"kernel": f"scan_{args.scan}_kernel", "bound": "hbm", "achieved": achieved,
                      "peak": peak, "peak_kind": f"{peak_kind} copy (MEASURED_PEAKS.json hbm_gbs)",
                      "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None,
@@ -418,8 +418,11 @@ def main():
     ap.add_argument("--sigma", type=float, default=None)
     ap.add_argument("--cpu-sample", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--acc", default="fp64", choices=["fp64", "fp32"],
-                    help="scan accumulation: fp64 as the reference (default) or fp32 FMA")
+    ap.add_argument("--acc", default="fp32", choices=["fp64", "fp32"],
+                    help="scan accumulation: fp32 FMA + exact fp64 re-score of the survivors "
+                         "(default) or fp64 for every candidate")
+    ap.add_argument("--scan", default="tma", choices=["tma", "ldg"],
+                    help="scan kernel: TMA bulk-copy staged (default) or direct LDG")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.window is None:

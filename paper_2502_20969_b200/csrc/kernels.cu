@@ -34,8 +34,10 @@
 #include <cfloat>
 #include <cstdint>
 #include <cstdio>
+#include <string>
 #include <type_traits>
 
+#include "host.hpp"
 #include "kernels.cuh"
 
 namespace laivg {
@@ -45,6 +47,15 @@ constexpr int kIP = 0;
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// Counts the launch and surfaces launch-configuration errors immediately.
+void after_launch() {
+  launch_counter()++;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    throw CudaError(std::string("kernel launch failed: ") + cudaGetErrorString(e));
+  }
+}
 
 // --------------------------------------------------------------------------
 // scoring terms
@@ -1062,7 +1073,7 @@ void launch_tma_t(const float* Q, uint32_t nq, uint32_t d, int metric, int k, in
     attr = g.smem;
   }
   fn<<<dim3(gx, nq), kTmaThreads, g.smem, st>>>(Q, d, metric, k, kk, ft, slab, ids, out, g.T, g.S);
-  launch_counter()++;
+  after_launch();
 }
 
 template <bool kFp64, int KPL, int NCH>
@@ -1077,7 +1088,7 @@ void launch_ldg_t(const float* Q, uint32_t nq, uint32_t d, int metric, int k, in
     attr = smem;
   }
   fn<<<dim3(gx, nq), kScanThreads, smem, st>>>(Q, d, metric, k, kk, ft, slab, ids, out);
-  launch_counter()++;
+  after_launch();
 }
 
 template <bool kFp64, int NCH>
@@ -1128,7 +1139,7 @@ void launch_coarse_scores(const float* Q, uint32_t nq, const float* centroids,
     coarse_scores_kernel<1><<<dim3((nc + warps - 1) / warps, nq), block, smem, st>>>(
         Q, nq, centroids, nc, d, metric, scores);
   }
-  launch_counter()++;
+  after_launch();
 }
 
 void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
@@ -1142,7 +1153,7 @@ void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
 #define LAIVG_SELECT(E)                                                                     \
   do {                                                                                      \
     static size_t attr = 0;                                                                 \
-    if (smem > 48 * 1024 && smem > attr) {                                                  \
+    if (smem > attr) { /* dynamic + the partition statics may pass 48 KB */                \
       cudaFuncSetAttribute(select_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                            int(smem));                                                      \
       attr = smem;                                                                          \
@@ -1156,14 +1167,14 @@ void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
   else if (p2 == 8192) LAIVG_SELECT(8);
   else LAIVG_SELECT(16);
 #undef LAIVG_SELECT
-  launch_counter()++;
+  after_launch();
 }
 
 void launch_partition(const uint32_t* probe, uint32_t nq, uint32_t lp,
                       const int64_t* res_off, const uint64_t* list_off,
                       FastTable ft, cudaStream_t st) {
   partition_kernel<<<nq, 256, 0, st>>>(probe, lp, res_off, list_off, ft);
-  launch_counter()++;
+  after_launch();
 }
 
 int scan_grid_x(uint32_t nq, int num_sms, ScanImpl impl) {
@@ -1195,7 +1206,7 @@ void launch_scan(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
 
 void launch_window(uint64_t ns, int num_sms, cudaStream_t st) {
   window_kernel<<<num_sms, 32, 0, st>>>(ns);
-  launch_counter()++;
+  after_launch();
 }
 
 } // namespace laivg

@@ -184,3 +184,24 @@ def test_ties_break_by_id(orc, laiv):
         res, _ = laiv.hybrid_search(dev, q, 4, 40)
         want = orc.ivf_search(cen, vecs, ids, off, metric, q, 4, 40)
         assert_topk_parity(metric, res.topk.ids, res.topk.scores, *want, exact=True)
+
+
+@pytest.mark.parametrize("nc", [1, 3, 33, 1000, 2048, 4096, 5000, 8192, 16384])
+def test_rank_clusters_all_sort_sizes(orc, laiv, nc):
+    # every on-chip sort geometry (1..16 elements per thread) vs the oracle
+    rng = np.random.default_rng(nc)
+    d = 64
+    cen = rng.standard_normal((nc, d)).astype(np.float32)
+    cen[nc // 2] = cen[0]  # an exact tie: must order by ascending cluster id
+    vecs = rng.standard_normal((nc, d)).astype(np.float32)
+    off = np.arange(nc + 1, dtype=np.uint64)
+    for metric in (L2, IP):
+        ix = laiv.IvfIndex(cen, vecs, np.arange(nc, dtype=np.uint64), off, laiv.Metric(metric))
+        dev = laiv.Device(ix, 1 << 24)
+        Q = rng.standard_normal((3, d)).astype(np.float32)
+        got = laiv.rank_clusters(dev, Q)
+        for t in range(3):
+            assert np.array_equal(got[t], orc.rank_clusters(cen, metric, Q[t]))
+        probe = laiv.coarse_probe(dev, Q, 17)
+        for t in range(3):
+            assert np.array_equal(probe[t], orc.coarse_probe(cen, metric, Q[t], 17))
