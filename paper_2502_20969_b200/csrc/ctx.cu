@@ -146,6 +146,8 @@ struct Ctx {
   float* d_Q = nullptr;
   double* d_scores = nullptr;
   uint32_t* d_order = nullptr;
+  uint64_t* d_run_k = nullptr;  // selection scratch (sorted runs)
+  uint32_t* d_run_v = nullptr;
   FastTable ft{};
   ScanOut so{};
   int part_cap = 0; // partial top-k rows available (CTAs x queries)
@@ -213,7 +215,7 @@ Ctx::~Ctx() {
   if (aux) cudaStreamSynchronize(aux);
   for (void* p : {(void*)d_cen, (void*)d_list_off, (void*)d_ids, (void*)d_res,
                   (void*)d_slab, (void*)d_tmp, (void*)d_Q, (void*)d_scores,
-                  (void*)d_order, (void*)ft.slab, (void*)ft.row, (void*)ft.len,
+                  (void*)d_order, (void*)d_run_k, (void*)d_run_v, (void*)ft.slab, (void*)ft.row, (void*)ft.len,
                   (void*)ft.cluster, (void*)ft.pre, (void*)ft.count,
                   (void*)so.part_s, (void*)so.part_id, (void*)so.part_vi, (void*)so.ticket,
                   (void*)so.out_s, (void*)so.out_id, (void*)so.out_count,
@@ -302,6 +304,8 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   d_Q = dev_alloc<float>(size_t(max_batch) * d);
   d_scores = dev_alloc<double>(size_t(max_batch) * nc);
   d_order = dev_alloc<uint32_t>(size_t(max_batch) * std::max(nc, 1u));
+  d_run_k = dev_alloc<uint64_t>(select_scratch_entries(max_batch, nc));
+  d_run_v = dev_alloc<uint32_t>(select_scratch_entries(max_batch, nc));
   ft.stride = max_probe;
   ft.slab = dev_alloc<int64_t>(size_t(max_batch) * max_probe);
   ft.row = dev_alloc<uint64_t>(size_t(max_batch) * max_probe);
@@ -412,7 +416,8 @@ void Ctx::clear_store() {
 
 void Ctx::coarse(const float* dQ, uint32_t nq, uint32_t n_out, cudaStream_t st) {
   launch_coarse_scores(dQ, nq, d_cen, ix->nc, ix->d, ix->metric, d_scores, st);
-  launch_select(d_scores, nq, ix->nc, ix->metric, n_out, d_order, nullptr, nullptr, nullptr,
+  launch_select(d_scores, nq, ix->nc, ix->metric, n_out, d_order, d_run_k, d_run_v, nullptr,
+                nullptr, nullptr,
                 st);
 }
 
@@ -454,7 +459,8 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
   } else {
     // coarse scores, then ranking + residency split fused in one CTA
     launch_coarse_scores(dq, 1, d_cen, ix->nc, ix->d, ix->metric, d_scores, comp);
-    launch_select(d_scores, 1, ix->nc, ix->metric, lp, d_order, d_res, d_list_off, &ft, comp);
+    launch_select(d_scores, 1, ix->nc, ix->metric, lp, d_order, d_run_k, d_run_v, d_res,
+                  d_list_off, &ft, comp);
     CK(cudaEventRecord(ev_b, comp));
     if (lp) {
       CK(cudaStreamWaitEvent(aux, ev_b, 0));

@@ -540,40 +540,103 @@ __device__ void block_bitonic_sort(uint64_t (&k)[E], uint32_t (&v)[E], uint64_t*
   }
 }
 
-// One CTA per query; blockDim * E = p2 (power of two >= nc, >= 32).
-template <int E>
+// Selection runs in two kernels so that no single SM sorts the whole ranking:
+//   seg_sort_kernel   — CTA (s, q) sorts the 256 scores of segment s of query
+//                       q (register/shuffle/smem bitonic) into a sorted run;
+//   merge_runs_kernel — one CTA per query merges the runs pairwise with the
+//                       bitonic min/max construction (C = min(A_i, B_{m-1-i})
+//                       holds the m smallest of A u B as a bitonic sequence),
+//                       keeping only the best P >= n_out per run when the
+//                       caller needs a prefix (coarse_probe) and every entry
+//                       when it needs the full ranking (rank_clusters).
+constexpr uint32_t kSeg = 256;
+
+__global__ void __launch_bounds__(kSeg)
+    seg_sort_kernel(const double* __restrict__ scores, uint32_t nc, int metric,
+                    uint64_t* __restrict__ run_k, uint32_t* __restrict__ run_v,
+                    uint32_t nseg_pad) {
+  __shared__ uint64_t sk[kSeg];
+  __shared__ uint32_t sv[kSeg];
+  const uint32_t q = blockIdx.y, s = blockIdx.x;
+  const uint32_t i = s * kSeg + threadIdx.x;
+  uint64_t k[1];
+  uint32_t v[1];
+  if (i < nc) {
+    k[0] = order_key(scores[static_cast<uint64_t>(q) * nc + i], metric);
+    v[0] = i;
+  } else {
+    k[0] = ~0ull;
+    v[0] = ~0u;
+  }
+  block_bitonic_sort<1>(k, v, sk, sv, kSeg);
+  const uint64_t o = (static_cast<uint64_t>(q) * nseg_pad + s) * kSeg + threadIdx.x;
+  run_k[o] = k[0];
+  run_v[o] = v[0];
+}
+
+__device__ __forceinline__ void cswap_up(uint64_t* k, uint32_t* v, uint32_t a, uint32_t b) {
+  // ascending compare-exchange of positions a < b
+  if (kv_gt(k[a], v[a], k[b], v[b])) {
+    const uint64_t tk = k[a];
+    k[a] = k[b];
+    k[b] = tk;
+    const uint32_t tv = v[a];
+    v[a] = v[b];
+    v[b] = tv;
+  }
+}
+
+// nseg_pad runs of kSeg sorted entries per query (power of two, sentinel
+// padded); P = run length kept per level (power of two, <= kSeg) or kSeg with
+// `full` to keep everything.
 __global__ void __launch_bounds__(1024)
-    select_kernel(const double* __restrict__ scores, uint32_t nc, int metric, uint32_t p2,
-                  uint32_t n_out, uint32_t* __restrict__ order, const int64_t* res_off,
-                  const uint64_t* list_off, FastTable ft, bool do_partition) {
-  extern __shared__ uint64_t sk[];
-  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + p2);
+    merge_runs_kernel(const uint64_t* __restrict__ run_k, const uint32_t* __restrict__ run_v,
+                      uint32_t nseg_pad, uint32_t P, bool full, uint32_t n_out,
+                      uint32_t* __restrict__ order, const int64_t* res_off,
+                      const uint64_t* list_off, FastTable ft, bool do_partition) {
+  extern __shared__ uint64_t mk[];
+  const uint32_t total = nseg_pad * P;
+  uint32_t* mv = reinterpret_cast<uint32_t*>(mk + total);
   const uint32_t q = blockIdx.x;
-  const double* sc = scores + static_cast<uint64_t>(q) * nc;
-  uint64_t k[E];
-  uint32_t v[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const uint32_t i = threadIdx.x * E + e;
-    if (i < nc) {
-      k[e] = order_key(sc[i], metric);
-      v[e] = i;
-    } else {
-      k[e] = ~0ull;
-      v[e] = ~0u;
+  const uint64_t base = static_cast<uint64_t>(q) * nseg_pad * kSeg;
+  for (uint32_t x = threadIdx.x; x < total; x += blockDim.x) {
+    const uint32_t r = x / P, i = x % P;
+    mk[x] = run_k[base + static_cast<uint64_t>(r) * kSeg + i];
+    mv[x] = run_v[base + static_cast<uint64_t>(r) * kSeg + i];
+  }
+  __syncthreads();
+  uint32_t nruns = nseg_pad, stride = P, m = P;
+  while (nruns > 1) {
+    const uint32_t pairs = nruns / 2;
+    // min/max pass: A[i] <-> B[m-1-i]
+    for (uint32_t x = threadIdx.x; x < pairs * m; x += blockDim.x) {
+      const uint32_t p = x / m, i = x % m;
+      const uint32_t a = p * 2 * stride + i, b = p * 2 * stride + stride + (m - 1 - i);
+      cswap_up(mk, mv, a, b);
     }
+    __syncthreads();
+    // bitonic clean of the low half (and of the high half in full mode)
+    const uint32_t halves = full ? 2 : 1;
+    for (uint32_t j = m >> 1; j > 0; j >>= 1) {
+      for (uint32_t x = threadIdx.x; x < pairs * halves * (m / 2); x += blockDim.x) {
+        const uint32_t per = m / 2;
+        const uint32_t hp = x / per, t = x % per;
+        const uint32_t p = hp / halves, h = hp % halves;
+        const uint32_t lo = (t / j) * 2 * j + (t % j);
+        const uint32_t o = p * 2 * stride + h * stride;
+        cswap_up(mk, mv, o + lo, o + lo + j);
+      }
+      __syncthreads();
+    }
+    nruns = pairs;
+    stride *= 2;
+    if (full) m *= 2;
   }
-  block_bitonic_sort<E>(k, v, sk, sv, p2);
   uint32_t* out = order + static_cast<uint64_t>(q) * n_out;
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const uint32_t i = threadIdx.x * E + e;
-    if (i < n_out) out[i] = v[e];
-    sv[i] = v[e];
-  }
+  for (uint32_t i = threadIdx.x; i < n_out; i += blockDim.x) out[i] = mv[i];
   if (do_partition) {
     __syncthreads();
-    partition_block(sv, n_out, res_off, list_off, ft, q);
+    partition_block(mv, n_out, res_off, list_off, ft, q);
   }
 }
 
@@ -606,7 +669,7 @@ template <int KPL>
 __device__ void scan_epilogue(WarpTopK<KPL>& top, int metric, int k, int kk, bool rerank,
                               MergeSmem m, const ScanOut& out, const float* sq,
                               const float* __restrict__ slab, uint32_t d, uint64_t V,
-                              int first, int nw, bool* am_last) {
+                              int first, int nw, size_t merge_cap, bool* am_last) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t q = blockIdx.y;
   const bool holder = warp >= first && warp < first + nw;
@@ -631,14 +694,38 @@ __device__ void scan_epilogue(WarpTopK<KPL>& top, int metric, int k, int kk, boo
   // ---- grid merge in the last CTA ----
   __threadfence();
   const uint64_t pbase = static_cast<uint64_t>(q) * gridDim.x * kk;
-  if (holder) {
-    top.init(metric);
-    for (uint32_t g = w; g < gridDim.x; g += nw) {
-      top.template merge_list<true>(metric, kk, out.part_s + pbase + g * kk,
-                                    out.part_id + pbase + g * kk,
-                                    out.part_vi + pbase + g * kk, kk);
+  const size_t nparts = static_cast<size_t>(gridDim.x) * kk;
+  if (nparts * 16 + 16 <= merge_cap) {
+    // stage every partial list in shared memory with coalesced loads, then
+    // merge on-chip (one L2 round trip instead of one per list)
+    float* gs = m.s;
+    uint64_t* gid = reinterpret_cast<uint64_t*>(
+        (reinterpret_cast<uintptr_t>(gs + nparts) + 7) & ~uintptr_t(7));
+    uint32_t* gvi = reinterpret_cast<uint32_t*>(gid + nparts);
+    for (size_t x = threadIdx.x; x < nparts; x += blockDim.x) {
+      gs[x] = __ldcg(out.part_s + pbase + x);
+      gid[x] = __ldcg(reinterpret_cast<const unsigned long long*>(out.part_id + pbase) + x);
+      gvi[x] = __ldcg(out.part_vi + pbase + x);
     }
-    top.store(kk, m.s + w * kk, m.id + w * kk, m.vi + w * kk);
+    __syncthreads();
+    if (holder) {
+      top.init(metric);
+      for (uint32_t g = w; g < gridDim.x; g += nw) {
+        top.template merge_list<false>(metric, kk, gs + g * kk, gid + g * kk, gvi + g * kk, kk);
+      }
+    }
+    __syncthreads();
+    if (holder) top.store(kk, m.s + w * kk, m.id + w * kk, m.vi + w * kk);
+  } else {
+    if (holder) {
+      top.init(metric);
+      for (uint32_t g = w; g < gridDim.x; g += nw) {
+        top.template merge_list<true>(metric, kk, out.part_s + pbase + g * kk,
+                                      out.part_id + pbase + g * kk,
+                                      out.part_vi + pbase + g * kk, kk);
+      }
+      top.store(kk, m.s + w * kk, m.id + w * kk, m.vi + w * kk);
+    }
   }
   __syncthreads();
   if (warp == first) {
@@ -652,9 +739,43 @@ __device__ void scan_epilogue(WarpTopK<KPL>& top, int metric, int k, int kk, boo
   if (rerank) {
     // exact fp64 re-score of the survivors, then re-rank on (score, id)
     if (holder) {
-      for (int c = w; c < navail; c += nw) {
-        const float es = exact_score(slab, m.vi[c], sq, d, metric);
-        if (lane == 0) m.s[c] = es;
+      // up to four candidates per warp with their loads in flight together
+      for (int c0 = w; c0 < navail; c0 += 4 * nw) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        const float* rows[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + u * nw;
+          rows[u] = slab + static_cast<uint64_t>(c < navail ? m.vi[c] : m.vi[c0]) * d;
+        }
+        if ((d & 3u) == 0) {
+          const uint32_t d4 = d >> 2;
+#pragma unroll 2
+          for (uint32_t j4 = lane; j4 < d4; j4 += 32) {
+            float4 x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = __ldg(reinterpret_cast<const float4*>(rows[u]) + j4);
+            const float4 qq = reinterpret_cast<const float4*>(sq)[j4];
+            const double q4[4] = {qq.x, qq.y, qq.z, qq.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) Acc4<true>::run(metric, q4, x[u], acc[u]);
+          }
+        } else {
+          for (uint32_t j = lane; j < d; j += 32) {
+            const double qj = sq[j];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              acc[u] = metric == kIP ? term_ip_d(qj, __ldg(rows[u] + j), acc[u])
+                                     : term_l2_d(qj, __ldg(rows[u] + j), acc[u]);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double t = warp_sum(acc[u]);
+          const int c = c0 + u * nw;
+          if (lane == 0 && c < navail) m.s[c] = finish_score<double>(metric, t);
+        }
       }
     }
     __syncthreads();
@@ -893,7 +1014,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   m.id = reinterpret_cast<uint64_t*>(
       (reinterpret_cast<uintptr_t>(m.s + kConsumers * kk) + 7) & ~uintptr_t(7));
   m.vi = reinterpret_cast<uint32_t*>(m.id + kConsumers * kk);
-  scan_epilogue<KPL>(top, metric, k, kk, !kFp64, m, out, sq, slab, d, V, 1, kConsumers,
+  scan_epilogue<KPL>(top, metric, k, kk, !kFp64, m, out, sq, slab, d, V, 1, kConsumers, off,
                      &am_last);
 }
 
@@ -1020,6 +1141,7 @@ __global__ void __launch_bounds__(kScanThreads, 2)
   }
   MergeSmem m{ms, mid, mvi};
   scan_epilogue<KPL>(top, metric, k, kk, !kFp64, m, out, sq, slab_vecs, d, V, 0, kScanWarps,
+                     size_t(kScanWarps) * kk * 16,
                      &am_last);
 }
 
@@ -1142,31 +1264,41 @@ void launch_coarse_scores(const float* Q, uint32_t nq, const float* centroids,
   after_launch();
 }
 
+uint32_t select_runs(uint32_t nc) {
+  uint32_t nseg = (nc + kSeg - 1) / kSeg, pad = 1;
+  while (pad < nseg) pad <<= 1;
+  return pad;
+}
+
+size_t select_scratch_entries(uint32_t nq, uint32_t nc) {
+  return size_t(nq) * select_runs(nc) * kSeg;
+}
+
 void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
-                   uint32_t n_out, uint32_t* order, const int64_t* res_off,
-                   const uint64_t* list_off, const FastTable* ft, cudaStream_t st) {
-  uint32_t p2 = 32;
-  while (p2 < nc) p2 <<= 1;
-  const size_t smem = size_t(p2) * (sizeof(uint64_t) + sizeof(uint32_t));
+                   uint32_t n_out, uint32_t* order, uint64_t* run_k, uint32_t* run_v,
+                   const int64_t* res_off, const uint64_t* list_off, const FastTable* ft,
+                   cudaStream_t st) {
+  const uint32_t nseg_pad = select_runs(nc);
+  seg_sort_kernel<<<dim3(nseg_pad, nq), kSeg, 0, st>>>(scores, nc, metric, run_k, run_v,
+                                                       nseg_pad);
+  after_launch();
+  // keep the best P per run when only a prefix is needed
+  const bool full = n_out > kSeg;
+  uint32_t P = kSeg;
+  if (!full) {
+    P = 1;
+    while (P < n_out) P <<= 1;
+  }
+  const size_t smem = size_t(nseg_pad) * P * (sizeof(uint64_t) + sizeof(uint32_t));
+  static size_t attr = 0;
+  if (smem > attr) { // dynamic + the partition statics may pass 48 KB
+    cudaFuncSetAttribute(merge_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    attr = smem;
+  }
   const FastTable f = ft ? *ft : FastTable{};
-  const bool part = ft != nullptr;
-#define LAIVG_SELECT(E)                                                                     \
-  do {                                                                                      \
-    static size_t attr = 0;                                                                 \
-    if (smem > attr) { /* dynamic + the partition statics may pass 48 KB */                \
-      cudaFuncSetAttribute(select_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                           int(smem));                                                      \
-      attr = smem;                                                                          \
-    }                                                                                       \
-    select_kernel<E><<<nq, p2 / E, smem, st>>>(scores, nc, metric, p2, n_out, order, res_off, \
-                                               list_off, f, part);                          \
-  } while (0)
-  if (p2 <= 1024) LAIVG_SELECT(1);
-  else if (p2 == 2048) LAIVG_SELECT(2);
-  else if (p2 == 4096) LAIVG_SELECT(4);
-  else if (p2 == 8192) LAIVG_SELECT(8);
-  else LAIVG_SELECT(16);
-#undef LAIVG_SELECT
+  merge_runs_kernel<<<nq, 1024, smem, st>>>(run_k, run_v, nseg_pad, P, full, n_out, order,
+                                            res_off, list_off, f, ft != nullptr);
   after_launch();
 }
 

@@ -51,10 +51,12 @@ void launch_coarse_scores(const float* Q, uint32_t nq, const float* centroids,
 // cluster id on ties (ivf.cpp:282-289); writes the first n_out entries of
 // each ranking to order[q * n_out + i]. nc <= kMaxSortNc. With `ft`, also
 // splits the first n_out entries by residency (fused partition).
+// run_k / run_v: scratch of select_scratch_entries(nq, nc) entries.
 void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
-                   uint32_t n_out, uint32_t* order, const int64_t* res_off,
-                   const uint64_t* list_off, const FastTable* ft,
+                   uint32_t n_out, uint32_t* order, uint64_t* run_k, uint32_t* run_v,
+                   const int64_t* res_off, const uint64_t* list_off, const FastTable* ft,
                    cudaStream_t st);
+size_t select_scratch_entries(uint32_t nq, uint32_t nc);
 // Splits each query's probe (probe[q * lp + i], i < lp) by residency
 // (res_off[c] >= 0) preserving probe order; fills the fast table.
 void launch_partition(const uint32_t* probe, uint32_t nq, uint32_t lp,
