@@ -333,7 +333,31 @@ __global__ void __launch_bounds__(256)
   double acc[QT];
 #pragma unroll
   for (int t = 0; t < QT; ++t) acc[t] = 0.0;
-  if ((d & 3u) == 0) {
+  if ((d & 3u) == 0 && d <= 1024) {
+    // all of the row's loads in flight before any math (d <= 1024: <= 8 per lane)
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    const uint32_t d4 = d >> 2;
+    float4 xs[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t j = lane + 32u * c;
+      xs[c] = j < d4 ? __ldg(r4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t j = lane + 32u * c;
+      if (j < d4) {
+#pragma unroll
+        for (int t = 0; t < QT; ++t) {
+          if (t < nqt) {
+            const float4 qq = reinterpret_cast<const float4*>(sq + t * d)[j];
+            const double qd[4] = {qq.x, qq.y, qq.z, qq.w};
+            Acc4<true>::run(metric, qd, xs[c], acc[t]);
+          }
+        }
+      }
+    }
+  } else if ((d & 3u) == 0) {
     const float4* r4 = reinterpret_cast<const float4*>(row);
     for (uint32_t j = lane; j < d / 4; j += 32) {
       const float4 x = __ldg(r4 + j);
@@ -599,38 +623,40 @@ __global__ void __launch_bounds__(1024)
   uint32_t* mv = reinterpret_cast<uint32_t*>(mk + total);
   const uint32_t q = blockIdx.x;
   const uint64_t base = static_cast<uint64_t>(q) * nseg_pad * kSeg;
+  // every size here is a power of two: index with shifts and masks
+  const uint32_t lP = __ffs(P) - 1;
   for (uint32_t x = threadIdx.x; x < total; x += blockDim.x) {
-    const uint32_t r = x / P, i = x % P;
+    const uint32_t r = x >> lP, i = x & (P - 1);
     mk[x] = run_k[base + static_cast<uint64_t>(r) * kSeg + i];
     mv[x] = run_v[base + static_cast<uint64_t>(r) * kSeg + i];
   }
   __syncthreads();
-  uint32_t nruns = nseg_pad, stride = P, m = P;
+  uint32_t nruns = nseg_pad, ls = lP, lm = lP;
   while (nruns > 1) {
-    const uint32_t pairs = nruns / 2;
+    const uint32_t pairs = nruns >> 1, m = 1u << lm, stride = 1u << ls;
     // min/max pass: A[i] <-> B[m-1-i]
-    for (uint32_t x = threadIdx.x; x < pairs * m; x += blockDim.x) {
-      const uint32_t p = x / m, i = x % m;
-      const uint32_t a = p * 2 * stride + i, b = p * 2 * stride + stride + (m - 1 - i);
+    for (uint32_t x = threadIdx.x; x < (pairs << lm); x += blockDim.x) {
+      const uint32_t p = x >> lm, i = x & (m - 1);
+      const uint32_t a = (p << (ls + 1)) + i, b = (p << (ls + 1)) + stride + (m - 1 - i);
       cswap_up(mk, mv, a, b);
     }
     __syncthreads();
     // bitonic clean of the low half (and of the high half in full mode)
-    const uint32_t halves = full ? 2 : 1;
-    for (uint32_t j = m >> 1; j > 0; j >>= 1) {
-      for (uint32_t x = threadIdx.x; x < pairs * halves * (m / 2); x += blockDim.x) {
-        const uint32_t per = m / 2;
-        const uint32_t hp = x / per, t = x % per;
-        const uint32_t p = hp / halves, h = hp % halves;
-        const uint32_t lo = (t / j) * 2 * j + (t % j);
-        const uint32_t o = p * 2 * stride + h * stride;
+    const uint32_t lh = full ? 1 : 0, lper = lm - 1;
+    for (uint32_t lj = lm; lj-- > 0;) {
+      const uint32_t j = 1u << lj;
+      for (uint32_t x = threadIdx.x; x < (pairs << (lh + lper)); x += blockDim.x) {
+        const uint32_t hp = x >> lper, t = x & ((1u << lper) - 1);
+        const uint32_t p = hp >> lh, h = hp & lh;
+        const uint32_t lo = ((t >> lj) << (lj + 1)) + (t & (j - 1));
+        const uint32_t o = (p << (ls + 1)) + (h << ls);
         cswap_up(mk, mv, o + lo, o + lo + j);
       }
       __syncthreads();
     }
     nruns = pairs;
-    stride *= 2;
-    if (full) m *= 2;
+    ++ls;
+    if (full) ++lm;
   }
   uint32_t* out = order + static_cast<uint64_t>(q) * n_out;
   for (uint32_t i = threadIdx.x; i < n_out; i += blockDim.x) out[i] = mv[i];
@@ -1297,7 +1323,9 @@ void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
     attr = smem;
   }
   const FastTable f = ft ? *ft : FastTable{};
-  merge_runs_kernel<<<nq, 1024, smem, st>>>(run_k, run_v, nseg_pad, P, full, n_out, order,
+  const uint32_t total = nseg_pad * P;
+  const uint32_t threads = std::min<uint32_t>(1024, std::max<uint32_t>(256, (total / 2 + 31) & ~31u));
+  merge_runs_kernel<<<nq, threads, smem, st>>>(run_k, run_v, nseg_pad, P, full, n_out, order,
                                             res_off, list_off, f, ft != nullptr);
   after_launch();
 }
