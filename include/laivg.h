@@ -105,7 +105,10 @@ typedef struct {
                               1: every candidate accumulated in fp64 */
   uint32_t scan_impl;      /* 0 (default): TMA bulk-copy staged scan;
                               1: direct 128-bit register loads */
-  uint32_t reserved[7];
+  uint32_t tma_tile;       /* vectors per TMA stage; 0 = auto (~48 KB) */
+  uint32_t tma_stages;     /* TMA ring depth; 0 = auto (~192 KB ring) */
+  uint32_t ctas_per_sm;    /* scan CTAs per SM; 0 = auto */
+  uint32_t reserved[4];
 } laivg_opts;
 void laivg_opts_default(laivg_opts* o);
 typedef struct laivg_ctx laivg_ctx;

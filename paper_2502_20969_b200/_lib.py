@@ -30,7 +30,8 @@ P = C.POINTER
 class Opts(C.Structure):
     _fields_ = [("device", i32), ("capacity_bytes", u64), ("miss_threads", u32),
                 ("max_batch", u32), ("max_probe", u32), ("acc_fp64", u32),
-                ("scan_impl", u32), ("reserved", u32 * 7)]
+                ("scan_impl", u32), ("tma_tile", u32), ("tma_stages", u32),
+                ("ctas_per_sm", u32), ("reserved", u32 * 4)]
 
 
 class Channel(C.Structure):

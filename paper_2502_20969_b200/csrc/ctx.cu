@@ -119,6 +119,7 @@ struct Ctx {
   int sms = 148;
   bool acc_fp64 = false;
   ScanImpl scan_impl = ScanImpl::kTma;
+  ScanTune tune{};
   cudaStream_t comp = nullptr, copy = nullptr, aux = nullptr;
 
   // static device data
@@ -258,6 +259,10 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   acc_fp64 = o.acc_fp64 != 0;
   if (o.scan_impl > 1) throw std::invalid_argument("scan_impl must be 0 (TMA) or 1 (LDG)");
   scan_impl = static_cast<ScanImpl>(o.scan_impl);
+  tune.tile = o.tma_tile;
+  tune.stages = o.tma_stages;
+  tune.ctas_per_sm = o.ctas_per_sm;
+  if (o.ctas_per_sm > 16) throw std::invalid_argument("ctas_per_sm must be <= 16");
   if (ix->nc > kMaxSortNc) {
     throw std::invalid_argument("device coarse ranking supports up to " +
                                 std::to_string(kMaxSortNc) + " clusters");
@@ -313,7 +318,8 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   ft.cluster = dev_alloc<uint32_t>(size_t(max_batch) * max_probe);
   ft.pre = dev_alloc<uint64_t>(size_t(max_batch) * (max_probe + 1));
   ft.count = dev_alloc<uint32_t>(max_batch);
-  part_cap = std::max<int>(2 * sms, int(max_batch)) + 2 * sms;
+  const int per_sm = std::max<int>(2, int(tune.ctas_per_sm));
+  part_cap = std::max<int>(per_sm * sms, int(max_batch)) + per_sm * sms;
   so.part_s = dev_alloc<float>(size_t(part_cap) * kMaxK);
   so.part_id = dev_alloc<uint64_t>(size_t(part_cap) * kMaxK);
   so.part_vi = dev_alloc<uint32_t>(size_t(part_cap) * kMaxK);
@@ -470,7 +476,8 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
   }
   CK(cudaEventRecord(ev_p, comp));
   launch_scan(dq, 1, ix->d, ix->metric, k, ft, d_slab, d_ids, so,
-              std::min(scan_grid_x(1, sms, scan_impl), part_cap), acc_fp64, scan_impl, comp);
+              std::min(scan_grid_x(1, sms, scan_impl, tune), part_cap), acc_fp64, scan_impl,
+              tune, comp);
   CK(cudaEventRecord(ev_s, comp));
   CK(cudaMemcpyAsync(h_out_s, so.out_s, k * sizeof(float), cudaMemcpyDeviceToHost, comp));
   CK(cudaMemcpyAsync(h_out_id, so.out_id, k * sizeof(uint64_t), cudaMemcpyDeviceToHost, comp));

@@ -1194,12 +1194,15 @@ struct TmaGeom {
   size_t smem;
 };
 
-TmaGeom tma_geom(uint32_t d, int kk) {
+TmaGeom tma_geom(uint32_t d, int kk, const ScanTune& tune) {
   const size_t row = size_t(d) * 4;
   TmaGeom g;
-  g.T = static_cast<uint32_t>(std::max<size_t>(1, std::min<size_t>(32, 49152 / row)));
+  g.T = tune.tile ? tune.tile
+                  : static_cast<uint32_t>(std::max<size_t>(1, std::min<size_t>(32, 49152 / row)));
   const size_t stage = g.T * row;
-  g.S = static_cast<uint32_t>(std::max<size_t>(2, std::min<size_t>(8, 196608 / stage)));
+  g.S = tune.stages
+            ? tune.stages
+            : static_cast<uint32_t>(std::max<size_t>(2, std::min<size_t>(8, 196608 / stage)));
   size_t off = (g.S * stage + 127) & ~size_t(127);
   const size_t merge = size_t(kConsumers) * kk * 16;
   if (off < merge) off = (merge + 127) & ~size_t(127);
@@ -1212,8 +1215,9 @@ TmaGeom tma_geom(uint32_t d, int kk) {
 template <bool kFp64, int KPL, int NCH>
 void launch_tma_t(const float* Q, uint32_t nq, uint32_t d, int metric, int k, int kk,
                   const FastTable& ft, const float* slab, const uint64_t* ids,
-                  const ScanOut& out, int gx, cudaStream_t st) {
-  const TmaGeom g = tma_geom(d, kk);
+                  const ScanOut& out, int gx, const ScanTune& tune, cudaStream_t st) {
+  const TmaGeom g = tma_geom(d, kk, tune);
+  if (g.smem > 227 * 1024) throw CudaError("TMA ring does not fit shared memory");
   auto fn = scan_tma_kernel<kFp64, KPL, NCH>;
   static size_t attr = 0;
   if (g.smem > attr) {
@@ -1242,10 +1246,10 @@ void launch_ldg_t(const float* Q, uint32_t nq, uint32_t d, int metric, int k, in
 template <bool kFp64, int NCH>
 void dispatch_k(bool tma, const float* Q, uint32_t nq, uint32_t d, int metric, int k, int kk,
                 const FastTable& ft, const float* slab, const uint64_t* ids,
-                const ScanOut& out, int gx, cudaStream_t st) {
+                const ScanOut& out, int gx, const ScanTune& tune, cudaStream_t st) {
 #define LAIVG_SCAN(KPL)                                                                    \
   do {                                                                                     \
-    if (tma) launch_tma_t<kFp64, KPL, NCH>(Q, nq, d, metric, k, kk, ft, slab, ids, out, gx, st); \
+    if (tma) launch_tma_t<kFp64, KPL, NCH>(Q, nq, d, metric, k, kk, ft, slab, ids, out, gx, tune, st); \
     else launch_ldg_t<kFp64, KPL, NCH>(Q, nq, d, metric, k, kk, ft, slab, ids, out, gx, st);     \
   } while (0)
   if (kk <= 32) LAIVG_SCAN(1);
@@ -1337,9 +1341,10 @@ void launch_partition(const uint32_t* probe, uint32_t nq, uint32_t lp,
   after_launch();
 }
 
-int scan_grid_x(uint32_t nq, int num_sms, ScanImpl impl) {
-  const int ctas = impl == ScanImpl::kTma ? num_sms : 2 * num_sms;
-  int gx = ctas / static_cast<int>(nq ? nq : 1);
+int scan_grid_x(uint32_t nq, int num_sms, ScanImpl impl, const ScanTune& tune) {
+  const int per_sm = tune.ctas_per_sm ? static_cast<int>(tune.ctas_per_sm)
+                                      : (impl == ScanImpl::kTma ? 1 : 2);
+  int gx = per_sm * num_sms / static_cast<int>(nq ? nq : 1);
   return gx < 1 ? 1 : gx;
 }
 
@@ -1351,17 +1356,20 @@ int scan_kk(int k, bool acc_fp64) {
 void launch_scan(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
                  const FastTable& ft, const float* slab_vecs,
                  const uint64_t* ids_all, const ScanOut& out, int grid_x,
-                 bool acc_fp64, ScanImpl impl, cudaStream_t st) {
+                 bool acc_fp64, ScanImpl impl, const ScanTune& tune, cudaStream_t st) {
   const int kk = scan_kk(k, acc_fp64);
   const bool tma = impl == ScanImpl::kTma && (d % 4) == 0;
   const bool d768 = d == 768;
+#define LAIVG_D(F64, NCH) \
+  dispatch_k<F64, NCH>(tma, Q, nq, d, metric, k, kk, ft, slab_vecs, ids_all, out, grid_x, tune, st)
   if (acc_fp64) {
-    if (d768) dispatch_k<true, 6>(tma, Q, nq, d, metric, k, kk, ft, slab_vecs, ids_all, out, grid_x, st);
-    else dispatch_k<true, 0>(tma, Q, nq, d, metric, k, kk, ft, slab_vecs, ids_all, out, grid_x, st);
+    if (d768) LAIVG_D(true, 6);
+    else LAIVG_D(true, 0);
   } else {
-    if (d768) dispatch_k<false, 6>(tma, Q, nq, d, metric, k, kk, ft, slab_vecs, ids_all, out, grid_x, st);
-    else dispatch_k<false, 0>(tma, Q, nq, d, metric, k, kk, ft, slab_vecs, ids_all, out, grid_x, st);
+    if (d768) LAIVG_D(false, 6);
+    else LAIVG_D(false, 0);
   }
+#undef LAIVG_D
 }
 
 void launch_window(uint64_t ns, int num_sms, cudaStream_t st) {

@@ -42,6 +42,13 @@ enum class ScanImpl : int {
   kLdg = 1,      // direct 128-bit loads into registers
 };
 
+// Optional geometry overrides of the TMA scan (0 = automatic).
+struct ScanTune {
+  uint32_t tile = 0;        // vectors per ring stage
+  uint32_t stages = 0;      // ring depth
+  uint32_t ctas_per_sm = 0; // scan CTAs per SM
+};
+
 // Coarse: fp64 scores[nq][nc] of Q[nq][d] against centroids[nc][d]
 // (dot for IP, squared L2 for L2; ivf.cpp:276-280).
 void launch_coarse_scores(const float* Q, uint32_t nq, const float* centroids,
@@ -67,8 +74,8 @@ void launch_partition(const uint32_t* probe, uint32_t nq, uint32_t lp,
 void launch_scan(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
                  const FastTable& ft, const float* slab_vecs,
                  const uint64_t* ids_all, const ScanOut& out, int grid_x,
-                 bool acc_fp64, ScanImpl impl, cudaStream_t st);
-int scan_grid_x(uint32_t nq, int num_sms, ScanImpl impl);
+                 bool acc_fp64, ScanImpl impl, const ScanTune& tune, cudaStream_t st);
+int scan_grid_x(uint32_t nq, int num_sms, ScanImpl impl, const ScanTune& tune);
 // Entries each per-CTA partial list holds for a given k (k + re-score margin).
 int scan_kk(int k, bool acc_fp64);
 // Generation-window stand-in: one CTA per SM spins on %globaltimer for ns.

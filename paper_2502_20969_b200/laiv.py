@@ -235,7 +235,8 @@ class Device:
 
     def __init__(self, ix: IvfIndex, capacity_bytes: int, device: int = 0,
                  miss_threads: int = 0, max_batch: int = 0, max_probe: int = 0,
-                 acc_fp64: bool = False, scan_impl: str = "tma"):
+                 acc_fp64: bool = False, scan_impl: str = "tma", tma_tile: int = 0,
+                 tma_stages: int = 0, ctas_per_sm: int = 0):
         L = lib()
         o = Opts()
         L.laivg_opts_default(C.byref(o))
@@ -248,6 +249,7 @@ class Device:
         if scan_impl not in ("tma", "ldg"):
             raise ValueError("scan_impl must be 'tma' or 'ldg'")
         o.scan_impl = 0 if scan_impl == "tma" else 1
+        o.tma_tile, o.tma_stages, o.ctas_per_sm = tma_tile, tma_stages, ctas_per_sm
         h = C.c_void_p()
         check(L.laivg_ctx_create(ix.h, C.byref(o), C.byref(h)))
         self.h = h
