@@ -191,6 +191,10 @@ __device__ __forceinline__ float sentinel_score(int metric) {
 // Warp-resident sorted top-k with a payload (slab vector index, for the exact
 // re-score): entry j = i * 32 + lane lives in slot i of that lane. Entries
 // j >= k are scratch.
+//
+// `id` holds the candidate's host-store ROW when `ids` is set: the datastore
+// id is only looked up (ids[row]) to break an exact score tie, and once at
+// output. A scan therefore never waits on an id load to admit a candidate.
 template <int KPL>
 struct WarpTopK {
   float s[KPL];
@@ -198,6 +202,16 @@ struct WarpTopK {
   uint32_t vi[KPL];
   float worst_s;
   uint64_t worst_id;
+  const uint64_t* ids = nullptr; // row -> id table (nullptr: keys are ids)
+
+  // (score, id) total order on keys (vectorstore.hpp:34-39)
+  __device__ __forceinline__ bool ranks_before(int metric, float sa, uint64_t ka, float sb,
+                                               uint64_t kb) const {
+    if (sa != sb) return metric == kIP ? sa > sb : sa < sb;
+    if (ids == nullptr || ka == ~0ull || kb == ~0ull) return ka < kb;
+    return __ldg(reinterpret_cast<const unsigned long long*>(ids) + ka) <
+           __ldg(reinterpret_cast<const unsigned long long*>(ids) + kb);
+  }
 
   __device__ void init(int metric) {
 #pragma unroll
@@ -815,7 +829,9 @@ __device__ void scan_epilogue(WarpTopK<KPL>& top, int metric, int k, int kk, boo
   if (warp == first) {
     for (int j = lane; j < k; j += 32) {
       out.out_s[static_cast<uint64_t>(q) * k + j] = m.s[j];
-      out.out_id[static_cast<uint64_t>(q) * k + j] = m.id[j];
+      const uint64_t key = m.id[j];
+      out.out_id[static_cast<uint64_t>(q) * k + j] =
+          (top.ids != nullptr && key != ~0ull) ? top.ids[key] : key; // row -> id
     }
     if (lane == 0) {
       out.out_count[q] = static_cast<uint32_t>(V < static_cast<uint64_t>(k) ? V : k);
@@ -913,6 +929,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   const uint32_t ntiles = static_cast<uint32_t>((v1 - v0 + T - 1) / T);
 
   WarpTopK<KPL> top;
+  top.ids = ids_all; // keys are host-store rows
   top.init(metric);
 
   if (warp == 0) {
@@ -1017,16 +1034,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         a0 = warp_sum(a0);
         a1 = warp_sum(a1);
         const float s0 = finish_score<ACC>(metric, a0);
-        if (top.may_enter(metric, s0)) {
-          const uint64_t id0 = ids_all[mrow[s * T + j]];
-          if (top.enters(metric, s0, id0)) top.insert(metric, kk, s0, id0, mvi[s * T + j]);
-        }
+        top.offer(metric, kk, s0, mrow[s * T + j], mvi[s * T + j]);
         if (two) {
           const float s1 = finish_score<ACC>(metric, a1);
-          if (top.may_enter(metric, s1)) {
-            const uint64_t id1 = ids_all[mrow[s * T + j2]];
-            if (top.enters(metric, s1, id1)) top.insert(metric, kk, s1, id1, mvi[s * T + j2]);
-          }
+          top.offer(metric, kk, s1, mrow[s * T + j2], mvi[s * T + j2]);
         }
       }
       __syncwarp();
@@ -1077,6 +1088,7 @@ __global__ void __launch_bounds__(kScanThreads, 2)
   const uint64_t V = pre[nf];
 
   WarpTopK<KPL> top;
+  top.ids = ids_all; // keys are host-store rows
   top.init(metric);
 
   const uint64_t tw = static_cast<uint64_t>(gridDim.x) * kScanWarps;
@@ -1156,12 +1168,7 @@ __global__ void __launch_bounds__(kScanThreads, 2)
         const ACC tot = warp_sum(acc[u]);
         if (!valid[u]) continue;
         const float cs = finish_score<ACC>(metric, tot);
-        if (top.may_enter(metric, cs)) {
-          const uint64_t cid = ids_all[rowi[u]];
-          if (top.enters(metric, cs, cid)) {
-            top.insert(metric, kk, cs, cid, static_cast<uint32_t>(vec[u]));
-          }
-        }
+        top.offer(metric, kk, cs, rowi[u], static_cast<uint32_t>(vec[u]));
       }
     }
   }
