@@ -217,8 +217,9 @@ Ctx::~Ctx() {
   for (void* p : {(void*)d_cen, (void*)d_list_off, (void*)d_ids, (void*)d_res,
                   (void*)d_slab, (void*)d_tmp, (void*)d_Q, (void*)d_scores,
                   (void*)d_order, (void*)d_run_k, (void*)d_run_v, (void*)ft.slab, (void*)ft.row, (void*)ft.len,
-                  (void*)ft.cluster, (void*)ft.pre, (void*)ft.count,
+                  (void*)ft.cluster, (void*)ft.pre, (void*)ft.count, (void*)ft.cta,
                   (void*)so.part_s, (void*)so.part_id, (void*)so.part_vi, (void*)so.ticket,
+                  (void*)so.gpart_s, (void*)so.gpart_id, (void*)so.gpart_vi,
                   (void*)so.out_s, (void*)so.out_id, (void*)so.out_count,
                   (void*)d_staged}) {
     if (p) cudaFree(p);
@@ -262,7 +263,7 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   tune.tile = o.tma_tile;
   tune.stages = o.tma_stages;
   tune.ctas_per_sm = o.ctas_per_sm;
-  if (o.ctas_per_sm > 16) throw std::invalid_argument("ctas_per_sm must be <= 16");
+  if (o.ctas_per_sm > 6) throw std::invalid_argument("ctas_per_sm must be <= 6");
   if (ix->nc > kMaxSortNc) {
     throw std::invalid_argument("device coarse ranking supports up to " +
                                 std::to_string(kMaxSortNc) + " clusters");
@@ -323,8 +324,12 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   so.part_s = dev_alloc<float>(size_t(part_cap) * kMaxK);
   so.part_id = dev_alloc<uint64_t>(size_t(part_cap) * kMaxK);
   so.part_vi = dev_alloc<uint32_t>(size_t(part_cap) * kMaxK);
-  so.ticket = dev_alloc<unsigned>(max_batch);
-  CK(cudaMemset(so.ticket, 0, max_batch * sizeof(unsigned)));
+  ft.cta = dev_alloc<CtaStart>(size_t(part_cap));
+  so.gpart_s = dev_alloc<float>(size_t(max_batch) * kMaxGroups * kMaxK);
+  so.gpart_id = dev_alloc<uint64_t>(size_t(max_batch) * kMaxGroups * kMaxK);
+  so.gpart_vi = dev_alloc<uint32_t>(size_t(max_batch) * kMaxGroups * kMaxK);
+  so.ticket = dev_alloc<unsigned>(size_t(max_batch) * (kMaxGroups + 1));
+  CK(cudaMemset(so.ticket, 0, size_t(max_batch) * (kMaxGroups + 1) * sizeof(unsigned)));
   so.out_s = dev_alloc<float>(size_t(max_batch) * kMaxK);
   so.out_id = dev_alloc<uint64_t>(size_t(max_batch) * kMaxK);
   so.out_count = dev_alloc<uint32_t>(max_batch);
@@ -454,6 +459,8 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
   // the residency table of the host store state.
   CK(cudaStreamWaitEvent(comp, ev_copy_tail, 0));
   commit_res(comp);
+  const int G = std::min(scan_grid_x(1, sms, scan_impl, tune), part_cap);
+  ft.grid = static_cast<uint32_t>(G); // the partition step lays out G scan CTAs
   CK(cudaEventRecord(ev_a, comp));
   if (explicit_probe) {
     if (lp) {
@@ -475,9 +482,8 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
     }
   }
   CK(cudaEventRecord(ev_p, comp));
-  launch_scan(dq, 1, ix->d, ix->metric, k, ft, d_slab, d_ids, so,
-              std::min(scan_grid_x(1, sms, scan_impl, tune), part_cap), acc_fp64, scan_impl,
-              tune, comp);
+  launch_scan(dq, 1, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl, tune,
+              comp);
   CK(cudaEventRecord(ev_s, comp));
   CK(cudaMemcpyAsync(h_out_s, so.out_s, k * sizeof(float), cudaMemcpyDeviceToHost, comp));
   CK(cudaMemcpyAsync(h_out_id, so.out_id, k * sizeof(uint64_t), cudaMemcpyDeviceToHost, comp));

@@ -480,6 +480,28 @@ __device__ void partition_block(const uint32_t* probe, uint32_t lp, const int64_
     ft.count[q] = base_cnt;
     pre[base_cnt] = base_len;
   }
+  if (ft.cta == nullptr) return;
+  // Scan CTA b covers [V*b/G, V*(b+1)/G): record the list and offset it
+  // starts at, so the scan's producer needs no search. CTA b starts inside
+  // list i iff b in [ceil(p*G/V), ceil((p+len)*G/V)), p = pre[i].
+  __syncthreads();
+  const uint32_t G = ft.grid, nf = base_cnt;
+  const uint64_t V = base_len;
+  CtaStart* cs = ft.cta + static_cast<uint64_t>(q) * G;
+  for (uint32_t b = threadIdx.x; b < G; b += blockDim.x) {
+    if (V == 0 || V * b / G >= V) cs[b] = CtaStart{0u, 0u, 0u, 0u};
+  }
+  if (V == 0) return;
+  for (uint32_t i = threadIdx.x; i < nf; i += blockDim.x) {
+    const uint64_t p = pre[i];
+    const uint64_t len = ft.len[tb + i];
+    if (len == 0) continue;
+    const uint64_t b0 = (p * G + V - 1) / V, b1 = ((p + len) * G + V - 1) / V;
+    for (uint64_t b = b0; b < b1 && b < G; ++b) {
+      const uint64_t v0 = V * b / G, v1 = V * (b + 1) / G;
+      cs[b] = CtaStart{i, static_cast<uint32_t>(v0 - p), static_cast<uint32_t>(v1 - v0), 0u};
+    }
+  }
 }
 
 __global__ void __launch_bounds__(256)
@@ -683,160 +705,228 @@ __global__ void __launch_bounds__(1024)
 // --------------------------------------------------------------------------
 // shared scan epilogue: CTA merge, grid merge, exact re-score of survivors
 // --------------------------------------------------------------------------
-struct MergeSmem {
+// Candidates in the epilogue carry (score, datastore id, slab vector index)
+// in three shared-memory arrays of a power-of-two length.
+struct Cands {
   float* s;
   uint64_t* id;
   uint32_t* vi;
 };
 
-// Exact fp64 score (vectorstore.cpp:93-115 arithmetic) of slab row `vi`.
-__device__ float exact_score(const float* __restrict__ slab, uint32_t vi, const float* sq,
-                             uint32_t d, int metric) {
-  const int lane = threadIdx.x & 31;
-  const float* row = slab + static_cast<uint64_t>(vi) * d;
-  double acc = 0.0;
-  for (uint32_t j = lane; j < d; j += 32) {
-    acc = metric == kIP ? term_ip_d(static_cast<double>(sq[j]), __ldg(row + j), acc)
-                        : term_l2_d(static_cast<double>(sq[j]), __ldg(row + j), acc);
-  }
-  acc = warp_sum(acc);
-  return finish_score<double>(metric, acc);
+__host__ __device__ inline uint32_t pow2_ceil(uint32_t x) {
+  uint32_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
 }
 
-// Called by every thread of the CTA once the warps [first, first + nw) hold
-// their top-kk in registers.
+// Scratch (bytes) the epilogue needs for `nw` holder warps and `grid` CTAs.
+__host__ __device__ inline size_t epilogue_scratch(int nw, int kk, uint32_t grid) {
+  const uint32_t groups = (grid + kGroup - 1) / kGroup;
+  uint32_t n = static_cast<uint32_t>(nw * kk);
+  n = n > kGroup * kk ? n : kGroup * kk;
+  n = n > groups * kk ? n : groups * kk;
+  return static_cast<size_t>(pow2_ceil(n)) * 16 + 16;
+}
+
+__device__ inline Cands cands_at(unsigned char* base, uint32_t cap) {
+  Cands c;
+  c.s = reinterpret_cast<float*>(base);
+  c.id = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(c.s + cap) + 7) & ~uintptr_t(7));
+  c.vi = reinterpret_cast<uint32_t*>(c.id + cap);
+  return c;
+}
+
+__device__ __forceinline__ bool better(int metric, float sa, uint64_t ia, float sb, uint64_t ib) {
+  if (sa != sb) return metric == kIP ? sa > sb : sa < sb;
+  return ia < ib;
+}
+
+// Block-wide bitonic sort of n (power of two) candidates, best first under
+// the (score, ascending id) total order. Every thread of the CTA calls it.
+__device__ void cands_sort(int metric, Cands c, uint32_t n) {
+  for (uint32_t kk = 2; kk <= n; kk <<= 1) {
+    for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+      for (uint32_t x = threadIdx.x; x < n / 2; x += blockDim.x) {
+        const uint32_t lo = 2 * x - (x & (j - 1)), hi = lo + j;
+        const bool up = (lo & kk) == 0;
+        const bool hi_first = better(metric, c.s[hi], c.id[hi], c.s[lo], c.id[lo]);
+        if (up == hi_first) {
+          const float ts = c.s[lo];
+          c.s[lo] = c.s[hi];
+          c.s[hi] = ts;
+          const uint64_t ti = c.id[lo];
+          c.id[lo] = c.id[hi];
+          c.id[hi] = ti;
+          const uint32_t tv = c.vi[lo];
+          c.vi[lo] = c.vi[hi];
+          c.vi[hi] = tv;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ void cands_pad(int metric, Cands c, uint32_t from, uint32_t to) {
+  for (uint32_t x = from + threadIdx.x; x < to; x += blockDim.x) {
+    c.s[x] = sentinel_score(metric);
+    c.id[x] = ~0ull;
+    c.vi[x] = ~0u;
+  }
+}
+
+// Loads `lists` consecutive partial lists of kk entries each (L2, bypassing
+// L1: other CTAs wrote them) into c[0, lists * kk), all loads in parallel.
+__device__ void cands_load(Cands c, const float* ps, const uint64_t* pid, const uint32_t* pvi,
+                           uint32_t n) {
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
+    c.s[x] = __ldcg(ps + x);
+    c.id[x] = __ldcg(reinterpret_cast<const unsigned long long*>(pid) + x);
+    c.vi[x] = __ldcg(pvi + x);
+  }
+}
+
+// Exact fp64 re-score (vectorstore.cpp:93-115 arithmetic) of c[0, n) by the
+// warps [first, first + nw), four candidates per warp in flight together.
+__device__ void cands_rescore(int metric, Cands c, uint32_t n, const float* __restrict__ slab,
+                              const float* sq, uint32_t d, int first, int nw) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < first || warp >= first + nw) return;
+  const int w = warp - first;
+  for (uint32_t c0 = w; c0 < n; c0 += 4 * nw) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const float* rows[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t ci = c0 + u * nw;
+      rows[u] = slab + static_cast<uint64_t>(ci < n ? c.vi[ci] : c.vi[c0]) * d;
+    }
+    if ((d & 3u) == 0) {
+      const uint32_t d4 = d >> 2;
+#pragma unroll 2
+      for (uint32_t j4 = lane; j4 < d4; j4 += 32) {
+        float4 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = __ldg(reinterpret_cast<const float4*>(rows[u]) + j4);
+        const float4 qq = reinterpret_cast<const float4*>(sq)[j4];
+        const double q4[4] = {qq.x, qq.y, qq.z, qq.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) Acc4<true>::run(metric, q4, x[u], acc[u]);
+      }
+    } else {
+      for (uint32_t j = lane; j < d; j += 32) {
+        const double qj = sq[j];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          acc[u] = metric == kIP ? term_ip_d(qj, __ldg(rows[u] + j), acc[u])
+                                 : term_l2_d(qj, __ldg(rows[u] + j), acc[u]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double t = warp_sum(acc[u]);
+      const uint32_t ci = c0 + u * nw;
+      if (lane == 0 && ci < n) c.s[ci] = finish_score<double>(metric, t);
+    }
+  }
+}
+
+// Scan epilogue, called by every thread once the warps [first, first + nw)
+// hold their top-kk (keys = host-store rows) in registers and `scratch` (cap
+// bytes, >= epilogue_scratch) is free:
+//   1. CTA:   the warps' lists, rows resolved to ids, sorted -> top-kk partial
+//   2. group: the last of each kGroup CTAs sorts the group's partials
+//   3. final: the last group sorts the group results, re-scores the survivors
+//             exactly (fp32 accumulation) and writes the top-k.
+// Tickets self-reset, so the same buffers serve the next launch.
 template <int KPL>
 __device__ void scan_epilogue(WarpTopK<KPL>& top, int metric, int k, int kk, bool rerank,
-                              MergeSmem m, const ScanOut& out, const float* sq,
-                              const float* __restrict__ slab, uint32_t d, uint64_t V,
-                              int first, int nw, size_t merge_cap, bool* am_last) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t q = blockIdx.y;
-  const bool holder = warp >= first && warp < first + nw;
-  const int w = warp - first;
-  if (holder) top.store(kk, m.s + w * kk, m.id + w * kk, m.vi + w * kk);
-  __syncthreads();
-  const uint64_t part = (static_cast<uint64_t>(q) * gridDim.x + blockIdx.x) * kk;
-  if (warp == first) {
-    for (int o = 1; o < nw; ++o) {
-      top.template merge_list<false>(metric, kk, m.s + o * kk, m.id + o * kk, m.vi + o * kk, kk);
-    }
-    top.store(kk, out.part_s + part, out.part_id + part, out.part_vi + part);
-    __threadfence();
-    if (lane == 0) {
-      const unsigned t = atomicAdd(out.ticket + q, 1u);
-      *am_last = (t == gridDim.x - 1);
-    }
-  }
-  __syncthreads();
-  if (!*am_last) return;
+                              unsigned char* scratch, const ScanOut& out, const float* sq,
+                              const float* __restrict__ slab, const uint64_t* __restrict__ ids_all,
+                              uint32_t d, uint64_t V, int first, int nw) {
+  __shared__ bool last;
+  const int warp = threadIdx.x >> 5;
+  const uint32_t q = blockIdx.y, G = gridDim.x;
+  const uint32_t ngroups = (G + kGroup - 1) / kGroup, g = blockIdx.x / kGroup;
+  const uint32_t gsize = min(kGroup, G - g * kGroup);
+  const uint32_t cap = pow2_ceil(static_cast<uint32_t>(
+      (epilogue_scratch(nw, kk, G) - 16) / 16));
+  const Cands c = cands_at(scratch, cap);
+  unsigned* tickets = out.ticket + static_cast<uint64_t>(q) * (kMaxGroups + 1);
 
-  // ---- grid merge in the last CTA ----
+  // ---- 1. CTA level ----
+  const bool holder = warp >= first && warp < first + nw;
+  if (holder) top.store(kk, c.s + (warp - first) * kk, c.id + (warp - first) * kk, c.vi + (warp - first) * kk);
+  uint32_t n = static_cast<uint32_t>(nw * kk), n2 = pow2_ceil(n);
+  cands_pad(metric, c, n, n2);
+  __syncthreads();
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) { // rows -> datastore ids
+    const uint64_t r = c.id[x];
+    c.id[x] = r == ~0ull ? ~0ull : __ldg(reinterpret_cast<const unsigned long long*>(ids_all) + r);
+  }
+  __syncthreads();
+  cands_sort(metric, c, n2);
+  const uint64_t pbase = static_cast<uint64_t>(q) * G * kk;
+  for (uint32_t x = threadIdx.x; x < static_cast<uint32_t>(kk); x += blockDim.x) {
+    const uint64_t o = pbase + static_cast<uint64_t>(blockIdx.x) * kk + x;
+    out.part_s[o] = c.s[x];
+    out.part_id[o] = c.id[x];
+    out.part_vi[o] = c.vi[x];
+  }
   __threadfence();
-  const uint64_t pbase = static_cast<uint64_t>(q) * gridDim.x * kk;
-  const size_t nparts = static_cast<size_t>(gridDim.x) * kk;
-  if (nparts * 16 + 16 <= merge_cap) {
-    // stage every partial list in shared memory with coalesced loads, then
-    // merge on-chip (one L2 round trip instead of one per list)
-    float* gs = m.s;
-    uint64_t* gid = reinterpret_cast<uint64_t*>(
-        (reinterpret_cast<uintptr_t>(gs + nparts) + 7) & ~uintptr_t(7));
-    uint32_t* gvi = reinterpret_cast<uint32_t*>(gid + nparts);
-    for (size_t x = threadIdx.x; x < nparts; x += blockDim.x) {
-      gs[x] = __ldcg(out.part_s + pbase + x);
-      gid[x] = __ldcg(reinterpret_cast<const unsigned long long*>(out.part_id + pbase) + x);
-      gvi[x] = __ldcg(out.part_vi + pbase + x);
-    }
-    __syncthreads();
-    if (holder) {
-      top.init(metric);
-      for (uint32_t g = w; g < gridDim.x; g += nw) {
-        top.template merge_list<false>(metric, kk, gs + g * kk, gid + g * kk, gvi + g * kk, kk);
-      }
-    }
-    __syncthreads();
-    if (holder) top.store(kk, m.s + w * kk, m.id + w * kk, m.vi + w * kk);
-  } else {
-    if (holder) {
-      top.init(metric);
-      for (uint32_t g = w; g < gridDim.x; g += nw) {
-        top.template merge_list<true>(metric, kk, out.part_s + pbase + g * kk,
-                                      out.part_id + pbase + g * kk,
-                                      out.part_vi + pbase + g * kk, kk);
-      }
-      top.store(kk, m.s + w * kk, m.id + w * kk, m.vi + w * kk);
-    }
-  }
   __syncthreads();
-  if (warp == first) {
-    for (int o = 1; o < nw; ++o) {
-      top.template merge_list<false>(metric, kk, m.s + o * kk, m.id + o * kk, m.vi + o * kk, kk);
-    }
-    top.store(kk, m.s, m.id, m.vi);
-  }
+  if (threadIdx.x == 0) last = atomicAdd(tickets + g, 1u) == gsize - 1;
   __syncthreads();
-  const int navail = static_cast<int>(V < static_cast<uint64_t>(kk) ? V : kk);
-  if (rerank) {
-    // exact fp64 re-score of the survivors, then re-rank on (score, id)
-    if (holder) {
-      // up to four candidates per warp with their loads in flight together
-      for (int c0 = w; c0 < navail; c0 += 4 * nw) {
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        const float* rows[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int c = c0 + u * nw;
-          rows[u] = slab + static_cast<uint64_t>(c < navail ? m.vi[c] : m.vi[c0]) * d;
-        }
-        if ((d & 3u) == 0) {
-          const uint32_t d4 = d >> 2;
-#pragma unroll 2
-          for (uint32_t j4 = lane; j4 < d4; j4 += 32) {
-            float4 x[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) x[u] = __ldg(reinterpret_cast<const float4*>(rows[u]) + j4);
-            const float4 qq = reinterpret_cast<const float4*>(sq)[j4];
-            const double q4[4] = {qq.x, qq.y, qq.z, qq.w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) Acc4<true>::run(metric, q4, x[u], acc[u]);
-          }
-        } else {
-          for (uint32_t j = lane; j < d; j += 32) {
-            const double qj = sq[j];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              acc[u] = metric == kIP ? term_ip_d(qj, __ldg(rows[u] + j), acc[u])
-                                     : term_l2_d(qj, __ldg(rows[u] + j), acc[u]);
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double t = warp_sum(acc[u]);
-          const int c = c0 + u * nw;
-          if (lane == 0 && c < navail) m.s[c] = finish_score<double>(metric, t);
-        }
-      }
-    }
-    __syncthreads();
-    if (warp == first) {
-      top.init(metric);
-      for (int c = 0; c < navail; ++c) top.offer(metric, k, m.s[c], m.id[c], m.vi[c]);
-      top.store(k, m.s, m.id, m.vi);
-    }
-    __syncthreads();
+  if (!last) return;
+  __threadfence();
+
+  // ---- 2. group level ----
+  n = gsize * kk;
+  n2 = pow2_ceil(n);
+  const uint64_t gofs = pbase + static_cast<uint64_t>(g) * kGroup * kk;
+  cands_load(c, out.part_s + gofs, out.part_id + gofs, out.part_vi + gofs, n);
+  cands_pad(metric, c, n, n2);
+  __syncthreads();
+  cands_sort(metric, c, n2);
+  const uint64_t gbase = static_cast<uint64_t>(q) * kMaxGroups * kk;
+  for (uint32_t x = threadIdx.x; x < static_cast<uint32_t>(kk); x += blockDim.x) {
+    const uint64_t o = gbase + static_cast<uint64_t>(g) * kk + x;
+    out.gpart_s[o] = c.s[x];
+    out.gpart_id[o] = c.id[x];
+    out.gpart_vi[o] = c.vi[x];
   }
-  if (warp == first) {
-    for (int j = lane; j < k; j += 32) {
-      out.out_s[static_cast<uint64_t>(q) * k + j] = m.s[j];
-      const uint64_t key = m.id[j];
-      out.out_id[static_cast<uint64_t>(q) * k + j] =
-          (top.ids != nullptr && key != ~0ull) ? top.ids[key] : key; // row -> id
-    }
-    if (lane == 0) {
-      out.out_count[q] = static_cast<uint32_t>(V < static_cast<uint64_t>(k) ? V : k);
-      out.ticket[q] = 0; // self-reset for the next launch / graph replay
-    }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(tickets + kMaxGroups, 1u) == ngroups - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+
+  // ---- 3. final ----
+  n = ngroups * kk;
+  n2 = pow2_ceil(n);
+  cands_load(c, out.gpart_s + gbase, out.gpart_id + gbase, out.gpart_vi + gbase, n);
+  cands_pad(metric, c, n, n2);
+  __syncthreads();
+  cands_sort(metric, c, n2);
+  const uint32_t navail = static_cast<uint32_t>(V < static_cast<uint64_t>(kk) ? V : kk);
+  if (rerank && navail > 0) {
+    const uint32_t r2 = pow2_ceil(navail);
+    cands_pad(metric, c, navail, r2);
+    cands_rescore(metric, c, navail, slab, sq, d, first, nw);
+    __syncthreads();
+    cands_sort(metric, c, r2);
+  }
+  for (uint32_t x = threadIdx.x; x < static_cast<uint32_t>(k); x += blockDim.x) {
+    out.out_s[static_cast<uint64_t>(q) * k + x] = c.s[x];
+    out.out_id[static_cast<uint64_t>(q) * k + x] = c.id[x];
+  }
+  for (uint32_t x = threadIdx.x; x <= ngroups; x += blockDim.x) {
+    tickets[x == ngroups ? kMaxGroups : x] = 0;
+  }
+  if (threadIdx.x == 0) {
+    out.out_count[q] = static_cast<uint32_t>(V < static_cast<uint64_t>(k) ? V : k);
   }
 }
 
@@ -894,11 +984,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                     const uint64_t* __restrict__ ids_all, ScanOut out, uint32_t T, uint32_t S) {
   using ACC = typename std::conditional<kFp64, double, float>::type;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ bool am_last;
   const size_t stage_floats = static_cast<size_t>(T) * d;
   float* stage = reinterpret_cast<float*>(smem);
+  // the stage ring doubles as the epilogue's scratch once every tile is used
   size_t off = (static_cast<size_t>(S) * stage_floats * 4 + 127) & ~size_t(127);
-  const size_t merge_bytes = static_cast<size_t>(kConsumers) * kk * 16;
+  const size_t merge_bytes = epilogue_scratch(kConsumers, kk, gridDim.x);
   if (off < merge_bytes) off = (merge_bytes + 127) & ~size_t(127);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + off);
   uint64_t* empty = full + S;
@@ -923,10 +1013,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 
   const uint64_t tb = static_cast<uint64_t>(q) * ft.stride;
   const uint64_t* pre = ft.pre + static_cast<uint64_t>(q) * (ft.stride + 1);
-  const uint32_t nf = ft.count[q];
-  const uint64_t V = pre[nf];
-  const uint64_t v0 = V * blockIdx.x / gridDim.x, v1 = V * (blockIdx.x + 1) / gridDim.x;
-  const uint32_t ntiles = static_cast<uint32_t>((v1 - v0 + T - 1) / T);
+  // this CTA's range, precomputed by the partition step (no search here)
+  const CtaStart cs = ft.cta[static_cast<uint64_t>(q) * gridDim.x + blockIdx.x];
+  const uint32_t nvec = cs.n;
+  const uint32_t ntiles = (nvec + T - 1) / T;
 
   WarpTopK<KPL> top;
   top.ids = ids_all; // keys are host-store rows
@@ -936,12 +1026,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     // ---------------- producer: one lane drives the bulk copies ----------
     if (lane == 0 && ntiles) {
       Cursor cur;
-      cur.seek(ft, tb, pre, nf, v0);
+      cur.li = cs.li;
+      cur.load(ft, tb);
+      cur.o = cs.o;
       for (uint32_t i = 0; i < ntiles; ++i) {
         const uint32_t s = i % S;
         mbar_wait(empty + s, ((i / S) & 1u) ^ 1u);
-        const uint64_t tile0 = v0 + uint64_t(i) * T;
-        const uint32_t n = static_cast<uint32_t>(umin64(T, v1 - tile0));
+        const uint32_t tile0 = i * T;
+        const uint32_t n = min(T, nvec - tile0);
         // tile metadata first (published by the arrive), then the copies
         uint32_t j = 0;
         Cursor c2 = cur;
@@ -964,7 +1056,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                    slab + static_cast<uint64_t>(cur.slab + static_cast<int64_t>(cur.o)) * d,
                    take * d * 4u, full + s);
           j += take;
-          if (tile0 + j >= v1) break;
+          if (tile0 + j >= nvec) break;
           cur.advance(ft, tb, take);
           if (j >= n) break;
         }
@@ -1046,13 +1138,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   }
   __syncthreads(); // every tile consumed: the stage ring is free for merging
 
-  MergeSmem m;
-  m.s = reinterpret_cast<float*>(smem);
-  m.id = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(m.s + kConsumers * kk) + 7) & ~uintptr_t(7));
-  m.vi = reinterpret_cast<uint32_t*>(m.id + kConsumers * kk);
-  scan_epilogue<KPL>(top, metric, k, kk, !kFp64, m, out, sq, slab, d, V, 1, kConsumers, off,
-                     &am_last);
+  const uint64_t V = pre[ft.count[q]];
+  scan_epilogue<KPL>(top, metric, k, kk, !kFp64, smem, out, sq, slab, ids_all, d, V, 1,
+                     kConsumers);
 }
 
 // --------------------------------------------------------------------------
@@ -1069,12 +1157,8 @@ __global__ void __launch_bounds__(kScanThreads, 2)
                     const uint64_t* __restrict__ ids_all, ScanOut out) {
   using ACC = typename std::conditional<kFp64, double, float>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ bool am_last;
   float* sq = reinterpret_cast<float*>(smem_raw);
-  float* ms = sq + ((d + 3) & ~3u);
-  uint64_t* mid = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(ms + kScanWarps * kk) + 7) & ~uintptr_t(7));
-  uint32_t* mvi = reinterpret_cast<uint32_t*>(mid + kScanWarps * kk);
+  unsigned char* scratch = smem_raw + ((static_cast<size_t>(d) * 4 + 15) & ~size_t(15));
 
   const uint32_t q = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1172,10 +1256,9 @@ __global__ void __launch_bounds__(kScanThreads, 2)
       }
     }
   }
-  MergeSmem m{ms, mid, mvi};
-  scan_epilogue<KPL>(top, metric, k, kk, !kFp64, m, out, sq, slab_vecs, d, V, 0, kScanWarps,
-                     size_t(kScanWarps) * kk * 16,
-                     &am_last);
+  __syncthreads();
+  scan_epilogue<KPL>(top, metric, k, kk, !kFp64, scratch, out, sq, slab_vecs, ids_all, d, V, 0,
+                     kScanWarps);
 }
 
 // --------------------------------------------------------------------------
@@ -1201,7 +1284,7 @@ struct TmaGeom {
   size_t smem;
 };
 
-TmaGeom tma_geom(uint32_t d, int kk, const ScanTune& tune) {
+TmaGeom tma_geom(uint32_t d, int kk, uint32_t grid, const ScanTune& tune) {
   const size_t row = size_t(d) * 4;
   TmaGeom g;
   g.T = tune.tile ? tune.tile
@@ -1211,7 +1294,7 @@ TmaGeom tma_geom(uint32_t d, int kk, const ScanTune& tune) {
             ? tune.stages
             : static_cast<uint32_t>(std::max<size_t>(2, std::min<size_t>(8, 196608 / stage)));
   size_t off = (g.S * stage + 127) & ~size_t(127);
-  const size_t merge = size_t(kConsumers) * kk * 16;
+  const size_t merge = epilogue_scratch(kConsumers, kk, grid);
   if (off < merge) off = (merge + 127) & ~size_t(127);
   off += g.S * 16 + g.S * g.T * 12 + g.S * 4 + 16;
   off += row + 16;
@@ -1223,7 +1306,7 @@ template <bool kFp64, int KPL, int NCH>
 void launch_tma_t(const float* Q, uint32_t nq, uint32_t d, int metric, int k, int kk,
                   const FastTable& ft, const float* slab, const uint64_t* ids,
                   const ScanOut& out, int gx, const ScanTune& tune, cudaStream_t st) {
-  const TmaGeom g = tma_geom(d, kk, tune);
+  const TmaGeom g = tma_geom(d, kk, static_cast<uint32_t>(gx), tune);
   if (g.smem > 227 * 1024) throw CudaError("TMA ring does not fit shared memory");
   auto fn = scan_tma_kernel<kFp64, KPL, NCH>;
   static size_t attr = 0;
@@ -1239,7 +1322,9 @@ template <bool kFp64, int KPL, int NCH>
 void launch_ldg_t(const float* Q, uint32_t nq, uint32_t d, int metric, int k, int kk,
                   const FastTable& ft, const float* slab, const uint64_t* ids,
                   const ScanOut& out, int gx, cudaStream_t st) {
-  const size_t smem = ((d + 3) & ~3u) * sizeof(float) + size_t(kScanWarps) * kk * 16 + 16;
+  const size_t smem = ((size_t(d) * 4 + 15) & ~size_t(15)) +
+                      epilogue_scratch(kScanWarps, kk, static_cast<uint32_t>(gx));
+  if (smem > 227 * 1024) throw CudaError("LDG scan epilogue does not fit shared memory");
   auto fn = scan_ldg_kernel<kFp64, KPL, NCH>;
   static size_t attr = 0;
   if (smem > attr) {

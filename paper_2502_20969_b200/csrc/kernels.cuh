@@ -17,6 +17,15 @@ constexpr uint32_t kMaxSortNc = 16384; // on-chip full ranking limit
 
 // Per-query fast-list table produced by the partition step and consumed by
 // the scan: entry f of query q lives at [q * stride + f].
+// Where scan CTA b of a query starts: list index, offset in the list and the
+// number of vectors it scans (the partition step fills it for `grid` CTAs).
+struct CtaStart {
+  uint32_t li;
+  uint32_t o;
+  uint32_t n;
+  uint32_t pad;
+};
+
 struct FastTable {
   int64_t* slab;      // device-cache vector offset of the list
   uint64_t* row;      // host-store row offset of the list (id table index)
@@ -24,14 +33,22 @@ struct FastTable {
   uint32_t* cluster;  // cluster id (for the host)
   uint64_t* pre;      // exclusive prefix of len, stride + 1 entries per query
   uint32_t* count;    // number of fast lists per query
+  CtaStart* cta;      // [nq][grid] scan CTA start table (nullable)
   uint32_t stride;
+  uint32_t grid;      // CTAs per query the cta table was built for
 };
+
+constexpr uint32_t kGroup = 16;     // CTAs merged by one group-last CTA
+constexpr uint32_t kMaxGroups = 64; // groups per query (grid <= 1024)
 
 struct ScanOut {
   float* part_s;      // [nq][grid][kk] per-CTA partial top-kk
-  uint64_t* part_id;
+  uint64_t* part_id;  // datastore ids
   uint32_t* part_vi;  // slab vector index of each partial entry (re-score)
-  unsigned* ticket;   // [nq] last-CTA-done counters (self-resetting)
+  float* gpart_s;     // [nq][kMaxGroups][kk] per-group partial top-kk
+  uint64_t* gpart_id;
+  uint32_t* gpart_vi;
+  unsigned* ticket;   // [nq][kMaxGroups + 1] group / final tickets (self-resetting)
   float* out_s;       // [nq][k]
   uint64_t* out_id;   // [nq][k]
   uint32_t* out_count;// [nq]

@@ -43,7 +43,14 @@ def main():
     ap.add_argument("--nprobe", type=int, default=128)
     ap.add_argument("--queries", type=int, default=30)
     ap.add_argument("--metric", default="ip")
+    ap.add_argument("--depth", action="store_true",
+                    help="scan time vs nprobe for the default variants (fixed cost + slope)")
     args = ap.parse_args()
+    global VARIANTS
+    if args.depth:
+        VARIANTS = [(a, "tma", 0, 0, 0, L) for a in ("fp32", "fp64") for L in (1, 8, 32, 128, 256)]
+    else:
+        VARIANTS = [v + (args.nprobe,) for v in VARIANTS]
     nc, per, d = args.lists, args.per_list, 768
     cen = laiv.synth_centroids(0, nc, d)
     vecs = laiv.pinned_empty((nc * per, d), np.float32)
@@ -54,19 +61,19 @@ def main():
     ix = laiv.IvfIndex(cen, vecs, ids, off, metric, borrow=True, trust=True)
     _, qo, _ = laiv.synth_queries(1, vecs, args.queries + 3, 0.008)
     member = 4 * d + 8
-    for acc, impl, tile, stages, cps in VARIANTS:
+    for acc, impl, tile, stages, cps, nprobe in VARIANTS:
         try:
             dev = laiv.Device(ix, nc * per * member, acc_fp64=acc == "fp64", scan_impl=impl,
                               tma_tile=tile, tma_stages=stages, ctas_per_sm=cps)
         except Exception as e:  # noqa: BLE001
-            print(json.dumps({"variant": [acc, impl, tile, stages, cps], "error": str(e)}))
+            print(json.dumps({"variant": [acc, impl, tile, stages, cps, nprobe], "error": str(e)}))
             continue
         plan = laiv.PrefetchPlan(list(range(nc)), 0, [])
         laiv.execute_prefetch(dev, plan, laiv.TransferChannel(1e9, laiv.ChannelMode.Device))
         dev.stage_queries(qo)
         ts, byts, ids0 = [], [], None
         for i in range(args.queries + 3):
-            got_ids, _, _, t = dev.hybrid_search_staged(i, args.nprobe, 10)
+            got_ids, _, _, t = dev.hybrid_search_staged(i, nprobe, 10)
             if i >= 3:
                 ts.append(t.t_scan)
                 byts.append(t.scanned_bytes)
@@ -74,7 +81,7 @@ def main():
                 ids0 = got_ids
         ts = np.array(ts)
         gbs = np.array(byts) / ts / 1e9
-        print(json.dumps({"variant": [acc, impl, tile, stages, cps],
+        print(json.dumps({"variant": [acc, impl, tile, stages, cps, nprobe],
                           "t_scan_us_median": float(np.median(ts) * 1e6),
                           "t_scan_us_min": float(ts.min() * 1e6),
                           "gbs_median": float(np.median(gbs)), "gbs_max": float(gbs.max()),
