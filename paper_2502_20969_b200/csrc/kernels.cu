@@ -705,11 +705,12 @@ __global__ void __launch_bounds__(1024)
 // --------------------------------------------------------------------------
 // shared scan epilogue: CTA merge, grid merge, exact re-score of survivors
 // --------------------------------------------------------------------------
-// Candidates in the epilogue carry (score, datastore id, slab vector index)
-// in three shared-memory arrays of a power-of-two length.
+// Epilogue candidates: (score, host-store row, slab vector index) in three
+// shared-memory arrays. Rows stand in for datastore ids until the output; an
+// exact score tie is broken by looking both ids up (vectorstore.hpp:34-39).
 struct Cands {
   float* s;
-  uint64_t* id;
+  uint64_t* r;
   uint32_t* vi;
 };
 
@@ -719,44 +720,98 @@ __host__ __device__ inline uint32_t pow2_ceil(uint32_t x) {
   return p;
 }
 
-// Scratch (bytes) the epilogue needs for `nw` holder warps and `grid` CTAs.
-__host__ __device__ inline size_t epilogue_scratch(int nw, int kk, uint32_t grid) {
+// Entries of one ping-pong buffer: the largest level, power-of-two lists of
+// power-of-two length.
+__host__ __device__ inline uint32_t epilogue_entries(int nw, int kk, uint32_t grid) {
+  const uint32_t m = pow2_ceil(static_cast<uint32_t>(kk));
   const uint32_t groups = (grid + kGroup - 1) / kGroup;
-  uint32_t n = static_cast<uint32_t>(nw * kk);
-  n = n > kGroup * kk ? n : kGroup * kk;
-  n = n > groups * kk ? n : groups * kk;
-  return static_cast<size_t>(pow2_ceil(n)) * 16 + 16;
+  uint32_t lists = pow2_ceil(static_cast<uint32_t>(nw));
+  lists = lists > kGroup ? lists : kGroup;
+  lists = lists > pow2_ceil(groups) ? lists : pow2_ceil(groups);
+  return lists * m;
+}
+// Scratch bytes the epilogue needs (two ping-pong buffers).
+__host__ __device__ inline size_t epilogue_scratch(int nw, int kk, uint32_t grid) {
+  return 2 * (static_cast<size_t>(epilogue_entries(nw, kk, grid)) * 16 + 16);
 }
 
 __device__ inline Cands cands_at(unsigned char* base, uint32_t cap) {
   Cands c;
   c.s = reinterpret_cast<float*>(base);
-  c.id = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(c.s + cap) + 7) & ~uintptr_t(7));
-  c.vi = reinterpret_cast<uint32_t*>(c.id + cap);
+  c.r = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(c.s + cap) + 7) & ~uintptr_t(7));
+  c.vi = reinterpret_cast<uint32_t*>(c.r + cap);
   return c;
 }
 
-__device__ __forceinline__ bool better(int metric, float sa, uint64_t ia, float sb, uint64_t ib) {
+__device__ __forceinline__ bool cand_before(int metric, const uint64_t* ids, float sa,
+                                            uint64_t ra, float sb, uint64_t rb) {
   if (sa != sb) return metric == kIP ? sa > sb : sa < sb;
-  return ia < ib;
+  if (ra == rb || ra == ~0ull) return false;
+  if (rb == ~0ull) return true;
+  return __ldg(reinterpret_cast<const unsigned long long*>(ids) + ra) <
+         __ldg(reinterpret_cast<const unsigned long long*>(ids) + rb);
 }
 
-// Block-wide bitonic sort of n (power of two) candidates, best first under
-// the (score, ascending id) total order. Every thread of the CTA calls it.
-__device__ void cands_sort(int metric, Cands c, uint32_t n) {
+__device__ __forceinline__ void cand_copy(Cands d, uint32_t i, Cands s, uint32_t j) {
+  d.s[i] = s.s[j];
+  d.r[i] = s.r[j];
+  d.vi[i] = s.vi[j];
+}
+
+// One merge-path level: `lists` sorted lists of length m in `a` (list l at
+// l * m) merge pairwise into lists / 2 lists of the best m in `b`. Every
+// output is one co-rank binary search, so a level costs log2(m) steps.
+__device__ void merge_level(int metric, const uint64_t* ids, Cands a, Cands b, uint32_t lists,
+                            uint32_t m) {
+  const uint32_t lm = __ffs(m) - 1;
+  for (uint32_t x = threadIdx.x; x < (lists / 2) << lm; x += blockDim.x) {
+    const uint32_t pr = x >> lm, p = x & (m - 1);
+    const uint32_t A = 2 * pr * m, B = A + m;
+    uint32_t lo = p > m ? p - m : 0, hi = p < m ? p : m;
+    while (lo < hi) { // i = how many of the first p outputs come from A
+      const uint32_t mid = (lo + hi) >> 1;
+      if (cand_before(metric, ids, a.s[A + mid], a.r[A + mid], a.s[B + p - mid - 1],
+                      a.r[B + p - mid - 1])) {
+        lo = mid + 1;
+      } else {
+        hi = mid;
+      }
+    }
+    const uint32_t i = lo, j = p - i;
+    const bool from_a =
+        j >= m || (i < m && cand_before(metric, ids, a.s[A + i], a.r[A + i], a.s[B + j], a.r[B + j]));
+    cand_copy(b, pr * m + p, a, from_a ? A + i : B + j);
+  }
+}
+
+// Reduces `lists` (power of two) sorted lists of length m held in *cur down
+// to one (the best m) at (*cur)[0, m), ping-ponging with *alt.
+__device__ void merge_tree(int metric, const uint64_t* ids, Cands* cur, Cands* alt,
+                           uint32_t lists, uint32_t m) {
+  while (lists > 1) {
+    merge_level(metric, ids, *cur, *alt, lists, m);
+    __syncthreads();
+    const Cands t = *cur;
+    *cur = *alt;
+    *alt = t;
+    lists >>= 1;
+  }
+}
+
+// Block bitonic sort of n (power of two) candidates, best first.
+__device__ void cands_sort(int metric, const uint64_t* ids, Cands c, uint32_t n) {
   for (uint32_t kk = 2; kk <= n; kk <<= 1) {
     for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
       for (uint32_t x = threadIdx.x; x < n / 2; x += blockDim.x) {
         const uint32_t lo = 2 * x - (x & (j - 1)), hi = lo + j;
         const bool up = (lo & kk) == 0;
-        const bool hi_first = better(metric, c.s[hi], c.id[hi], c.s[lo], c.id[lo]);
-        if (up == hi_first) {
+        if (up == cand_before(metric, ids, c.s[hi], c.r[hi], c.s[lo], c.r[lo])) {
           const float ts = c.s[lo];
           c.s[lo] = c.s[hi];
           c.s[hi] = ts;
-          const uint64_t ti = c.id[lo];
-          c.id[lo] = c.id[hi];
-          c.id[hi] = ti;
+          const uint64_t tr = c.r[lo];
+          c.r[lo] = c.r[hi];
+          c.r[hi] = tr;
           const uint32_t tv = c.vi[lo];
           c.vi[lo] = c.vi[hi];
           c.vi[hi] = tv;
@@ -767,22 +822,33 @@ __device__ void cands_sort(int metric, Cands c, uint32_t n) {
   }
 }
 
-__device__ void cands_pad(int metric, Cands c, uint32_t from, uint32_t to) {
+__device__ void cands_fill(int metric, Cands c, uint32_t from, uint32_t to) {
   for (uint32_t x = from + threadIdx.x; x < to; x += blockDim.x) {
     c.s[x] = sentinel_score(metric);
-    c.id[x] = ~0ull;
+    c.r[x] = ~0ull;
     c.vi[x] = ~0u;
   }
 }
 
-// Loads `lists` consecutive partial lists of kk entries each (L2, bypassing
-// L1: other CTAs wrote them) into c[0, lists * kk), all loads in parallel.
-__device__ void cands_load(Cands c, const float* ps, const uint64_t* pid, const uint32_t* pvi,
-                           uint32_t n) {
-  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
-    c.s[x] = __ldcg(ps + x);
-    c.id[x] = __ldcg(reinterpret_cast<const unsigned long long*>(pid) + x);
-    c.vi[x] = __ldcg(pvi + x);
+// Loads `lists` global lists of kk entries (written by other CTAs: L2, not
+// L1) into lists of length m (padded with sentinels), then pads the list
+// count to `lists2`; all loads in flight together.
+__device__ void cands_load(int metric, Cands c, const float* ps, const uint64_t* pr,
+                           const uint32_t* pvi, uint32_t lists, uint32_t kk, uint32_t m,
+                           uint32_t lists2) {
+  const uint32_t lm = __ffs(m) - 1;
+  for (uint32_t x = threadIdx.x; x < lists2 << lm; x += blockDim.x) {
+    const uint32_t l = x >> lm, e = x & (m - 1);
+    if (l < lists && e < kk) {
+      const uint64_t g = static_cast<uint64_t>(l) * kk + e;
+      c.s[x] = __ldcg(ps + g);
+      c.r[x] = __ldcg(reinterpret_cast<const unsigned long long*>(pr) + g);
+      c.vi[x] = __ldcg(pvi + g);
+    } else {
+      c.s[x] = sentinel_score(metric);
+      c.r[x] = ~0ull;
+      c.vi[x] = ~0u;
+    }
   }
 }
 
@@ -833,46 +899,52 @@ __device__ void cands_rescore(int metric, Cands c, uint32_t n, const float* __re
 }
 
 // Scan epilogue, called by every thread once the warps [first, first + nw)
-// hold their top-kk (keys = host-store rows) in registers and `scratch` (cap
-// bytes, >= epilogue_scratch) is free:
-//   1. CTA:   the warps' lists, rows resolved to ids, sorted -> top-kk partial
-//   2. group: the last of each kGroup CTAs sorts the group's partials
-//   3. final: the last group sorts the group results, re-scores the survivors
-//             exactly (fp32 accumulation) and writes the top-k.
+// hold their top-kk (keys = host-store rows) in registers and `scratch`
+// (>= epilogue_scratch bytes) is free. Merges are merge-path trees over
+// sorted lists:
+//   1. CTA:   the nw warp lists -> the CTA's top-kk partial
+//   2. group: the last of each kGroup CTAs merges the group's partials
+//   3. final: the last group merges the group results, re-scores the
+//             survivors exactly (fp32 accumulation), resolves rows to ids and
+//             writes the top-k.
 // Tickets self-reset, so the same buffers serve the next launch.
 template <int KPL>
 __device__ void scan_epilogue(WarpTopK<KPL>& top, int metric, int k, int kk, bool rerank,
                               unsigned char* scratch, const ScanOut& out, const float* sq,
-                              const float* __restrict__ slab, const uint64_t* __restrict__ ids_all,
+                              const float* __restrict__ slab, const uint64_t* __restrict__ ids,
                               uint32_t d, uint64_t V, int first, int nw) {
   __shared__ bool last;
   const int warp = threadIdx.x >> 5;
   const uint32_t q = blockIdx.y, G = gridDim.x;
   const uint32_t ngroups = (G + kGroup - 1) / kGroup, g = blockIdx.x / kGroup;
   const uint32_t gsize = min(kGroup, G - g * kGroup);
-  const uint32_t cap = pow2_ceil(static_cast<uint32_t>(
-      (epilogue_scratch(nw, kk, G) - 16) / 16));
-  const Cands c = cands_at(scratch, cap);
+  const uint32_t m = pow2_ceil(static_cast<uint32_t>(kk));
+  const uint32_t cap = epilogue_entries(nw, kk, G);
+  Cands cur = cands_at(scratch, cap);
+  Cands alt = cands_at(scratch + cap * 16 + 16, cap);
   unsigned* tickets = out.ticket + static_cast<uint64_t>(q) * (kMaxGroups + 1);
 
   // ---- 1. CTA level ----
-  const bool holder = warp >= first && warp < first + nw;
-  if (holder) top.store(kk, c.s + (warp - first) * kk, c.id + (warp - first) * kk, c.vi + (warp - first) * kk);
-  uint32_t n = static_cast<uint32_t>(nw * kk), n2 = pow2_ceil(n);
-  cands_pad(metric, c, n, n2);
-  __syncthreads();
-  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) { // rows -> datastore ids
-    const uint64_t r = c.id[x];
-    c.id[x] = r == ~0ull ? ~0ull : __ldg(reinterpret_cast<const unsigned long long*>(ids_all) + r);
+  const uint32_t wl = pow2_ceil(static_cast<uint32_t>(nw));
+  if (warp >= first && warp < first + nw) {
+    const uint32_t o = (warp - first) * m;
+    top.store(kk, cur.s + o, cur.r + o, cur.vi + o);
+  }
+  for (uint32_t x = threadIdx.x; x < wl * m; x += blockDim.x) {
+    if ((x & (m - 1)) >= static_cast<uint32_t>(kk) || (x >> (__ffs(m) - 1)) >= static_cast<uint32_t>(nw)) {
+      cur.s[x] = sentinel_score(metric);
+      cur.r[x] = ~0ull;
+      cur.vi[x] = ~0u;
+    }
   }
   __syncthreads();
-  cands_sort(metric, c, n2);
+  merge_tree(metric, ids, &cur, &alt, wl, m);
   const uint64_t pbase = static_cast<uint64_t>(q) * G * kk;
   for (uint32_t x = threadIdx.x; x < static_cast<uint32_t>(kk); x += blockDim.x) {
     const uint64_t o = pbase + static_cast<uint64_t>(blockIdx.x) * kk + x;
-    out.part_s[o] = c.s[x];
-    out.part_id[o] = c.id[x];
-    out.part_vi[o] = c.vi[x];
+    out.part_s[o] = cur.s[x];
+    out.part_id[o] = cur.r[x];
+    out.part_vi[o] = cur.vi[x];
   }
   __threadfence();
   __syncthreads();
@@ -882,19 +954,18 @@ __device__ void scan_epilogue(WarpTopK<KPL>& top, int metric, int k, int kk, boo
   __threadfence();
 
   // ---- 2. group level ----
-  n = gsize * kk;
-  n2 = pow2_ceil(n);
   const uint64_t gofs = pbase + static_cast<uint64_t>(g) * kGroup * kk;
-  cands_load(c, out.part_s + gofs, out.part_id + gofs, out.part_vi + gofs, n);
-  cands_pad(metric, c, n, n2);
+  const uint32_t gl = pow2_ceil(gsize);
+  cands_load(metric, cur, out.part_s + gofs, out.part_id + gofs, out.part_vi + gofs, gsize, kk,
+             m, gl);
   __syncthreads();
-  cands_sort(metric, c, n2);
+  merge_tree(metric, ids, &cur, &alt, gl, m);
   const uint64_t gbase = static_cast<uint64_t>(q) * kMaxGroups * kk;
   for (uint32_t x = threadIdx.x; x < static_cast<uint32_t>(kk); x += blockDim.x) {
     const uint64_t o = gbase + static_cast<uint64_t>(g) * kk + x;
-    out.gpart_s[o] = c.s[x];
-    out.gpart_id[o] = c.id[x];
-    out.gpart_vi[o] = c.vi[x];
+    out.gpart_s[o] = cur.s[x];
+    out.gpart_id[o] = cur.r[x];
+    out.gpart_vi[o] = cur.vi[x];
   }
   __threadfence();
   __syncthreads();
@@ -904,23 +975,22 @@ __device__ void scan_epilogue(WarpTopK<KPL>& top, int metric, int k, int kk, boo
   __threadfence();
 
   // ---- 3. final ----
-  n = ngroups * kk;
-  n2 = pow2_ceil(n);
-  cands_load(c, out.gpart_s + gbase, out.gpart_id + gbase, out.gpart_vi + gbase, n);
-  cands_pad(metric, c, n, n2);
+  const uint32_t fl = pow2_ceil(ngroups);
+  cands_load(metric, cur, out.gpart_s + gbase, out.gpart_id + gbase, out.gpart_vi + gbase,
+             ngroups, kk, m, fl);
   __syncthreads();
-  cands_sort(metric, c, n2);
+  merge_tree(metric, ids, &cur, &alt, fl, m);
   const uint32_t navail = static_cast<uint32_t>(V < static_cast<uint64_t>(kk) ? V : kk);
   if (rerank && navail > 0) {
-    const uint32_t r2 = pow2_ceil(navail);
-    cands_pad(metric, c, navail, r2);
-    cands_rescore(metric, c, navail, slab, sq, d, first, nw);
+    cands_fill(metric, cur, navail, m);
+    cands_rescore(metric, cur, navail, slab, sq, d, first, nw);
     __syncthreads();
-    cands_sort(metric, c, r2);
+    cands_sort(metric, ids, cur, m);
   }
   for (uint32_t x = threadIdx.x; x < static_cast<uint32_t>(k); x += blockDim.x) {
-    out.out_s[static_cast<uint64_t>(q) * k + x] = c.s[x];
-    out.out_id[static_cast<uint64_t>(q) * k + x] = c.id[x];
+    const uint64_t r = cur.r[x];
+    out.out_s[static_cast<uint64_t>(q) * k + x] = cur.s[x];
+    out.out_id[static_cast<uint64_t>(q) * k + x] = r == ~0ull ? ~0ull : ids[r]; // row -> id
   }
   for (uint32_t x = threadIdx.x; x <= ngroups; x += blockDim.x) {
     tickets[x == ngroups ? kMaxGroups : x] = 0;
