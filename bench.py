@@ -418,9 +418,9 @@ def main():
     ap.add_argument("--sigma", type=float, default=None)
     ap.add_argument("--cpu-sample", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--acc", default="fp32", choices=["fp64", "fp32"],
-                    help="scan accumulation: fp32 FMA + exact fp64 re-score of the survivors "
-                         "(default) or fp64 for every candidate")
+    ap.add_argument("--acc", default="fp64", choices=["fp64", "fp32"],
+                    help="scan accumulation: fp64 for every candidate as the reference "
+                         "(default) or fp32 FMA + exact fp64 re-score of the survivors")
     ap.add_argument("--scan", default="tma", choices=["tma", "ldg"],
                     help="scan kernel: TMA bulk-copy staged (default) or direct LDG")
     args = ap.parse_args()

@@ -117,7 +117,7 @@ struct Ctx {
   const Index* ix = nullptr;
   int dev = 0;
   int sms = 148;
-  bool acc_fp64 = false;
+  bool acc_fp64 = true;
   ScanImpl scan_impl = ScanImpl::kTma;
   ScanTune tune{};
   cudaStream_t comp = nullptr, copy = nullptr, aux = nullptr;
@@ -753,7 +753,7 @@ uint64_t laivg_index_total_payload_bytes(const laivg_index* ix) {
 void laivg_opts_default(laivg_opts* o) {
   if (!o) return;
   std::memset(o, 0, sizeof(*o));
-  o->acc_fp64 = 0;
+  o->acc_fp64 = 1;
   o->scan_impl = 0;
 }
 

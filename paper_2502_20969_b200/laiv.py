@@ -235,7 +235,7 @@ class Device:
 
     def __init__(self, ix: IvfIndex, capacity_bytes: int, device: int = 0,
                  miss_threads: int = 0, max_batch: int = 0, max_probe: int = 0,
-                 acc_fp64: bool = False, scan_impl: str = "tma", tma_tile: int = 0,
+                 acc_fp64: bool = True, scan_impl: str = "tma", tma_tile: int = 0,
                  tma_stages: int = 0, ctas_per_sm: int = 0):
         L = lib()
         o = Opts()
