@@ -261,7 +261,7 @@ def config_block(cfg, args, sigma):
 # our arm
 # --------------------------------------------------------------------------
 def run_ours(args, cfg):
-    from paper_2502_20969_b200 import laiv
+    from paper_2502_20969_b200 import laiv, shard
 
     rank, world, local = dist_env()
     dist = None
@@ -289,7 +289,7 @@ def run_ours(args, cfg):
     sigma, cov = (args.sigma, None) if args.sigma else calibrate_sigma(laiv, dev, vecs, L)
     nq_total = (args.warmup + args.steps) * world + 8
     qi, qo, _ = laiv.synth_queries(QSEED, vecs, nq_total, sigma)
-    mine = np.arange(rank, nq_total, world)[: args.warmup + args.steps]
+    mine = shard.shard_indices(nq_total, rank, world)[: args.warmup + args.steps]
     dev.stage_queries(qo[mine])
     chan = laiv.TransferChannel(b_link, laiv.ChannelMode.Device)
     log(f"[bench] rank {rank}: B_link {b_link / 1e9:.1f} GB/s, budget {budget / 1e9:.2f} GB, "
@@ -336,12 +336,8 @@ def run_ours(args, cfg):
     lat_v = np.array([r["lat_value"] for r in rec])
     lat_e = np.array([r["lat_e2e"] for r in rec])
     sum_v, sum_e = float(lat_v.sum()), float(lat_e.sum())
-    if dist:
-        import torch
-
-        t = torch.tensor([sum_v, sum_e, wall], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        sum_v, sum_e, wall = (float(x) for x in t.tolist())
+    if dist:  # the slowest rank defines the job
+        sum_v, sum_e, wall = shard.max_over_ranks([sum_v, sum_e, wall], device="cuda")
     n_total = args.steps * world
     bytes_scan = sum(r["bytes"] for r in rec)
     t_scan = sum(r["t_scan"] for r in rec)

@@ -278,6 +278,11 @@ int laivg_assign_cache_aware(laivg_ctx* ctx, const uint64_t* batch_off,
                              const uint8_t* resident, uint32_t nw,
                              const float* queries, uint64_t nq, int L,
                              uint32_t* assignment_out);
+/* The greedy of assign_cache_aware (sched.cpp:114-142) over a precomputed
+ * row-major nb x nw overlap matrix: a multi-process router all-gathers the
+ * workers' resident sets, builds the matrix and every rank assigns alike. */
+int laivg_greedy_assign(const uint64_t* overlap, uint32_t nb, uint32_t nw,
+                        uint32_t* assignment_out);
 /* assign_round_robin (sched.cpp:146-155) */
 int laivg_assign_round_robin(uint64_t nb, uint64_t nw, uint32_t* out);
 /* assignment_overlap (sched.cpp:157-168) */

@@ -106,6 +106,7 @@ SIGNATURES = {
     "laivg_group_microbatches": (i32, [vp, u64, u32, u64, vp, vp, P(u32)]),
     "laivg_chunk_microbatches": (i32, [u64, u64, vp, vp, P(u32)]),
     "laivg_assign_cache_aware": (i32, [vp, vp, vp, u32, vp, u32, vp, u64, i32, vp]),
+    "laivg_greedy_assign": (i32, [vp, u32, u32, vp]),
     "laivg_assign_round_robin": (i32, [u64, u64, vp]),
     "laivg_assignment_overlap": (i32, [vp, vp, vp, u32, vp, u32, vp, vp, u64, i32, P(u64)]),
     "laivg_split_budget": (i32, [u64, vp, u64, vp]),

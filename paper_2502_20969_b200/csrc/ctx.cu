@@ -1223,6 +1223,20 @@ int laivg_assign_cache_aware(laivg_ctx* ctx, const uint64_t* batch_off, const ui
   });
 }
 
+int laivg_greedy_assign(const uint64_t* overlap, uint32_t nb, uint32_t nw,
+                        uint32_t* assignment_out) {
+  return guard([&] {
+    if (nw == 0) throw std::invalid_argument("need at least one worker");
+    if (nb) {
+      need(overlap, "overlap");
+      need(assignment_out, "assignment_out");
+    }
+    std::vector<uint64_t> ov(overlap, overlap + size_t(nb) * nw);
+    auto a = laivg::greedy_assign(ov, nb, nw);
+    std::copy(a.begin(), a.end(), assignment_out);
+  });
+}
+
 int laivg_assign_round_robin(uint64_t nb, uint64_t nw, uint32_t* out) {
   return guard([&] {
     if (nw == 0) throw std::invalid_argument("need at least one worker");

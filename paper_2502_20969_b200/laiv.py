@@ -555,6 +555,17 @@ def assign_cache_aware(dev: Device, batches: list[MicroBatch], workers: list[Wor
     return out[: len(batches)].tolist()
 
 
+def greedy_assign(overlap) -> list[int]:                          # sched.cpp:114-142
+    """assign_cache_aware's greedy over a precomputed [nb, nw] overlap matrix."""
+    ov = _c(overlap, np.uint64)
+    if ov.ndim != 2:
+        raise ValueError("overlap must be [batches, workers]")
+    nb, nw = ov.shape
+    out = np.empty(max(nb, 1), np.uint32)
+    check(lib().laivg_greedy_assign(ov.ctypes.data, nb, nw, out.ctypes.data))
+    return out[:nb].tolist()
+
+
 def assign_round_robin(n_batches: int, n_workers: int) -> list[int]:  # sched.hpp:48
     out = np.empty(max(n_batches, 1), np.uint32)
     check(lib().laivg_assign_round_robin(n_batches, n_workers, out.ctypes.data))
