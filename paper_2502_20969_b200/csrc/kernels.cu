@@ -667,6 +667,48 @@ __global__ void __launch_bounds__(1024)
     mv[x] = run_v[base + static_cast<uint64_t>(r) * kSeg + i];
   }
   __syncthreads();
+  if (!full) {
+    // prefix mode: merge-path tree, the best P of each pair per level (one
+    // co-rank binary search per output, one barrier per level)
+    uint64_t* ak = mk;
+    uint32_t* av = mv;
+    uint64_t* bk = reinterpret_cast<uint64_t*>(mv + total);
+    bk = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(bk) + 7) & ~uintptr_t(7));
+    uint32_t* bv = reinterpret_cast<uint32_t*>(bk + total);
+    for (uint32_t lists = nseg_pad; lists > 1; lists >>= 1) {
+      for (uint32_t x = threadIdx.x; x < (lists / 2) << lP; x += blockDim.x) {
+        const uint32_t pr = x >> lP, p = x & (P - 1);
+        const uint32_t A = 2 * pr * P, B = A + P;
+        uint32_t lo = 0, hi = p;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (!kv_gt(ak[A + mid], av[A + mid], ak[B + p - mid - 1], av[B + p - mid - 1])) {
+            lo = mid + 1;
+          } else {
+            hi = mid;
+          }
+        }
+        const uint32_t i = lo, j = p - i;
+        const bool from_a = j >= P || (i < P && !kv_gt(ak[A + i], av[A + i], ak[B + j], av[B + j]));
+        bk[pr * P + p] = from_a ? ak[A + i] : ak[B + j];
+        bv[pr * P + p] = from_a ? av[A + i] : av[B + j];
+      }
+      __syncthreads();
+      uint64_t* tk = ak;
+      ak = bk;
+      bk = tk;
+      uint32_t* tv = av;
+      av = bv;
+      bv = tv;
+    }
+    uint32_t* out = order + static_cast<uint64_t>(q) * n_out;
+    for (uint32_t i = threadIdx.x; i < n_out; i += blockDim.x) out[i] = av[i];
+    if (do_partition) {
+      __syncthreads();
+      partition_block(av, n_out, res_off, list_off, ft, q);
+    }
+    return;
+  }
   uint32_t nruns = nseg_pad, ls = lP, lm = lP;
   while (nruns > 1) {
     const uint32_t pairs = nruns >> 1, m = 1u << lm, stride = 1u << ls;
@@ -1481,7 +1523,9 @@ void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
     P = 1;
     while (P < n_out) P <<= 1;
   }
-  const size_t smem = size_t(nseg_pad) * P * (sizeof(uint64_t) + sizeof(uint32_t));
+  // prefix mode ping-pongs between two buffers
+  const size_t smem = size_t(nseg_pad) * P * (sizeof(uint64_t) + sizeof(uint32_t)) *
+                          (full ? 1 : 2) + 16;
   static size_t attr = 0;
   if (smem > attr) { // dynamic + the partition statics may pass 48 KB
     cudaFuncSetAttribute(merge_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
