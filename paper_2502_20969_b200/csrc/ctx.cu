@@ -163,8 +163,9 @@ struct Ctx {
   std::vector<float> staged_host;
 
   // events
-  cudaEvent_t ev_a, ev_b, ev_p, ev_s, ev_c, ev_probe, ev_base, ev_win, ev_cp0,
-      ev_cp1, ev_copy_tail, ev_comp_tail;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_p = nullptr, ev_s = nullptr, ev_c = nullptr,
+              ev_probe = nullptr, ev_base = nullptr, ev_win = nullptr, ev_cp0 = nullptr,
+              ev_cp1 = nullptr, ev_copy_tail = nullptr, ev_comp_tail = nullptr;
 
   std::unique_ptr<ThreadPool> pool;
 
@@ -208,6 +209,77 @@ struct Ctx {
   // quantizer picks min(L, nc) of them (hybrid/ivf search).
   Result search(const float* dq, const float* hq, int L, int k,
                 const std::vector<uint32_t>* explicit_probe);
+
+  // ---- the coarse -> select -> scan chain as one CUDA graph per (L, k) ----
+  std::map<uint64_t, cudaGraphExec_t> graphs;
+  bool use_graphs = true;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr; // capture-internal fork/join
+  void rec(cudaEvent_t e, cudaStream_t st) { // host-visible even inside a graph
+    CK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+  }
+  void enqueue_results(int k) {
+    CK(cudaMemcpyAsync(h_out_s, so.out_s, k * sizeof(float), cudaMemcpyDeviceToHost, comp));
+    CK(cudaMemcpyAsync(h_out_id, so.out_id, k * sizeof(uint64_t), cudaMemcpyDeviceToHost, comp));
+    CK(cudaMemcpyAsync(h_out_cnt, so.out_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, comp));
+    CK(cudaMemcpyAsync(h_fcount, ft.count, sizeof(uint32_t), cudaMemcpyDeviceToHost, comp));
+    rec(ev_c, comp);
+  }
+  // Query in d_Q: coarse scores, ranking + residency split, scan, results;
+  // the probe goes to the host on the aux stream as soon as it exists.
+  void enqueue_coarse_path(uint32_t lp, int k, int G) {
+    rec(ev_a, comp);
+    launch_coarse_scores(d_Q, 1, d_cen, ix->nc, ix->d, ix->metric, d_scores, comp);
+    launch_select(d_scores, 1, ix->nc, ix->metric, lp, d_order, d_run_k, d_run_v, d_res,
+                  d_list_off, &ft, comp);
+    rec(ev_b, comp);
+    CK(cudaEventRecord(ev_fork, comp));
+    CK(cudaStreamWaitEvent(aux, ev_fork, 0));
+    if (lp) {
+      CK(cudaMemcpyAsync(h_order, d_order, lp * sizeof(uint32_t), cudaMemcpyDeviceToHost, aux));
+    }
+    rec(ev_probe, aux);
+    CK(cudaEventRecord(ev_join, aux));
+    rec(ev_p, comp);
+    launch_scan(d_Q, 1, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl,
+                tune, comp);
+    rec(ev_s, comp);
+    CK(cudaStreamWaitEvent(comp, ev_join, 0));
+    enqueue_results(k);
+  }
+  void run_coarse_path(uint32_t lp, int k, int G) {
+    const uint64_t key = (uint64_t(lp) << 32) | uint32_t(k);
+    auto it = graphs.find(key);
+    if (it == graphs.end() && use_graphs) {
+      // first call for this shape runs eagerly (sets kernel attributes), then
+      // the chain is captured for the following calls
+      enqueue_coarse_path(lp, k, G);
+      cudaGraph_t g = nullptr;
+      cudaGraphExec_t ge = nullptr;
+      const uint64_t launched = launch_counter().load();
+      bool ok = cudaStreamBeginCapture(comp, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+      if (ok) {
+        try {
+          enqueue_coarse_path(lp, k, G);
+        } catch (...) {
+          ok = false;
+        }
+        ok = (cudaStreamEndCapture(comp, &g) == cudaSuccess) && ok && g != nullptr;
+      }
+      launch_counter() = launched; // captured launches did not run
+      ok = ok && cudaGraphInstantiate(&ge, g, 0) == cudaSuccess;
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      if (ok) graphs[key] = ge;
+      else use_graphs = false; // capture unsupported here: stay eager
+      return;
+    }
+    if (it != graphs.end()) {
+      CK(cudaGraphLaunch(it->second, comp));
+      launch_counter() += 4; // coarse, seg_sort, merge_runs, scan
+      return;
+    }
+    enqueue_coarse_path(lp, k, G);
+  }
 };
 
 Ctx::~Ctx() {
@@ -229,9 +301,10 @@ Ctx::~Ctx() {
                   (void*)h_out_cnt, (void*)h_fcount}) {
     if (p) cudaFreeHost(p);
   }
+  for (auto& [key, ge] : graphs) cudaGraphExecDestroy(ge);
   for (cudaEvent_t e : {ev_a, ev_b, ev_p, ev_s, ev_c, ev_probe, ev_base, ev_win,
                         ev_cp0, ev_cp1, ev_copy_tail, ev_comp_tail, res_ev[0],
-                        res_ev[1]}) {
+                        res_ev[1], ev_fork, ev_join}) {
     if (e) cudaEventDestroy(e);
   }
   if (comp) cudaStreamDestroy(comp);
@@ -273,7 +346,7 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   CK(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
   for (cudaEvent_t* e : {&ev_a, &ev_b, &ev_p, &ev_s, &ev_c, &ev_probe, &ev_base,
                          &ev_win, &ev_cp0, &ev_cp1, &ev_copy_tail, &ev_comp_tail,
-                         &res_ev[0], &res_ev[1]}) {
+                         &res_ev[0], &res_ev[1], &ev_fork, &ev_join}) {
     CK(cudaEventCreate(e));
   }
   CK(cudaEventRecord(ev_copy_tail, copy));
@@ -461,35 +534,26 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
   commit_res(comp);
   const int G = std::min(scan_grid_x(1, sms, scan_impl, tune), part_cap);
   ft.grid = static_cast<uint32_t>(G); // the partition step lays out G scan CTAs
-  CK(cudaEventRecord(ev_a, comp));
   if (explicit_probe) {
+    CK(cudaEventRecord(ev_a, comp));
     if (lp) {
       std::memcpy(h_order, explicit_probe->data(), lp * sizeof(uint32_t));
       CK(cudaMemcpyAsync(d_order, h_order, lp * sizeof(uint32_t), cudaMemcpyHostToDevice, comp));
     }
     CK(cudaEventRecord(ev_b, comp));
     launch_partition(d_order, 1, lp, d_res, d_list_off, ft, comp);
+    CK(cudaEventRecord(ev_p, comp));
+    launch_scan(dq, 1, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl,
+                tune, comp);
+    CK(cudaEventRecord(ev_s, comp));
+    enqueue_results(k);
   } else {
-    // coarse scores, then ranking + residency split fused in one CTA
-    launch_coarse_scores(dq, 1, d_cen, ix->nc, ix->d, ix->metric, d_scores, comp);
-    launch_select(d_scores, 1, ix->nc, ix->metric, lp, d_order, d_run_k, d_run_v, d_res,
-                  d_list_off, &ft, comp);
-    CK(cudaEventRecord(ev_b, comp));
-    if (lp) {
-      CK(cudaStreamWaitEvent(aux, ev_b, 0));
-      CK(cudaMemcpyAsync(h_order, d_order, lp * sizeof(uint32_t), cudaMemcpyDeviceToHost, aux));
-      CK(cudaEventRecord(ev_probe, aux));
+    // the query always runs from d_Q so one captured graph serves every call
+    if (dq != d_Q) {
+      CK(cudaMemcpyAsync(d_Q, dq, ix->d * sizeof(float), cudaMemcpyDeviceToDevice, comp));
     }
+    run_coarse_path(lp, k, G);
   }
-  CK(cudaEventRecord(ev_p, comp));
-  launch_scan(dq, 1, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl, tune,
-              comp);
-  CK(cudaEventRecord(ev_s, comp));
-  CK(cudaMemcpyAsync(h_out_s, so.out_s, k * sizeof(float), cudaMemcpyDeviceToHost, comp));
-  CK(cudaMemcpyAsync(h_out_id, so.out_id, k * sizeof(uint64_t), cudaMemcpyDeviceToHost, comp));
-  CK(cudaMemcpyAsync(h_out_cnt, so.out_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, comp));
-  CK(cudaMemcpyAsync(h_fcount, ft.count, sizeof(uint32_t), cudaMemcpyDeviceToHost, comp));
-  CK(cudaEventRecord(ev_c, comp));
 
   // Host: split the probe by residency (tiered.cpp:155-161) and scan the
   // misses while the GPU scans the hits.
