@@ -214,8 +214,12 @@ struct Ctx {
   std::map<uint64_t, cudaGraphExec_t> graphs;
   bool use_graphs = true;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr; // capture-internal fork/join
-  void rec(cudaEvent_t e, cudaStream_t st) { // host-visible even inside a graph
-    CK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+  bool capturing = false;
+  // Timing events stay host-visible inside a captured graph (external record
+  // nodes); the external flag is only legal while capturing.
+  void rec(cudaEvent_t e, cudaStream_t st) {
+    if (capturing) CK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+    else CK(cudaEventRecord(e, st));
   }
   void enqueue_results(int k) {
     CK(cudaMemcpyAsync(h_out_s, so.out_s, k * sizeof(float), cudaMemcpyDeviceToHost, comp));
@@ -258,11 +262,13 @@ struct Ctx {
       const uint64_t launched = launch_counter().load();
       bool ok = cudaStreamBeginCapture(comp, cudaStreamCaptureModeRelaxed) == cudaSuccess;
       if (ok) {
+        capturing = true;
         try {
           enqueue_coarse_path(lp, k, G);
         } catch (...) {
           ok = false;
         }
+        capturing = false;
         ok = (cudaStreamEndCapture(comp, &g) == cudaSuccess) && ok && g != nullptr;
       }
       launch_counter() = launched; // captured launches did not run

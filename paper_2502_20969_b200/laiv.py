@@ -13,6 +13,7 @@ RuntimeError, std::logic_error -> LogicError, CUDA failures -> CudaError.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 import enum
 from dataclasses import dataclass, field
 
@@ -169,11 +170,16 @@ class TieredStore:
     """The GPU cluster cache of a Device (tiered.hpp:22-56)."""
 
     def __init__(self, dev: "Device"):
-        self._dev = dev
+        # weak: a Device must be freed by refcount as soon as the caller drops
+        # it (its cluster cache can hold most of HBM)
+        self._dev = weakref.ref(dev)
 
     @property
     def _h(self):
-        return self._dev.h
+        dev = self._dev()
+        if dev is None or not dev.h:
+            raise LogicError("TieredStore used after its Device was closed")
+        return dev.h
 
     def capacity_bytes(self) -> int:
         return int(lib().laivg_store_capacity_bytes(self._h))

@@ -25,3 +25,12 @@ def laiv():
     from paper_2502_20969_b200 import laiv as m
 
     return m
+
+
+@pytest.fixture(autouse=True)
+def _free_devices():
+    """Device contexts own multi-GB HBM caches: collect them between tests."""
+    yield
+    import gc
+
+    gc.collect()
