@@ -108,7 +108,11 @@ typedef struct {
   uint32_t tma_tile;       /* vectors per TMA stage; 0 = auto (~48 KB) */
   uint32_t tma_stages;     /* TMA ring depth; 0 = auto (~192 KB ring) */
   uint32_t ctas_per_sm;    /* scan CTAs per SM; 0 = auto */
-  uint32_t reserved[4];
+  uint32_t coarse_impl;    /* 0 (default): tensor cores (tcgen05 tf32 GEMM +
+                              exact fp64 re-score of boundary candidates) for
+                              batches >= 8 queries, fp64 SIMT otherwise;
+                              1: always fp64 SIMT; 2: always tensor cores */
+  uint32_t reserved[3];
 } laivg_opts;
 void laivg_opts_default(laivg_opts* o);
 typedef struct laivg_ctx laivg_ctx;
@@ -260,6 +264,30 @@ int laivg_hybrid_search_staged(laivg_ctx* ctx, uint32_t qi, int L, int k,
                                uint64_t* ids_out, float* scores_out,
                                uint32_t* count_out, uint32_t* nfast_out,
                                laivg_hybrid_timing* timing);
+
+/* ---- batched retrieval (extension point (2) of SURVEY §8b: the reference
+ * loops hybrid_search over a batch, pipeline.cpp:391-428) ------------------
+ * hybrid_search for nq <= max_batch queries Q[nq*d] in one device pass: one
+ * coarse launch (tensor cores for nq >= 8), one residency split, one scan
+ * launch for the whole batch; the misses of all queries are scanned
+ * list-major on the host while the GPU scans the hits. Per query the result
+ * equals laivg_hybrid_search. ids_out/scores_out [nq*k], count_out [nq],
+ * nfast_out [nq] (nullable); timing (nullable) is for the whole batch. */
+int laivg_hybrid_search_batch(laivg_ctx* ctx, const float* Q, uint32_t nq, int L,
+                              int k, const laivg_cost_model* cost,
+                              uint64_t* ids_out, float* scores_out,
+                              uint32_t* count_out, uint32_t* nfast_out,
+                              laivg_hybrid_timing* timing);
+/* The same over staged queries [q0, q0 + nq) (inputs already in HBM). */
+int laivg_hybrid_search_batch_staged(laivg_ctx* ctx, uint32_t q0, uint32_t nq,
+                                     int L, int k, uint64_t* ids_out,
+                                     float* scores_out, uint32_t* count_out,
+                                     uint32_t* nfast_out,
+                                     laivg_hybrid_timing* timing);
+/* Diagnostics: the raw tf32 tensor-core scores approx_out[nq*nc] the batched
+ * coarse quantizer filters with (never reported as results). */
+int laivg_debug_coarse_approx(laivg_ctx* ctx, const float* Q, uint32_t nq,
+                              float* approx_out);
 
 /* ---- schedulers (sched.cpp) ---------------------------------------------- */
 /* group_microbatches (sched.cpp:39-70): order_out[n] holds the queries batch

@@ -31,7 +31,7 @@ class Opts(C.Structure):
     _fields_ = [("device", i32), ("capacity_bytes", u64), ("miss_threads", u32),
                 ("max_batch", u32), ("max_probe", u32), ("acc_fp64", u32),
                 ("scan_impl", u32), ("tma_tile", u32), ("tma_stages", u32),
-                ("ctas_per_sm", u32), ("reserved", u32 * 4)]
+                ("ctas_per_sm", u32), ("coarse_impl", u32), ("reserved", u32 * 3)]
 
 
 class Channel(C.Structure):
@@ -103,6 +103,11 @@ SIGNATURES = {
     "laivg_stage_queries": (i32, [vp, vp, u32]),
     "laivg_hybrid_search_staged": (i32, [vp, u32, i32, i32, vp, vp, P(u32), P(u32),
                                          P(HybridTimingC)]),
+    "laivg_hybrid_search_batch": (i32, [vp, vp, u32, i32, i32, vp, vp, vp, vp, vp,
+                                        P(HybridTimingC)]),
+    "laivg_hybrid_search_batch_staged": (i32, [vp, u32, u32, i32, i32, vp, vp, vp, vp,
+                                               P(HybridTimingC)]),
+    "laivg_debug_coarse_approx": (i32, [vp, vp, u32, vp]),
     "laivg_group_microbatches": (i32, [vp, u64, u32, u64, vp, vp, P(u32)]),
     "laivg_chunk_microbatches": (i32, [u64, u64, vp, vp, P(u32)]),
     "laivg_assign_cache_aware": (i32, [vp, vp, vp, u32, vp, u32, vp, u64, i32, vp]),

@@ -144,6 +144,11 @@ struct Ctx {
 
   // scratch
   uint32_t max_batch = 256, max_probe = 0;
+  // batched coarse quantizer on tensor cores (coarse_tc.cu)
+  uint32_t coarse_impl = 0; // 0 auto, 1 fp64 SIMT, 2 tensor cores
+  bool tc_ok = false;
+  float* d_approx = nullptr; // [max_batch][nc] tf32 scores
+  float* d_cnorm = nullptr;  // [nc] ||c|| rounded up
   float* d_Q = nullptr;
   double* d_scores = nullptr;
   uint32_t* d_order = nullptr;
@@ -197,7 +202,15 @@ struct Ctx {
   void clear_store();
 
   // ---- search --------------------------------------------------------------
-  void coarse(const float* dQ, uint32_t nq, uint32_t n_out, cudaStream_t st);
+  bool use_tc(uint32_t nq, uint32_t n_out) const {
+    if (coarse_impl == 1 || !tc_ok || n_out == 0) return false;
+    if (coarse_impl == 2) return true;
+    return nq >= kTcMinBatch && n_out < ix->nc;
+  }
+  // Coarse ranking prefix of nq queries into d_order[q * n_out + i]; with
+  // `part`, also the residency split into ft (ft.grid scan CTAs per query).
+  void coarse(const float* dQ, uint32_t nq, uint32_t n_out, cudaStream_t st, bool part = false,
+              bool need_scores = false);
   struct Result {
     std::vector<Scored> top;
     std::vector<uint32_t> fast, slow;
@@ -209,6 +222,16 @@ struct Ctx {
   // quantizer picks min(L, nc) of them (hybrid/ivf search).
   Result search(const float* dq, const float* hq, int L, int k,
                 const std::vector<uint32_t>* explicit_probe);
+  // Batched hybrid search of nq <= max_batch queries (dQ on device, hQ on
+  // host): one coarse + partition launch and one scan launch for the batch,
+  // the misses scanned list-major on the host while the GPU scans the hits.
+  struct BatchResult {
+    std::vector<std::vector<Scored>> top;
+    std::vector<uint32_t> nfast, nslow;
+    double t_g = 0, t_c = 0, t_2 = 0, t_coarse = 0, t_scan = 0;
+    uint64_t vecs_gpu = 0, bytes_gpu = 0;
+  };
+  BatchResult search_batch(const float* dQ, const float* hQ, uint32_t nq, int L, int k);
 
   // ---- the coarse -> select -> scan chain as one CUDA graph per (L, k) ----
   std::map<uint64_t, cudaGraphExec_t> graphs;
@@ -299,7 +322,7 @@ Ctx::~Ctx() {
                   (void*)so.part_s, (void*)so.part_id, (void*)so.part_vi, (void*)so.ticket,
                   (void*)so.gpart_s, (void*)so.gpart_id, (void*)so.gpart_vi,
                   (void*)so.out_s, (void*)so.out_id, (void*)so.out_count,
-                  (void*)d_staged}) {
+                  (void*)d_staged, (void*)d_approx, (void*)d_cnorm}) {
     if (p) cudaFree(p);
   }
   for (void* p : {(void*)res_stage[0], (void*)res_stage[1], (void*)h_Q,
@@ -383,10 +406,31 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   for (uint32_t c = 0; c < nc; ++c) maxlen = std::max(maxlen, ix->list_len(c));
   tmp_vecs = maxlen;
 
+  coarse_impl = o.coarse_impl;
+  if (coarse_impl > 2) throw std::invalid_argument("coarse_impl must be 0 (auto), 1 or 2");
+  tc_ok = coarse_tc_supported(nc, d);
+  if (coarse_impl == 2 && !tc_ok) {
+    throw std::invalid_argument("tensor-core coarse quantizer needs d % 4 == 0 and nc <= " +
+                                std::to_string(kTcMaxNc));
+  }
   max_batch = o.max_batch ? o.max_batch : 256;
   max_probe = o.max_probe ? std::min(o.max_probe, nc) : nc;
   if (max_probe == 0) max_probe = 1;
   d_Q = dev_alloc<float>(size_t(max_batch) * d);
+  if (tc_ok) {
+    d_approx = dev_alloc<float>(size_t(max_batch) * nc);
+    std::vector<float> cn(nc);
+    for (uint32_t c = 0; c < nc; ++c) {
+      double s2 = 0.0;
+      for (uint32_t j = 0; j < d; ++j) {
+        const double x = ix->centroids[size_t(c) * d + j];
+        s2 += x * x;
+      }
+      cn[c] = std::nextafter(static_cast<float>(std::sqrt(s2) * (1.0 + 1e-9)), INFINITY);
+    }
+    d_cnorm = dev_alloc<float>(nc);
+    CK(cudaMemcpy(d_cnorm, cn.data(), nc * sizeof(float), cudaMemcpyHostToDevice));
+  }
   d_scores = dev_alloc<double>(size_t(max_batch) * nc);
   d_order = dev_alloc<uint32_t>(size_t(max_batch) * std::max(nc, 1u));
   d_run_k = dev_alloc<uint64_t>(select_scratch_entries(max_batch, nc));
@@ -504,11 +548,113 @@ void Ctx::clear_store() {
   res_dirty = true;
 }
 
-void Ctx::coarse(const float* dQ, uint32_t nq, uint32_t n_out, cudaStream_t st) {
+void Ctx::coarse(const float* dQ, uint32_t nq, uint32_t n_out, cudaStream_t st, bool part,
+                 bool need_scores) {
+  const FastTable* f = part ? &ft : nullptr;
+  if (!need_scores && use_tc(nq, n_out)) {
+    launch_coarse_tc(dQ, nq, d_cen, ix->nc, ix->d, d_approx, st);
+    launch_tc_select(d_approx, dQ, nq, ix->d, d_cen, d_cnorm, ix->nc, ix->metric, n_out,
+                     d_order, part ? d_res : nullptr, part ? d_list_off : nullptr, f, st);
+    return;
+  }
   launch_coarse_scores(dQ, nq, d_cen, ix->nc, ix->d, ix->metric, d_scores, st);
-  launch_select(d_scores, nq, ix->nc, ix->metric, n_out, d_order, d_run_k, d_run_v, nullptr,
-                nullptr, nullptr,
-                st);
+  launch_select(d_scores, nq, ix->nc, ix->metric, n_out, d_order, d_run_k, d_run_v,
+                part ? d_res : nullptr, part ? d_list_off : nullptr, f, st);
+}
+
+Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq, int L,
+                                   int k) {
+  if (k < 1) throw std::invalid_argument("k must be >= 1");
+  if (k > kMaxK) {
+    throw std::invalid_argument("k = " + std::to_string(k) +
+                                " exceeds the device top-k limit " + std::to_string(kMaxK));
+  }
+  if (nq > max_batch) throw std::invalid_argument("batch exceeds the context's max_batch");
+  const auto t0 = Clock::now();
+  BatchResult r;
+  r.top.resize(nq);
+  r.nfast.assign(nq, 0);
+  r.nslow.assign(nq, 0);
+  const uint32_t lp = uint32_t(std::min<int64_t>(std::max(L, 0), ix->nc));
+  if (lp > max_probe) {
+    throw std::invalid_argument("probe of " + std::to_string(lp) +
+                                " clusters exceeds the context's max_probe " +
+                                std::to_string(max_probe));
+  }
+  if (nq == 0) return r;
+  if (lp == 0) {
+    r.t_2 = secs(t0, Clock::now());
+    return r;
+  }
+  CK(cudaStreamWaitEvent(comp, ev_copy_tail, 0));
+  commit_res(comp);
+  const int G = std::max(1, std::min(scan_grid_x(nq, sms, scan_impl, tune), part_cap / int(nq)));
+  ft.grid = static_cast<uint32_t>(G);
+  rec(ev_a, comp);
+  coarse(dQ, nq, lp, comp, /*part=*/true);
+  rec(ev_b, comp);
+  CK(cudaEventRecord(ev_fork, comp));
+  CK(cudaStreamWaitEvent(aux, ev_fork, 0));
+  CK(cudaMemcpyAsync(h_order, d_order, size_t(nq) * lp * sizeof(uint32_t),
+                     cudaMemcpyDeviceToHost, aux));
+  rec(ev_probe, aux);
+  rec(ev_p, comp);
+  launch_scan(dQ, nq, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl, tune,
+              comp);
+  rec(ev_s, comp);
+  CK(cudaMemcpyAsync(h_out_s, so.out_s, size_t(nq) * k * sizeof(float), cudaMemcpyDeviceToHost,
+                     comp));
+  CK(cudaMemcpyAsync(h_out_id, so.out_id, size_t(nq) * k * sizeof(uint64_t),
+                     cudaMemcpyDeviceToHost, comp));
+  CK(cudaMemcpyAsync(h_out_cnt, so.out_count, nq * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                     comp));
+  CK(cudaMemcpyAsync(h_fcount, ft.count, nq * sizeof(uint32_t), cudaMemcpyDeviceToHost, comp));
+  rec(ev_c, comp);
+
+  // host: split every probe by residency and scan the misses list-major
+  CK(cudaEventSynchronize(ev_probe));
+  std::vector<std::vector<uint32_t>> slow(nq);
+  bool any_slow = false;
+  for (uint32_t q = 0; q < nq; ++q) {
+    for (uint32_t i = 0; i < lp; ++i) {
+      const uint32_t c = h_order[size_t(q) * lp + i];
+      if (h_res[c] >= 0) {
+        ++r.nfast[q];
+        r.vecs_gpu += ix->list_len(c);
+        r.bytes_gpu += ix->cluster_bytes(c);
+      } else {
+        slow[q].push_back(c);
+        any_slow = true;
+      }
+    }
+    r.nslow[q] = uint32_t(slow[q].size());
+  }
+  std::vector<std::vector<Scored>> miss(nq);
+  if (any_slow) {
+    const auto tc = Clock::now();
+    miss = miss_scan_batch(*ix, hQ, nq, slow, k, *pool);
+    r.t_c = secs(tc, Clock::now());
+  }
+  CK(cudaEventSynchronize(ev_c));
+  for (uint32_t q = 0; q < nq; ++q) {
+    if (h_fcount[q] != r.nfast[q]) {
+      throw std::runtime_error("device residency table disagrees with the store");
+    }
+    std::vector<Scored> gpu(h_out_cnt[q]);
+    for (uint32_t i = 0; i < h_out_cnt[q]; ++i) {
+      gpu[i] = {h_out_s[size_t(q) * k + i], h_out_id[size_t(q) * k + i]};
+    }
+    r.top[q] = merge_topk(ix->metric, gpu, miss[q], k);
+  }
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, ev_a, ev_s));
+  r.t_g = ms * 1e-3;
+  CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
+  r.t_coarse = ms * 1e-3;
+  CK(cudaEventElapsedTime(&ms, ev_p, ev_s));
+  r.t_scan = ms * 1e-3;
+  r.t_2 = secs(t0, Clock::now());
+  return r;
 }
 
 Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
@@ -680,6 +826,36 @@ void write_top(const std::vector<laivg::Scored>& top, int k, uint64_t* ids,
     scores[i] = std::nanf("");
   }
   if (count) *count = uint32_t(top.size());
+}
+
+void stage_batch(Ctx& c, const float* Q, uint32_t nq) {
+  const size_t n = size_t(nq) * c.ix->d;
+  std::memcpy(c.h_Q, Q, n * sizeof(float));
+  CK(cudaMemcpyAsync(c.d_Q, c.h_Q, n * sizeof(float), cudaMemcpyHostToDevice, c.comp));
+}
+
+void fill_batch_timing(laivg_hybrid_timing* t, const Ctx::BatchResult& r,
+                       const laivg_cost_model* cost) {
+  if (!t) return;
+  t->t_g = r.t_g;
+  t->t_c = r.t_c;
+  t->t_2 = r.t_2;
+  t->t_coarse = r.t_coarse;
+  t->t_scan = r.t_scan;
+  t->scanned_vectors = r.vecs_gpu;
+  t->scanned_bytes = r.bytes_gpu;
+  if (cost) { // tiered.cpp:190-196 summed over the batch
+    double miss = 0, hit = 0;
+    for (size_t q = 0; q < r.nfast.size(); ++q) {
+      miss += r.nslow[q];
+      hit += r.nfast[q];
+    }
+    t->model_t_c = std::ceil(miss / cost->parallel_slots) * cost->t_cc;
+    t->model_t_g = hit * cost->t_gc;
+    t->model_t_2 = std::max(t->model_t_c, t->model_t_g);
+  } else {
+    t->model_t_c = t->model_t_g = t->model_t_2 = 0.0;
+  }
 }
 
 void stage_query(Ctx& c, const float* q) {
@@ -866,7 +1042,7 @@ void coarse_batch(Ctx& c, const float* Q, uint32_t nq, uint32_t n_out,
     const uint32_t b = std::min(c.max_batch, nq - q0);
     std::memcpy(c.h_Q, Q + size_t(q0) * d, size_t(b) * d * sizeof(float));
     CK(cudaMemcpyAsync(c.d_Q, c.h_Q, size_t(b) * d * sizeof(float), cudaMemcpyHostToDevice, c.comp));
-    c.coarse(c.d_Q, b, n_out, c.comp);
+    c.coarse(c.d_Q, b, n_out, c.comp, false, scores_out != nullptr);
     if (n_out) {
       CK(cudaMemcpyAsync(c.h_order, c.d_order, size_t(b) * n_out * sizeof(uint32_t),
                          cudaMemcpyDeviceToHost, c.comp));
@@ -926,12 +1102,22 @@ int laivg_ivf_search(laivg_ctx* ctx, const float* Q, uint32_t nq, int L, int k, 
     need(ids_out, "ids_out");
     need(scores_out, "scores_out");
     Ctx& c = ctx->c;
-    for (uint32_t i = 0; i < nq; ++i) {
-      const float* q = Q + size_t(i) * c.ix->d;
-      stage_query(c, q);
-      auto r = c.search(c.d_Q, q, L, k, nullptr);
-      write_top(r.top, k, ids_out + size_t(i) * k, scores_out + size_t(i) * k,
-                count_out ? count_out + i : nullptr);
+    if (nq) need(Q, "queries");
+    if (nq == 1) {
+      stage_query(c, Q);
+      auto r = c.search(c.d_Q, Q, L, k, nullptr);
+      write_top(r.top, k, ids_out, scores_out, count_out);
+      return;
+    }
+    for (uint32_t q0 = 0; q0 < nq; q0 += c.max_batch) {
+      const uint32_t b = std::min(c.max_batch, nq - q0);
+      const float* Qb = Q + size_t(q0) * c.ix->d;
+      stage_batch(c, Qb, b);
+      auto r = c.search_batch(c.d_Q, Qb, b, L, k);
+      for (uint32_t i = 0; i < b; ++i) {
+        write_top(r.top[i], k, ids_out + size_t(q0 + i) * k, scores_out + size_t(q0 + i) * k,
+                  count_out ? count_out + q0 + i : nullptr);
+      }
     }
   });
 }
@@ -1221,6 +1407,69 @@ int laivg_hybrid_search_staged(laivg_ctx* ctx, uint32_t qi, int L, int k, uint64
     if (ids_out && scores_out) write_top(r.top, k, ids_out, scores_out, count_out);
     if (nfast_out) *nfast_out = uint32_t(r.fast.size());
     fill_timing(timing, r, nullptr);
+  });
+}
+
+int laivg_hybrid_search_batch(laivg_ctx* ctx, const float* Q, uint32_t nq, int L, int k,
+                              const laivg_cost_model* cost, uint64_t* ids_out,
+                              float* scores_out, uint32_t* count_out, uint32_t* nfast_out,
+                              laivg_hybrid_timing* timing) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    if (k < 1) throw std::invalid_argument("k must be >= 1");
+    need(ids_out, "ids_out");
+    need(scores_out, "scores_out");
+    if (nq) need(Q, "queries");
+    Ctx& c = ctx->c;
+    if (nq > c.max_batch) throw std::invalid_argument("batch exceeds the context's max_batch");
+    stage_batch(c, Q, nq);
+    auto r = c.search_batch(c.d_Q, Q, nq, L, k);
+    for (uint32_t i = 0; i < nq; ++i) {
+      write_top(r.top[i], k, ids_out + size_t(i) * k, scores_out + size_t(i) * k,
+                count_out ? count_out + i : nullptr);
+      if (nfast_out) nfast_out[i] = r.nfast[i];
+    }
+    fill_batch_timing(timing, r, cost);
+  });
+}
+
+int laivg_hybrid_search_batch_staged(laivg_ctx* ctx, uint32_t q0, uint32_t nq, int L, int k,
+                                     uint64_t* ids_out, float* scores_out, uint32_t* count_out,
+                                     uint32_t* nfast_out, laivg_hybrid_timing* timing) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    Ctx& c = ctx->c;
+    if (uint64_t(q0) + nq > c.n_staged) throw std::invalid_argument("staged range out of range");
+    if (nq > c.max_batch) throw std::invalid_argument("batch exceeds the context's max_batch");
+    const size_t off = size_t(q0) * c.ix->d;
+    auto r = c.search_batch(c.d_staged + off, c.staged_host.data() + off, nq, L, k);
+    for (uint32_t i = 0; i < nq; ++i) {
+      if (ids_out && scores_out) {
+        write_top(r.top[i], k, ids_out + size_t(i) * k, scores_out + size_t(i) * k,
+                  count_out ? count_out + i : nullptr);
+      }
+      if (nfast_out) nfast_out[i] = r.nfast[i];
+    }
+    fill_batch_timing(timing, r, nullptr);
+  });
+}
+
+int laivg_debug_coarse_approx(laivg_ctx* ctx, const float* Q, uint32_t nq, float* approx_out) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    need(Q, "queries");
+    need(approx_out, "approx_out");
+    Ctx& c = ctx->c;
+    if (!c.tc_ok) throw std::invalid_argument("tensor-core coarse quantizer unsupported here");
+    const uint32_t nc = c.ix->nc;
+    for (uint32_t q0 = 0; q0 < nq; q0 += c.max_batch) {
+      const uint32_t b = std::min(c.max_batch, nq - q0);
+      stage_batch(c, Q + size_t(q0) * c.ix->d, b);
+      laivg::launch_coarse_tc(c.d_Q, b, c.d_cen, nc, c.ix->d, c.d_approx, c.comp);
+      CK(cudaMemcpyAsync(approx_out + size_t(q0) * nc, c.d_approx, size_t(b) * nc * sizeof(float),
+                         cudaMemcpyDeviceToHost, c.comp));
+      CK(cudaStreamSynchronize(c.comp));
+    }
   });
 }
 

@@ -165,6 +165,52 @@ std::vector<Scored> miss_scan(const Index& ix, const float* q,
   return std::move(all.e);
 }
 
+std::vector<std::vector<Scored>> miss_scan_batch(const Index& ix, const float* Q, uint32_t nq,
+                                                 const std::vector<std::vector<uint32_t>>& slow,
+                                                 int k, ThreadPool& pool) {
+  // list-major: every missed list is streamed once per chunk and scored
+  // against all queries that miss it
+  std::map<uint32_t, std::vector<uint32_t>> by_list;
+  for (uint32_t q = 0; q < nq; ++q) {
+    for (uint32_t c : slow[q]) by_list[c].push_back(q);
+  }
+  struct Task {
+    uint64_t r0, r1;
+    const std::vector<uint32_t>* qs;
+  };
+  std::vector<Task> tasks;
+  for (auto& [c, qs] : by_list) {
+    for (uint64_t r = ix.list_off[c]; r < ix.list_off[c + 1]; r += kMissChunk) {
+      tasks.push_back({r, std::min(r + kMissChunk, ix.list_off[c + 1]), &qs});
+    }
+  }
+  const unsigned nw = pool.size();
+  std::vector<TopList> per(size_t(nw) * nq, TopList{ix.metric, k, {}});
+  const uint32_t d = ix.d;
+  pool.parallel_for(tasks.size(), [&](size_t t, unsigned wid) {
+    const Task& tk = tasks[t];
+    for (uint64_t r = tk.r0; r < tk.r1; ++r) {
+      const float* x = ix.vecs + r * d;
+      for (uint32_t q : *tk.qs) {
+        const float* qv = Q + size_t(q) * d;
+        const float s = ix.metric == kMetricIP
+                            ? static_cast<float>(dot_f64(qv, x, d))
+                            : static_cast<float>(std::sqrt(l2sq_f64(qv, x, d)));
+        per[size_t(wid) * nq + q].push({s, ix.ids[r]});
+      }
+    }
+  });
+  std::vector<std::vector<Scored>> out(nq);
+  for (uint32_t q = 0; q < nq; ++q) {
+    TopList all{ix.metric, k, {}};
+    for (unsigned w = 0; w < nw; ++w) {
+      for (const auto& e : per[size_t(w) * nq + q].e) all.push(e);
+    }
+    out[q] = std::move(all.e);
+  }
+  return out;
+}
+
 std::vector<Scored> merge_topk(int metric, const std::vector<Scored>& a,
                                const std::vector<Scored>& b, int k) {
   std::vector<Scored> out;

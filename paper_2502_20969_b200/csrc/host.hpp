@@ -82,6 +82,13 @@ std::vector<Scored> miss_scan(const Index& ix, const float* q,
                               const std::vector<uint32_t>& lists, int k,
                               ThreadPool& pool);
 
+// Batched miss path: slow[q] are the missed lists of query q (rows of Q).
+// List-major: each missed list is read once and scored for every query that
+// misses it. Returns each query's best-k, best-first.
+std::vector<std::vector<Scored>> miss_scan_batch(const Index& ix, const float* Q, uint32_t nq,
+                                                 const std::vector<std::vector<uint32_t>>& slow,
+                                                 int k, ThreadPool& pool);
+
 // Best-k merge of two best-first lists (the hybrid merge, tiered.cpp:172-185:
 // a global sort of the concatenation truncated to k equals this merge).
 std::vector<Scored> merge_topk(int metric, const std::vector<Scored>& a,

@@ -39,14 +39,10 @@
 
 #include "host.hpp"
 #include "kernels.cuh"
+#include "dev_common.cuh"
 
 namespace laivg {
-namespace {
-
-constexpr int kIP = 0;
-constexpr unsigned kFull = 0xffffffffu;
-
-__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+using namespace dev;
 
 // Counts the launch and surfaces launch-configuration errors immediately.
 void after_launch() {
@@ -57,124 +53,7 @@ void after_launch() {
   }
 }
 
-// --------------------------------------------------------------------------
-// scoring terms
-// --------------------------------------------------------------------------
-__device__ __forceinline__ double term_ip_d(double q, float x, double acc) {
-  return __fma_rn(q, static_cast<double>(x), acc); // exact product: == mul+add
-}
-__device__ __forceinline__ double term_l2_d(double q, float x, double acc) {
-  const double t = __dsub_rn(q, static_cast<double>(x));
-  return __dadd_rn(acc, __dmul_rn(t, t));
-}
-__device__ __forceinline__ float term_ip_f(float q, float x, float acc) {
-  return __fmaf_rn(q, x, acc);
-}
-__device__ __forceinline__ float term_l2_f(float q, float x, float acc) {
-  const float t = q - x;
-  return __fmaf_rn(t, t, acc);
-}
-
-template <typename T>
-__device__ __forceinline__ T warp_sum(T v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  return v;
-}
-
-template <typename ACC>
-__device__ __forceinline__ float finish_score(int metric, ACC acc) {
-  if (metric == kIP) return static_cast<float>(acc);
-  return static_cast<float>(sqrt(static_cast<double>(acc)));
-}
-
-__device__ __forceinline__ float4 ldg_stream(const float4* p) {
-  float4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-               : "l"(p));
-  return r;
-}
-
-// Accumulates one float4 of a row into acc with the metric's term.
-template <bool kFp64>
-struct Acc4;
-template <>
-struct Acc4<true> {
-  __device__ __forceinline__ static void run(int metric, const double* q, float4 x,
-                                             double& a) {
-    if (metric == kIP) {
-      a = term_ip_d(q[0], x.x, a);
-      a = term_ip_d(q[1], x.y, a);
-      a = term_ip_d(q[2], x.z, a);
-      a = term_ip_d(q[3], x.w, a);
-    } else {
-      a = term_l2_d(q[0], x.x, a);
-      a = term_l2_d(q[1], x.y, a);
-      a = term_l2_d(q[2], x.z, a);
-      a = term_l2_d(q[3], x.w, a);
-    }
-  }
-};
-template <>
-struct Acc4<false> {
-  __device__ __forceinline__ static void run(int metric, const float* q, float4 x, float& a) {
-    if (metric == kIP) {
-      a = term_ip_f(q[0], x.x, a);
-      a = term_ip_f(q[1], x.y, a);
-      a = term_ip_f(q[2], x.z, a);
-      a = term_ip_f(q[3], x.w, a);
-    } else {
-      a = term_l2_f(q[0], x.x, a);
-      a = term_l2_f(q[1], x.y, a);
-      a = term_l2_f(q[2], x.z, a);
-      a = term_l2_f(q[3], x.w, a);
-    }
-  }
-};
-
-// --------------------------------------------------------------------------
-// mbarrier + bulk copy (TMA) primitives
-// --------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
+namespace {
 
 // --------------------------------------------------------------------------
 // total order (vectorstore.hpp:34-39)
@@ -516,13 +395,6 @@ __global__ void __launch_bounds__(256)
 // selection: block bitonic sort of (orderable key, cluster id); strides below
 // E stay in registers, below 32E use warp shuffles, the rest shared memory
 // --------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t order_key(double s, int metric) {
-  s = s + 0.0;                      // -0.0 -> +0.0: equal scores tie on id
-  if (metric == kIP) s = -s;        // descending -> ascending
-  const uint64_t b = static_cast<uint64_t>(__double_as_longlong(s));
-  return (b >> 63) ? ~b : (b | (1ull << 63));
-}
-
 __device__ __forceinline__ bool kv_gt(uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
   return ka > kb || (ka == kb && va > vb);
 }
@@ -741,6 +613,175 @@ __global__ void __launch_bounds__(1024)
   if (do_partition) {
     __syncthreads();
     partition_block(mv, n_out, res_off, list_off, ft, q);
+  }
+}
+
+
+// --------------------------------------------------------------------------
+// exact selection from tensor-core scores (batched coarse_probe)
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t float_order(float f) { // ascending with f
+  const uint32_t b = __float_as_uint(f + 0.0f);
+  return (b >> 31) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float order_float(uint32_t u) {
+  return __uint_as_float((u >> 31) ? (u & 0x7fffffffu) : ~u);
+}
+
+// Bounds on the exact "goodness" g (IP: score, L2: -squared distance) of
+// centroid c from its tensor-core score a: g in [lo, hi].
+__device__ __forceinline__ void tc_bounds(int metric, float a, double qn, double qn2, float cn,
+                                          float& lo, float& hi) {
+  const double cnd = cn;
+  double g, e;
+  if (metric == kIP) {
+    g = a;
+    e = kTcErr * qn * cnd;
+  } else {
+    const double cn2 = cnd * cnd;
+    g = -(qn2 + cn2 - 2.0 * static_cast<double>(a));
+    e = 2.0 * kTcErr * qn * cnd + 1e-6 * (qn2 + cn2);
+  }
+  lo = __double2float_rd(g - e);
+  hi = __double2float_ru(g + e);
+}
+
+// One CTA per query. smem: q[d], 32-bit keys of the lower bounds[nc],
+// candidate keys/ids[cap] (cap = pow2 >= nc, so every centroid fits).
+__global__ void __launch_bounds__(1024)
+    tc_select_kernel(const float* __restrict__ approx, const float* __restrict__ Q, uint32_t d,
+                     const float* __restrict__ cen, const float* __restrict__ cnorm,
+                     uint32_t nc, int metric, uint32_t n_out, uint32_t cap,
+                     uint32_t* __restrict__ order, const int64_t* res_off,
+                     const uint64_t* list_off, FastTable ft, bool do_partition) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  float* sq = reinterpret_cast<float*>(sm);
+  uint32_t* lok = reinterpret_cast<uint32_t*>(sm + ((static_cast<size_t>(d) * 4 + 15) & ~size_t(15)));
+  uint64_t* ck = reinterpret_cast<uint64_t*>(
+      reinterpret_cast<unsigned char*>(lok) + ((static_cast<size_t>(nc) * 4 + 15) & ~size_t(15)));
+  uint32_t* cv = reinterpret_cast<uint32_t*>(ck + cap);
+  __shared__ uint32_t hist[256];
+  __shared__ double red[32];
+  __shared__ uint32_t s_prefix, s_rank, s_count;
+  const uint32_t q = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* qv = Q + static_cast<uint64_t>(q) * d;
+  const float* aq = approx + static_cast<uint64_t>(q) * nc;
+
+  // ||q||^2 in fp64
+  double part = 0.0;
+  for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) {
+    const float x = qv[i];
+    sq[i] = x;
+    part += static_cast<double>(x) * x;
+  }
+  part = warp_sum(part);
+  if (lane == 0) red[warp] = part;
+  if (threadIdx.x == 0) {
+    s_prefix = 0;
+    s_rank = n_out - 1;
+    s_count = 0;
+  }
+  __syncthreads();
+  double qn2 = 0.0;
+  for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) qn2 += red[w];
+  const double qn = sqrt(qn2) * (1.0 + 1e-12);
+
+  // lower-bound keys, inverted so that ascending key = best first
+  for (uint32_t c = threadIdx.x; c < nc; c += blockDim.x) {
+    float lo, hi;
+    tc_bounds(metric, aq[c], qn, qn2, cnorm[c], lo, hi);
+    lok[c] = ~float_order(lo);
+  }
+  // radix select: the (n_out-1)-th smallest key, 8 bits at a time
+  uint32_t mask = 0;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const uint32_t prefix = s_prefix;
+    for (uint32_t c = threadIdx.x; c < nc; c += blockDim.x) {
+      const uint32_t key = lok[c];
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t h[8], tot = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        h[i] = hist[lane * 8 + i];
+        tot += h[i];
+      }
+      uint32_t inc = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += t;
+      }
+      const uint32_t rank = s_rank, excl = inc - tot;
+      if (rank >= excl && rank < inc) { // exactly one lane
+        uint32_t r = rank - excl, b = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (r >= h[i] && b == static_cast<uint32_t>(i)) {
+            r -= h[i];
+            ++b;
+          }
+        }
+        s_rank = r;
+        s_prefix = prefix | ((lane * 8u + b) << shift);
+      }
+    }
+    mask |= 255u << shift;
+    __syncthreads();
+  }
+  const float T = order_float(~s_prefix); // the n_out-th best lower bound
+
+  // candidates: upper bound reaches T (includes every exact top-n_out member)
+  for (uint32_t c = threadIdx.x; c < nc; c += blockDim.x) {
+    float lo, hi;
+    tc_bounds(metric, aq[c], qn, qn2, cnorm[c], lo, hi);
+    if (hi >= T) cv[atomicAdd(&s_count, 1u)] = c;
+  }
+  __syncthreads();
+  const uint32_t n = s_count;
+  uint32_t m = 2;
+  while (m < n) m <<= 1;
+  // exact fp64 re-score (same arithmetic as coarse_scores_kernel)
+  for (uint32_t i = warp; i < n; i += blockDim.x >> 5) {
+    const uint32_t c = cv[i];
+    const double sc = warp_coarse_score(sq, cen + static_cast<uint64_t>(c) * d, d, metric, lane);
+    if (lane == 0) ck[i] = order_key(sc, metric);
+  }
+  for (uint32_t i = n + threadIdx.x; i < m; i += blockDim.x) {
+    ck[i] = ~0ull;
+    cv[i] = ~0u;
+  }
+  __syncthreads();
+  // bitonic sort on (key, cluster id)
+  for (uint32_t kk = 2; kk <= m; kk <<= 1) {
+    for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const uint32_t p = i ^ j;
+        if (p > i) {
+          const bool up = (i & kk) == 0;
+          if (kv_gt(ck[i], cv[i], ck[p], cv[p]) == up) {
+            const uint64_t tk = ck[i];
+            ck[i] = ck[p];
+            ck[p] = tk;
+            const uint32_t tv = cv[i];
+            cv[i] = cv[p];
+            cv[p] = tv;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  uint32_t* out = order + static_cast<uint64_t>(q) * n_out;
+  for (uint32_t i = threadIdx.x; i < n_out; i += blockDim.x) out[i] = cv[i];
+  if (do_partition) {
+    __syncthreads();
+    partition_block(cv, n_out, res_off, list_off, ft, q);
   }
 }
 
@@ -1537,6 +1578,35 @@ void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
   const uint32_t threads = std::min<uint32_t>(1024, std::max<uint32_t>(256, (total / 2 + 31) & ~31u));
   merge_runs_kernel<<<nq, threads, smem, st>>>(run_k, run_v, nseg_pad, P, full, n_out, order,
                                             res_off, list_off, f, ft != nullptr);
+  after_launch();
+}
+
+
+size_t tc_select_smem(uint32_t nc, uint32_t d) {
+  uint32_t cap = 2;
+  while (cap < nc) cap <<= 1;
+  return ((size_t(d) * 4 + 15) & ~size_t(15)) + ((size_t(nc) * 4 + 15) & ~size_t(15)) +
+         size_t(cap) * 12;
+}
+
+void launch_tc_select(const float* approx, const float* Q, uint32_t nq, uint32_t d,
+                      const float* centroids, const float* cnorm, uint32_t nc, int metric,
+                      uint32_t n_out, uint32_t* order, const int64_t* res_off,
+                      const uint64_t* list_off, const FastTable* ft, cudaStream_t st) {
+  if (nq == 0 || n_out == 0) return;
+  uint32_t cap = 2;
+  while (cap < nc) cap <<= 1;
+  const size_t smem = tc_select_smem(nc, d);
+  if (smem > 227 * 1024) throw CudaError("tc_select: shared memory exceeds 227 KB");
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(tc_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    attr = smem;
+  }
+  const FastTable f = ft ? *ft : FastTable{};
+  tc_select_kernel<<<nq, 1024, smem, st>>>(approx, Q, d, centroids, cnorm, nc, metric, n_out,
+                                           cap, order, res_off, list_off, f, ft != nullptr);
   after_launch();
 }
 

@@ -10,6 +10,8 @@ namespace laivg {
 // Every kernel launch of this library increments this (evidence for the
 // bench's gpu_launches).
 std::atomic<uint64_t>& launch_counter();
+// Counts a launch and throws CudaError on a launch-configuration error.
+void after_launch();
 
 constexpr int kMaxK = 256;             // device top-k limit (8 entries per lane)
 constexpr int kRerankMargin = 16;      // extra fp32 survivors re-scored in fp64
@@ -95,6 +97,26 @@ void launch_scan(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
 int scan_grid_x(uint32_t nq, int num_sms, ScanImpl impl, const ScanTune& tune);
 // Entries each per-CTA partial list holds for a given k (k + re-score margin).
 int scan_kk(int k, bool acc_fp64);
+// ---- batched coarse quantizer on tensor cores (coarse_tc.cu) ----
+// Used for batches of >= kTcMinBatch queries when nc <= kTcMaxNc and d % 4 == 0.
+constexpr uint32_t kTcMinBatch = 8;
+constexpr uint32_t kTcMaxNc = 8192;
+// |tf32 score - exact score| <= kTcErr * ||q|| * ||c|| (2^-9 operand truncation
+// + fp32 accumulation over d <= 4096 terms, with a 2x margin).
+constexpr double kTcErr = 4.0e-3;
+bool coarse_tc_supported(uint32_t nc, uint32_t d);
+// approx[nq][nc] = tf32 tensor-core Q . C^T (tcgen05.mma kind::tf32).
+void launch_coarse_tc(const float* Q, uint32_t nq, const float* centroids, uint32_t nc,
+                      uint32_t d, float* approx, cudaStream_t st);
+// Exact first n_out of each query's ranking from the approximate scores:
+// candidates whose upper bound reaches the n_out-th best lower bound are
+// re-scored with the fp64 arithmetic of launch_coarse_scores and sorted on
+// (score, cluster id). With `ft`, also splits the probe by residency.
+// cnorm[c] = ||c|| rounded up.
+void launch_tc_select(const float* approx, const float* Q, uint32_t nq, uint32_t d,
+                      const float* centroids, const float* cnorm, uint32_t nc, int metric,
+                      uint32_t n_out, uint32_t* order, const int64_t* res_off,
+                      const uint64_t* list_off, const FastTable* ft, cudaStream_t st);
 // Generation-window stand-in: one CTA per SM spins on %globaltimer for ns.
 void launch_window(uint64_t ns, int num_sms, cudaStream_t st);
 

@@ -28,7 +28,8 @@ __all__ = [
     "HybridResult", "HybridTiming", "MicroBatch", "WorkerState", "HotnessTable",
     "CacheParams", "rank_clusters", "coarse_probe", "search_clusters", "ivf_search",
     "plan_prefetch", "execute_prefetch", "incremental_prefetch", "hybrid_search",
-    "coverage", "group_microbatches", "chunk_microbatches", "assign_cache_aware",
+    "coverage", "hybrid_search_batch", "BatchResult", "ivf_search_batch",
+    "group_microbatches", "chunk_microbatches", "assign_cache_aware",
     "assign_round_robin", "assignment_overlap", "split_budget", "default_nprobe",
     "LogicError", "CudaError", "synth_centroids", "synth_lists", "synth_queries",
 ]
@@ -242,7 +243,7 @@ class Device:
     def __init__(self, ix: IvfIndex, capacity_bytes: int, device: int = 0,
                  miss_threads: int = 0, max_batch: int = 0, max_probe: int = 0,
                  acc_fp64: bool = True, scan_impl: str = "tma", tma_tile: int = 0,
-                 tma_stages: int = 0, ctas_per_sm: int = 0):
+                 tma_stages: int = 0, ctas_per_sm: int = 0, coarse_impl: str = "auto"):
         L = lib()
         o = Opts()
         L.laivg_opts_default(C.byref(o))
@@ -256,6 +257,10 @@ class Device:
             raise ValueError("scan_impl must be 'tma' or 'ldg'")
         o.scan_impl = 0 if scan_impl == "tma" else 1
         o.tma_tile, o.tma_stages, o.ctas_per_sm = tma_tile, tma_stages, ctas_per_sm
+        impls = {"auto": 0, "fp64": 1, "tensor": 2}
+        if coarse_impl not in impls:
+            raise ValueError("coarse_impl must be 'auto', 'fp64' or 'tensor'")
+        o.coarse_impl = impls[coarse_impl]
         h = C.c_void_p()
         check(L.laivg_ctx_create(ix.h, C.byref(o), C.byref(h)))
         self.h = h
@@ -295,6 +300,27 @@ class Device:
                                                sc.ctypes.data, C.byref(cnt), C.byref(nf),
                                                C.byref(t)))
         return ids[: cnt.value], sc[: cnt.value], nf.value, _timing(t)
+
+    def hybrid_search_batch_staged(self, q0: int, nq: int, L: int, k: int):
+        """Batched hybrid search over staged queries [q0, q0 + nq): returns
+        ids[nq][k], scores[nq][k], counts[nq], nfast[nq] and the batch timing."""
+        ids = np.empty((nq, k), np.uint64)
+        sc = np.empty((nq, k), np.float32)
+        cnt = np.empty(nq, np.uint32)
+        nf = np.empty(nq, np.uint32)
+        t = HybridTimingC()
+        check(lib().laivg_hybrid_search_batch_staged(self.h, q0, nq, L, k, ids.ctypes.data,
+                                                     sc.ctypes.data, cnt.ctypes.data,
+                                                     nf.ctypes.data, C.byref(t)))
+        return ids, sc, cnt, nf, _timing(t)
+
+    def coarse_approx(self, Q) -> np.ndarray:
+        """Diagnostics: raw tf32 tensor-core coarse scores [nq][nc]."""
+        Q = _c(Q, np.float32).reshape(-1, self.ix.d)
+        out = np.empty((Q.shape[0], self.ix.nc), np.float32)
+        check(lib().laivg_debug_coarse_approx(self.h, Q.ctypes.data, Q.shape[0],
+                                              out.ctypes.data))
+        return out
 
 
 # --------------------------------------------------------------------------
@@ -350,6 +376,19 @@ def ivf_search(dev: Device, q, L: int, k: int) -> TopK:           # ivf.hpp:90-9
     check(lib().laivg_ivf_search(dev.h, q.ctypes.data, 1, int(L), int(k), ids.ctypes.data,
                                  sc.ctypes.data, cnt.ctypes.data))
     return TopK(k, [ScoredId(int(ids[i]), float(sc[i])) for i in range(int(cnt[0]))])
+
+
+def ivf_search_batch(dev: Device, Q, L: int, k: int) -> list[TopK]:
+    """ivf_search for a batch (one device pass per max_batch queries)."""
+    Q = _c(Q, np.float32).reshape(-1, dev.ix.d)
+    nq = Q.shape[0]
+    ids = np.empty((nq, max(k, 1)), np.uint64)
+    sc = np.empty((nq, max(k, 1)), np.float32)
+    cnt = np.zeros(nq, np.uint32)
+    check(lib().laivg_ivf_search(dev.h, Q.ctypes.data, nq, int(L), int(k), ids.ctypes.data,
+                                 sc.ctypes.data, cnt.ctypes.data))
+    return [TopK(k, [ScoredId(int(ids[q, i]), float(sc[q, i])) for i in range(int(cnt[q]))])
+            for q in range(nq)]
 
 
 # --------------------------------------------------------------------------
@@ -478,6 +517,37 @@ def hybrid_search(dev: Device, q_out, L: int, k: int,
     res = HybridResult(TopK(k, [ScoredId(int(ids[i]), float(sc[i])) for i in range(cnt.value)]),
                        fast[: nf.value].tolist(), slow[: ns.value].tolist(), hr.value)
     return res, _timing(t)
+
+
+@dataclass
+class BatchResult:
+    """Per-query results of hybrid_search_batch (extension point (2))."""
+    ids: np.ndarray      # [nq][k] uint64 (unused slots: ~0)
+    scores: np.ndarray   # [nq][k] float32
+    counts: np.ndarray   # [nq]
+    nfast: np.ndarray    # [nq] resident probed lists per query
+
+    def topk(self, q: int) -> TopK:
+        k = self.ids.shape[1]
+        return TopK(k, [ScoredId(int(self.ids[q, i]), float(self.scores[q, i]))
+                        for i in range(int(self.counts[q]))])
+
+
+def hybrid_search_batch(dev: Device, Q, L: int, k: int, cost: CostModel | None = None):
+    """hybrid_search for a batch of queries in one device pass (<= max_batch)."""
+    Q = _c(Q, np.float32).reshape(-1, dev.ix.d)
+    nq = Q.shape[0]
+    cost = cost or CostModel()
+    ids = np.empty((nq, max(k, 1)), np.uint64)
+    sc = np.empty((nq, max(k, 1)), np.float32)
+    cnt = np.empty(nq, np.uint32)
+    nf = np.empty(nq, np.uint32)
+    t = HybridTimingC()
+    cm = CostModelC(cost.bandwidth_bytes_per_s, cost.t_cc, cost.t_gc, cost.parallel_slots)
+    check(lib().laivg_hybrid_search_batch(dev.h, Q.ctypes.data, nq, int(L), int(k),
+                                          C.byref(cm), ids.ctypes.data, sc.ctypes.data,
+                                          cnt.ctypes.data, nf.ctypes.data, C.byref(t)))
+    return BatchResult(ids, sc, cnt, nf), _timing(t)
 
 
 def coverage(dev: Device, q_in, q_out, L: int) -> float:          # tiered.hpp:132-133

@@ -1,0 +1,174 @@
+"""Batched retrieval on the GPU (SURVEY §8b extension point (2); north-star
+subsystem (1): the coarse quantizer on tensor cores when queries batch).
+
+* the tcgen05 tf32 coarse GEMM stays inside its error bound
+  (|s~ - s| <= kTcErr ||q|| ||c||, kTcErr = 4e-3) against fp64 numpy;
+* the batched probe (tensor-core scores + exact fp64 re-score of the
+  boundary candidates) is bit-identical to the fp64 device ranking and meets
+  the §8c rule against the C oracle;
+* hybrid_search_batch / ivf_search_batch return, per query, exactly what the
+  single-query path returns, and the reference's goldens (bit-exact at
+  D = 8 / 16) under any residency (hybrid == monolithic, tiered.hpp:120-124).
+"""
+import numpy as np
+import pytest
+
+from common import (IP, L2, accept1_case, assert_topk_parity, expected_row, hybrid_d8_case,
+                    planted_data, probe_parity)
+
+pytestmark = pytest.mark.gpu
+BIG = 1 << 34
+TC_ERR = 4.0e-3
+
+
+def set_residency(dev, mask):
+    dev.store.clear()
+    for c in np.nonzero(mask)[0]:
+        dev.store.insert(int(c))
+
+
+def synth_index(laiv, nc, per, d, metric, seed=3, nq=64, sigma=0.02):
+    cen = laiv.synth_centroids(seed, nc, d)
+    vecs, ids = laiv.synth_lists(seed, cen, per, 0.05)
+    off = np.arange(0, nc * per + 1, per, dtype=np.uint64)
+    qi, qo, _ = laiv.synth_queries(seed + 1, vecs, nq, sigma)
+    ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric(metric))
+    return cen, vecs, ids, off, qi, qo, ix
+
+
+@pytest.mark.parametrize("nc,d", [(300, 768), (4096, 768), (1000, 100), (77, 8)])
+def test_tc_coarse_error_bound(laiv, nc, d):
+    rng = np.random.default_rng(nc + d)
+    cen = rng.standard_normal((nc, d)).astype(np.float32)
+    vecs = rng.standard_normal((nc, d)).astype(np.float32)
+    ids = np.arange(nc, dtype=np.uint64)
+    off = np.arange(nc + 1, dtype=np.uint64)
+    ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric.InnerProduct)
+    dev = laiv.Device(ix, 1 << 20)
+    for nq in (8, 33, 256, 300):
+        Q = rng.standard_normal((nq, d)).astype(np.float32) * rng.uniform(0.1, 10)
+        approx = dev.coarse_approx(Q).astype(np.float64)
+        exact = Q.astype(np.float64) @ cen.astype(np.float64).T
+        bound = np.outer(np.linalg.norm(Q.astype(np.float64), axis=1),
+                         np.linalg.norm(cen.astype(np.float64), axis=1))
+        ratio = np.abs(approx - exact) / bound
+        assert ratio.max() <= TC_ERR, ratio.max()
+        # the bound carries a real margin (tf32 error ~ 2^-11 relative)
+        assert ratio.max() < TC_ERR / 2, ratio.max()
+
+
+@pytest.mark.parametrize("metric", [IP, L2])
+@pytest.mark.parametrize("nc,d", [(300, 768), (4096, 768), (1000, 100)])
+def test_tc_probe_bit_exact(orc, laiv, metric, nc, d):
+    cen, vecs, ids, off, qi, qo, ix = synth_index(laiv, nc, 4, d, metric, nq=48)
+    dev_tc = laiv.Device(ix, 1 << 20, coarse_impl="tensor")
+    dev_64 = laiv.Device(ix, 1 << 20, coarse_impl="fp64")
+    dev_auto = laiv.Device(ix, 1 << 20)
+    Q = np.concatenate([qi, qo])
+    for L in (1, 17, 128, nc - 1, nc, nc + 5):
+        a = laiv.coarse_probe(dev_tc, Q, L)
+        b = laiv.coarse_probe(dev_64, Q, L)
+        c = laiv.coarse_probe(dev_auto, Q, L)
+        assert np.array_equal(a, b), L
+        assert np.array_equal(a, c), L
+        Lc = min(L, nc)
+        for t in range(0, Q.shape[0], 7):
+            order, scores = orc.rank_clusters(cen, metric, Q[t], with_scores=True)
+            probe_parity(a[t], order, scores, Lc)
+    # single query forced onto the tensor cores
+    for t in range(4):
+        assert np.array_equal(laiv.coarse_probe(dev_tc, Q[t], 64),
+                              laiv.coarse_probe(dev_64, Q[t], 64))
+
+
+def test_tc_probe_exact_ties(laiv):
+    # duplicated centroids: exact score ties ordered by ascending cluster id
+    rng = np.random.default_rng(9)
+    base = rng.standard_normal((50, 64)).astype(np.float32)
+    cen = np.concatenate([base, base, base])  # 150 clusters, triples tie
+    vecs = cen.copy()
+    ids = np.arange(150, dtype=np.uint64)
+    off = np.arange(151, dtype=np.uint64)
+    for metric in (laiv.Metric.InnerProduct, laiv.Metric.L2):
+        ix = laiv.IvfIndex(cen, vecs, ids, off, metric)
+        dev_tc = laiv.Device(ix, 1 << 20, coarse_impl="tensor")
+        dev_64 = laiv.Device(ix, 1 << 20, coarse_impl="fp64")
+        Q = rng.standard_normal((16, 64)).astype(np.float32)
+        for L in (1, 2, 3, 10, 149):
+            assert np.array_equal(laiv.coarse_probe(dev_tc, Q, L), laiv.coarse_probe(dev_64, Q, L))
+
+
+@pytest.mark.parametrize("name,metric", [("l2", L2), ("ip", IP)])
+def test_batch_matches_single_planted(orc, laiv, name, metric):
+    cen, vecs, ids, off, qi, qo, g = planted_data()
+    ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric(metric))
+    dev = laiv.Device(ix, BIG)
+    rng = np.random.default_rng(17)
+    for trial in range(4):
+        set_residency(dev, (rng.random(64) < [0.0, 1.0, 0.5, 0.2][trial]).astype(np.uint8))
+        L, k = [8, 16, 64, 5][trial], [10, 32, 7, 100][trial]
+        res, timing = laiv.hybrid_search_batch(dev, qo, L, k)
+        for t in range(40):
+            single, _ = laiv.hybrid_search(dev, qo[t], L, k)
+            got = res.topk(t)
+            assert np.array_equal(got.ids, single.topk.ids), t
+            assert np.array_equal(got.scores, single.topk.scores), t
+            assert res.nfast[t] == len(single.fast_clusters)
+            want = orc.ivf_search(cen, vecs, ids, off, metric, qo[t], L, k)
+            assert_topk_parity(metric, got.ids, got.scores, *want)
+        assert timing.scanned_vectors == 300 * int(res.nfast.sum())
+
+
+@pytest.mark.parametrize("name", ["l2", "ip"])
+def test_batch_d8_golden(orc, laiv, name):
+    # reference goldens are residency-independent (hybrid == monolithic):
+    # replay them through the batch path under three residencies
+    case, queries, g = hybrid_d8_case(orc, name)
+    ix = laiv.IvfIndex(case.centroids, case.vecs, case.ids, case.list_off,
+                       laiv.Metric(case.metric))
+    dev = laiv.Device(ix, BIG, max_batch=32)
+    p = f"{name}_"
+    Ls, ks = g[p + "L"], g[p + "k"]
+    for mask in (np.zeros(case.nc, np.uint8), np.ones(case.nc, np.uint8), g[p + "masks"][0]):
+        set_residency(dev, mask)
+        for L, k in sorted(set(zip(Ls.tolist(), ks.tolist()))):
+            sel = [t for t in range(200) if Ls[t] == L and ks[t] == k]
+            got = laiv.ivf_search_batch(dev, queries[sel], L, k)
+            for t, tk in zip(sel, got):
+                want_ids, want_sc = expected_row(g, p, t)
+                assert_topk_parity(case.metric, tk.ids, tk.scores, want_ids, want_sc, exact=True)
+
+
+def test_batch_accept1_golden(orc, laiv):
+    case, queries, masks, full_q, g = accept1_case(orc)
+    ix = laiv.IvfIndex(case.centroids, case.vecs, case.ids, case.list_off, laiv.Metric.L2)
+    dev = laiv.Device(ix, BIG)
+    set_residency(dev, masks[0])
+    Ls, ks = g["L"], g["k"]
+    for L, k in sorted(set(zip(Ls.tolist(), ks.tolist()))):
+        sel = [t for t in range(1000) if Ls[t] == L and ks[t] == k]
+        got = laiv.ivf_search_batch(dev, queries[sel], L, k)
+        for t, tk in zip(sel, got):
+            want_ids, want_sc = expected_row(g, "", t)
+            assert_topk_parity(L2, tk.ids, tk.scores, want_ids, want_sc, exact=True)
+
+
+def test_batch_edges(orc, laiv):
+    cen, vecs, ids, off, qi, qo, g = planted_data()
+    ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric.InnerProduct)
+    dev = laiv.Device(ix, BIG, max_batch=16)
+    set_residency(dev, np.arange(64) % 3 == 0)
+    # L = 0 / negative: empty results
+    res, _ = laiv.hybrid_search_batch(dev, qo[:8], 0, 5)
+    assert (res.counts == 0).all()
+    res, _ = laiv.hybrid_search_batch(dev, qo[:8], -2, 5)
+    assert (res.counts == 0).all()
+    # L > nc clamps; more queries than max_batch chunk through ivf_search_batch
+    got = laiv.ivf_search_batch(dev, qo, 1000, 12)
+    for t in range(40):
+        want = orc.ivf_search(cen, vecs, ids, off, IP, qo[t], 64, 12)
+        assert_topk_parity(IP, got[t].ids, got[t].scores, *want)
+    with pytest.raises(ValueError):
+        laiv.hybrid_search_batch(dev, qo[:17], 8, 5)  # > max_batch
+    with pytest.raises(ValueError):
+        laiv.hybrid_search_batch(dev, qo[:4], 8, 0)
