@@ -51,6 +51,16 @@ CONFIGS = {
     "c1": dict(workload="synthetic IVF-Flat 1M x 768 fp32, 1024 lists, nprobe=32, k=10, batch=1",
                n_lists=1024, per_list=977, d=768, nprobe=32, k=10, window_s=0.02,
                cache_frac=0.10),
+    # BASELINE.json configs[2]: micro-batch of 32 with lookahead prefetch
+    "c3": dict(workload="synthetic IVF-Flat 20M x 768 fp32 (~61 GB host datastore), 4096 lists, "
+                        "nprobe=256, batch=32, GPU cache sized to 10% of lists",
+               n_lists=4096, per_list=4883, d=768, nprobe=256, k=10, window_s=0.15,
+               cache_frac=0.10, batch=32),
+    # C3's shape at half the datastore (fits a 1-GPU box next to the reference copy)
+    "c3s": dict(workload="synthetic IVF-Flat 10M x 768 fp32, 4096 lists, nprobe=256, batch=32, "
+                         "GPU cache sized to 10% of lists",
+                n_lists=4096, per_list=2442, d=768, nprobe=256, k=10, window_s=0.15,
+                cache_frac=0.10, batch=32),
     "small": dict(workload="synthetic IVF-Flat 100K x 768 fp32, 256 lists, nprobe=16, k=10",
                   n_lists=256, per_list=400, d=768, nprobe=16, k=10, window_s=0.005,
                   cache_frac=0.25),
@@ -251,7 +261,7 @@ METRIC = "IVF retrieval queries/sec and p50 retrieval latency (prefetch-overlapp
 def config_block(cfg, args, sigma):
     return {"workload": cfg["workload"], "n_vectors": cfg["n_lists"] * cfg["per_list"],
             "dim": cfg["d"], "n_lists": cfg["n_lists"], "nprobe": cfg["nprobe"], "k": cfg["k"],
-            "metric": args.metric, "batch": 1, "window_s": args.window,
+            "metric": args.metric, "batch": cfg.get("batch", 1), "window_s": args.window,
             "cache_fraction_of_lists": cfg["cache_frac"], "q_out_sigma": sigma,
             "l2_flush": "not needed: each query scans up to ~1 GB of lists > 126 MB L2, "
                         "and every step re-fetches its lists into a cleared cache"}
@@ -401,6 +411,168 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
     return 0
 
+def run_ours_batch(args, cfg):
+    """Micro-batch pipeline round (pipeline.cpp:346-441) on one GPU per rank:
+    clear cache -> lookahead prefetch of the batch (one window, per-query
+    budgets from split_budget) -> batched hybrid search of the batch's q_out.
+    Retrieval latency of a batch = exposed H2D + the batched hybrid search."""
+    from paper_2502_20969_b200 import laiv, shard
+
+    rank, world, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    B = cfg["batch"]
+    cen, vecs, ids, off = make_datastore(cfg, world, rank)
+    metric = laiv.Metric.InnerProduct if args.metric == "ip" else laiv.Metric.L2
+    ix = laiv.IvfIndex(cen, vecs, ids, off, metric, borrow=True, trust=True)
+    member = 4 * cfg["d"] + 8
+    capacity = int(cfg["cache_frac"] * cfg["n_lists"]) * cfg["per_list"] * member
+    dev = laiv.Device(ix, capacity, device=local if world > 1 else 0, max_batch=B,
+                      acc_fp64=args.acc == "fp64", scan_impl=args.scan)
+    L, k = cfg["nprobe"], cfg["k"]
+    probe_plan = laiv.plan_prefetch(dev, cen[0], min(capacity, 64 * cfg["per_list"] * member))
+    rep = laiv.execute_prefetch(dev, probe_plan, laiv.TransferChannel(1, laiv.ChannelMode.Device))
+    dev.store.clear()
+    b_link = rep.h2d_gbps * 1e9
+    budget = int(min(b_link * args.window, capacity))
+    budgets = laiv.split_budget(budget, laiv.MicroBatch(list(range(B))))
+    sigma, cov = (args.sigma, None) if args.sigma else calibrate_sigma(laiv, dev, vecs, L)
+    nsteps = args.warmup + args.steps
+    nq_total = nsteps * B * world
+    qi, qo, _ = laiv.synth_queries(QSEED, vecs, nq_total, sigma)
+    mine = np.concatenate([np.arange((j * world + rank) * B, (j * world + rank + 1) * B)
+                           for j in range(nsteps)])
+    dev.stage_queries(qo[mine])
+    chan = laiv.TransferChannel(b_link, laiv.ChannelMode.Device)
+    log(f"[bench] rank {rank}: batch {B}, B_link {b_link / 1e9:.1f} GB/s, budget "
+        f"{budget / 1e9:.2f} GB ({budgets[0] / 1e6:.0f} MB/query), sigma {sigma} "
+        f"(coverage {cov}), capacity {capacity / 1e9:.2f} GB")
+
+    def step(j, rec):
+        sel = mine[j * B:(j + 1) * B]
+        dev.store.clear()
+        t0 = time.perf_counter()
+        rp, npl = laiv.prefetch_batch(dev, qi[sel], budgets, chan, args.window)
+        t1 = time.perf_counter()
+        got_ids, got_sc, cnt, nfast, tm = dev.hybrid_search_batch_staged(j * B, B, L, k)
+        t2 = time.perf_counter()
+        res, tm2 = laiv.hybrid_search_batch(dev, qo[sel], L, k)
+        t3 = time.perf_counter()
+        if rec is not None:
+            nhit = int(nfast.sum())
+            rec.append(dict(
+                exposed=rp.overshoot_s, t_p=rp.t_p, window=rp.window_s, h2d_gbps=rp.h2d_gbps,
+                lat_value=rp.overshoot_s + tm.t_2, lat_e2e=rp.overshoot_s + (t3 - t2),
+                t_scan=tm.t_scan, t_coarse=tm.t_coarse, t_g=tm.t_g, t_c=tm.t_c, t_2=tm.t_2,
+                bytes=tm.scanned_bytes, hit=nhit / (B * L), plan_s=t1 - t0,
+                fetched_lists=tm.fetched_lists, cpu_lists=tm.cpu_lists,
+                fetched_bytes=tm.fetched_bytes, t_fetch=tm.t_fetch,
+                miss_bytes=(B * L - nhit) * cfg["per_list"] * 4 * cfg["d"],
+                prefetched=len(rp.transferred),
+                h2d_bytes=B * 4 * cfg["d"] * 2 + rp.bytes // member * 4 * cfg["d"],
+                d2h_bytes=B * (L * 4 + k * 12 + 8),
+                same=bool(np.array_equal(got_ids, res.ids))))
+
+    for j in range(args.warmup):
+        step(j, None)
+    if dist:
+        dist.barrier()
+    dev.sync()
+    clocks = ClockSampler(local if world > 1 else 0)
+    launches0 = laiv.lib().laivg_kernel_launches()
+    rec = []
+    t0 = time.perf_counter()
+    for j in range(args.warmup, nsteps):
+        step(j, rec)
+    dev.sync()
+    wall = time.perf_counter() - t0
+    launches = laiv.lib().laivg_kernel_launches() - launches0
+    clk = clocks.stop()
+    lat_v = np.array([r["lat_value"] for r in rec])
+    lat_e = np.array([r["lat_e2e"] for r in rec])
+    sum_v, sum_e = float(lat_v.sum()), float(lat_e.sum())
+    if dist:
+        sum_v, sum_e, wall = shard.max_over_ranks([sum_v, sum_e, wall], device="cuda")
+    n_total = args.steps * B * world
+    bytes_scan = sum(r["bytes"] for r in rec)
+    t_scan = sum(r["t_scan"] for r in rec)
+    peak, peak_kind = measured_peaks()
+    achieved = bytes_scan / t_scan / 1e9 if t_scan > 0 else 0.0
+    exposed = np.array([r["exposed"] for r in rec])
+    t_p = np.array([r["t_p"] for r in rec])
+    t_c = np.array([r["t_c"] for r in rec])
+    miss_b = np.array([r["miss_bytes"] for r in rec])
+    line = {
+        "metric": METRIC, "value": n_total / sum_v, "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum_v / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": f"f32 data, {args.acc} accumulate", "data": "synthetic (planted clusters, SURVEY §8d)",
+        "p50_latency_ms": float(np.median(lat_v) * 1e3),
+        "p50_batch_note": "latency of one micro-batch of queries (all returned together)",
+        "pipeline_ms_per_step": wall / args.steps * 1e3,
+        "config": config_block(cfg, args, sigma),
+        "roofline": {"kernel": f"scan_{args.scan}_kernel", "bound": "hbm", "achieved": achieved,
+                     "peak": peak, "peak_kind": f"{peak_kind} copy (MEASURED_PEAKS.json hbm_gbs)",
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "algorithmic_bytes_per_launch": bytes_scan / max(len(rec), 1),
+                     "avg_launch_ms": t_scan / max(len(rec), 1) * 1e3},
+        "miss_path": {"host_scan_ms_mean": float(t_c.mean() * 1e3),
+                      "host_bytes_mean_gb": float(miss_b.mean() / 1e9),
+                      "host_gbps_per_query_bytes": float(miss_b.sum() / t_c.sum() / 1e9)
+                      if t_c.sum() else 0.0,
+                      "host_threads": os.cpu_count(),
+                      "runtime_fetch": {
+                          "lists_mean": float(np.mean([r["fetched_lists"] for r in rec])),
+                          "host_lists_mean": float(np.mean([r["cpu_lists"] for r in rec])),
+                          "gb_mean": float(np.mean([r["fetched_bytes"] for r in rec]) / 1e9),
+                          "copy_ms_mean": float(np.mean([r["t_fetch"] for r in rec]) * 1e3),
+                          "h2d_gbps": float(sum(r["fetched_bytes"] for r in rec) /
+                                            max(sum(r["t_fetch"] for r in rec), 1e-12) / 1e9)}},
+        "prefetch": {"h2d_gbps": float(np.mean([r["h2d_gbps"] for r in rec])),
+                     "b_link_gbps": b_link / 1e9, "budget_gb": budget / 1e9,
+                     "hidden_frac": float(1.0 - exposed.sum() / t_p.sum()) if t_p.sum() else 1.0,
+                     "exposed_ms_mean": float(exposed.mean() * 1e3),
+                     "hit_rate": float(np.mean([r["hit"] for r in rec])),
+                     "lists_prefetched_mean": float(np.mean([r["prefetched"] for r in rec]))},
+        "breakdown_ms": {k_: float(np.mean([r[k_] for r in rec]) * 1e3)
+                         for k_ in ("t_coarse", "t_scan", "t_g", "t_c", "t_2", "plan_s")},
+        "e2e": {"value": n_total / sum_e, "unit": "queries/s",
+                "p50_latency_ms": float(np.median(lat_e) * 1e3),
+                "h2d_bytes_per_step": int(np.mean([r["h2d_bytes"] for r in rec])),
+                "d2h_bytes_per_step": int(np.mean([r["d2h_bytes"] for r in rec]))},
+        "value_e2e_results_identical": all(r["same"] for r in rec),
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        ri = reference_index(cen, np.asarray(vecs), ids, off, int(metric))
+        threads = os.cpu_count() or 1
+        sample = min(args.cpu_sample, args.steps * B)
+        tq = mine[args.warmup * B: args.warmup * B + sample]
+        cb = cpu_baseline(ri, qo[tq], L, k, threads, sample)
+        eq = 0
+        got_ids, got_sc, _, _, _ = dev.hybrid_search_batch_staged(args.warmup * B, B, L, k)
+        for j in range(min(sample, B)):
+            eq += bool(np.array_equal(got_ids[j], cb["ids"][j]) and
+                       np.array_equal(got_sc[j], cb["scores"][j]))
+        line["cpu_baseline"] = {"value": cb["qps"], "unit": "queries/s", "cores": threads,
+                                "kind": "reference", "p50_latency_ms": cb["p50_ms"],
+                                "sample": f"{sample} of the timed q_out queries, "
+                                          f"laiv::ivf_search (oracle/_ref) one query per host "
+                                          f"thread"}
+        line["parity_vs_reference"] = {"queries": min(sample, B), "bit_identical": eq}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
 
 def main():
     ap = argparse.ArgumentParser()
@@ -425,6 +597,8 @@ def main():
         args.window = cfg["window_s"]
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if cfg.get("batch", 1) > 1:
+        return run_ours_batch(args, cfg)
     return run_ours(args, cfg)
 
 

@@ -112,7 +112,15 @@ typedef struct {
                               exact fp64 re-score of boundary candidates) for
                               batches >= 8 queries, fp64 SIMT otherwise;
                               1: always fp64 SIMT; 2: always tensor cores */
-  uint32_t reserved[3];
+  uint32_t miss_fetch;     /* batched search, cache misses: 0 = all scanned by
+                              the host (reference semantics); 1 (default) =
+                              adaptive runtime fetch: the most-shared misses
+                              stream H2D through a 2-slot HBM ring and are
+                              scanned on the GPU while the host scans the
+                              rest, split by measured rates; 2 = every miss
+                              the ring can take goes to the GPU */
+  uint32_t fetch_chunk_mb; /* ring slot size in MiB; 0 = 512 */
+  uint32_t reserved[1];
 } laivg_opts;
 void laivg_opts_default(laivg_opts* o);
 typedef struct laivg_ctx laivg_ctx;
@@ -218,6 +226,19 @@ int laivg_incremental_prefetch(laivg_ctx* ctx, const float* q_round,
                                double overlap_window_s,
                                uint32_t* transferred_out,
                                laivg_transfer_report* rep);
+/* Lookahead prefetch of a micro-batch (replaces the per-trace plan/execute
+ * loop of serve_microbatch, pipeline.cpp:357-371): one GPU coarse pass ranks
+ * all nq predictor embeddings Q_in[nq*d]; query i then plans against the
+ * store already holding the earlier plans with budget min(budgets[i], free
+ * bytes) (plan_prefetch rule, tiered.cpp:67-84), and every planned list
+ * streams host->HBM on the copy stream while ONE generation window of
+ * overlap_window_s runs on the compute stream. Device channel only.
+ * transferred_out (nullable, nc entries) gets the lists in transfer order,
+ * nplan_out (nullable, nq entries) each query's planned count. */
+int laivg_prefetch_batch(laivg_ctx* ctx, const float* Q_in, uint32_t nq,
+                         const uint64_t* budgets, const laivg_channel* chan,
+                         double overlap_window_s, uint32_t* transferred_out,
+                         uint32_t* nplan_out, laivg_transfer_report* rep);
 /* Runs only the generation-window kernel (seconds) on the compute stream and
  * returns its measured duration. */
 int laivg_window(laivg_ctx* ctx, double seconds, double* measured_s);
@@ -241,6 +262,11 @@ typedef struct {
   double t_scan;   /* device: list scan + block/grid merge (s) */
   uint64_t scanned_vectors; /* vectors scanned on the GPU */
   uint64_t scanned_bytes;   /* reference bytes: n*(4D+8) over fast lists */
+  /* batched search, runtime fetch of misses (zero otherwise): */
+  uint32_t fetched_lists;   /* distinct missed lists fetched H2D + GPU-scanned */
+  uint32_t cpu_lists;       /* distinct missed lists scanned by the host */
+  uint64_t fetched_bytes;   /* vector bytes fetched on demand */
+  double t_fetch;           /* copy-stream time of those fetches (s) */
 } laivg_hybrid_timing;
 
 /* hybrid_search for one query. fast_out / slow_out (nullable, L entries)

@@ -31,7 +31,8 @@ class Opts(C.Structure):
     _fields_ = [("device", i32), ("capacity_bytes", u64), ("miss_threads", u32),
                 ("max_batch", u32), ("max_probe", u32), ("acc_fp64", u32),
                 ("scan_impl", u32), ("tma_tile", u32), ("tma_stages", u32),
-                ("ctas_per_sm", u32), ("coarse_impl", u32), ("reserved", u32 * 3)]
+                ("ctas_per_sm", u32), ("coarse_impl", u32), ("miss_fetch", u32),
+                ("fetch_chunk_mb", u32), ("reserved", u32 * 1)]
 
 
 class Channel(C.Structure):
@@ -51,7 +52,8 @@ class CostModelC(C.Structure):
 class HybridTimingC(C.Structure):
     _fields_ = [("t_g", f64), ("t_c", f64), ("t_2", f64), ("model_t_g", f64),
                 ("model_t_c", f64), ("model_t_2", f64), ("t_coarse", f64), ("t_scan", f64),
-                ("scanned_vectors", u64), ("scanned_bytes", u64)]
+                ("scanned_vectors", u64), ("scanned_bytes", u64), ("fetched_lists", u32),
+                ("cpu_lists", u32), ("fetched_bytes", u64), ("t_fetch", f64)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/laivg.h
@@ -108,6 +110,8 @@ SIGNATURES = {
     "laivg_hybrid_search_batch_staged": (i32, [vp, u32, u32, i32, i32, vp, vp, vp, vp,
                                                P(HybridTimingC)]),
     "laivg_debug_coarse_approx": (i32, [vp, vp, u32, vp]),
+    "laivg_prefetch_batch": (i32, [vp, vp, u32, vp, P(Channel), f64, vp, vp,
+                                   P(TransferReportC)]),
     "laivg_group_microbatches": (i32, [vp, u64, u32, u64, vp, vp, P(u32)]),
     "laivg_chunk_microbatches": (i32, [u64, u64, vp, vp, P(u32)]),
     "laivg_assign_cache_aware": (i32, [vp, vp, vp, u32, vp, u32, vp, u64, i32, vp]),

@@ -103,6 +103,31 @@ class SlabAlloc {
   std::map<uint64_t, uint64_t> free_;
 };
 
+constexpr uint32_t kMaxFetchChunks = 32;
+
+// Enqueues many host->device copies with one cudaMemcpyBatchAsync call
+// (CUDA 12.8+), falling back to one cudaMemcpyAsync per copy.
+void h2d_batch(std::vector<void*>& dst, std::vector<void*>& src, std::vector<size_t>& size,
+               cudaStream_t st) {
+  if (dst.empty()) return;
+  static bool batch_ok = true;
+  if (batch_ok) {
+    cudaMemcpyAttributes attr;
+    std::memset(&attr, 0, sizeof(attr));
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+    size_t idx = 0, fail = 0;
+    const cudaError_t e = cudaMemcpyBatchAsync(dst.data(), src.data(), size.data(), dst.size(),
+                                               &attr, &idx, 1, &fail, st);
+    if (e == cudaSuccess) return;
+    cudaGetLastError();
+    batch_ok = false;
+  }
+  for (size_t i = 0; i < dst.size(); ++i) {
+    CK(cudaMemcpyAsync(dst[i], src[i], size[i], cudaMemcpyHostToDevice, st));
+  }
+}
+
 struct Resident {
   int tag;
   uint64_t bytes;
@@ -156,6 +181,24 @@ struct Ctx {
   uint32_t* d_run_v = nullptr;
   FastTable ft{};
   ScanOut so{};
+  // runtime-fetch miss path (batched search): missed lists stream host->HBM
+  // through a 2-slot ring and are scanned there, in parallel with the host
+  // scan of the remaining misses
+  uint32_t miss_fetch = 1;       // 0 off, 1 adaptive split, 2 every fetchable miss
+  uint64_t ring_vecs = 0;        // vectors per ring slot
+  float* d_ring = nullptr;       // [2][ring_vecs][d]
+  int64_t* d_res_ring[2] = {nullptr, nullptr};
+  int64_t* h_res_ring = nullptr; // pinned [kMaxFetchChunks][nc] staging
+  FastTable fft{};
+  ScanOut fso{};
+  float* h_fetch_s = nullptr;    // pinned [kMaxFetchChunks][max_batch][kMaxK]
+  uint64_t* h_fetch_id = nullptr;
+  uint32_t* h_fetch_cnt = nullptr;
+  cudaEvent_t ev_landed[2] = {nullptr, nullptr}, ev_freed[2] = {nullptr, nullptr};
+  cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr, ev_fdone = nullptr;
+  double link_rate = 50e9;       // EMA of fetch H2D bytes/s
+  double cpu_rate = 0;           // EMA of host miss scan (per-query bytes)/s
+  void alloc_scan_set(FastTable& f, ScanOut& o);
   int part_cap = 0; // partial top-k rows available (CTAs x queries)
   float* h_Q = nullptr;
   uint32_t* h_order = nullptr;
@@ -230,6 +273,10 @@ struct Ctx {
     std::vector<uint32_t> nfast, nslow;
     double t_g = 0, t_c = 0, t_2 = 0, t_coarse = 0, t_scan = 0;
     uint64_t vecs_gpu = 0, bytes_gpu = 0;
+    // runtime fetch: misses scanned on the GPU after an on-demand H2D
+    uint32_t fetch_lists = 0, cpu_lists = 0;
+    uint64_t fetch_bytes = 0, cpu_query_bytes = 0;
+    double t_fetch = 0; // copy-stream time of the fetch copies
   };
   BatchResult search_batch(const float* dQ, const float* hQ, uint32_t nq, int L, int k);
 
@@ -329,6 +376,21 @@ Ctx::~Ctx() {
                   (void*)h_order, (void*)h_out_s, (void*)h_out_id,
                   (void*)h_out_cnt, (void*)h_fcount}) {
     if (p) cudaFreeHost(p);
+  }
+  for (void* p : {(void*)fft.slab, (void*)fft.row, (void*)fft.len, (void*)fft.cluster,
+                  (void*)fft.pre, (void*)fft.count, (void*)fft.cta, (void*)fso.part_s,
+                  (void*)fso.part_id, (void*)fso.part_vi, (void*)fso.ticket, (void*)fso.gpart_s,
+                  (void*)fso.gpart_id, (void*)fso.gpart_vi, (void*)fso.out_s,
+                  (void*)fso.out_id, (void*)fso.out_count, (void*)d_ring,
+                  (void*)d_res_ring[0], (void*)d_res_ring[1]}) {
+    if (p) cudaFree(p);
+  }
+  for (void* p : {(void*)h_res_ring, (void*)h_fetch_s, (void*)h_fetch_id, (void*)h_fetch_cnt}) {
+    if (p) cudaFreeHost(p);
+  }
+  for (cudaEvent_t e : {ev_landed[0], ev_landed[1], ev_freed[0], ev_freed[1], ev_f0, ev_f1,
+                        ev_fdone}) {
+    if (e) cudaEventDestroy(e);
   }
   for (auto& [key, ge] : graphs) cudaGraphExecDestroy(ge);
   for (cudaEvent_t e : {ev_a, ev_b, ev_p, ev_s, ev_c, ev_probe, ev_base, ev_win,
@@ -435,27 +497,30 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   d_order = dev_alloc<uint32_t>(size_t(max_batch) * std::max(nc, 1u));
   d_run_k = dev_alloc<uint64_t>(select_scratch_entries(max_batch, nc));
   d_run_v = dev_alloc<uint32_t>(select_scratch_entries(max_batch, nc));
-  ft.stride = max_probe;
-  ft.slab = dev_alloc<int64_t>(size_t(max_batch) * max_probe);
-  ft.row = dev_alloc<uint64_t>(size_t(max_batch) * max_probe);
-  ft.len = dev_alloc<uint32_t>(size_t(max_batch) * max_probe);
-  ft.cluster = dev_alloc<uint32_t>(size_t(max_batch) * max_probe);
-  ft.pre = dev_alloc<uint64_t>(size_t(max_batch) * (max_probe + 1));
-  ft.count = dev_alloc<uint32_t>(max_batch);
   const int per_sm = std::max<int>(2, int(tune.ctas_per_sm));
   part_cap = std::max<int>(per_sm * sms, int(max_batch)) + per_sm * sms;
-  so.part_s = dev_alloc<float>(size_t(part_cap) * kMaxK);
-  so.part_id = dev_alloc<uint64_t>(size_t(part_cap) * kMaxK);
-  so.part_vi = dev_alloc<uint32_t>(size_t(part_cap) * kMaxK);
-  ft.cta = dev_alloc<CtaStart>(size_t(part_cap));
-  so.gpart_s = dev_alloc<float>(size_t(max_batch) * kMaxGroups * kMaxK);
-  so.gpart_id = dev_alloc<uint64_t>(size_t(max_batch) * kMaxGroups * kMaxK);
-  so.gpart_vi = dev_alloc<uint32_t>(size_t(max_batch) * kMaxGroups * kMaxK);
-  so.ticket = dev_alloc<unsigned>(size_t(max_batch) * (kMaxGroups + 1));
-  CK(cudaMemset(so.ticket, 0, size_t(max_batch) * (kMaxGroups + 1) * sizeof(unsigned)));
-  so.out_s = dev_alloc<float>(size_t(max_batch) * kMaxK);
-  so.out_id = dev_alloc<uint64_t>(size_t(max_batch) * kMaxK);
-  so.out_count = dev_alloc<uint32_t>(max_batch);
+  alloc_scan_set(ft, so);
+  miss_fetch = o.miss_fetch;
+  if (miss_fetch > 2) throw std::invalid_argument("miss_fetch must be 0, 1 or 2");
+  if (miss_fetch) {
+    const uint64_t chunk_mb = o.fetch_chunk_mb ? o.fetch_chunk_mb : 512;
+    ring_vecs = std::max<uint64_t>(maxlen, (chunk_mb << 20) / (uint64_t(d) * 4));
+    d_ring = dev_alloc<float>(2 * ring_vecs * d);
+    for (int i = 0; i < 2; ++i) {
+      d_res_ring[i] = dev_alloc<int64_t>(nc);
+      CK(cudaEventCreate(&ev_landed[i]));
+      CK(cudaEventCreate(&ev_freed[i]));
+      CK(cudaEventRecord(ev_freed[i], comp));
+    }
+    CK(cudaEventCreate(&ev_f0));
+    CK(cudaEventCreate(&ev_f1));
+    CK(cudaEventCreate(&ev_fdone));
+    h_res_ring = pin_alloc<int64_t>(size_t(kMaxFetchChunks) * nc);
+    alloc_scan_set(fft, fso);
+    h_fetch_s = pin_alloc<float>(size_t(kMaxFetchChunks) * max_batch * kMaxK);
+    h_fetch_id = pin_alloc<uint64_t>(size_t(kMaxFetchChunks) * max_batch * kMaxK);
+    h_fetch_cnt = pin_alloc<uint32_t>(size_t(kMaxFetchChunks) * max_batch);
+  }
   h_Q = pin_alloc<float>(size_t(max_batch) * d);
   h_order = pin_alloc<uint32_t>(size_t(max_batch) * std::max(nc, 1u));
   h_out_s = pin_alloc<float>(size_t(max_batch) * kMaxK);
@@ -467,6 +532,28 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   if (threads == 0) threads = std::max(1u, std::thread::hardware_concurrency());
   pool = std::make_unique<ThreadPool>(threads - 1);
   CK(cudaDeviceSynchronize());
+}
+
+void Ctx::alloc_scan_set(FastTable& f, ScanOut& o) {
+  f.stride = max_probe;
+  f.slab = dev_alloc<int64_t>(size_t(max_batch) * max_probe);
+  f.row = dev_alloc<uint64_t>(size_t(max_batch) * max_probe);
+  f.len = dev_alloc<uint32_t>(size_t(max_batch) * max_probe);
+  f.cluster = dev_alloc<uint32_t>(size_t(max_batch) * max_probe);
+  f.pre = dev_alloc<uint64_t>(size_t(max_batch) * (max_probe + 1));
+  f.count = dev_alloc<uint32_t>(max_batch);
+  f.cta = dev_alloc<CtaStart>(size_t(part_cap));
+  o.part_s = dev_alloc<float>(size_t(part_cap) * kMaxK);
+  o.part_id = dev_alloc<uint64_t>(size_t(part_cap) * kMaxK);
+  o.part_vi = dev_alloc<uint32_t>(size_t(part_cap) * kMaxK);
+  o.gpart_s = dev_alloc<float>(size_t(max_batch) * kMaxGroups * kMaxK);
+  o.gpart_id = dev_alloc<uint64_t>(size_t(max_batch) * kMaxGroups * kMaxK);
+  o.gpart_vi = dev_alloc<uint32_t>(size_t(max_batch) * kMaxGroups * kMaxK);
+  o.ticket = dev_alloc<unsigned>(size_t(max_batch) * (kMaxGroups + 1));
+  CK(cudaMemset(o.ticket, 0, size_t(max_batch) * (kMaxGroups + 1) * sizeof(unsigned)));
+  o.out_s = dev_alloc<float>(size_t(max_batch) * kMaxK);
+  o.out_id = dev_alloc<uint64_t>(size_t(max_batch) * kMaxK);
+  o.out_count = dev_alloc<uint32_t>(max_batch);
 }
 
 void Ctx::compact() {
@@ -629,13 +716,129 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
     }
     r.nslow[q] = uint32_t(slow[q].size());
   }
+  // runtime fetch: the most-shared misses go to the GPU (H2D into the ring +
+  // the same scan kernel) until the modeled GPU time meets the host's
+  const uint32_t d = ix->d;
+  std::vector<std::vector<uint32_t>> chunks;
+  if (miss_fetch && any_slow) {
+    std::map<uint32_t, uint32_t> share;
+    for (uint32_t q = 0; q < nq; ++q) {
+      for (uint32_t c : slow[q]) ++share[c];
+    }
+    std::vector<std::pair<uint32_t, uint32_t>> cand; // (share, list)
+    for (auto& [c, n] : share) cand.emplace_back(n, c);
+    std::sort(cand.begin(), cand.end(), [](auto& a, auto& b) {
+      return a.first != b.first ? a.first > b.first : a.second < b.second;
+    });
+    const double cr = cpu_rate > 0 ? cpu_rate : 6e9 * double(pool->size());
+    double cpu_t = 0, gpu_t = 0;
+    for (auto& [n, c] : cand) cpu_t += double(n) * double(ix->list_len(c)) * d * 4 / cr;
+    std::vector<uint32_t> fetch;
+    uint64_t fill = 0;
+    for (auto& [n, c] : cand) {
+      const uint64_t len = ix->list_len(c);
+      const double b = double(len) * d * 4;
+      const double ng = gpu_t + b / link_rate, nct = cpu_t - double(n) * b / cr;
+      if (miss_fetch == 1 && std::max(ng, nct) >= std::max(gpu_t, cpu_t)) break;
+      if (len == 0) continue;
+      if (chunks.empty() || fill + len > ring_vecs) {
+        if (chunks.size() == kMaxFetchChunks) break;
+        chunks.emplace_back();
+        fill = 0;
+      }
+      chunks.back().push_back(c);
+      fill += len;
+      fetch.push_back(c);
+      gpu_t = ng;
+      cpu_t = nct;
+    }
+    if (!fetch.empty()) {
+      std::vector<uint8_t> on_gpu(ix->nc, 0);
+      for (uint32_t c : fetch) on_gpu[c] = 1;
+      any_slow = false;
+      for (uint32_t q = 0; q < nq; ++q) {
+        auto& v = slow[q];
+        v.erase(std::remove_if(v.begin(), v.end(), [&](uint32_t c) { return on_gpu[c] != 0; }),
+                v.end());
+        any_slow = any_slow || !v.empty();
+      }
+      r.fetch_lists = uint32_t(fetch.size());
+    }
+  }
+  if (!chunks.empty()) {
+    CK(cudaEventRecord(ev_f0, copy));
+    std::vector<void*> dsts, srcs;
+    std::vector<size_t> sizes;
+    for (size_t j = 0; j < chunks.size(); ++j) {
+      const int slot = int(j & 1);
+      float* ring = d_ring + size_t(slot) * ring_vecs * d;
+      int64_t* hres = h_res_ring + j * ix->nc;
+      std::fill(hres, hres + ix->nc, int64_t(-1));
+      // ring order = cluster order, so lists adjacent in the list-major host
+      // store become one copy
+      std::sort(chunks[j].begin(), chunks[j].end());
+      dsts.clear();
+      srcs.clear();
+      sizes.clear();
+      uint64_t off = 0;
+      for (uint32_t c : chunks[j]) {
+        const uint64_t len = ix->list_len(c);
+        hres[c] = int64_t(off);
+        const float* src = ix->vecs + ix->list_off[c] * d;
+        float* dst = ring + off * d;
+        if (!srcs.empty() && static_cast<float*>(srcs.back()) +
+                                     sizes.back() / sizeof(float) == src) {
+          sizes.back() += len * d * sizeof(float);
+        } else {
+          dsts.push_back(dst);
+          srcs.push_back(const_cast<float*>(src));
+          sizes.push_back(len * d * sizeof(float));
+        }
+        off += len;
+        r.fetch_bytes += len * d * 4;
+      }
+      CK(cudaStreamWaitEvent(copy, ev_freed[slot], 0));
+      CK(cudaMemcpyAsync(d_res_ring[slot], hres, ix->nc * sizeof(int64_t),
+                         cudaMemcpyHostToDevice, copy));
+      h2d_batch(dsts, srcs, sizes, copy);
+      CK(cudaEventRecord(ev_landed[slot], copy));
+      if (j + 1 == chunks.size()) CK(cudaEventRecord(ev_f1, copy));
+      CK(cudaStreamWaitEvent(comp, ev_landed[slot], 0));
+      fft.grid = static_cast<uint32_t>(G);
+      launch_partition(d_order, nq, lp, d_res_ring[slot], d_list_off, fft, comp);
+      launch_scan(dQ, nq, d, ix->metric, k, fft, ring, d_ids, fso, G, acc_fp64, scan_impl, tune,
+                  comp);
+      CK(cudaEventRecord(ev_freed[slot], comp));
+      const size_t o = j * max_batch;
+      CK(cudaMemcpyAsync(h_fetch_s + o * k, fso.out_s, size_t(nq) * k * sizeof(float),
+                         cudaMemcpyDeviceToHost, comp));
+      CK(cudaMemcpyAsync(h_fetch_id + o * k, fso.out_id, size_t(nq) * k * sizeof(uint64_t),
+                         cudaMemcpyDeviceToHost, comp));
+      CK(cudaMemcpyAsync(h_fetch_cnt + o, fso.out_count, nq * sizeof(uint32_t),
+                         cudaMemcpyDeviceToHost, comp));
+    }
+    rec(ev_fdone, comp);
+  }
   std::vector<std::vector<Scored>> miss(nq);
   if (any_slow) {
+    std::map<uint32_t, uint32_t> cl;
+    for (uint32_t q = 0; q < nq; ++q) {
+      for (uint32_t c : slow[q]) {
+        ++cl[c];
+        r.cpu_query_bytes += ix->list_len(c) * d * 4;
+      }
+    }
+    r.cpu_lists = uint32_t(cl.size());
     const auto tc = Clock::now();
     miss = miss_scan_batch(*ix, hQ, nq, slow, k, *pool);
     r.t_c = secs(tc, Clock::now());
+    if (r.t_c > 0 && r.cpu_query_bytes > (64ull << 20)) {
+      const double rate = double(r.cpu_query_bytes) / r.t_c;
+      cpu_rate = cpu_rate > 0 ? 0.5 * cpu_rate + 0.5 * rate : rate;
+    }
   }
   CK(cudaEventSynchronize(ev_c));
+  if (!chunks.empty()) CK(cudaEventSynchronize(ev_fdone));
   for (uint32_t q = 0; q < nq; ++q) {
     if (h_fcount[q] != r.nfast[q]) {
       throw std::runtime_error("device residency table disagrees with the store");
@@ -644,10 +847,26 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
     for (uint32_t i = 0; i < h_out_cnt[q]; ++i) {
       gpu[i] = {h_out_s[size_t(q) * k + i], h_out_id[size_t(q) * k + i]};
     }
+    for (size_t j = 0; j < chunks.size(); ++j) {
+      const size_t o = j * max_batch + q;
+      std::vector<Scored> f(h_fetch_cnt[o]);
+      for (uint32_t i = 0; i < h_fetch_cnt[o]; ++i) {
+        f[i] = {h_fetch_s[o * k + i], h_fetch_id[o * k + i]};
+      }
+      gpu = merge_topk(ix->metric, gpu, f, k);
+    }
     r.top[q] = merge_topk(ix->metric, gpu, miss[q], k);
   }
+  if (!chunks.empty()) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev_f0, ev_f1));
+    r.t_fetch = ms * 1e-3;
+    if (ms > 0 && r.fetch_bytes > (64ull << 20)) {
+      link_rate = 0.5 * link_rate + 0.5 * double(r.fetch_bytes) / (ms * 1e-3);
+    }
+  }
   float ms = 0;
-  CK(cudaEventElapsedTime(&ms, ev_a, ev_s));
+  CK(cudaEventElapsedTime(&ms, ev_a, chunks.empty() ? ev_s : ev_fdone));
   r.t_g = ms * 1e-3;
   CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
   r.t_coarse = ms * 1e-3;
@@ -805,6 +1024,10 @@ void fill_timing(laivg_hybrid_timing* t, const Ctx::Result& r,
   t->t_scan = r.t_scan;
   t->scanned_vectors = r.vecs_gpu;
   t->scanned_bytes = r.bytes_gpu;
+  t->fetched_lists = 0;
+  t->cpu_lists = uint32_t(r.slow.size());
+  t->fetched_bytes = 0;
+  t->t_fetch = 0;
   if (cost) { // tiered.cpp:190-196
     const double miss = double(r.slow.size());
     t->model_t_c = std::ceil(miss / cost->parallel_slots) * cost->t_cc;
@@ -844,6 +1067,10 @@ void fill_batch_timing(laivg_hybrid_timing* t, const Ctx::BatchResult& r,
   t->t_scan = r.t_scan;
   t->scanned_vectors = r.vecs_gpu;
   t->scanned_bytes = r.bytes_gpu;
+  t->fetched_lists = r.fetch_lists;
+  t->cpu_lists = r.cpu_lists;
+  t->fetched_bytes = r.fetch_bytes;
+  t->t_fetch = r.t_fetch;
   if (cost) { // tiered.cpp:190-196 summed over the batch
     double miss = 0, hit = 0;
     for (size_t q = 0; q < r.nfast.size(); ++q) {
@@ -1001,6 +1228,7 @@ void laivg_opts_default(laivg_opts* o) {
   std::memset(o, 0, sizeof(*o));
   o->acc_fp64 = 1;
   o->scan_impl = 0;
+  o->miss_fetch = 1;
 }
 
 int laivg_ctx_create(const laivg_index* ix, const laivg_opts* opts, laivg_ctx** out) {
@@ -1291,6 +1519,81 @@ int laivg_execute_prefetch(laivg_ctx* ctx, const uint32_t* plan, uint32_t n,
       // exposed transfer: copy end past window end (both from ev_base)
       r.overshoot_s = std::max(0.0, double(ms_end - (win ? ms_win : 0.0f)) * 1e-3);
     }
+    if (rep) *rep = r;
+  });
+}
+
+int laivg_prefetch_batch(laivg_ctx* ctx, const float* Q_in, uint32_t nq,
+                         const uint64_t* budgets, const laivg_channel* chan,
+                         double overlap_window_s, uint32_t* transferred_out,
+                         uint32_t* nplan_out, laivg_transfer_report* rep) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    need(chan, "chan");
+    if (chan->mode != LAIVG_CHAN_DEVICE) {
+      throw std::invalid_argument("prefetch_batch runs on the device channel");
+    }
+    Ctx& x = ctx->c;
+    const uint32_t nc = x.ix->nc;
+    if (nq) {
+      need(Q_in, "queries");
+      need(budgets, "budgets");
+    }
+    // one coarse pass ranks every predictor embedding of the micro-batch
+    std::vector<uint32_t> order(size_t(nq) * nc);
+    if (nq) coarse_batch(x, Q_in, nq, nc, order.data(), nullptr);
+    laivg_transfer_report r{};
+    const auto w0 = Clock::now();
+    (void)w0;
+    CK(cudaEventRecord(x.ev_base, x.comp));
+    CK(cudaStreamWaitEvent(x.copy, x.ev_base, 0));
+    const bool win = overlap_window_s > 0;
+    if (win) laivg::launch_window(uint64_t(overlap_window_s * 1e9), x.sms, x.comp);
+    CK(cudaEventRecord(x.ev_win, x.comp));
+    CK(cudaEventRecord(x.ev_cp0, x.copy));
+    uint64_t bytes = 0;
+    uint32_t done = 0;
+    try {
+      // pipeline.cpp:357-371: each query plans against the store already
+      // holding the earlier plans (shared clusters travel once), with budget
+      // min(budget_i, free bytes); the transfers share the copy stream
+      for (uint32_t q = 0; q < nq; ++q) {
+        std::vector<uint32_t> plan, skipped;
+        uint64_t planned = 0;
+        const uint64_t budget = std::min<uint64_t>(budgets[q], x.capacity - x.used);
+        laivg::plan_walk(*x.ix, order.data() + size_t(q) * nc,
+                         [&](uint32_t c) { return x.h_res[c] >= 0; }, budget, plan, planned,
+                         skipped);
+        for (uint32_t c : plan) {
+          x.insert_async(c, LAIVG_TAG_PREFETCHED);
+          bytes += x.ix->cluster_bytes(c);
+          if (transferred_out) transferred_out[done] = c;
+          ++done;
+        }
+        if (nplan_out) nplan_out[q] = uint32_t(plan.size());
+      }
+    } catch (...) {
+      x.commit_res(x.copy);
+      CK(cudaEventRecord(x.ev_copy_tail, x.copy));
+      CK(cudaStreamSynchronize(x.copy));
+      CK(cudaStreamSynchronize(x.comp));
+      throw;
+    }
+    x.commit_res(x.copy);
+    CK(cudaEventRecord(x.ev_cp1, x.copy));
+    CK(cudaEventRecord(x.ev_copy_tail, x.copy));
+    CK(cudaEventSynchronize(x.ev_cp1));
+    CK(cudaEventSynchronize(x.ev_win));
+    float ms_cp = 0, ms_win = 0, ms_end = 0;
+    CK(cudaEventElapsedTime(&ms_cp, x.ev_cp0, x.ev_cp1));
+    CK(cudaEventElapsedTime(&ms_win, x.ev_base, x.ev_win));
+    CK(cudaEventElapsedTime(&ms_end, x.ev_base, x.ev_cp1));
+    r.bytes = bytes;
+    r.n_transferred = done;
+    r.window_s = win ? ms_win * 1e-3 : 0.0;
+    r.h2d_gbps = ms_cp > 0 ? double(bytes) / (ms_cp * 1e-3) / 1e9 : 0.0;
+    r.t_p = ms_cp * 1e-3;
+    r.overshoot_s = std::max(0.0, double(ms_end - (win ? ms_win : 0.0f)) * 1e-3);
     if (rep) *rep = r;
   });
 }

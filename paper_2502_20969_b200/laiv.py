@@ -28,7 +28,7 @@ __all__ = [
     "HybridResult", "HybridTiming", "MicroBatch", "WorkerState", "HotnessTable",
     "CacheParams", "rank_clusters", "coarse_probe", "search_clusters", "ivf_search",
     "plan_prefetch", "execute_prefetch", "incremental_prefetch", "hybrid_search",
-    "coverage", "hybrid_search_batch", "BatchResult", "ivf_search_batch",
+    "coverage", "hybrid_search_batch", "prefetch_batch", "BatchResult", "ivf_search_batch",
     "group_microbatches", "chunk_microbatches", "assign_cache_aware",
     "assign_round_robin", "assignment_overlap", "split_budget", "default_nprobe",
     "LogicError", "CudaError", "synth_centroids", "synth_lists", "synth_queries",
@@ -243,7 +243,8 @@ class Device:
     def __init__(self, ix: IvfIndex, capacity_bytes: int, device: int = 0,
                  miss_threads: int = 0, max_batch: int = 0, max_probe: int = 0,
                  acc_fp64: bool = True, scan_impl: str = "tma", tma_tile: int = 0,
-                 tma_stages: int = 0, ctas_per_sm: int = 0, coarse_impl: str = "auto"):
+                 tma_stages: int = 0, ctas_per_sm: int = 0, coarse_impl: str = "auto",
+                 miss_fetch: str = "auto", fetch_chunk_mb: int = 0):
         L = lib()
         o = Opts()
         L.laivg_opts_default(C.byref(o))
@@ -261,6 +262,11 @@ class Device:
         if coarse_impl not in impls:
             raise ValueError("coarse_impl must be 'auto', 'fp64' or 'tensor'")
         o.coarse_impl = impls[coarse_impl]
+        fetches = {"off": 0, "auto": 1, "all": 2}
+        if miss_fetch not in fetches:
+            raise ValueError("miss_fetch must be 'off', 'auto' or 'all'")
+        o.miss_fetch = fetches[miss_fetch]
+        o.fetch_chunk_mb = fetch_chunk_mb
         h = C.c_void_p()
         check(L.laivg_ctx_create(ix.h, C.byref(o), C.byref(h)))
         self.h = h
@@ -445,6 +451,10 @@ class HybridTiming:                                               # tiered.hpp:8
     t_scan: float = 0.0
     scanned_vectors: int = 0
     scanned_bytes: int = 0
+    fetched_lists: int = 0     # misses fetched H2D on demand and scanned on the GPU
+    cpu_lists: int = 0         # distinct misses scanned by the host
+    fetched_bytes: int = 0
+    t_fetch: float = 0.0
 
 
 @dataclass
@@ -457,7 +467,8 @@ class HybridResult:                                               # tiered.hpp:9
 
 def _timing(t: HybridTimingC) -> HybridTiming:
     return HybridTiming(t.t_g, t.t_c, t.t_2, t.model_t_g, t.model_t_c, t.model_t_2,
-                        t.t_coarse, t.t_scan, int(t.scanned_vectors), int(t.scanned_bytes))
+                        t.t_coarse, t.t_scan, int(t.scanned_vectors), int(t.scanned_bytes),
+                        int(t.fetched_lists), int(t.cpu_lists), int(t.fetched_bytes), t.t_fetch)
 
 
 def plan_prefetch(dev: Device, q_in, budget_bytes: int) -> PrefetchPlan:  # tiered.hpp:100-101
@@ -485,6 +496,26 @@ def execute_prefetch(dev: Device, plan: PrefetchPlan, chan: TransferChannel,
     check(lib().laivg_execute_prefetch(dev.h, cl.ctypes.data, cl.size, C.byref(ch),
                                        overlap_window_s, out.ctypes.data, C.byref(r)))
     return _report(r, out[: r.n_transferred].tolist())
+
+
+def prefetch_batch(dev: Device, Q_in, budgets, chan: TransferChannel,
+                   overlap_window_s: float = 0.0):
+    """Lookahead prefetch of a micro-batch: one coarse pass, sequential plans
+    against the filling store (pipeline.cpp:357-371), one window. Returns the
+    TransferReport and each query's planned count."""
+    Q = _c(Q_in, np.float32).reshape(-1, dev.ix.d)
+    nq = Q.shape[0]
+    b = _c(budgets, np.uint64)
+    if b.size != nq:
+        raise ValueError("one budget per query")
+    out = np.empty(max(dev.ix.nc, 1), np.uint32)
+    npl = np.empty(max(nq, 1), np.uint32)
+    ch = Channel(chan.bandwidth_bytes_per_s, int(chan.mode))
+    r = TransferReportC()
+    check(lib().laivg_prefetch_batch(dev.h, Q.ctypes.data, nq, b.ctypes.data, C.byref(ch),
+                                     overlap_window_s, out.ctypes.data, npl.ctypes.data,
+                                     C.byref(r)))
+    return _report(r, out[: r.n_transferred].tolist()), npl[:nq].copy()
 
 
 def incremental_prefetch(dev: Device, q_round, budget_bytes: int, chan: TransferChannel,

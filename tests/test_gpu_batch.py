@@ -99,10 +99,13 @@ def test_tc_probe_exact_ties(laiv):
 
 
 @pytest.mark.parametrize("name,metric", [("l2", L2), ("ip", IP)])
-def test_batch_matches_single_planted(orc, laiv, name, metric):
+@pytest.mark.parametrize("fetch,chunk_mb", [("off", 0), ("auto", 0), ("all", 1), ("all", 3)])
+def test_batch_matches_single_planted(orc, laiv, name, metric, fetch, chunk_mb):
+    # misses on the host, adaptively split, or fetched on demand through a
+    # 1-list / 3-list ring (many chunks, the 32-chunk cap, three-way merge)
     cen, vecs, ids, off, qi, qo, g = planted_data()
     ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric(metric))
-    dev = laiv.Device(ix, BIG)
+    dev = laiv.Device(ix, BIG, miss_fetch=fetch, fetch_chunk_mb=chunk_mb)
     rng = np.random.default_rng(17)
     for trial in range(4):
         set_residency(dev, (rng.random(64) < [0.0, 1.0, 0.5, 0.2][trial]).astype(np.uint8))
@@ -117,16 +120,22 @@ def test_batch_matches_single_planted(orc, laiv, name, metric):
             want = orc.ivf_search(cen, vecs, ids, off, metric, qo[t], L, k)
             assert_topk_parity(metric, got.ids, got.scores, *want)
         assert timing.scanned_vectors == 300 * int(res.nfast.sum())
+        if fetch == "off":
+            assert timing.fetched_lists == 0
+        if fetch == "all" and trial in (0, 3):
+            assert timing.fetched_lists > 0
+            assert timing.fetched_bytes == timing.fetched_lists * 300 * 768 * 4
 
 
 @pytest.mark.parametrize("name", ["l2", "ip"])
-def test_batch_d8_golden(orc, laiv, name):
+@pytest.mark.parametrize("fetch", ["off", "all"])
+def test_batch_d8_golden(orc, laiv, name, fetch):
     # reference goldens are residency-independent (hybrid == monolithic):
     # replay them through the batch path under three residencies
     case, queries, g = hybrid_d8_case(orc, name)
     ix = laiv.IvfIndex(case.centroids, case.vecs, case.ids, case.list_off,
                        laiv.Metric(case.metric))
-    dev = laiv.Device(ix, BIG, max_batch=32)
+    dev = laiv.Device(ix, BIG, max_batch=32, miss_fetch=fetch, fetch_chunk_mb=1)
     p = f"{name}_"
     Ls, ks = g[p + "L"], g[p + "k"]
     for mask in (np.zeros(case.nc, np.uint8), np.ones(case.nc, np.uint8), g[p + "masks"][0]):
@@ -172,3 +181,39 @@ def test_batch_edges(orc, laiv):
         laiv.hybrid_search_batch(dev, qo[:17], 8, 5)  # > max_batch
     with pytest.raises(ValueError):
         laiv.hybrid_search_batch(dev, qo[:4], 8, 0)
+
+
+def test_prefetch_batch_matches_sequential(laiv):
+    # pipeline.cpp:357-371: query i plans against the store holding the earlier
+    # plans with budget min(budget_i, free bytes); shared lists travel once
+    cen, vecs, ids, off, qi, qo, g = planted_data()
+    ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric.InnerProduct)
+    cb = 300 * (4 * 768 + 8)
+    cap = 20 * cb
+    dev_a = laiv.Device(ix, cap)
+    dev_b = laiv.Device(ix, cap)
+    chan = laiv.TransferChannel(50e9, laiv.ChannelMode.Device)
+    for trial, (nq, per_q) in enumerate([(8, 3 * cb), (6, 5 * cb + 7), (12, 2 * cb - 1)]):
+        Q = qi[trial * 12: trial * 12 + nq]
+        budgets = laiv.split_budget(per_q * nq, laiv.MicroBatch(list(range(nq))))
+        dev_a.store.clear()
+        dev_b.store.clear()
+        dev_a.store.insert(int(laiv.coarse_probe(dev_a, Q[0], 1)[0]))  # one already resident
+        dev_b.store.insert(int(laiv.coarse_probe(dev_b, Q[0], 1)[0]))
+        rep, npl = laiv.prefetch_batch(dev_a, Q, budgets, chan, 0.001)
+        want = []
+        for i in range(nq):
+            b = min(budgets[i], dev_b.store.free_bytes())
+            plan = laiv.plan_prefetch(dev_b, Q[i], b)
+            laiv.execute_prefetch(dev_b, plan, chan)
+            assert npl[i] == len(plan.clusters)
+            want += plan.clusters
+        assert rep.transferred == want
+        assert rep.bytes == len(want) * cb
+        assert dev_a.store.resident() == dev_b.store.resident()
+        assert rep.window_s >= 0.001 and rep.t_p > 0
+        # the prefetched lists are scanned from HBM: batch search still exact
+        res, _ = laiv.hybrid_search_batch(dev_a, qo[trial * 12: trial * 12 + nq], 8, 10)
+        for t in range(nq):
+            single, _ = laiv.hybrid_search(dev_b, qo[trial * 12 + t], 8, 10)
+            assert np.array_equal(res.topk(t).ids, single.topk.ids)
