@@ -383,6 +383,17 @@ int laivg_synth_queries(uint64_t seed, const float* vecs, uint64_t n_rows,
                         uint32_t d, uint32_t nq, float sigma, float* q_in_out,
                         float* q_out_out, uint64_t* rows_out);
 
+/* Topical queries for the routed batches (C3-C5 skew): topic
+ * t ~ Zipf(zipf_s) over n_topics random centre lists; each query's source
+ * row is drawn from one of the `neigh` lists nearest its topic centre, then
+ * q_in / q_out as laivg_synth_queries. topic_out (nullable) gets t. */
+int laivg_synth_queries_topical(uint64_t seed, const float* centroids, uint32_t nc,
+                                const float* vecs, const uint64_t* list_off,
+                                uint32_t d, uint32_t n_topics, double zipf_s,
+                                uint32_t neigh, uint32_t nq, float sigma,
+                                float* q_in_out, float* q_out_out,
+                                uint64_t* rows_out, uint32_t* topic_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -110,6 +110,8 @@ SIGNATURES = {
     "laivg_hybrid_search_batch_staged": (i32, [vp, u32, u32, i32, i32, vp, vp, vp, vp,
                                                P(HybridTimingC)]),
     "laivg_debug_coarse_approx": (i32, [vp, vp, u32, vp]),
+    "laivg_synth_queries_topical": (i32, [u64, vp, u32, vp, vp, u32, u32, f64, u32, u32, f32,
+                                          vp, vp, vp, vp]),
     "laivg_prefetch_batch": (i32, [vp, vp, u32, vp, P(Channel), f64, vp, vp,
                                    P(TransferReportC)]),
     "laivg_group_microbatches": (i32, [vp, u64, u32, u64, vp, vp, P(u32)]),

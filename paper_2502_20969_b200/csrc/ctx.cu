@@ -103,7 +103,7 @@ class SlabAlloc {
   std::map<uint64_t, uint64_t> free_;
 };
 
-constexpr uint32_t kMaxFetchChunks = 32;
+constexpr uint32_t kMaxFetchChunks = 128;
 
 // Enqueues many host->device copies with one cudaMemcpyBatchAsync call
 // (CUDA 12.8+), falling back to one cudaMemcpyAsync per copy.
@@ -194,6 +194,17 @@ struct Ctx {
   float* h_fetch_s = nullptr;    // pinned [kMaxFetchChunks][max_batch][kMaxK]
   uint64_t* h_fetch_id = nullptr;
   uint32_t* h_fetch_cnt = nullptr;
+  int fetch_k = 0;               // k the chunk result buffers are sized for
+  void fetch_results_for(int k) {
+    if (k <= fetch_k) return;
+    if (h_fetch_s) cudaFreeHost(h_fetch_s);
+    if (h_fetch_id) cudaFreeHost(h_fetch_id);
+    h_fetch_s = nullptr;
+    h_fetch_id = nullptr;
+    h_fetch_s = pin_alloc<float>(size_t(kMaxFetchChunks) * max_batch * k);
+    h_fetch_id = pin_alloc<uint64_t>(size_t(kMaxFetchChunks) * max_batch * k);
+    fetch_k = k;
+  }
   cudaEvent_t ev_landed[2] = {nullptr, nullptr}, ev_freed[2] = {nullptr, nullptr};
   cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr, ev_fdone = nullptr;
   double link_rate = 50e9;       // EMA of fetch H2D bytes/s
@@ -517,8 +528,6 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
     CK(cudaEventCreate(&ev_fdone));
     h_res_ring = pin_alloc<int64_t>(size_t(kMaxFetchChunks) * nc);
     alloc_scan_set(fft, fso);
-    h_fetch_s = pin_alloc<float>(size_t(kMaxFetchChunks) * max_batch * kMaxK);
-    h_fetch_id = pin_alloc<uint64_t>(size_t(kMaxFetchChunks) * max_batch * kMaxK);
     h_fetch_cnt = pin_alloc<uint32_t>(size_t(kMaxFetchChunks) * max_batch);
   }
   h_Q = pin_alloc<float>(size_t(max_batch) * d);
@@ -766,6 +775,7 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
     }
   }
   if (!chunks.empty()) {
+    fetch_results_for(k);
     CK(cudaEventRecord(ev_f0, copy));
     std::vector<void*> dsts, srcs;
     std::vector<size_t> sizes;
@@ -1973,6 +1983,20 @@ int laivg_synth_queries(uint64_t seed, const float* vecs, uint64_t n_rows, uint3
     need(vecs, "vecs");
     if (n_rows == 0) throw std::invalid_argument("no rows");
     laivg::synth_queries(seed, vecs, n_rows, d, nq, sigma, q_in_out, q_out_out, rows_out);
+  });
+}
+
+int laivg_synth_queries_topical(uint64_t seed, const float* centroids, uint32_t nc,
+                                const float* vecs, const uint64_t* list_off, uint32_t d,
+                                uint32_t n_topics, double zipf_s, uint32_t neigh, uint32_t nq,
+                                float sigma, float* q_in_out, float* q_out_out,
+                                uint64_t* rows_out, uint32_t* topic_out) {
+  return guard([&] {
+    need(centroids, "centroids");
+    need(vecs, "vecs");
+    need(list_off, "list_off");
+    laivg::synth_queries_topical(seed, centroids, nc, vecs, list_off, d, n_topics, zipf_s, neigh,
+                                 nq, sigma, q_in_out, q_out_out, rows_out, topic_out);
   });
 }
 

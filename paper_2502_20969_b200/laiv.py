@@ -32,6 +32,7 @@ __all__ = [
     "group_microbatches", "chunk_microbatches", "assign_cache_aware",
     "assign_round_robin", "assignment_overlap", "split_budget", "default_nprobe",
     "LogicError", "CudaError", "synth_centroids", "synth_lists", "synth_queries",
+    "synth_queries_topical",
 ]
 
 
@@ -810,3 +811,21 @@ def synth_queries(seed: int, vecs: np.ndarray, nq: int, sigma: float):
     check(lib().laivg_synth_queries(seed, vecs.ctypes.data, n, d, nq, sigma, qi.ctypes.data,
                                     qo.ctypes.data, rows.ctypes.data))
     return qi, qo, rows
+
+
+def synth_queries_topical(seed: int, centroids: np.ndarray, vecs: np.ndarray, list_off,
+                          nq: int, sigma: float, n_topics: int = 32, zipf_s: float = 1.0,
+                          neigh: int = 16):
+    """Topical (Zipf-skewed) q_in / q_out pairs: returns qi, qo, rows, topic."""
+    cen = _c(centroids, np.float32)
+    nc, d = cen.shape
+    off = _c(list_off, np.uint64)
+    qi = np.empty((nq, d), np.float32)
+    qo = np.empty((nq, d), np.float32)
+    rows = np.empty(nq, np.uint64)
+    topic = np.empty(nq, np.uint32)
+    check(lib().laivg_synth_queries_topical(seed, cen.ctypes.data, nc, vecs.ctypes.data,
+                                            off.ctypes.data, d, n_topics, zipf_s, neigh, nq,
+                                            sigma, qi.ctypes.data, qo.ctypes.data,
+                                            rows.ctypes.data, topic.ctypes.data))
+    return qi, qo, rows, topic
