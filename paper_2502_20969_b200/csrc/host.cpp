@@ -8,6 +8,8 @@
 #include <cstring>
 #include <numeric>
 
+#include <immintrin.h>
+
 namespace laivg {
 
 // ==========================================================================
@@ -129,6 +131,72 @@ struct TopList {
 
 constexpr uint64_t kMissChunk = 1024; // vectors per miss-scan task
 
+// Register-blocked host scoring of one fp32 row against G queries held in
+// fp64 (converted once per batch): the row is read from memory once and
+// every term is the reference's (vectorstore.cpp:93-108). IP uses FMA, which
+// is exact here: the product of two fp32 values is exact in fp64, so
+// fma(q, x, acc) == acc + q * x. L2 keeps the separately rounded sub/mul/add.
+// Partial sums run over 4 lanes x 2 chains, reduced at the end (any order is
+// within the parity rule; see the GPU scan).
+template <int G, bool kIP>
+__attribute__((target("avx2,fma"))) void score_rows_avx2(const float* x, const double* const* q,
+                                                         uint32_t d, double* out) {
+  __m256d a0[G], a1[G];
+  for (int g = 0; g < G; ++g) {
+    a0[g] = _mm256_setzero_pd();
+    a1[g] = _mm256_setzero_pd();
+  }
+  uint32_t j = 0;
+  for (; j + 8 <= d; j += 8) {
+    const __m256d x0 = _mm256_cvtps_pd(_mm_loadu_ps(x + j));
+    const __m256d x1 = _mm256_cvtps_pd(_mm_loadu_ps(x + j + 4));
+    for (int g = 0; g < G; ++g) {
+      const __m256d q0 = _mm256_loadu_pd(q[g] + j), q1 = _mm256_loadu_pd(q[g] + j + 4);
+      if constexpr (kIP) {
+        a0[g] = _mm256_fmadd_pd(q0, x0, a0[g]);
+        a1[g] = _mm256_fmadd_pd(q1, x1, a1[g]);
+      } else {
+        const __m256d t0 = _mm256_sub_pd(q0, x0), t1 = _mm256_sub_pd(q1, x1);
+        a0[g] = _mm256_add_pd(a0[g], _mm256_mul_pd(t0, t0));
+        a1[g] = _mm256_add_pd(a1[g], _mm256_mul_pd(t1, t1));
+      }
+    }
+  }
+  for (int g = 0; g < G; ++g) {
+    alignas(32) double l[4];
+    _mm256_store_pd(l, _mm256_add_pd(a0[g], a1[g]));
+    double sacc = (l[0] + l[1]) + (l[2] + l[3]);
+    for (uint32_t t = j; t < d; ++t) {
+      const double xv = static_cast<double>(x[t]);
+      if constexpr (kIP) {
+        sacc += q[g][t] * xv;
+      } else {
+        const double u = q[g][t] - xv;
+        sacc += u * u;
+      }
+    }
+    out[g] = sacc;
+  }
+}
+
+bool host_has_avx2() {
+  static const bool ok = __builtin_cpu_supports("avx2") && __builtin_cpu_supports("fma");
+  return ok;
+}
+
+template <bool kIP>
+void score_row_blocked(const float* x, const double* const* q, uint32_t n, uint32_t d,
+                       double* out) {
+  uint32_t g = 0;
+  for (; g + 4 <= n; g += 4) score_rows_avx2<4, kIP>(x, q + g, d, out + g);
+  switch (n - g) {
+    case 3: score_rows_avx2<3, kIP>(x, q + g, d, out + g); break;
+    case 2: score_rows_avx2<2, kIP>(x, q + g, d, out + g); break;
+    case 1: score_rows_avx2<1, kIP>(x, q + g, d, out + g); break;
+    default: break;
+  }
+}
+
 } // namespace
 
 std::vector<Scored> miss_scan(const Index& ix, const float* q,
@@ -145,11 +213,27 @@ std::vector<Scored> miss_scan(const Index& ix, const float* q,
   }
   std::vector<TopList> per(pool.size(), TopList{ix.metric, k, {}});
   const uint32_t d = ix.d;
+  const bool fast = host_has_avx2();
+  std::vector<double> qd(fast ? d : 0);
+  for (uint32_t j = 0; fast && j < d; ++j) qd[j] = q[j];
+  const double* qp = qd.data();
   pool.parallel_for(tasks.size(), [&](size_t t, unsigned wid) {
     TopList& tl = per[wid];
     for (uint64_t r = tasks[t].r0; r < tasks[t].r1; ++r) {
       const float* x = ix.vecs + r * d;
       float s;
+      if (fast) { // same per-query arithmetic as the batched miss scan
+        double v;
+        if (ix.metric == kMetricIP) {
+          score_row_blocked<true>(x, &qp, 1, d, &v);
+          s = static_cast<float>(v);
+        } else {
+          score_row_blocked<false>(x, &qp, 1, d, &v);
+          s = static_cast<float>(std::sqrt(v));
+        }
+        tl.push({s, ix.ids[r]});
+        continue;
+      }
       if (ix.metric == kMetricIP) {
         s = static_cast<float>(dot_f64(q, x, d));
       } else {
@@ -187,8 +271,43 @@ std::vector<std::vector<Scored>> miss_scan_batch(const Index& ix, const float* Q
   const unsigned nw = pool.size();
   std::vector<TopList> per(size_t(nw) * nq, TopList{ix.metric, k, {}});
   const uint32_t d = ix.d;
+  const bool fast = host_has_avx2();
+  // queries in fp64 once per batch (only those with misses)
+  std::vector<double> Qd;
+  std::vector<int64_t> qslot(nq, -1);
+  if (fast) {
+    size_t n = 0;
+    for (uint32_t q = 0; q < nq; ++q) {
+      if (!slow[q].empty()) qslot[q] = int64_t(n++);
+    }
+    Qd.resize(n * d);
+    for (uint32_t q = 0; q < nq; ++q) {
+      if (qslot[q] < 0) continue;
+      for (uint32_t j = 0; j < d; ++j) Qd[size_t(qslot[q]) * d + j] = Q[size_t(q) * d + j];
+    }
+  }
   pool.parallel_for(tasks.size(), [&](size_t t, unsigned wid) {
     const Task& tk = tasks[t];
+    if (fast) {
+      const std::vector<uint32_t>& qs = *tk.qs;
+      std::vector<const double*> qp(qs.size());
+      for (size_t i = 0; i < qs.size(); ++i) qp[i] = Qd.data() + size_t(qslot[qs[i]]) * d;
+      std::vector<double> sc(qs.size());
+      for (uint64_t r = tk.r0; r < tk.r1; ++r) {
+        const float* x = ix.vecs + r * d;
+        if (ix.metric == kMetricIP) {
+          score_row_blocked<true>(x, qp.data(), uint32_t(qs.size()), d, sc.data());
+        } else {
+          score_row_blocked<false>(x, qp.data(), uint32_t(qs.size()), d, sc.data());
+        }
+        for (size_t i = 0; i < qs.size(); ++i) {
+          const float s = ix.metric == kMetricIP ? static_cast<float>(sc[i])
+                                                 : static_cast<float>(std::sqrt(sc[i]));
+          per[size_t(wid) * nq + qs[i]].push({s, ix.ids[r]});
+        }
+      }
+      return;
+    }
     for (uint64_t r = tk.r0; r < tk.r1; ++r) {
       const float* x = ix.vecs + r * d;
       for (uint32_t q : *tk.qs) {
