@@ -194,6 +194,31 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def profiled_traffic(kernel_prefix: str):
+    """dram read+write bytes per launch of the scan kernel from the committed
+    `ncu --set full` summary of the C2 workload (profiles/rNN/), or None."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*",
+                                              "ncu_scan_full_summary.json")), reverse=True):
+        try:
+            with open(path) as f:
+                ks = json.load(f)["kernels"]
+            vals = []
+            for k in ks:
+                if kernel_prefix in k["name"]:
+                    rd = float(k["dram__bytes_read.sum"].split()[0])
+                    wr = float(k["dram__bytes_write.sum"].split()[0])
+                    unit = k["dram__bytes_read.sum"].split()[1]
+                    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
+                    vals.append((rd + wr) * scale)
+            if vals:
+                return float(np.mean(vals)), os.path.relpath(path, ROOT)
+        except (OSError, KeyError, ValueError, IndexError):
+            continue
+    return None, None
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -369,6 +394,8 @@ def run_ours(args, cfg):
     achieved = bytes_scan / t_scan / 1e9 if t_scan > 0 else 0.0
     exposed = np.array([r["exposed"] for r in rec])
     t_p = np.array([r["t_p"] for r in rec])
+    traffic, traffic_src = (profiled_traffic("scan_tma_kernel")
+                            if args.config == "c2" and args.scan == "tma" else (None, None))
     line = {
         "metric": METRIC, "value": n_total / sum_v, "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum_v / args.steps * 1e3,
@@ -381,7 +408,7 @@ def run_ours(args, cfg):
         "roofline": {"kernel": f"scan_{args.scan}_kernel", "bound": "hbm", "achieved": achieved,
                      "peak": peak, "peak_kind": f"{peak_kind} copy (MEASURED_PEAKS.json hbm_gbs)",
                      "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None,
+                     "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": bytes_scan / max(len(rec), 1),
                      "avg_launch_ms": t_scan / max(len(rec), 1) * 1e3},
         "prefetch": {"h2d_gbps": float(np.mean([r["h2d_gbps"] for r in rec])),
