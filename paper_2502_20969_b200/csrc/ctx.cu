@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -33,6 +34,29 @@ thread_local std::string g_err;
   } while (0)
 
 using Clock = std::chrono::steady_clock;
+
+// LAIVG_TRACE=1: per-call host phase timestamps of the single-query search,
+// printed to stderr (diagnostics for the latency budget; off by default).
+struct PhaseTrace {
+  bool on = std::getenv("LAIVG_TRACE") != nullptr;
+  Clock::time_point t[12];
+  const char* name[12];
+  int n = 0;
+  void mark(const char* nm) {
+    if (!on || n >= 12) return;
+    t[n] = Clock::now();
+    name[n++] = nm;
+  }
+  void dump() {
+    if (!on || n < 2) return;
+    std::string s = "[laivg trace]";
+    for (int i = 1; i < n; ++i) {
+      s += std::string(" ") + name[i] + "=" +
+           std::to_string(std::chrono::duration<double, std::micro>(t[i] - t[i - 1]).count());
+    }
+    std::fprintf(stderr, "%s\n", s.c_str());
+  }
+};
 double secs(Clock::time_point a, Clock::time_point b) {
   return std::chrono::duration<double>(b - a).count();
 }
@@ -49,6 +73,19 @@ T* pin_alloc(size_t n) {
   void* p = nullptr;
   if (n == 0) n = 1;
   CK(cudaHostAlloc(&p, n * sizeof(T), cudaHostAllocPortable));
+  return static_cast<T*>(p);
+}
+
+// Pinned host memory the device also addresses (kernels write results
+// straight into it: no copy nodes on the latency path).
+template <class T>
+T* pin_alloc_mapped(size_t n, T** dev) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  CK(cudaHostAlloc(&p, n * sizeof(T), cudaHostAllocPortable | cudaHostAllocMapped));
+  void* d = nullptr;
+  CK(cudaHostGetDevicePointer(&d, p, 0));
+  *dev = static_cast<T*>(d);
   return static_cast<T*>(p);
 }
 
@@ -209,7 +246,7 @@ struct Ctx {
   cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr, ev_fdone = nullptr;
   double link_rate = 50e9;       // EMA of fetch H2D bytes/s
   double cpu_rate = 0;           // EMA of host miss scan (per-query bytes)/s
-  void alloc_scan_set(FastTable& f, ScanOut& o);
+  void alloc_scan_set(FastTable& f, ScanOut& o, bool device_outputs = true);
   int part_cap = 0; // partial top-k rows available (CTAs x queries)
   float* h_Q = nullptr;
   uint32_t* h_order = nullptr;
@@ -217,6 +254,11 @@ struct Ctx {
   uint64_t* h_out_id = nullptr;
   uint32_t* h_out_cnt = nullptr;
   uint32_t* h_fcount = nullptr;
+  uint32_t* dm_order = nullptr; // device aliases of the mapped buffers above
+  float* dm_out_s = nullptr;
+  uint64_t* dm_out_id = nullptr;
+  uint32_t* dm_out_cnt = nullptr;
+  uint32_t* dm_fcount = nullptr;
   float* d_staged = nullptr;
   uint32_t n_staged = 0;
   std::vector<float> staged_host;
@@ -292,8 +334,7 @@ struct Ctx {
   BatchResult search_batch(const float* dQ, const float* hQ, uint32_t nq, int L, int k);
 
   // ---- the coarse -> select -> scan chain as one CUDA graph per (L, k) ----
-  std::map<uint64_t, cudaGraphExec_t> graphs;
-  bool use_graphs = true;
+  bool use_graphs = std::getenv("LAIVG_GRAPHS") ? std::atoi(std::getenv("LAIVG_GRAPHS")) != 0 : true;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr; // capture-internal fork/join
   bool capturing = false;
   // Timing events stay host-visible inside a captured graph (external record
@@ -302,70 +343,104 @@ struct Ctx {
     if (capturing) CK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
     else CK(cudaEventRecord(e, st));
   }
-  void enqueue_results(int k) {
-    CK(cudaMemcpyAsync(h_out_s, so.out_s, k * sizeof(float), cudaMemcpyDeviceToHost, comp));
-    CK(cudaMemcpyAsync(h_out_id, so.out_id, k * sizeof(uint64_t), cudaMemcpyDeviceToHost, comp));
-    CK(cudaMemcpyAsync(h_out_cnt, so.out_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, comp));
-    CK(cudaMemcpyAsync(h_fcount, ft.count, sizeof(uint32_t), cudaMemcpyDeviceToHost, comp));
-    rec(ev_c, comp);
-  }
-  // Query in d_Q: coarse scores, ranking + residency split, scan, results;
-  // the probe goes to the host on the aux stream as soon as it exists.
-  void enqueue_coarse_path(uint32_t lp, int k, int G) {
+  // The scan's final CTA wrote the results (and the fast-list count) into
+  // mapped host memory; completion is all the host needs.
+  void enqueue_results(int) { rec(ev_c, comp); }
+  // Query in `src` (device or pinned host): copied into d_Q by the chain's
+  // first node, then coarse scores, ranking + residency split, scan,
+  // results; the probe goes to the host on the aux stream as soon as it
+  // exists.
+  void enqueue_coarse_path(uint32_t lp, int k, int G, const float* src) {
+    CK(cudaMemcpyAsync(d_Q, src, ix->d * sizeof(float), cudaMemcpyDefault, comp));
     rec(ev_a, comp);
     launch_coarse_scores(d_Q, 1, d_cen, ix->nc, ix->d, ix->metric, d_scores, comp);
-    launch_select(d_scores, 1, ix->nc, ix->metric, lp, d_order, d_run_k, d_run_v, d_res,
+    // the ranking prefix lands directly in host memory (mapped)
+    launch_select(d_scores, 1, ix->nc, ix->metric, lp, dm_order, d_run_k, d_run_v, d_res,
                   d_list_off, &ft, comp);
     rec(ev_b, comp);
-    CK(cudaEventRecord(ev_fork, comp));
-    CK(cudaStreamWaitEvent(aux, ev_fork, 0));
-    if (lp) {
-      CK(cudaMemcpyAsync(h_order, d_order, lp * sizeof(uint32_t), cudaMemcpyDeviceToHost, aux));
-    }
-    rec(ev_probe, aux);
-    CK(cudaEventRecord(ev_join, aux));
-    rec(ev_p, comp);
     launch_scan(d_Q, 1, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl,
                 tune, comp);
     rec(ev_s, comp);
-    CK(cudaStreamWaitEvent(comp, ev_join, 0));
     enqueue_results(k);
   }
-  void run_coarse_path(uint32_t lp, int k, int G) {
-    const uint64_t key = (uint64_t(lp) << 32) | uint32_t(k);
-    auto it = graphs.find(key);
-    if (it == graphs.end() && use_graphs) {
+  struct GraphEntry {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    cudaGraphNode_t qnode = nullptr; // the query copy, re-pointed per launch
+    const float* src = nullptr;
+  };
+  std::map<uint64_t, GraphEntry> graph_tab;
+  void run_coarse_path(uint32_t lp, int k, int G, const float* src) {
+    cudaPointerAttributes pa{};
+    const bool dev_src = cudaPointerGetAttributes(&pa, src) == cudaSuccess &&
+                         pa.type == cudaMemoryTypeDevice;
+    cudaGetLastError();
+    const uint64_t key = (uint64_t(lp) << 33) | (uint64_t(uint32_t(k)) << 1) | (dev_src ? 1 : 0);
+    auto it = graph_tab.find(key);
+    if (it == graph_tab.end() && use_graphs) {
       // first call for this shape runs eagerly (sets kernel attributes), then
       // the chain is captured for the following calls
-      enqueue_coarse_path(lp, k, G);
-      cudaGraph_t g = nullptr;
-      cudaGraphExec_t ge = nullptr;
+      enqueue_coarse_path(lp, k, G, src);
+      GraphEntry e;
       const uint64_t launched = launch_counter().load();
       bool ok = cudaStreamBeginCapture(comp, cudaStreamCaptureModeRelaxed) == cudaSuccess;
       if (ok) {
         capturing = true;
         try {
-          enqueue_coarse_path(lp, k, G);
+          enqueue_coarse_path(lp, k, G, src);
         } catch (...) {
           ok = false;
         }
         capturing = false;
-        ok = (cudaStreamEndCapture(comp, &g) == cudaSuccess) && ok && g != nullptr;
+        ok = (cudaStreamEndCapture(comp, &e.g) == cudaSuccess) && ok && e.g != nullptr;
       }
       launch_counter() = launched; // captured launches did not run
-      ok = ok && cudaGraphInstantiate(&ge, g, 0) == cudaSuccess;
-      if (g) cudaGraphDestroy(g);
+      if (ok) { // locate the query copy node (the one writing d_Q)
+        size_t n = 0;
+        ok = cudaGraphGetNodes(e.g, nullptr, &n) == cudaSuccess;
+        std::vector<cudaGraphNode_t> nodes(n);
+        ok = ok && cudaGraphGetNodes(e.g, nodes.data(), &n) == cudaSuccess;
+        for (size_t i = 0; ok && i < n; ++i) {
+          cudaGraphNodeType t;
+          if (cudaGraphNodeGetType(nodes[i], &t) != cudaSuccess || t != cudaGraphNodeTypeMemcpy) {
+            continue;
+          }
+          cudaMemcpy3DParms mp{};
+          if (cudaGraphMemcpyNodeGetParams(nodes[i], &mp) == cudaSuccess &&
+              mp.dstPtr.ptr == static_cast<void*>(d_Q)) {
+            e.qnode = nodes[i];
+          }
+        }
+        ok = ok && e.qnode != nullptr;
+      }
+      ok = ok && cudaGraphInstantiate(&e.ge, e.g, 0) == cudaSuccess;
       cudaGetLastError();
-      if (ok) graphs[key] = ge;
-      else use_graphs = false; // capture unsupported here: stay eager
+      if (ok) {
+        e.src = src;
+        graph_tab[key] = e;
+      } else {
+        if (e.g) cudaGraphDestroy(e.g);
+        use_graphs = false; // capture unsupported here: stay eager
+      }
       return;
     }
-    if (it != graphs.end()) {
-      CK(cudaGraphLaunch(it->second, comp));
+    if (it != graph_tab.end()) {
+      GraphEntry& e = it->second;
+      if (e.src != src) {
+        if (cudaGraphExecMemcpyNodeSetParams1D(e.ge, e.qnode, d_Q, src, ix->d * sizeof(float),
+                                               cudaMemcpyDefault) != cudaSuccess) {
+          cudaGetLastError();
+          use_graphs = false;
+          enqueue_coarse_path(lp, k, G, src);
+          return;
+        }
+        e.src = src;
+      }
+      CK(cudaGraphLaunch(e.ge, comp));
       launch_counter() += 4; // coarse, seg_sort, merge_runs, scan
       return;
     }
-    enqueue_coarse_path(lp, k, G);
+    enqueue_coarse_path(lp, k, G, src);
   }
 };
 
@@ -379,7 +454,6 @@ Ctx::~Ctx() {
                   (void*)ft.cluster, (void*)ft.pre, (void*)ft.count, (void*)ft.cta,
                   (void*)so.part_s, (void*)so.part_id, (void*)so.part_vi, (void*)so.ticket,
                   (void*)so.gpart_s, (void*)so.gpart_id, (void*)so.gpart_vi,
-                  (void*)so.out_s, (void*)so.out_id, (void*)so.out_count,
                   (void*)d_staged, (void*)d_approx, (void*)d_cnorm}) {
     if (p) cudaFree(p);
   }
@@ -403,7 +477,10 @@ Ctx::~Ctx() {
                         ev_fdone}) {
     if (e) cudaEventDestroy(e);
   }
-  for (auto& [key, ge] : graphs) cudaGraphExecDestroy(ge);
+  for (auto& [key, e] : graph_tab) {
+    if (e.ge) cudaGraphExecDestroy(e.ge);
+    if (e.g) cudaGraphDestroy(e.g);
+  }
   for (cudaEvent_t e : {ev_a, ev_b, ev_p, ev_s, ev_c, ev_probe, ev_base, ev_win,
                         ev_cp0, ev_cp1, ev_copy_tail, ev_comp_tail, res_ev[0],
                         res_ev[1], ev_fork, ev_join}) {
@@ -510,7 +587,7 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   d_run_v = dev_alloc<uint32_t>(select_scratch_entries(max_batch, nc));
   const int per_sm = std::max<int>(2, int(tune.ctas_per_sm));
   part_cap = std::max<int>(per_sm * sms, int(max_batch)) + per_sm * sms;
-  alloc_scan_set(ft, so);
+  alloc_scan_set(ft, so, /*device_outputs=*/false);
   miss_fetch = o.miss_fetch;
   if (miss_fetch > 2) throw std::invalid_argument("miss_fetch must be 0, 1 or 2");
   if (miss_fetch) {
@@ -531,11 +608,17 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
     h_fetch_cnt = pin_alloc<uint32_t>(size_t(kMaxFetchChunks) * max_batch);
   }
   h_Q = pin_alloc<float>(size_t(max_batch) * d);
-  h_order = pin_alloc<uint32_t>(size_t(max_batch) * std::max(nc, 1u));
-  h_out_s = pin_alloc<float>(size_t(max_batch) * kMaxK);
-  h_out_id = pin_alloc<uint64_t>(size_t(max_batch) * kMaxK);
-  h_out_cnt = pin_alloc<uint32_t>(max_batch);
-  h_fcount = pin_alloc<uint32_t>(max_batch);
+  h_order = pin_alloc_mapped<uint32_t>(size_t(max_batch) * std::max(nc, 1u), &dm_order);
+  h_out_s = pin_alloc_mapped<float>(size_t(max_batch) * kMaxK, &dm_out_s);
+  h_out_id = pin_alloc_mapped<uint64_t>(size_t(max_batch) * kMaxK, &dm_out_id);
+  h_out_cnt = pin_alloc_mapped<uint32_t>(max_batch, &dm_out_cnt);
+  h_fcount = pin_alloc_mapped<uint32_t>(max_batch, &dm_fcount);
+  // the main scan writes its results straight into host memory
+  so.out_s = dm_out_s;
+  so.out_id = dm_out_id;
+  so.out_count = dm_out_cnt;
+  so.fcount_in = ft.count;
+  so.fcount_out = dm_fcount;
 
   unsigned threads = o.miss_threads;
   if (threads == 0) threads = std::max(1u, std::thread::hardware_concurrency());
@@ -543,7 +626,7 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   CK(cudaDeviceSynchronize());
 }
 
-void Ctx::alloc_scan_set(FastTable& f, ScanOut& o) {
+void Ctx::alloc_scan_set(FastTable& f, ScanOut& o, bool device_outputs) {
   f.stride = max_probe;
   f.slab = dev_alloc<int64_t>(size_t(max_batch) * max_probe);
   f.row = dev_alloc<uint64_t>(size_t(max_batch) * max_probe);
@@ -560,9 +643,11 @@ void Ctx::alloc_scan_set(FastTable& f, ScanOut& o) {
   o.gpart_vi = dev_alloc<uint32_t>(size_t(max_batch) * kMaxGroups * kMaxK);
   o.ticket = dev_alloc<unsigned>(size_t(max_batch) * (kMaxGroups + 1));
   CK(cudaMemset(o.ticket, 0, size_t(max_batch) * (kMaxGroups + 1) * sizeof(unsigned)));
-  o.out_s = dev_alloc<float>(size_t(max_batch) * kMaxK);
-  o.out_id = dev_alloc<uint64_t>(size_t(max_batch) * kMaxK);
-  o.out_count = dev_alloc<uint32_t>(max_batch);
+  if (device_outputs) {
+    o.out_s = dev_alloc<float>(size_t(max_batch) * kMaxK);
+    o.out_id = dev_alloc<uint64_t>(size_t(max_batch) * kMaxK);
+    o.out_count = dev_alloc<uint32_t>(max_batch);
+  }
 }
 
 void Ctx::compact() {
@@ -698,14 +783,7 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
   launch_scan(dQ, nq, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl, tune,
               comp);
   rec(ev_s, comp);
-  CK(cudaMemcpyAsync(h_out_s, so.out_s, size_t(nq) * k * sizeof(float), cudaMemcpyDeviceToHost,
-                     comp));
-  CK(cudaMemcpyAsync(h_out_id, so.out_id, size_t(nq) * k * sizeof(uint64_t),
-                     cudaMemcpyDeviceToHost, comp));
-  CK(cudaMemcpyAsync(h_out_cnt, so.out_count, nq * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                     comp));
-  CK(cudaMemcpyAsync(h_fcount, ft.count, nq * sizeof(uint32_t), cudaMemcpyDeviceToHost, comp));
-  rec(ev_c, comp);
+  rec(ev_c, comp); // results are in mapped host memory
 
   // host: split every probe by residency and scan the misses list-major
   CK(cudaEventSynchronize(ev_probe));
@@ -867,6 +945,7 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
     }
     r.top[q] = merge_topk(ix->metric, gpu, miss[q], k);
   }
+  r.t_2 = secs(t0, Clock::now()); // merged results exist: timing bookkeeping follows
   if (!chunks.empty()) {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, ev_f0, ev_f1));
@@ -882,7 +961,6 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
   r.t_coarse = ms * 1e-3;
   CK(cudaEventElapsedTime(&ms, ev_p, ev_s));
   r.t_scan = ms * 1e-3;
-  r.t_2 = secs(t0, Clock::now());
   return r;
 }
 
@@ -894,6 +972,8 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
                                 " exceeds the device top-k limit " + std::to_string(kMaxK));
   }
   const auto t0 = Clock::now();
+  PhaseTrace tr;
+  tr.mark("start");
   Result r;
   uint32_t lp;
   if (explicit_probe) {
@@ -913,9 +993,11 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
   // the residency table of the host store state.
   CK(cudaStreamWaitEvent(comp, ev_copy_tail, 0));
   commit_res(comp);
+  tr.mark("commit");
   const int G = std::min(scan_grid_x(1, sms, scan_impl, tune), part_cap);
   ft.grid = static_cast<uint32_t>(G); // the partition step lays out G scan CTAs
   if (explicit_probe) {
+    CK(cudaMemcpyAsync(d_Q, dq, ix->d * sizeof(float), cudaMemcpyDefault, comp));
     CK(cudaEventRecord(ev_a, comp));
     if (lp) {
       std::memcpy(h_order, explicit_probe->data(), lp * sizeof(uint32_t));
@@ -924,21 +1006,20 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
     CK(cudaEventRecord(ev_b, comp));
     launch_partition(d_order, 1, lp, d_res, d_list_off, ft, comp);
     CK(cudaEventRecord(ev_p, comp));
-    launch_scan(dq, 1, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl,
+    launch_scan(d_Q, 1, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl,
                 tune, comp);
     CK(cudaEventRecord(ev_s, comp));
     enqueue_results(k);
   } else {
     // the query always runs from d_Q so one captured graph serves every call
-    if (dq != d_Q) {
-      CK(cudaMemcpyAsync(d_Q, dq, ix->d * sizeof(float), cudaMemcpyDeviceToDevice, comp));
-    }
-    run_coarse_path(lp, k, G);
+    run_coarse_path(lp, k, G, dq);
   }
+  tr.mark("launch");
 
   // Host: split the probe by residency (tiered.cpp:155-161) and scan the
   // misses while the GPU scans the hits.
-  if (!explicit_probe && lp) CK(cudaEventSynchronize(ev_probe));
+  if (!explicit_probe && lp) CK(cudaEventSynchronize(ev_b));
+  tr.mark("probe_wait");
   for (uint32_t i = 0; i < lp; ++i) {
     const uint32_t c = h_order[i];
     (h_res[c] >= 0 ? r.fast : r.slow).push_back(c);
@@ -949,25 +1030,29 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
     miss = miss_scan(*ix, hq, r.slow, k, *pool);
     r.t_c = secs(tc, Clock::now());
   }
+  tr.mark("split_miss");
   CK(cudaEventSynchronize(ev_c));
+  tr.mark("scan_wait");
   if (*h_fcount != r.fast.size()) {
     throw std::runtime_error("device residency table disagrees with the store");
   }
   std::vector<Scored> gpu(*h_out_cnt);
   for (uint32_t i = 0; i < *h_out_cnt; ++i) gpu[i] = {h_out_s[i], h_out_id[i]};
   r.top = merge_topk(ix->metric, gpu, miss, k);
+  r.t_2 = secs(t0, Clock::now()); // the merged result exists: timing bookkeeping follows
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, ev_a, ev_s));
   r.t_g = ms * 1e-3;
   CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
   r.t_coarse = ms * 1e-3;
-  CK(cudaEventElapsedTime(&ms, ev_p, ev_s));
+  CK(cudaEventElapsedTime(&ms, explicit_probe ? ev_p : ev_b, ev_s));
   r.t_scan = ms * 1e-3;
   for (uint32_t c : r.fast) {
     r.vecs_gpu += ix->list_len(c);
     r.bytes_gpu += ix->cluster_bytes(c);
   }
-  r.t_2 = secs(t0, Clock::now());
+  tr.mark("merge");
+  tr.dump();
   return r;
 }
 
@@ -1095,10 +1180,11 @@ void fill_batch_timing(laivg_hybrid_timing* t, const Ctx::BatchResult& r,
   }
 }
 
+// The query goes to the pinned staging row; the search's first node copies
+// it to the device.
 void stage_query(Ctx& c, const float* q) {
   need(q, "query");
   std::memcpy(c.h_Q, q, c.ix->d * sizeof(float));
-  CK(cudaMemcpyAsync(c.d_Q, c.h_Q, c.ix->d * sizeof(float), cudaMemcpyHostToDevice, c.comp));
 }
 
 } // namespace
@@ -1327,7 +1413,7 @@ int laivg_search_clusters(laivg_ctx* ctx, const float* q, const uint32_t* cluste
     Ctx& c = ctx->c;
     stage_query(c, q);
     std::vector<uint32_t> probe(clusters, clusters + n);
-    auto r = c.search(c.d_Q, q, 0, k, &probe);
+    auto r = c.search(c.h_Q, q, 0, k, &probe);
     write_top(r.top, k, ids_out, scores_out, count_out);
   });
 }
@@ -1343,7 +1429,7 @@ int laivg_ivf_search(laivg_ctx* ctx, const float* Q, uint32_t nq, int L, int k, 
     if (nq) need(Q, "queries");
     if (nq == 1) {
       stage_query(c, Q);
-      auto r = c.search(c.d_Q, Q, L, k, nullptr);
+      auto r = c.search(c.h_Q, Q, L, k, nullptr);
       write_top(r.top, k, ids_out, scores_out, count_out);
       return;
     }
@@ -1654,7 +1740,7 @@ int laivg_hybrid_search(laivg_ctx* ctx, const float* q_out, int L, int k,
     need(scores_out, "scores_out");
     Ctx& c = ctx->c;
     stage_query(c, q_out);
-    auto r = c.search(c.d_Q, q_out, L, k, nullptr);
+    auto r = c.search(c.h_Q, q_out, L, k, nullptr);
     write_top(r.top, k, ids_out, scores_out, count_out);
     if (fast_out) std::copy(r.fast.begin(), r.fast.end(), fast_out);
     if (slow_out) std::copy(r.slow.begin(), r.slow.end(), slow_out);

@@ -54,6 +54,10 @@ struct ScanOut {
   float* out_s;       // [nq][k]
   uint64_t* out_id;   // [nq][k]
   uint32_t* out_count;// [nq]
+  // optional: the final CTA also copies fcount_in[q] (the partition's fast
+  // list count) to fcount_out[q]; outputs may live in mapped host memory
+  const uint32_t* fcount_in = nullptr;
+  uint32_t* fcount_out = nullptr;
 };
 
 enum class ScanImpl : int {
