@@ -110,7 +110,7 @@ typedef struct {
   uint32_t ctas_per_sm;    /* scan CTAs per SM; 0 = auto */
   uint32_t coarse_impl;    /* 0 (default): tensor cores (tcgen05 tf32 GEMM +
                               exact fp64 re-score of boundary candidates) for
-                              batches >= 8 queries, fp64 SIMT otherwise;
+                              batches >= 16 queries, fp64 SIMT otherwise;
                               1: always fp64 SIMT; 2: always tensor cores */
   uint32_t miss_fetch;     /* batched search, cache misses: 0 = all scanned by
                               the host (reference semantics); 1 (default) =
@@ -294,7 +294,7 @@ int laivg_hybrid_search_staged(laivg_ctx* ctx, uint32_t qi, int L, int k,
 /* ---- batched retrieval (extension point (2) of SURVEY §8b: the reference
  * loops hybrid_search over a batch, pipeline.cpp:391-428) ------------------
  * hybrid_search for nq <= max_batch queries Q[nq*d] in one device pass: one
- * coarse launch (tensor cores for nq >= 8), one residency split, one scan
+ * coarse launch (tensor cores for nq >= 16), one residency split, one scan
  * launch for the whole batch; the misses of all queries are scanned
  * list-major on the host while the GPU scans the hits. Per query the result
  * equals laivg_hybrid_search. ids_out/scores_out [nq*k], count_out [nq],

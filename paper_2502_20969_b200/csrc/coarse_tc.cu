@@ -25,6 +25,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -106,7 +107,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t m0 = blockIdx.x * kTcM, q0 = blockIdx.y * N;
-  const uint32_t nkb = (d + kTcKB - 1) / kTcKB;
+  // split-K: CTA z accumulates k-blocks [kb0, kb1) into partial plane z
+  const uint32_t nkb_all = (d + kTcKB - 1) / kTcKB;
+  const uint32_t kb0 = nkb_all * blockIdx.z / gridDim.z;
+  const uint32_t kb1 = nkb_all * (blockIdx.z + 1) / gridDim.z;
+  const uint32_t nkb = kb1 - kb0;
+  approx += static_cast<uint64_t>(blockIdx.z) * nq * nc;
 
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < kTcStages; ++s) {
@@ -137,9 +143,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (kb >= kTcStages) mbar_wait(empty + s, ((kb / kTcStages) - 1) & 1u);
       unsigned char* a = smem + s * kStage;
       mbar_arrive_expect_tx(full + s, kStage);
-      tma_load_2d(a, &cen_map, static_cast<int32_t>(kb * kTcKB), static_cast<int32_t>(m0),
-                  full + s);
-      tma_load_2d(a + kABytes, &q_map, static_cast<int32_t>(kb * kTcKB),
+      tma_load_2d(a, &cen_map, static_cast<int32_t>((kb0 + kb) * kTcKB),
+                  static_cast<int32_t>(m0), full + s);
+      tma_load_2d(a + kABytes, &q_map, static_cast<int32_t>((kb0 + kb) * kTcKB),
                   static_cast<int32_t>(q0), full + s);
     }
   } else if (warp == 1 && lane == 0) {
@@ -236,7 +242,7 @@ CUtensorMap make_map(const float* base, uint32_t rows, uint32_t d, uint32_t box_
 
 template <uint32_t N>
 void launch_tc_n(const float* Q, uint32_t nq, const float* cen, uint32_t nc, uint32_t d,
-                 float* approx, cudaStream_t st) {
+                 float* approx, uint32_t splits, cudaStream_t st) {
   const CUtensorMap cm = make_map(cen, nc, d, kTcM);
   const CUtensorMap qm = make_map(Q, nq, d, N);
   const size_t smem = size_t(kTcStages) * (kTcM + N) * kTcKB * 4 + 1024;
@@ -246,8 +252,8 @@ void launch_tc_n(const float* Q, uint32_t nq, const float* cen, uint32_t nc, uin
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     attr = true;
   }
-  fn<<<dim3((nc + kTcM - 1) / kTcM, (nq + N - 1) / N), kTcThreads, smem, st>>>(cm, qm, nc, nq,
-                                                                               d, approx);
+  fn<<<dim3((nc + kTcM - 1) / kTcM, (nq + N - 1) / N, splits), kTcThreads, smem, st>>>(
+      cm, qm, nc, nq, d, approx);
   after_launch();
 }
 
@@ -257,13 +263,24 @@ bool coarse_tc_supported(uint32_t nc, uint32_t d) {
   return (d % 4) == 0 && d >= 4 && nc <= kTcMaxNc && encode_fn() != nullptr;
 }
 
-void launch_coarse_tc(const float* Q, uint32_t nq, const float* centroids, uint32_t nc,
-                      uint32_t d, float* approx, cudaStream_t st) {
-  if (nq == 0 || nc == 0) return;
-  if (nq <= 32) launch_tc_n<32>(Q, nq, centroids, nc, d, approx, st);
-  else if (nq <= 64) launch_tc_n<64>(Q, nq, centroids, nc, d, approx, st);
-  else if (nq <= 128) launch_tc_n<128>(Q, nq, centroids, nc, d, approx, st);
-  else launch_tc_n<256>(Q, nq, centroids, nc, d, approx, st);
+uint32_t coarse_tc_splits(uint32_t nq, uint32_t nc, uint32_t d, int num_sms) {
+  const uint32_t N = nq <= 32 ? 32 : nq <= 64 ? 64 : nq <= 128 ? 128 : 256;
+  const uint32_t tiles = ((nc + kTcM - 1) / kTcM) * ((nq + N - 1) / N);
+  const uint32_t nkb = (d + kTcKB - 1) / kTcKB;
+  uint32_t s = tiles >= uint32_t(num_sms) ? 1u : uint32_t(num_sms) / tiles;
+  s = std::min<uint32_t>(std::min<uint32_t>(s, kTcMaxSplit), nkb);
+  return std::max(1u, s);
+}
+
+uint32_t launch_coarse_tc(const float* Q, uint32_t nq, const float* centroids, uint32_t nc,
+                          uint32_t d, float* approx, int num_sms, cudaStream_t st) {
+  if (nq == 0 || nc == 0) return 1;
+  const uint32_t S = coarse_tc_splits(nq, nc, d, num_sms);
+  if (nq <= 32) launch_tc_n<32>(Q, nq, centroids, nc, d, approx, S, st);
+  else if (nq <= 64) launch_tc_n<64>(Q, nq, centroids, nc, d, approx, S, st);
+  else if (nq <= 128) launch_tc_n<128>(Q, nq, centroids, nc, d, approx, S, st);
+  else launch_tc_n<256>(Q, nq, centroids, nc, d, approx, S, st);
+  return S;
 }
 
 } // namespace laivg

@@ -568,7 +568,7 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   if (max_probe == 0) max_probe = 1;
   d_Q = dev_alloc<float>(size_t(max_batch) * d);
   if (tc_ok) {
-    d_approx = dev_alloc<float>(size_t(max_batch) * nc);
+    d_approx = dev_alloc<float>(size_t(kTcMaxSplit) * max_batch * nc);
     std::vector<float> cn(nc);
     for (uint32_t c = 0; c < nc; ++c) {
       double s2 = 0.0;
@@ -733,8 +733,8 @@ void Ctx::coarse(const float* dQ, uint32_t nq, uint32_t n_out, cudaStream_t st, 
                  bool need_scores) {
   const FastTable* f = part ? &ft : nullptr;
   if (!need_scores && use_tc(nq, n_out)) {
-    launch_coarse_tc(dQ, nq, d_cen, ix->nc, ix->d, d_approx, st);
-    launch_tc_select(d_approx, dQ, nq, ix->d, d_cen, d_cnorm, ix->nc, ix->metric, n_out,
+    const uint32_t S = launch_coarse_tc(dQ, nq, d_cen, ix->nc, ix->d, d_approx, sms, st);
+    launch_tc_select(d_approx, S, dQ, nq, ix->d, d_cen, d_cnorm, ix->nc, ix->metric, n_out,
                      d_order, part ? d_res : nullptr, part ? d_list_off : nullptr, f, st);
     return;
   }
@@ -1864,9 +1864,17 @@ int laivg_debug_coarse_approx(laivg_ctx* ctx, const float* Q, uint32_t nq, float
     for (uint32_t q0 = 0; q0 < nq; q0 += c.max_batch) {
       const uint32_t b = std::min(c.max_batch, nq - q0);
       stage_batch(c, Q + size_t(q0) * c.ix->d, b);
-      laivg::launch_coarse_tc(c.d_Q, b, c.d_cen, nc, c.ix->d, c.d_approx, c.comp);
-      CK(cudaMemcpyAsync(approx_out + size_t(q0) * nc, c.d_approx, size_t(b) * nc * sizeof(float),
+      const uint32_t S =
+          laivg::launch_coarse_tc(c.d_Q, b, c.d_cen, nc, c.ix->d, c.d_approx, c.sms, c.comp);
+      std::vector<float> planes(size_t(S) * b * nc);
+      CK(cudaMemcpyAsync(planes.data(), c.d_approx, planes.size() * sizeof(float),
                          cudaMemcpyDeviceToHost, c.comp));
+      CK(cudaStreamSynchronize(c.comp));
+      for (size_t i = 0; i < size_t(b) * nc; ++i) { // plane sum, as tc_select forms it
+        double a = planes[i];
+        for (uint32_t z = 1; z < S; ++z) a += planes[size_t(z) * b * nc + i];
+        approx_out[size_t(q0) * nc + i] = static_cast<float>(a);
+      }
       CK(cudaStreamSynchronize(c.comp));
     }
   });

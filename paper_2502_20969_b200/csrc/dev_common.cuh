@@ -165,5 +165,51 @@ __device__ __forceinline__ double warp_coarse_score(const float* sq, const float
   return warp_sum(acc);
 }
 
+// warp_coarse_score for up to R centroid rows at once (rows cen + c[u] * d):
+// every row follows exactly warp_coarse_score's sequence of operations, the
+// rows only share the warp's load latency.
+template <int R>
+__device__ __forceinline__ void warp_coarse_score_n(const float* sq, const float* cen,
+                                                    const uint32_t* c, uint32_t nr, uint32_t d,
+                                                    int metric, int lane, double (&out)[R]) {
+  if ((d & 3u) != 0 || d > 1024) {
+    for (uint32_t u = 0; u < R; ++u) {
+      out[u] = u < nr ? warp_coarse_score(sq, cen + static_cast<uint64_t>(c[u]) * d, d, metric,
+                                          lane)
+                      : 0.0;
+    }
+    return;
+  }
+  const uint32_t d4 = d >> 2;
+  const float4* q4 = reinterpret_cast<const float4*>(sq);
+  float4 x[R][8];
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    const float4* r4 = reinterpret_cast<const float4*>(cen + static_cast<uint64_t>(
+                                                                 c[u < static_cast<int>(nr) ? u : 0]) * d);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const uint32_t j = lane + 32u * t;
+      x[u][t] = (u < static_cast<int>(nr) && j < d4) ? __ldg(r4 + j)
+                                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  double acc[R];
+#pragma unroll
+  for (int u = 0; u < R; ++u) acc[u] = 0.0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const uint32_t j = lane + 32u * t;
+    if (j < d4) {
+      const float4 qq = q4[j];
+      const double qd[4] = {qq.x, qq.y, qq.z, qq.w};
+#pragma unroll
+      for (int u = 0; u < R; ++u) Acc4<true>::run(metric, qd, x[u][t], acc[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < R; ++u) out[u] = warp_sum(acc[u]);
+}
+
 } // namespace dev
 } // namespace laivg

@@ -632,7 +632,7 @@ __device__ __forceinline__ float order_float(uint32_t u) {
 
 // Bounds on the exact "goodness" g (IP: score, L2: -squared distance) of
 // centroid c from its tensor-core score a: g in [lo, hi].
-__device__ __forceinline__ void tc_bounds(int metric, float a, double qn, double qn2, float cn,
+__device__ __forceinline__ void tc_bounds(int metric, double a, double qn, double qn2, float cn,
                                           float& lo, float& hi) {
   const double cnd = cn;
   double g, e;
@@ -641,17 +641,20 @@ __device__ __forceinline__ void tc_bounds(int metric, float a, double qn, double
     e = kTcErr * qn * cnd;
   } else {
     const double cn2 = cnd * cnd;
-    g = -(qn2 + cn2 - 2.0 * static_cast<double>(a));
+    g = -(qn2 + cn2 - 2.0 * a);
     e = 2.0 * kTcErr * qn * cnd + 1e-6 * (qn2 + cn2);
   }
   lo = __double2float_rd(g - e);
   hi = __double2float_ru(g + e);
 }
 
-// One CTA per query. smem: q[d], 32-bit keys of the lower bounds[nc],
-// candidate keys/ids[cap] (cap = pow2 >= nc, so every centroid fits).
-__global__ void __launch_bounds__(1024)
-    tc_select_kernel(const float* __restrict__ approx, const float* __restrict__ Q, uint32_t d,
+// One CTA (1024 threads) per query. smem: q[d], 32-bit keys of the lower
+// bounds[nc], upper bounds[nc], candidate keys/ids[cap] (cap = pow2 >= nc,
+// so every centroid fits).
+constexpr int kSelThreads = 1024;
+__global__ void __launch_bounds__(kSelThreads)
+    tc_select_kernel(const float* __restrict__ approx, uint32_t splits,
+                     const float* __restrict__ Q, uint32_t d,
                      const float* __restrict__ cen, const float* __restrict__ cnorm,
                      uint32_t nc, int metric, uint32_t n_out, uint32_t cap,
                      uint32_t* __restrict__ order, const int64_t* res_off,
@@ -659,8 +662,10 @@ __global__ void __launch_bounds__(1024)
   extern __shared__ __align__(16) unsigned char sm[];
   float* sq = reinterpret_cast<float*>(sm);
   uint32_t* lok = reinterpret_cast<uint32_t*>(sm + ((static_cast<size_t>(d) * 4 + 15) & ~size_t(15)));
-  uint64_t* ck = reinterpret_cast<uint64_t*>(
+  float* hik = reinterpret_cast<float*>(
       reinterpret_cast<unsigned char*>(lok) + ((static_cast<size_t>(nc) * 4 + 15) & ~size_t(15)));
+  uint64_t* ck = reinterpret_cast<uint64_t*>(
+      reinterpret_cast<unsigned char*>(hik) + ((static_cast<size_t>(nc) * 4 + 15) & ~size_t(15)));
   uint32_t* cv = reinterpret_cast<uint32_t*>(ck + cap);
   __shared__ uint32_t hist[256];
   __shared__ double red[32];
@@ -669,6 +674,7 @@ __global__ void __launch_bounds__(1024)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* qv = Q + static_cast<uint64_t>(q) * d;
   const float* aq = approx + static_cast<uint64_t>(q) * nc;
+  const uint64_t plane = static_cast<uint64_t>(gridDim.x) * nc; // split-K partial planes
 
   // ||q||^2 in fp64
   double part = 0.0;
@@ -689,11 +695,32 @@ __global__ void __launch_bounds__(1024)
   for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) qn2 += red[w];
   const double qn = sqrt(qn2) * (1.0 + 1e-12);
 
-  // lower-bound keys, inverted so that ascending key = best first
-  for (uint32_t c = threadIdx.x; c < nc; c += blockDim.x) {
-    float lo, hi;
-    tc_bounds(metric, aq[c], qn, qn2, cnorm[c], lo, hi);
-    lok[c] = ~float_order(lo);
+  // bounds of every cluster, once: lower-bound keys (inverted so that
+  // ascending key = best first) and upper bounds; 4 clusters per thread with
+  // all their loads in flight
+  for (uint32_t c0 = threadIdx.x; c0 < nc; c0 += 4 * blockDim.x) {
+    double a[4];
+    float cn[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t c = c0 + u * blockDim.x;
+      a[u] = 0.0;
+      cn[u] = 0.0f;
+      if (c < nc) {
+        cn[u] = cnorm[c];
+        for (uint32_t z = 0; z < splits; ++z) a[u] += aq[z * plane + c];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t c = c0 + u * blockDim.x;
+      if (c < nc) {
+        float lo, hi;
+        tc_bounds(metric, a[u], qn, qn2, cn[u], lo, hi);
+        lok[c] = ~float_order(lo);
+        hik[c] = hi;
+      }
+    }
   }
   // radix select: the (n_out-1)-th smallest key, 8 bits at a time
   uint32_t mask = 0;
@@ -701,9 +728,14 @@ __global__ void __launch_bounds__(1024)
     for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     const uint32_t prefix = s_prefix;
-    for (uint32_t c = threadIdx.x; c < nc; c += blockDim.x) {
-      const uint32_t key = lok[c];
-      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    for (uint32_t c0 = 0; c0 < nc; c0 += blockDim.x) { // warp-uniform trip count
+      const uint32_t c = c0 + threadIdx.x;
+      const bool in = c < nc && (lok[c] & mask) == prefix;
+      const uint32_t bin = in ? (lok[c] >> shift) & 255u : 256u;
+      // one atomic per distinct bin per warp (the top digits are shared by
+      // almost every key)
+      const unsigned peers = __match_any_sync(kFull, bin);
+      if (in && (__ffs(peers) - 1) == lane) atomicAdd(&hist[bin], __popc(peers));
     }
     __syncthreads();
     if (warp == 0) {
@@ -740,19 +772,18 @@ __global__ void __launch_bounds__(1024)
 
   // candidates: upper bound reaches T (includes every exact top-n_out member)
   for (uint32_t c = threadIdx.x; c < nc; c += blockDim.x) {
-    float lo, hi;
-    tc_bounds(metric, aq[c], qn, qn2, cnorm[c], lo, hi);
-    if (hi >= T) cv[atomicAdd(&s_count, 1u)] = c;
+    if (hik[c] >= T) cv[atomicAdd(&s_count, 1u)] = c;
   }
   __syncthreads();
   const uint32_t n = s_count;
   uint32_t m = 2;
   while (m < n) m <<= 1;
   // exact fp64 re-score (same arithmetic as coarse_scores_kernel)
-  for (uint32_t i = warp; i < n; i += blockDim.x >> 5) {
-    const uint32_t c = cv[i];
-    const double sc = warp_coarse_score(sq, cen + static_cast<uint64_t>(c) * d, d, metric, lane);
-    if (lane == 0) ck[i] = order_key(sc, metric);
+  const uint32_t nwarps = blockDim.x >> 5;
+  for (uint32_t i = warp; i < n; i += nwarps) {
+    double sc[1];
+    warp_coarse_score_n<1>(sq, cen, cv + i, 1, d, metric, lane, sc);
+    if (lane == 0) ck[i] = order_key(sc[0], metric);
   }
   for (uint32_t i = n + threadIdx.x; i < m; i += blockDim.x) {
     ck[i] = ~0ull;
@@ -1589,12 +1620,12 @@ void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
 size_t tc_select_smem(uint32_t nc, uint32_t d) {
   uint32_t cap = 2;
   while (cap < nc) cap <<= 1;
-  return ((size_t(d) * 4 + 15) & ~size_t(15)) + ((size_t(nc) * 4 + 15) & ~size_t(15)) +
+  return ((size_t(d) * 4 + 15) & ~size_t(15)) + 2 * ((size_t(nc) * 4 + 15) & ~size_t(15)) +
          size_t(cap) * 12;
 }
 
-void launch_tc_select(const float* approx, const float* Q, uint32_t nq, uint32_t d,
-                      const float* centroids, const float* cnorm, uint32_t nc, int metric,
+void launch_tc_select(const float* approx, uint32_t splits, const float* Q, uint32_t nq,
+                      uint32_t d, const float* centroids, const float* cnorm, uint32_t nc, int metric,
                       uint32_t n_out, uint32_t* order, const int64_t* res_off,
                       const uint64_t* list_off, const FastTable* ft, cudaStream_t st) {
   if (nq == 0 || n_out == 0) return;
@@ -1609,7 +1640,8 @@ void launch_tc_select(const float* approx, const float* Q, uint32_t nq, uint32_t
     attr = smem;
   }
   const FastTable f = ft ? *ft : FastTable{};
-  tc_select_kernel<<<nq, 1024, smem, st>>>(approx, Q, d, centroids, cnorm, nc, metric, n_out,
+  tc_select_kernel<<<nq, kSelThreads, smem, st>>>(approx, splits, Q, d, centroids, cnorm, nc, metric,
+                                           n_out,
                                            cap, order, res_off, list_off, f, ft != nullptr);
   after_launch();
 }

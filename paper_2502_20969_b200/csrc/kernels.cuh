@@ -103,21 +103,26 @@ int scan_grid_x(uint32_t nq, int num_sms, ScanImpl impl, const ScanTune& tune);
 int scan_kk(int k, bool acc_fp64);
 // ---- batched coarse quantizer on tensor cores (coarse_tc.cu) ----
 // Used for batches of >= kTcMinBatch queries when nc <= kTcMaxNc and d % 4 == 0.
-constexpr uint32_t kTcMinBatch = 8;
+constexpr uint32_t kTcMinBatch = 16; // measured crossover (profiles/r01/coarse_bench.jsonl)
 constexpr uint32_t kTcMaxNc = 8192;
 // |tf32 score - exact score| <= kTcErr * ||q|| * ||c|| (2^-9 operand truncation
 // + fp32 accumulation over d <= 4096 terms, with a 2x margin).
 constexpr double kTcErr = 4.0e-3;
 bool coarse_tc_supported(uint32_t nc, uint32_t d);
-// approx[nq][nc] = tf32 tensor-core Q . C^T (tcgen05.mma kind::tf32).
-void launch_coarse_tc(const float* Q, uint32_t nq, const float* centroids, uint32_t nc,
-                      uint32_t d, float* approx, cudaStream_t st);
+// Split-K partial planes approx[S][nq][nc] of the tf32 tensor-core Q . C^T
+// (tcgen05.mma kind::tf32); S (returned, <= kTcMaxSplit) sizes the grid to
+// the SM count. The exact score is within kTcErr ||q|| ||c|| of the plane sum.
+constexpr uint32_t kTcMaxSplit = 8;
+uint32_t coarse_tc_splits(uint32_t nq, uint32_t nc, uint32_t d, int num_sms);
+uint32_t launch_coarse_tc(const float* Q, uint32_t nq, const float* centroids, uint32_t nc,
+                          uint32_t d, float* approx, int num_sms, cudaStream_t st);
 // Exact first n_out of each query's ranking from the approximate scores:
 // candidates whose upper bound reaches the n_out-th best lower bound are
 // re-scored with the fp64 arithmetic of launch_coarse_scores and sorted on
 // (score, cluster id). With `ft`, also splits the probe by residency.
 // cnorm[c] = ||c|| rounded up.
-void launch_tc_select(const float* approx, const float* Q, uint32_t nq, uint32_t d,
+void launch_tc_select(const float* approx, uint32_t splits, const float* Q, uint32_t nq,
+                      uint32_t d,
                       const float* centroids, const float* cnorm, uint32_t nc, int metric,
                       uint32_t n_out, uint32_t* order, const int64_t* res_off,
                       const uint64_t* list_off, const FastTable* ft, cudaStream_t st);
