@@ -86,6 +86,21 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+def init_dist(world, local):
+    """One process per GPU. torch.distributed carries only the control plane
+    (barriers, the resident-set all-gather of the routed config, the max of
+    the ranks' timings): gloo on the host. The retrieval data path has no
+    collective. Returns (dist or None, this rank's CUDA ordinal)."""
+    if world == 1:
+        return None, 0
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo")
+    n = max(1, torch.cuda.device_count())
+    return dist, local % n
+
+
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
@@ -121,8 +136,13 @@ def make_datastore(cfg, world, rank, pinned=True):
         dist.barrier()
         vecs = np.memmap(path, np.float32, "r+", shape=(n, d))
         ids = np.arange(n, dtype=np.uint64)  # synth ids are j*per+i == row index
+        dist.barrier()
+        if rank == 0:  # every rank holds its mapping; the name can go now
+            os.unlink(path)
         if pinned:
-            laiv._lib.check(laiv.lib().laivg_host_register(vecs.ctypes.data, vecs.nbytes))
+            from paper_2502_20969_b200._lib import check
+
+            check(laiv.lib().laivg_host_register(vecs.ctypes.data, vecs.nbytes))
     off = np.arange(0, n + 1, per, dtype=np.uint64)
     log(f"[bench] datastore {n}x{d} ({n * (4 * d + 8) / 1e9:.1f} GB) in {time.time() - t0:.1f}s")
     return cen, vecs, ids, off
@@ -314,18 +334,13 @@ def run_ours(args, cfg):
 
     rank, world, local = dist_env()
     dist = None
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist, gpu = init_dist(world, local)
     cen, vecs, ids, off = make_datastore(cfg, world, rank)
     metric = laiv.Metric.InnerProduct if args.metric == "ip" else laiv.Metric.L2
     ix = laiv.IvfIndex(cen, vecs, ids, off, metric, borrow=True, trust=True)
     member = 4 * cfg["d"] + 8
     capacity = int(cfg["cache_frac"] * cfg["n_lists"]) * cfg["per_list"] * member
-    dev = laiv.Device(ix, capacity, device=local if world > 1 else 0,
+    dev = laiv.Device(ix, capacity, device=gpu,
                       acc_fp64=args.acc == "fp64", scan_impl=args.scan)
     L, k = cfg["nprobe"], cfg["k"]
 
@@ -371,7 +386,7 @@ def run_ours(args, cfg):
     if dist:
         dist.barrier()
     dev.sync()
-    clocks = ClockSampler(local if world > 1 else 0)
+    clocks = ClockSampler(gpu)
     launches0 = laiv.lib().laivg_kernel_launches()
     rec = []
     t0 = time.perf_counter()
@@ -386,7 +401,7 @@ def run_ours(args, cfg):
     lat_e = np.array([r["lat_e2e"] for r in rec])
     sum_v, sum_e = float(lat_v.sum()), float(lat_e.sum())
     if dist:  # the slowest rank defines the job
-        sum_v, sum_e, wall = shard.max_over_ranks([sum_v, sum_e, wall], device="cuda")
+        sum_v, sum_e, wall = shard.max_over_ranks([sum_v, sum_e, wall])
     n_total = args.steps * world
     bytes_scan = sum(r["bytes"] for r in rec)
     t_scan = sum(r["t_scan"] for r in rec)
@@ -461,19 +476,14 @@ def run_ours_batch(args, cfg):
 
     rank, world, local = dist_env()
     dist = None
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist, gpu = init_dist(world, local)
     B = cfg["batch"]
     cen, vecs, ids, off = make_datastore(cfg, world, rank)
     metric = laiv.Metric.InnerProduct if args.metric == "ip" else laiv.Metric.L2
     ix = laiv.IvfIndex(cen, vecs, ids, off, metric, borrow=True, trust=True)
     member = 4 * cfg["d"] + 8
     capacity = int(cfg["cache_frac"] * cfg["n_lists"]) * cfg["per_list"] * member
-    dev = laiv.Device(ix, capacity, device=local if world > 1 else 0, max_batch=B,
+    dev = laiv.Device(ix, capacity, device=gpu, max_batch=B,
                       acc_fp64=args.acc == "fp64", scan_impl=args.scan)
     L, k = cfg["nprobe"], cfg["k"]
     probe_plan = laiv.plan_prefetch(dev, cen[0], min(capacity, 64 * cfg["per_list"] * member))
@@ -524,7 +534,7 @@ def run_ours_batch(args, cfg):
     if dist:
         dist.barrier()
     dev.sync()
-    clocks = ClockSampler(local if world > 1 else 0)
+    clocks = ClockSampler(gpu)
     launches0 = laiv.lib().laivg_kernel_launches()
     rec = []
     t0 = time.perf_counter()
@@ -538,7 +548,7 @@ def run_ours_batch(args, cfg):
     lat_e = np.array([r["lat_e2e"] for r in rec])
     sum_v, sum_e = float(lat_v.sum()), float(lat_e.sum())
     if dist:
-        sum_v, sum_e, wall = shard.max_over_ranks([sum_v, sum_e, wall], device="cuda")
+        sum_v, sum_e, wall = shard.max_over_ranks([sum_v, sum_e, wall])
     n_total = args.steps * B * world
     bytes_scan = sum(r["bytes"] for r in rec)
     t_scan = sum(r["t_scan"] for r in rec)
@@ -628,12 +638,7 @@ def run_ours_routed(args, cfg):
 
     rank, world, local = dist_env()
     dist = None
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist, gpu = init_dist(world, local)
     emulated = world == 1 and args.workers > 1
     W = world if world > 1 else max(1, args.workers)
     B, m = cfg["batch"], cfg["micro"]
@@ -643,7 +648,7 @@ def run_ours_routed(args, cfg):
     member = 4 * cfg["d"] + 8
     capacity = int(cfg["cache_frac"] * cfg["n_lists"]) * cfg["per_list"] * member
     mine = list(range(W)) if emulated or world == 1 else [rank]
-    devs = {w: laiv.Device(ix, capacity, device=local if world > 1 else 0,
+    devs = {w: laiv.Device(ix, capacity, device=gpu,
                            max_batch=max(m, 32),
                            acc_fp64=args.acc == "fp64", scan_impl=args.scan) for w in mine}
     params = laiv.CacheParams(cache_fraction=cfg["hot_fraction"])
@@ -706,8 +711,7 @@ def run_ours_routed(args, cfg):
         batches = laiv.group_microbatches(qi[g0:g0 + B], m)
         # routing input: every worker's resident set (control plane)
         if world > 1:
-            resident = shard.gather_resident(devs[rank].store.resident_mask(cfg["n_lists"]),
-                                             device="cuda")
+            resident = shard.gather_resident(devs[rank].store.resident_mask(cfg["n_lists"]))
         else:
             resident = np.stack([devs[w].store.resident_mask(cfg["n_lists"]) for w in range(W)])
         probes = laiv.coarse_probe(d0, qi[g0:g0 + B], L)
@@ -739,7 +743,7 @@ def run_ours_routed(args, cfg):
         dist.barrier()
     for dv in devs.values():
         dv.sync()
-    clocks = ClockSampler(local if world > 1 else 0)
+    clocks = ClockSampler(gpu)
     launches0 = laiv.lib().laivg_kernel_launches()
     rec = []
     t0 = time.perf_counter()
@@ -753,9 +757,9 @@ def run_ours_routed(args, cfg):
     lat = np.array([r["lat"] for r in rec])
     lat_e = np.array([r["lat_e2e"] for r in rec])
     if dist:  # per-step makespan: the slowest rank of each step
-        lat = np.array(shard.max_over_ranks(lat.tolist(), device="cuda"))
-        lat_e = np.array(shard.max_over_ranks(lat_e.tolist(), device="cuda"))
-        wall = shard.max_over_ranks([wall], device="cuda")[0]
+        lat = np.array(shard.max_over_ranks(lat.tolist()))
+        lat_e = np.array(shard.max_over_ranks(lat_e.tolist()))
+        wall = shard.max_over_ranks([wall])[0]
     n_total = args.steps * B
     t_scan = sum(r["t_scan"] for r in rec)
     bytes_scan = sum(r["bytes"] for r in rec)
