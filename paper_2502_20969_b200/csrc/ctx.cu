@@ -344,7 +344,8 @@ struct Ctx {
     else CK(cudaEventRecord(e, st));
   }
   // The scan's final CTA wrote the results (and the fast-list count) into
-  // mapped host memory; completion is all the host needs.
+  // mapped host memory; completion (event synchronize) orders those writes
+  // before the host reads them.
   void enqueue_results(int) { rec(ev_c, comp); }
   // Query in `src` (device or pinned host): copied into d_Q by the chain's
   // first node, then coarse scores, ranking + residency split, scan,

@@ -575,7 +575,6 @@ __global__ void __launch_bounds__(1024)
     }
     uint32_t* out = order + static_cast<uint64_t>(q) * n_out;
     for (uint32_t i = threadIdx.x; i < n_out; i += blockDim.x) out[i] = av[i];
-    __threadfence_system(); // `order` may be mapped host memory
     if (do_partition) {
       __syncthreads();
       partition_block(av, n_out, res_off, list_off, ft, q);
@@ -611,7 +610,6 @@ __global__ void __launch_bounds__(1024)
   }
   uint32_t* out = order + static_cast<uint64_t>(q) * n_out;
   for (uint32_t i = threadIdx.x; i < n_out; i += blockDim.x) out[i] = mv[i];
-  __threadfence_system(); // `order` may be mapped host memory
   if (do_partition) {
     __syncthreads();
     partition_block(mv, n_out, res_off, list_off, ft, q);
@@ -1115,7 +1113,6 @@ __device__ void scan_epilogue(WarpTopK<KPL>& top, int metric, int k, int kk, boo
     out.out_count[q] = static_cast<uint32_t>(V < static_cast<uint64_t>(k) ? V : k);
     if (out.fcount_out) out.fcount_out[q] = out.fcount_in[q];
   }
-  __threadfence_system(); // outputs may be mapped host memory
 }
 
 // Cursor over a query's flattened fast-list vector space.
