@@ -332,6 +332,23 @@ int laivg_assign_cache_aware(laivg_ctx* ctx, const uint64_t* batch_off,
                              const uint8_t* resident, uint32_t nw,
                              const float* queries, uint64_t nq, int L,
                              uint32_t* assignment_out);
+/* group_microbatches on the GPU (same outputs as laivg_group_microbatches,
+ * bit-identical: pairwise fp64 L2^2 in the reference's serial order, then the
+ * greedy in one CTA). n <= 8192. */
+int laivg_group_microbatches_gpu(laivg_ctx* ctx, const float* queries, uint64_t n,
+                                 uint64_t m, uint64_t* order_out,
+                                 uint64_t* batch_off_out, uint32_t* nb_out);
+/* The routing step of run_batch (pipeline.cpp:541-589) in one call, on the
+ * GPU: group_microbatches (m per batch), every query's coarse probe (L),
+ * the overlap matrix of each batch's probe union with each worker's resident
+ * set ([nw][nc] bytes) as bitset popcounts, then the cache-aware greedy
+ * (sched.cpp:114-142). Outputs: batches in CSR form (order_out[n],
+ * batch_off_out[nb+1], *nb_out), assignment_out[nb] (nullable) and the
+ * overlap matrix overlap_out[nb*nw] (nullable). n <= 8192. */
+int laivg_schedule(laivg_ctx* ctx, const float* queries, uint64_t n, uint64_t m, int L,
+                   const uint8_t* resident, uint32_t nw, uint64_t* order_out,
+                   uint64_t* batch_off_out, uint32_t* nb_out, uint32_t* assignment_out,
+                   uint64_t* overlap_out);
 /* The greedy of assign_cache_aware (sched.cpp:114-142) over a precomputed
  * row-major nb x nw overlap matrix: a multi-process router all-gathers the
  * workers' resident sets, builds the matrix and every rank assigns alike. */

@@ -115,6 +115,8 @@ SIGNATURES = {
     "laivg_prefetch_batch": (i32, [vp, vp, u32, vp, P(Channel), f64, vp, vp,
                                    P(TransferReportC)]),
     "laivg_group_microbatches": (i32, [vp, u64, u32, u64, vp, vp, P(u32)]),
+    "laivg_group_microbatches_gpu": (i32, [vp, vp, u64, u64, vp, vp, P(u32)]),
+    "laivg_schedule": (i32, [vp, vp, u64, u64, i32, vp, u32, vp, vp, P(u32), vp, vp]),
     "laivg_chunk_microbatches": (i32, [u64, u64, vp, vp, P(u32)]),
     "laivg_assign_cache_aware": (i32, [vp, vp, vp, u32, vp, u32, vp, u64, i32, vp]),
     "laivg_greedy_assign": (i32, [vp, u32, u32, vp]),

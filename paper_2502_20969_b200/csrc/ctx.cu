@@ -247,6 +247,45 @@ struct Ctx {
   double link_rate = 50e9;       // EMA of fetch H2D bytes/s
   double cpu_rate = 0;           // EMA of host miss scan (per-query bytes)/s
   void alloc_scan_set(FastTable& f, ScanOut& o, bool device_outputs = true);
+
+  // GPU schedulers (sched.cu): grown on demand, freed with the context
+  struct SchedBufs {
+    float* q = nullptr;
+    double* dist = nullptr;
+    uint64_t* order = nullptr;
+    uint64_t* off = nullptr;
+    uint32_t* nb = nullptr;
+    uint32_t* probes = nullptr;
+    unsigned long long* resident = nullptr;
+    unsigned long long* overlap = nullptr;
+    uint64_t n = 0, L = 0, nw = 0;
+  } sb;
+  void sched_reserve(uint64_t n, uint64_t L, uint64_t nw) {
+    const uint32_t words = (ix->nc + 63) / 64;
+    if (n > sb.n) {
+      for (void* p : {(void*)sb.q, (void*)sb.dist, (void*)sb.order, (void*)sb.off, (void*)sb.nb}) {
+        if (p) cudaFree(p);
+      }
+      sb.q = dev_alloc<float>(n * ix->d);
+      sb.dist = dev_alloc<double>(n * n);
+      sb.order = dev_alloc<uint64_t>(n);
+      sb.off = dev_alloc<uint64_t>(n + 1);
+      sb.nb = dev_alloc<uint32_t>(1);
+    }
+    if (n * L > sb.n * sb.L || sb.probes == nullptr) {
+      if (sb.probes) cudaFree(sb.probes);
+      sb.probes = dev_alloc<uint32_t>(std::max<uint64_t>(1, n * L));
+    }
+    if (n > sb.n || nw > sb.nw) {
+      if (sb.resident) cudaFree(sb.resident);
+      if (sb.overlap) cudaFree(sb.overlap);
+      sb.resident = dev_alloc<unsigned long long>(std::max<uint64_t>(1, nw) * words);
+      sb.overlap = dev_alloc<unsigned long long>(std::max<uint64_t>(1, n * nw));
+    }
+    sb.n = std::max(sb.n, n);
+    sb.L = std::max(sb.L, L);
+    sb.nw = std::max(sb.nw, nw);
+  }
   int part_cap = 0; // partial top-k rows available (CTAs x queries)
   float* h_Q = nullptr;
   uint32_t* h_order = nullptr;
@@ -477,6 +516,10 @@ Ctx::~Ctx() {
   for (cudaEvent_t e : {ev_landed[0], ev_landed[1], ev_freed[0], ev_freed[1], ev_f0, ev_f1,
                         ev_fdone}) {
     if (e) cudaEventDestroy(e);
+  }
+  for (void* p : {(void*)sb.q, (void*)sb.dist, (void*)sb.order, (void*)sb.off, (void*)sb.nb,
+                  (void*)sb.probes, (void*)sb.resident, (void*)sb.overlap}) {
+    if (p) cudaFree(p);
   }
   for (auto& [key, e] : graph_tab) {
     if (e.ge) cudaGraphExecDestroy(e.ge);
@@ -1947,6 +1990,119 @@ int laivg_assign_cache_aware(laivg_ctx* ctx, const uint64_t* batch_off, const ui
     auto ov = overlap_matrix(ctx->c, batch_off, members, nb, resident, nw, queries, nq, L);
     auto a = laivg::greedy_assign(ov, nb, nw);
     std::copy(a.begin(), a.end(), assignment_out);
+  });
+}
+
+namespace {
+// group_microbatches on the device: queries already in c.sb.q; fills order /
+// off on the host.
+uint32_t group_on_device(Ctx& c, uint64_t n, uint64_t m, std::vector<uint64_t>& order,
+                         std::vector<uint64_t>& off) {
+  laivg::launch_pair_dist(c.sb.q, uint32_t(n), c.ix->d, c.sb.dist, c.comp);
+  laivg::launch_group(c.sb.dist, uint32_t(n), uint32_t(m), c.sb.order, c.sb.off, c.sb.nb, c.comp);
+  uint32_t nb = 0;
+  CK(cudaMemcpyAsync(&nb, c.sb.nb, sizeof(uint32_t), cudaMemcpyDeviceToHost, c.comp));
+  CK(cudaStreamSynchronize(c.comp));
+  order.resize(n);
+  off.resize(size_t(nb) + 1);
+  CK(cudaMemcpyAsync(order.data(), c.sb.order, n * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                     c.comp));
+  CK(cudaMemcpyAsync(off.data(), c.sb.off, (size_t(nb) + 1) * sizeof(uint64_t),
+                     cudaMemcpyDeviceToHost, c.comp));
+  CK(cudaStreamSynchronize(c.comp));
+  return nb;
+}
+
+void upload_queries(Ctx& c, const float* Q, uint64_t n) {
+  CK(cudaMemcpyAsync(c.sb.q, Q, n * c.ix->d * sizeof(float), cudaMemcpyHostToDevice, c.comp));
+}
+} // namespace
+
+int laivg_group_microbatches_gpu(laivg_ctx* ctx, const float* queries, uint64_t n, uint64_t m,
+                                 uint64_t* order_out, uint64_t* batch_off_out, uint32_t* nb_out) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    if (m < 1) throw std::invalid_argument("micro-batch size must be >= 1");
+    Ctx& c = ctx->c;
+    if (n > laivg::group_max_queries()) {
+      throw std::invalid_argument("GPU grouping supports up to " +
+                                  std::to_string(laivg::group_max_queries()) + " queries");
+    }
+    if (n == 0) {
+      if (batch_off_out) batch_off_out[0] = 0;
+      if (nb_out) *nb_out = 0;
+      return;
+    }
+    need(queries, "queries");
+    c.sched_reserve(n, 0, 0);
+    upload_queries(c, queries, n);
+    std::vector<uint64_t> order, off;
+    const uint32_t nb = group_on_device(c, n, m, order, off);
+    std::copy(order.begin(), order.end(), order_out);
+    std::copy(off.begin(), off.end(), batch_off_out);
+    if (nb_out) *nb_out = nb;
+  });
+}
+
+int laivg_schedule(laivg_ctx* ctx, const float* queries, uint64_t n, uint64_t m, int L,
+                   const uint8_t* resident, uint32_t nw, uint64_t* order_out,
+                   uint64_t* batch_off_out, uint32_t* nb_out, uint32_t* assignment_out,
+                   uint64_t* overlap_out) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    if (m < 1) throw std::invalid_argument("micro-batch size must be >= 1");
+    if (nw == 0) throw std::invalid_argument("need at least one worker");
+    Ctx& c = ctx->c;
+    if (n > laivg::group_max_queries()) {
+      throw std::invalid_argument("GPU scheduling supports up to " +
+                                  std::to_string(laivg::group_max_queries()) + " queries");
+    }
+    if (n == 0) {
+      if (batch_off_out) batch_off_out[0] = 0;
+      if (nb_out) *nb_out = 0;
+      return;
+    }
+    need(queries, "queries");
+    need(resident, "resident");
+    const uint32_t nc = c.ix->nc, d = c.ix->d;
+    const uint32_t lp = uint32_t(std::min<int64_t>(std::max(L, 0), nc));
+    c.sched_reserve(n, lp, nw);
+    upload_queries(c, queries, n);
+    // 1. group_microbatches (sched.cpp:39-70) on the device
+    std::vector<uint64_t> order, off;
+    const uint32_t nb = group_on_device(c, n, m, order, off);
+    // 2. every query's probe (coarse_probe, batched: tensor cores for >= 16)
+    for (uint64_t q0 = 0; q0 < n && lp; q0 += c.max_batch) {
+      const uint32_t b = uint32_t(std::min<uint64_t>(c.max_batch, n - q0));
+      c.coarse(c.sb.q + q0 * d, b, lp, c.comp);
+      CK(cudaMemcpyAsync(c.sb.probes + q0 * lp, c.d_order, size_t(b) * lp * sizeof(uint32_t),
+                         cudaMemcpyDeviceToDevice, c.comp));
+    }
+    // 3. overlap[b][w] = |probe union of b  ∩  resident_w| as bitset popcounts
+    const uint32_t words = (nc + 63) / 64;
+    std::vector<unsigned long long> bits(size_t(nw) * words, 0ull);
+    for (uint32_t w = 0; w < nw; ++w) {
+      for (uint32_t cl = 0; cl < nc; ++cl) {
+        if (resident[size_t(w) * nc + cl]) bits[size_t(w) * words + cl / 64] |= 1ull << (cl % 64);
+      }
+    }
+    CK(cudaMemcpyAsync(c.sb.resident, bits.data(), bits.size() * sizeof(unsigned long long),
+                       cudaMemcpyHostToDevice, c.comp));
+    std::vector<uint64_t> ov(size_t(nb) * nw, 0);
+    if (lp) {
+      laivg::launch_overlap(c.sb.probes, lp, c.sb.order, c.sb.off, nb, c.sb.resident, nw, words,
+                            c.sb.overlap, c.comp);
+      CK(cudaMemcpyAsync(ov.data(), c.sb.overlap, ov.size() * sizeof(uint64_t),
+                         cudaMemcpyDeviceToHost, c.comp));
+    }
+    CK(cudaStreamSynchronize(c.comp));
+    // 4. the greedy (sched.cpp:114-142) on the host
+    const auto a = laivg::greedy_assign(ov, nb, nw);
+    std::copy(order.begin(), order.end(), order_out);
+    std::copy(off.begin(), off.end(), batch_off_out);
+    if (nb_out) *nb_out = nb;
+    if (assignment_out) std::copy(a.begin(), a.end(), assignment_out);
+    if (overlap_out) std::copy(ov.begin(), ov.end(), overlap_out);
   });
 }
 

@@ -126,6 +126,18 @@ void launch_tc_select(const float* approx, uint32_t splits, const float* Q, uint
                       const float* centroids, const float* cnorm, uint32_t nc, int metric,
                       uint32_t n_out, uint32_t* order, const int64_t* res_off,
                       const uint64_t* list_off, const FastTable* ft, cudaStream_t st);
+// ---- schedulers on the GPU (sched.cu) ----
+// dist[i * n + j] (j > i) = serial fp64 L2^2 of queries i and j (the
+// reference's l2_sq_d order: bit-identical to the CPU).
+void launch_pair_dist(const float* Q, uint32_t n, uint32_t d, double* dist, cudaStream_t st);
+// group_microbatches' greedy (sched.cpp:39-70) over dist, one CTA.
+uint32_t group_max_queries();
+void launch_group(const double* dist, uint32_t n, uint32_t m, uint64_t* order, uint64_t* off,
+                  uint32_t* nb, cudaStream_t st);
+// overlap[b][w] = |probe union of batch b  ∩  resident bitset of worker w|.
+void launch_overlap(const uint32_t* probes, uint32_t L, const uint64_t* order,
+                    const uint64_t* off, uint32_t nb, const unsigned long long* resident,
+                    uint32_t nw, uint32_t words, unsigned long long* overlap, cudaStream_t st);
 // Generation-window stand-in: one CTA per SM spins on %globaltimer for ns.
 void launch_window(uint64_t ns, int num_sms, cudaStream_t st);
 

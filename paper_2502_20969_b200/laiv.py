@@ -32,7 +32,7 @@ __all__ = [
     "group_microbatches", "chunk_microbatches", "assign_cache_aware",
     "assign_round_robin", "assignment_overlap", "split_budget", "default_nprobe",
     "LogicError", "CudaError", "synth_centroids", "synth_lists", "synth_queries",
-    "synth_queries_topical",
+    "synth_queries_topical", "group_microbatches_gpu", "schedule",
 ]
 
 
@@ -829,3 +829,37 @@ def synth_queries_topical(seed: int, centroids: np.ndarray, vecs: np.ndarray, li
                                             sigma, qi.ctypes.data, qo.ctypes.data,
                                             rows.ctypes.data, topic.ctypes.data))
     return qi, qo, rows, topic
+
+
+def group_microbatches_gpu(dev: Device, queries, m: int) -> list[MicroBatch]:
+    """group_microbatches (sched.cpp:39-70) on the GPU; same batches."""
+    Q = _c(queries, np.float32).reshape(-1, dev.ix.d)
+    n = Q.shape[0]
+    order = np.empty(max(n, 1), np.uint64)
+    off = np.empty(n + 1, np.uint64)
+    nb = C.c_uint32()
+    check(lib().laivg_group_microbatches_gpu(dev.h, Q.ctypes.data, n, int(m), order.ctypes.data,
+                                             off.ctypes.data, C.byref(nb)))
+    return _batches_from_csr(order, off, nb.value)
+
+
+def schedule(dev: Device, queries, m: int, L: int, resident):
+    """The routing step of run_batch on the GPU: micro-batches of m
+    (group_microbatches), each batch's probe-union overlap with every
+    worker's resident set ([nw][nc] 0/1) as bitset popcounts, then the
+    cache-aware greedy. Returns (batches, assignment, overlap[nb][nw])."""
+    Q = _c(queries, np.float32).reshape(-1, dev.ix.d)
+    n = Q.shape[0]
+    res = np.ascontiguousarray(np.asarray(resident, np.uint8).reshape(-1, dev.ix.nc))
+    nw = res.shape[0]
+    order = np.empty(max(n, 1), np.uint64)
+    off = np.empty(n + 1, np.uint64)
+    nb = C.c_uint32()
+    asg = np.empty(max(n, 1), np.uint32)
+    ov = np.empty(max(n * nw, 1), np.uint64)
+    check(lib().laivg_schedule(dev.h, Q.ctypes.data, n, int(m), int(L), res.ctypes.data, nw,
+                               order.ctypes.data, off.ctypes.data, C.byref(nb), asg.ctypes.data,
+                               ov.ctypes.data))
+    k = nb.value
+    return (_batches_from_csr(order, off, k), asg[:k].tolist(),
+            ov[: k * nw].reshape(k, nw).copy())

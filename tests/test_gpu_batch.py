@@ -217,3 +217,61 @@ def test_prefetch_batch_matches_sequential(laiv):
         for t in range(nq):
             single, _ = laiv.hybrid_search(dev_b, qo[trial * 12 + t], 8, 10)
             assert np.array_equal(res.topk(t).ids, single.topk.ids)
+
+
+# ---- GPU schedulers ----------------------------------------
+def test_group_microbatches_gpu_golden(orc, laiv):
+    # acceptance.cpp:408-417 fixture: 256 x 768 queries, m = 4
+    from common import golden, sha
+
+    g = golden("sched.npz")
+    q = orc.random_matrix(256, 768, 717)
+    assert sha(q) == str(g["group_sha"])
+    cen = laiv.synth_centroids(0, 16, 768)
+    vecs, ids = laiv.synth_lists(0, cen, 2, 0.05)
+    ix = laiv.IvfIndex(cen, vecs, ids, np.arange(0, 33, 2, dtype=np.uint64),
+                       laiv.Metric.InnerProduct)
+    dev = laiv.Device(ix, 1 << 20)
+    got = laiv.group_microbatches_gpu(dev, q, 4)
+    want = laiv.group_microbatches(q, 4)
+    assert [b.queries for b in got] == [b.queries for b in want]
+    ref = orc.group_microbatches(q, 4)
+    assert [b.queries for b in got] == [list(b) for b in ref]
+
+
+@pytest.mark.parametrize("n,m,d", [(1, 4, 8), (5, 3, 8), (37, 4, 16), (300, 7, 64),
+                                   (1000, 4, 32), (64, 1, 8)])
+def test_group_microbatches_gpu_matches_host(laiv, n, m, d):
+    rng = np.random.default_rng(n * 31 + m)
+    q = rng.standard_normal((n, d)).astype(np.float32)
+    if n >= 37:  # exact distance ties: duplicated rows
+        q[n // 2: n // 2 + 5] = q[3]
+    cen = rng.standard_normal((8, d)).astype(np.float32)
+    ix = laiv.IvfIndex(cen, cen.copy(), np.arange(8, dtype=np.uint64),
+                       np.arange(9, dtype=np.uint64), laiv.Metric.L2)
+    dev = laiv.Device(ix, 1 << 20)
+    got = laiv.group_microbatches_gpu(dev, q, m)
+    want = laiv.group_microbatches(q, m)
+    assert [b.queries for b in got] == [b.queries for b in want]
+
+
+@pytest.mark.parametrize("nw", [1, 2, 3, 8])
+def test_schedule_matches_oracle(orc, laiv, nw):
+    from paper_2502_20969_b200 import shard
+
+    rng = np.random.default_rng(nw)
+    nc, d, nq, L = 64, 16, 40, 6
+    cen = orc.random_matrix(nc, d, 5)
+    queries = orc.random_matrix(nq, d, 6)
+    ix = laiv.IvfIndex(cen, cen.copy(), np.arange(nc, dtype=np.uint64),
+                       np.arange(nc + 1, dtype=np.uint64), laiv.Metric.L2)
+    dev = laiv.Device(ix, 1 << 20)
+    resident = (rng.random((nw, nc)) < 0.3).astype(np.uint8)
+    batches, assign, ov = laiv.schedule(dev, queries, 4, L, resident)
+    want_b = laiv.group_microbatches(queries, 4)
+    assert [b.queries for b in batches] == [b.queries for b in want_b]
+    probes = np.array([orc.coarse_probe(cen, 1, qv, L) for qv in queries])
+    want_ov = shard.overlap_matrix(shard.probe_union_masks(probes, want_b, nc), resident)
+    assert np.array_equal(ov, want_ov)
+    want = orc.assign_cache_aware([b.queries for b in want_b], resident, cen, 1, queries, L)
+    assert assign == list(want)
