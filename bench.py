@@ -117,6 +117,9 @@ def make_datastore(cfg, world, rank, pinned=True):
 
     nc, per, d = cfg["n_lists"], cfg["per_list"], cfg["d"]
     n = nc * per
+    key = (nc, per, d, pinned)
+    if world == 1 and key in _DATASTORES:  # sweeps reuse one datastore
+        return _DATASTORES[key]
     cen = laiv.synth_centroids(SEED, nc, d)
     t0 = time.time()
     if world == 1:
@@ -145,7 +148,12 @@ def make_datastore(cfg, world, rank, pinned=True):
             check(laiv.lib().laivg_host_register(vecs.ctypes.data, vecs.nbytes))
     off = np.arange(0, n + 1, per, dtype=np.uint64)
     log(f"[bench] datastore {n}x{d} ({n * (4 * d + 8) / 1e9:.1f} GB) in {time.time() - t0:.1f}s")
+    if world == 1:
+        _DATASTORES[key] = (cen, vecs, ids, off)
     return cen, vecs, ids, off
+
+
+_DATASTORES = {}
 
 
 def calibrate_sigma(laiv, dev, vecs, L, target=0.8, nq=32):
