@@ -359,7 +359,9 @@ def run_ours(args, cfg):
     b_link = rep.h2d_gbps * 1e9
     budget = int(min(b_link * args.window, capacity))
     sigma, cov = (args.sigma, None) if args.sigma else calibrate_sigma(laiv, dev, vecs, L)
-    nq_total = (args.warmup + args.steps) * world + 8
+    # (one rank: extra queries of the same generator extend the CPU sample)
+    nq_total = max((args.warmup + args.steps) * world + 8,
+                   args.warmup + args.steps + (args.cpu_sample if world == 1 else 0))
     qi, qo, _ = laiv.synth_queries(QSEED, vecs, nq_total, sigma)
     mine = shard.shard_indices(nq_total, rank, world)[: args.warmup + args.steps]
     dev.stage_queries(qo[mine])
@@ -478,27 +480,29 @@ def run_ours(args, cfg):
         ri = reference_index(cen, np.asarray(vecs), ids, off, int(metric))
         threads = os.cpu_count() or 1
         sample = args.cpu_sample
-        cb = cpu_baseline(ri, qo[mine[args.warmup:]].repeat(1, axis=0), L, k, threads,
-                          min(sample, len(mine) - args.warmup))
+        # the timed queries first, then more of the same generator
+        cb = cpu_baseline(ri, qo[args.warmup:args.warmup + sample], L, k, threads, sample)
         # parity of the timed queries with the reference on the same inputs
+        npar = min(sample, args.steps)
         eq = 0
-        for j in range(min(sample, len(mine) - args.warmup)):
+        for j in range(npar):
             got_ids, got_sc, _, _ = dev.hybrid_search_staged(args.warmup + j, L, k)
             eq += bool(np.array_equal(got_ids, cb["ids"][j]) and
                        np.array_equal(got_sc, cb["scores"][j]))
         line["cpu_baseline"] = {"value": cb["qps"], "unit": "queries/s", "cores": threads,
                                 "kind": "reference",
-                                "p50_latency_ms": cb["p50_ms"],
-                                "sample": f"{min(sample, len(mine) - args.warmup)} of the timed "
-                                          f"q_out queries, laiv::ivf_search (oracle/_ref) one "
-                                          f"query per host thread"}
-        line["parity_vs_reference"] = {"queries": min(sample, len(mine) - args.warmup),
-                                       "bit_identical": eq}
+                                "p50_latency_ms": cb["p50_ms"], "wall_s": cb["wall_s"],
+                                "cpu_seconds": cb["wall_s"] * threads,
+                                "sample": f"{sample} q_out queries of the bench generator (the "
+                                          f"{npar} timed ones first), laiv::ivf_search "
+                                          f"(oracle/_ref) one query per host thread"}
+        line["parity_vs_reference"] = {"queries": npar, "bit_identical": eq}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
     return 0
+
 
 def run_ours_batch(args, cfg):
     """Micro-batch pipeline round (pipeline.cpp:346-441) on one GPU per rank:
@@ -859,7 +863,9 @@ def main():
     ap.add_argument("--metric", default="ip", choices=["ip", "l2"])
     ap.add_argument("--window", type=float, default=None)
     ap.add_argument("--sigma", type=float, default=None)
-    ap.add_argument("--cpu-sample", type=int, default=16)
+    ap.add_argument("--cpu-sample", type=int, default=128,
+                    help="queries in the reference CPU baseline sample (C2: ~20 s of CPU "
+                         "work on 16 host threads)")
     ap.add_argument("--workers", type=int, default=0,
                     help="routed configs on one process: emulate this many GPU workers "
                          "(separate contexts and caches on cuda:0, run one after another; "

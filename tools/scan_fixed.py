@@ -16,7 +16,9 @@ cen = laiv.synth_centroids(0, nc, d)
 vecs, ids = laiv.synth_lists(0, cen, per, 0.05)
 off = np.arange(0, nc * per + 1, per, dtype=np.uint64)
 ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric.InnerProduct)
-dev = laiv.Device(ix, nc * per * (4 * d + 8), scan_impl=os.environ.get("SCAN", "tma"))
+dev = laiv.Device(ix, nc * per * (4 * d + 8), scan_impl=os.environ.get("SCAN", "tma"),
+                  tma_tile=int(os.environ.get("TILE", 0)), tma_stages=int(os.environ.get("STAGES", 0)),
+                  ctas_per_sm=int(os.environ.get("CPS", 0)))
 for c in range(nc):
     dev.store.insert(c)
 qi, qo, _ = laiv.synth_queries(1, vecs, 64, 0.01)
