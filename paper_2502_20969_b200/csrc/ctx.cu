@@ -245,7 +245,7 @@ struct Ctx {
   cudaEvent_t ev_landed[2] = {nullptr, nullptr}, ev_freed[2] = {nullptr, nullptr};
   cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr, ev_fdone = nullptr;
   double link_rate = 50e9;       // EMA of fetch H2D bytes/s
-  double cpu_rate = 0;           // EMA of host miss scan (per-query bytes)/s
+  double cpu_rate = 0;           // EMA of the host miss scan rate on distinct list bytes
   void alloc_scan_set(FastTable& f, ScanOut& o, bool device_outputs = true);
 
   // GPU schedulers (sched.cu): grown on demand, freed with the context
@@ -779,12 +779,14 @@ void Ctx::coarse(const float* dQ, uint32_t nq, uint32_t n_out, cudaStream_t st, 
   if (!need_scores && use_tc(nq, n_out)) {
     const uint32_t S = launch_coarse_tc(dQ, nq, d_cen, ix->nc, ix->d, d_approx, sms, st);
     launch_tc_select(d_approx, S, dQ, nq, ix->d, d_cen, d_cnorm, ix->nc, ix->metric, n_out,
-                     d_order, part ? d_res : nullptr, part ? d_list_off : nullptr, f, st);
+                     d_order, part ? d_res : nullptr, part ? d_list_off : nullptr, f, st,
+                     /*scan_sorted=*/part && nq > 1);
     return;
   }
   launch_coarse_scores(dQ, nq, d_cen, ix->nc, ix->d, ix->metric, d_scores, st);
   launch_select(d_scores, nq, ix->nc, ix->metric, n_out, d_order, d_run_k, d_run_v,
-                part ? d_res : nullptr, part ? d_list_off : nullptr, f, st);
+                part ? d_res : nullptr, part ? d_list_off : nullptr, f, st,
+                /*scan_sorted=*/part && nq > 1);
 }
 
 Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq, int L,
@@ -861,18 +863,38 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
     std::sort(cand.begin(), cand.end(), [](auto& a, auto& b) {
       return a.first != b.first ? a.first > b.first : a.second < b.second;
     });
-    const double cr = cpu_rate > 0 ? cpu_rate : 6e9 * double(pool->size());
-    double cpu_t = 0, gpu_t = 0;
-    for (auto& [n, c] : cand) cpu_t += double(n) * double(ix->list_len(c)) * d * 4 / cr;
+    // Host model: memory-bound on the distinct missed bytes (each row is read
+    // once for all queries sharing its list) at the measured rate, scaled by
+    // the parallelism the tasks allow; GPU model: fetched bytes over the
+    // measured link rate plus a per-chunk launch cost.
+    const double threads = double(pool->size());
+    const double cr = cpu_rate > 0 ? cpu_rate : 6e9 * threads;
+    auto tasks_of = [&](uint32_t c) {
+      return double((ix->list_len(c) + kMissChunk - 1) / kMissChunk);
+    };
+    double host_bytes = 0, host_tasks = 0;
+    for (auto& [n, c] : cand) {
+      host_bytes += double(ix->list_len(c)) * d * 4;
+      host_tasks += tasks_of(c);
+    }
+    auto host_time = [&](double bytes, double tasks) {
+      return tasks <= 0 ? 0.0 : bytes / (cr * std::min(1.0, tasks / threads));
+    };
+    double gpu_t = 0;
     std::vector<uint32_t> fetch;
     uint64_t fill = 0;
     for (auto& [n, c] : cand) {
       const uint64_t len = ix->list_len(c);
-      const double b = double(len) * d * 4;
-      const double ng = gpu_t + b / link_rate, nct = cpu_t - double(n) * b / cr;
-      if (miss_fetch == 1 && std::max(ng, nct) >= std::max(gpu_t, cpu_t)) break;
       if (len == 0) continue;
-      if (chunks.empty() || fill + len > ring_vecs) {
+      const double b = double(len) * d * 4;
+      const bool new_chunk = chunks.empty() || fill + len > ring_vecs;
+      const double ng = gpu_t + b / link_rate + (new_chunk ? 50e-6 : 0.0); // partition + scan launch
+      const double nct = host_time(host_bytes - b, host_tasks - tasks_of(c));
+      if (miss_fetch == 1 &&
+          std::max(ng, nct) >= std::max(gpu_t, host_time(host_bytes, host_tasks))) {
+        break;
+      }
+      if (new_chunk) {
         if (chunks.size() == kMaxFetchChunks) break;
         chunks.emplace_back();
         fill = 0;
@@ -881,7 +903,8 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
       fill += len;
       fetch.push_back(c);
       gpu_t = ng;
-      cpu_t = nct;
+      host_bytes -= b;
+      host_tasks -= tasks_of(c);
     }
     if (!fetch.empty()) {
       std::vector<uint8_t> on_gpu(ix->nc, 0);
@@ -964,8 +987,15 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
     const auto tc = Clock::now();
     miss = miss_scan_batch(*ix, hQ, nq, slow, k, *pool);
     r.t_c = secs(tc, Clock::now());
-    if (r.t_c > 0 && r.cpu_query_bytes > (64ull << 20)) {
-      const double rate = double(r.cpu_query_bytes) / r.t_c;
+    // measured host rate on distinct bytes, parallelism-corrected
+    double dbytes = 0, dtasks = 0;
+    for (auto& [c, n] : cl) {
+      dbytes += double(ix->list_len(c)) * d * 4;
+      dtasks += double((ix->list_len(c) + kMissChunk - 1) / kMissChunk);
+    }
+    if (r.t_c > 0 && dbytes > double(16ull << 20)) {
+      const double eff = std::min(1.0, dtasks / double(pool->size()));
+      const double rate = dbytes / (r.t_c * eff);
       cpu_rate = cpu_rate > 0 ? 0.5 * cpu_rate + 0.5 * rate : rate;
     }
   }

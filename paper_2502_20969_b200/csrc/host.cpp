@@ -129,7 +129,6 @@ struct TopList {
   }
 };
 
-constexpr uint64_t kMissChunk = 1024; // vectors per miss-scan task
 
 // Register-blocked host scoring of one fp32 row against G queries held in
 // fp64 (converted once per batch): the row is read from memory once and

@@ -20,6 +20,7 @@ namespace laivg {
 
 constexpr int kMetricIP = 0;
 constexpr int kMetricL2 = 1;
+constexpr uint64_t kMissChunk = 512; // vectors per host miss-scan task
 
 // CUDA failures map to LAIVG_ECUDA at the ABI.
 struct CudaError : std::runtime_error {

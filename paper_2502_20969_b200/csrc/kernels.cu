@@ -483,6 +483,31 @@ __device__ void block_bitonic_sort(uint64_t (&k)[E], uint32_t (&v)[E], uint64_t*
 //                       when it needs the full ranking (rank_clusters).
 constexpr uint32_t kSeg = 256;
 
+// Ascending in-place bitonic sort of a[0, n) in shared memory (the buffer
+// holds at least pow2(n) entries; the tail is overwritten with sentinels).
+// Used to hand the scan each query's lists in cluster order: queries of a
+// batch that share lists then stream them at about the same time, so the
+// second and later reads of a list are L2 hits.
+__device__ void sort_ids_block(uint32_t* a, uint32_t n) {
+  uint32_t m = 1;
+  while (m < n) m <<= 1;
+  for (uint32_t i = n + threadIdx.x; i < m; i += blockDim.x) a[i] = 0xffffffffu;
+  __syncthreads();
+  for (uint32_t kk = 2; kk <= m; kk <<= 1) {
+    for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const uint32_t p = i ^ j;
+        if (p > i && ((a[i] > a[p]) == ((i & kk) == 0))) {
+          const uint32_t t = a[i];
+          a[i] = a[p];
+          a[p] = t;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kSeg)
     seg_sort_kernel(const double* __restrict__ scores, uint32_t nc, int metric,
                     uint64_t* __restrict__ run_k, uint32_t* __restrict__ run_v,
@@ -525,7 +550,8 @@ __global__ void __launch_bounds__(1024)
     merge_runs_kernel(const uint64_t* __restrict__ run_k, const uint32_t* __restrict__ run_v,
                       uint32_t nseg_pad, uint32_t P, bool full, uint32_t n_out,
                       uint32_t* __restrict__ order, const int64_t* res_off,
-                      const uint64_t* list_off, FastTable ft, bool do_partition) {
+                      const uint64_t* list_off, FastTable ft, bool do_partition,
+                      bool scan_sorted) {
   extern __shared__ uint64_t mk[];
   const uint32_t total = nseg_pad * P;
   uint32_t* mv = reinterpret_cast<uint32_t*>(mk + total);
@@ -577,6 +603,7 @@ __global__ void __launch_bounds__(1024)
     for (uint32_t i = threadIdx.x; i < n_out; i += blockDim.x) out[i] = av[i];
     if (do_partition) {
       __syncthreads();
+      if (scan_sorted) sort_ids_block(av, n_out);
       partition_block(av, n_out, res_off, list_off, ft, q);
     }
     return;
@@ -612,6 +639,7 @@ __global__ void __launch_bounds__(1024)
   for (uint32_t i = threadIdx.x; i < n_out; i += blockDim.x) out[i] = mv[i];
   if (do_partition) {
     __syncthreads();
+    if (scan_sorted) sort_ids_block(mv, n_out);
     partition_block(mv, n_out, res_off, list_off, ft, q);
   }
 }
@@ -656,7 +684,8 @@ __global__ void __launch_bounds__(kSelThreads)
                      const float* __restrict__ cen, const float* __restrict__ cnorm,
                      uint32_t nc, int metric, uint32_t n_out, uint32_t cap,
                      uint32_t* __restrict__ order, const int64_t* res_off,
-                     const uint64_t* list_off, FastTable ft, bool do_partition) {
+                     const uint64_t* list_off, FastTable ft, bool do_partition,
+                     bool scan_sorted) {
   extern __shared__ __align__(16) unsigned char sm[];
   float* sq = reinterpret_cast<float*>(sm);
   uint32_t* lok = reinterpret_cast<uint32_t*>(sm + ((static_cast<size_t>(d) * 4 + 15) & ~size_t(15)));
@@ -812,6 +841,7 @@ __global__ void __launch_bounds__(kSelThreads)
   for (uint32_t i = threadIdx.x; i < n_out; i += blockDim.x) out[i] = cv[i];
   if (do_partition) {
     __syncthreads();
+    if (scan_sorted) sort_ids_block(cv, n_out);
     partition_block(cv, n_out, res_off, list_off, ft, q);
   }
 }
@@ -1584,7 +1614,7 @@ size_t select_scratch_entries(uint32_t nq, uint32_t nc) {
 void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
                    uint32_t n_out, uint32_t* order, uint64_t* run_k, uint32_t* run_v,
                    const int64_t* res_off, const uint64_t* list_off, const FastTable* ft,
-                   cudaStream_t st) {
+                   cudaStream_t st, bool scan_sorted) {
   const uint32_t nseg_pad = select_runs(nc);
   seg_sort_kernel<<<dim3(nseg_pad, nq), kSeg, 0, st>>>(scores, nc, metric, run_k, run_v,
                                                        nseg_pad);
@@ -1609,7 +1639,7 @@ void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
   const uint32_t total = nseg_pad * P;
   const uint32_t threads = std::min<uint32_t>(1024, std::max<uint32_t>(256, (total / 2 + 31) & ~31u));
   merge_runs_kernel<<<nq, threads, smem, st>>>(run_k, run_v, nseg_pad, P, full, n_out, order,
-                                            res_off, list_off, f, ft != nullptr);
+                                            res_off, list_off, f, ft != nullptr, scan_sorted);
   after_launch();
 }
 
@@ -1624,7 +1654,8 @@ size_t tc_select_smem(uint32_t nc, uint32_t d) {
 void launch_tc_select(const float* approx, uint32_t splits, const float* Q, uint32_t nq,
                       uint32_t d, const float* centroids, const float* cnorm, uint32_t nc, int metric,
                       uint32_t n_out, uint32_t* order, const int64_t* res_off,
-                      const uint64_t* list_off, const FastTable* ft, cudaStream_t st) {
+                      const uint64_t* list_off, const FastTable* ft, cudaStream_t st,
+                      bool scan_sorted) {
   if (nq == 0 || n_out == 0) return;
   uint32_t cap = 2;
   while (cap < nc) cap <<= 1;
@@ -1639,7 +1670,8 @@ void launch_tc_select(const float* approx, uint32_t splits, const float* Q, uint
   const FastTable f = ft ? *ft : FastTable{};
   tc_select_kernel<<<nq, kSelThreads, smem, st>>>(approx, splits, Q, d, centroids, cnorm, nc, metric,
                                            n_out,
-                                           cap, order, res_off, list_off, f, ft != nullptr);
+                                           cap, order, res_off, list_off, f, ft != nullptr,
+                                           scan_sorted);
   after_launch();
 }
 

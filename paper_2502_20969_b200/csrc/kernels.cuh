@@ -85,7 +85,7 @@ void launch_coarse_scores(const float* Q, uint32_t nq, const float* centroids,
 void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
                    uint32_t n_out, uint32_t* order, uint64_t* run_k, uint32_t* run_v,
                    const int64_t* res_off, const uint64_t* list_off, const FastTable* ft,
-                   cudaStream_t st);
+                   cudaStream_t st, bool scan_sorted = false);
 size_t select_scratch_entries(uint32_t nq, uint32_t nc);
 // Splits each query's probe (probe[q * lp + i], i < lp) by residency
 // (res_off[c] >= 0) preserving probe order; fills the fast table.
@@ -125,7 +125,8 @@ void launch_tc_select(const float* approx, uint32_t splits, const float* Q, uint
                       uint32_t d,
                       const float* centroids, const float* cnorm, uint32_t nc, int metric,
                       uint32_t n_out, uint32_t* order, const int64_t* res_off,
-                      const uint64_t* list_off, const FastTable* ft, cudaStream_t st);
+                      const uint64_t* list_off, const FastTable* ft, cudaStream_t st,
+                      bool scan_sorted = false);
 // ---- schedulers on the GPU (sched.cu) ----
 // dist[i * n + j] (j > i) = serial fp64 L2^2 of queries i and j (the
 // reference's l2_sq_d order: bit-identical to the CPU).
