@@ -247,6 +247,9 @@ struct Ctx {
   double link_rate = 50e9;       // EMA of fetch H2D bytes/s
   double cpu_rate = 0;           // EMA of the host miss scan rate on distinct list bytes
   void alloc_scan_set(FastTable& f, ScanOut& o, bool device_outputs = true);
+  // The scan's result for query q: the device-merged top-k, or (host-final
+  // mode) the k-way merge of the G CTA lists with ids looked up here.
+  std::vector<Scored> scan_result(uint32_t q, uint32_t G, int k, uint64_t V) const;
 
   // GPU schedulers (sched.cu): grown on demand, freed with the context
   struct SchedBufs {
@@ -293,6 +296,9 @@ struct Ctx {
   uint64_t* h_out_id = nullptr;
   uint32_t* h_out_cnt = nullptr;
   uint32_t* h_fcount = nullptr;
+  float* h_cta_s = nullptr;      // host-final grid merge input [part_cap][kMaxK]
+  uint64_t* h_cta_r = nullptr;
+  bool host_final = false;
   uint32_t* dm_order = nullptr; // device aliases of the mapped buffers above
   float* dm_out_s = nullptr;
   uint64_t* dm_out_id = nullptr;
@@ -510,7 +516,8 @@ Ctx::~Ctx() {
                   (void*)d_res_ring[0], (void*)d_res_ring[1]}) {
     if (p) cudaFree(p);
   }
-  for (void* p : {(void*)h_res_ring, (void*)h_fetch_s, (void*)h_fetch_id, (void*)h_fetch_cnt}) {
+  for (void* p : {(void*)h_res_ring, (void*)h_fetch_s, (void*)h_fetch_id, (void*)h_fetch_cnt,
+                  (void*)h_cta_s, (void*)h_cta_r}) {
     if (p) cudaFreeHost(p);
   }
   for (cudaEvent_t e : {ev_landed[0], ev_landed[1], ev_freed[0], ev_freed[1], ev_f0, ev_f1,
@@ -663,6 +670,17 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   so.out_count = dm_out_cnt;
   so.fcount_in = ft.count;
   so.fcount_out = dm_fcount;
+  // fp64 accumulation needs no device re-score: the host merges the scan
+  // CTAs' lists (saves the device grid merge chain)
+  host_final = acc_fp64 && !(std::getenv("LAIVG_DEVICE_MERGE"));
+  if (host_final) {
+    float* ds = nullptr;
+    uint64_t* dr = nullptr;
+    h_cta_s = pin_alloc_mapped<float>(size_t(part_cap) * kMaxK, &ds);
+    h_cta_r = pin_alloc_mapped<uint64_t>(size_t(part_cap) * kMaxK, &dr);
+    so.cta_s = ds;
+    so.cta_r = dr;
+  }
 
   unsigned threads = o.miss_threads;
   if (threads == 0) threads = std::max(1u, std::thread::hardware_concurrency());
@@ -692,6 +710,59 @@ void Ctx::alloc_scan_set(FastTable& f, ScanOut& o, bool device_outputs) {
     o.out_id = dev_alloc<uint64_t>(size_t(max_batch) * kMaxK);
     o.out_count = dev_alloc<uint32_t>(max_batch);
   }
+}
+
+std::vector<Scored> Ctx::scan_result(uint32_t q, uint32_t G, int k, uint64_t V) const {
+  const int kk = scan_kk(k, acc_fp64);
+  if (!host_final) {
+    std::vector<Scored> g(h_out_cnt[q]);
+    for (uint32_t i = 0; i < h_out_cnt[q]; ++i) {
+      g[i] = {h_out_s[size_t(q) * k + i], h_out_id[size_t(q) * k + i]};
+    }
+    return g;
+  }
+  // k-way merge of G sorted lists (score, then id: vectorstore.hpp:34-39);
+  // ids are looked up only to break an exact score tie and for the output
+  const size_t base = size_t(q) * G * kk;
+  struct Head {
+    float s;
+    uint64_t row;
+    uint32_t list, pos;
+  };
+  const int metric = ix->metric;
+  const uint64_t* idt = ix->ids;
+  auto worse = [&](const Head& a, const Head& b) { // a ranks after b
+    if (a.s != b.s) return metric == kMetricIP ? a.s < b.s : a.s > b.s;
+    return idt[a.row] > idt[b.row];
+  };
+  std::vector<Head> heap;
+  heap.reserve(G);
+  auto entry = [&](uint32_t l, uint32_t p, Head& h) {
+    const size_t o = base + size_t(l) * kk + p;
+    if (p >= uint32_t(kk) || h_cta_r[o] == ~0ull) return false;
+    h = {h_cta_s[o], h_cta_r[o], l, p};
+    return true;
+  };
+  for (uint32_t l = 0; l < G; ++l) {
+    Head h;
+    if (entry(l, 0, h)) heap.push_back(h);
+  }
+  std::make_heap(heap.begin(), heap.end(), worse);
+  std::vector<Scored> out;
+  const size_t want = size_t(std::min<uint64_t>(V, uint64_t(k)));
+  out.reserve(want);
+  while (out.size() < want && !heap.empty()) {
+    std::pop_heap(heap.begin(), heap.end(), worse);
+    const Head h = heap.back();
+    heap.pop_back();
+    out.push_back({h.s, idt[h.row]});
+    Head nx;
+    if (entry(h.list, h.pos + 1, nx)) {
+      heap.push_back(nx);
+      std::push_heap(heap.begin(), heap.end(), worse);
+    }
+  }
+  return out;
 }
 
 void Ctx::compact() {
@@ -834,12 +905,14 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
   // host: split every probe by residency and scan the misses list-major
   CK(cudaEventSynchronize(ev_probe));
   std::vector<std::vector<uint32_t>> slow(nq);
+  std::vector<uint64_t> vfast(nq, 0);
   bool any_slow = false;
   for (uint32_t q = 0; q < nq; ++q) {
     for (uint32_t i = 0; i < lp; ++i) {
       const uint32_t c = h_order[size_t(q) * lp + i];
       if (h_res[c] >= 0) {
         ++r.nfast[q];
+        vfast[q] += ix->list_len(c);
         r.vecs_gpu += ix->list_len(c);
         r.bytes_gpu += ix->cluster_bytes(c);
       } else {
@@ -1005,10 +1078,7 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
     if (h_fcount[q] != r.nfast[q]) {
       throw std::runtime_error("device residency table disagrees with the store");
     }
-    std::vector<Scored> gpu(h_out_cnt[q]);
-    for (uint32_t i = 0; i < h_out_cnt[q]; ++i) {
-      gpu[i] = {h_out_s[size_t(q) * k + i], h_out_id[size_t(q) * k + i]};
-    }
+    std::vector<Scored> gpu = scan_result(q, uint32_t(G), k, vfast[q]);
     for (size_t j = 0; j < chunks.size(); ++j) {
       const size_t o = j * max_batch + q;
       std::vector<Scored> f(h_fetch_cnt[o]);
@@ -1110,8 +1180,9 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
   if (*h_fcount != r.fast.size()) {
     throw std::runtime_error("device residency table disagrees with the store");
   }
-  std::vector<Scored> gpu(*h_out_cnt);
-  for (uint32_t i = 0; i < *h_out_cnt; ++i) gpu[i] = {h_out_s[i], h_out_id[i]};
+  uint64_t vfast = 0;
+  for (uint32_t c : r.fast) vfast += ix->list_len(c);
+  std::vector<Scored> gpu = scan_result(0, uint32_t(G), k, vfast);
   r.top = merge_topk(ix->metric, gpu, miss, k);
   r.t_2 = secs(t0, Clock::now()); // the merged result exists: timing bookkeeping follows
   float ms = 0;

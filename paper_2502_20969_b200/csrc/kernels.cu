@@ -1084,6 +1084,18 @@ __device__ void scan_epilogue(WarpTopK<KPL>& top, int metric, int k, int kk, boo
   __syncthreads();
   merge_tree(metric, ids, &cur, &alt, wl, m);
   const uint64_t pbase = static_cast<uint64_t>(q) * G * kk;
+  if (out.cta_s != nullptr && !rerank) {
+    // host-final mode: the host merges the grid's sorted lists
+    for (uint32_t x = threadIdx.x; x < static_cast<uint32_t>(kk); x += blockDim.x) {
+      const uint64_t o = pbase + static_cast<uint64_t>(blockIdx.x) * kk + x;
+      out.cta_s[o] = cur.s[x];
+      out.cta_r[o] = cur.r[x];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && out.fcount_out) {
+      out.fcount_out[q] = out.fcount_in[q];
+    }
+    return;
+  }
   for (uint32_t x = threadIdx.x; x < static_cast<uint32_t>(kk); x += blockDim.x) {
     const uint64_t o = pbase + static_cast<uint64_t>(blockIdx.x) * kk + x;
     out.part_s[o] = cur.s[x];

@@ -58,6 +58,11 @@ struct ScanOut {
   // list count) to fcount_out[q]; outputs may live in mapped host memory
   const uint32_t* fcount_in = nullptr;
   uint32_t* fcount_out = nullptr;
+  // host-final mode (fp64 accumulation only): every CTA writes its sorted
+  // top-kk (score, host-store row) to cta_s / cta_r [nq][grid][kk] (mapped
+  // host memory) and the host merges the grid; no device grid merge
+  float* cta_s = nullptr;
+  uint64_t* cta_r = nullptr;
 };
 
 enum class ScanImpl : int {
