@@ -247,11 +247,7 @@ void launch_tc_n(const float* Q, uint32_t nq, const float* cen, uint32_t nc, uin
   const CUtensorMap qm = make_map(Q, nq, d, N);
   const size_t smem = size_t(kTcStages) * (kTcM + N) * kTcKB * 4 + 1024;
   auto fn = coarse_tc_kernel<N>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(fn), smem);
   fn<<<dim3((nc + kTcM - 1) / kTcM, (nq + N - 1) / N, splits), kTcThreads, smem, st>>>(
       cm, qm, nc, nq, d, approx);
   after_launch();

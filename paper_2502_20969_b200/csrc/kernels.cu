@@ -31,6 +31,8 @@
 // order are the reference's. acc_fp64 instead accumulates every candidate in
 // fp64 (no re-score needed).
 #include <algorithm>
+#include <mutex>
+#include <map>
 #include <cfloat>
 #include <cstdint>
 #include <cstdio>
@@ -43,6 +45,22 @@
 
 namespace laivg {
 using namespace dev;
+
+// Raises a kernel's dynamic shared-memory limit once per (kernel, device):
+// function attributes are per device, so one process driving several GPUs
+// must set them on each.
+void ensure_dyn_smem(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  size_t& cur = done[{fn, dev}];
+  if (bytes > cur) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    cur = bytes;
+  }
+}
 
 // Counts the launch and surfaces launch-configuration errors immediately.
 void after_launch() {
@@ -1539,11 +1557,7 @@ void launch_tma_t(const float* Q, uint32_t nq, uint32_t d, int metric, int k, in
   const TmaGeom g = tma_geom(d, kk, static_cast<uint32_t>(gx), tune);
   if (g.smem > 227 * 1024) throw CudaError("TMA ring does not fit shared memory");
   auto fn = scan_tma_kernel<kFp64, KPL, NCH>;
-  static size_t attr = 0;
-  if (g.smem > attr) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.smem));
-    attr = g.smem;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(fn), g.smem);
   fn<<<dim3(gx, nq), kTmaThreads, g.smem, st>>>(Q, d, metric, k, kk, ft, slab, ids, out, g.T, g.S);
   after_launch();
 }
@@ -1556,11 +1570,7 @@ void launch_ldg_t(const float* Q, uint32_t nq, uint32_t d, int metric, int k, in
                       epilogue_scratch(kScanWarps, kk, static_cast<uint32_t>(gx));
   if (smem > 227 * 1024) throw CudaError("LDG scan epilogue does not fit shared memory");
   auto fn = scan_ldg_kernel<kFp64, KPL, NCH>;
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = smem;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(fn), smem);
   fn<<<dim3(gx, nq), kScanThreads, smem, st>>>(Q, d, metric, k, kk, ft, slab, ids, out);
   after_launch();
 }
@@ -1599,16 +1609,14 @@ void launch_coarse_scores(const float* Q, uint32_t nq, const float* centroids,
   if (nq >= 8) {
     const size_t smem = size_t(8) * d * sizeof(float);
     if (smem > 48 * 1024) {
-      cudaFuncSetAttribute(coarse_scores_kernel<8>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      ensure_dyn_smem(reinterpret_cast<const void*>(coarse_scores_kernel<8>), smem);
     }
     coarse_scores_kernel<8><<<dim3((nc + warps - 1) / warps, (nq + 7) / 8), block, smem, st>>>(
         Q, nq, centroids, nc, d, metric, scores);
   } else {
     const size_t smem = size_t(d) * sizeof(float);
     if (smem > 48 * 1024) {
-      cudaFuncSetAttribute(coarse_scores_kernel<1>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      ensure_dyn_smem(reinterpret_cast<const void*>(coarse_scores_kernel<1>), smem);
     }
     coarse_scores_kernel<1><<<dim3((nc + warps - 1) / warps, nq), block, smem, st>>>(
         Q, nq, centroids, nc, d, metric, scores);
@@ -1644,12 +1652,8 @@ void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
   // prefix mode ping-pongs between two buffers
   const size_t smem = size_t(nseg_pad) * P * (sizeof(uint64_t) + sizeof(uint32_t)) *
                           (full ? 1 : 2) + 16;
-  static size_t attr = 0;
-  if (smem > attr) { // dynamic + the partition statics may pass 48 KB
-    cudaFuncSetAttribute(merge_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
-    attr = smem;
-  }
+  // dynamic + the partition statics may pass 48 KB
+  ensure_dyn_smem(reinterpret_cast<const void*>(merge_runs_kernel), smem);
   const FastTable f = ft ? *ft : FastTable{};
   const uint32_t total = nseg_pad * P;
   const uint32_t threads = std::min<uint32_t>(1024, std::max<uint32_t>(256, (total / 2 + 31) & ~31u));
@@ -1676,12 +1680,7 @@ void launch_tc_select(const float* approx, uint32_t splits, const float* Q, uint
   while (cap < nc) cap <<= 1;
   const size_t smem = tc_select_smem(nc, d);
   if (smem > 227 * 1024) throw CudaError("tc_select: shared memory exceeds 227 KB");
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(tc_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
-    attr = smem;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(tc_select_kernel), smem);
   const FastTable f = ft ? *ft : FastTable{};
   tc_select_kernel<<<nq, kSelThreads, smem, st>>>(approx, splits, Q, d, centroids, cnorm, nc, metric,
                                            n_out,

@@ -12,6 +12,8 @@ namespace laivg {
 std::atomic<uint64_t>& launch_counter();
 // Counts a launch and throws CudaError on a launch-configuration error.
 void after_launch();
+// Raises a kernel's dynamic shared-memory limit once per (kernel, device).
+void ensure_dyn_smem(const void* fn, size_t bytes);
 
 constexpr int kMaxK = 256;             // device top-k limit (8 entries per lane)
 constexpr int kRerankMargin = 16;      // extra fp32 survivors re-scored in fp64

@@ -275,3 +275,19 @@ def test_schedule_matches_oracle(orc, laiv, nw):
     assert np.array_equal(ov, want_ov)
     want = orc.assign_cache_aware([b.queries for b in want_b], resident, cen, 1, queries, L)
     assert assign == list(want)
+
+
+def test_batch_single_query_and_fetch_metrics(orc, laiv):
+    # a batch of one, and the fetch path's accounting under both metrics
+    cen, vecs, ids, off, qi, qo, g = planted_data()
+    for metric in (laiv.Metric.InnerProduct, laiv.Metric.L2):
+        ix = laiv.IvfIndex(cen, vecs, ids, off, metric)
+        dev = laiv.Device(ix, BIG, miss_fetch="all", fetch_chunk_mb=2)
+        set_residency(dev, np.arange(64) % 4 == 0)
+        res, tm = laiv.hybrid_search_batch(dev, qo[:1], 24, 10)
+        single, _ = laiv.hybrid_search(dev, qo[0], 24, 10)
+        assert np.array_equal(res.topk(0).ids, single.topk.ids)
+        assert np.array_equal(res.topk(0).scores, single.topk.scores)
+        want = orc.ivf_search(cen, vecs, ids, off, int(metric), qo[0], 24, 10)
+        assert_topk_parity(int(metric), res.topk(0).ids, res.topk(0).scores, *want)
+        assert tm.fetched_lists + tm.cpu_lists == 24 - int(res.nfast[0])
