@@ -266,7 +266,10 @@ typedef struct {
   uint32_t fetched_lists;   /* distinct missed lists fetched H2D + GPU-scanned */
   uint32_t cpu_lists;       /* distinct missed lists scanned by the host */
   uint64_t fetched_bytes;   /* vector bytes fetched on demand */
-  double t_fetch;           /* copy-stream time of those fetches (s) */
+  double t_fetch;           /* copy-stream time of all fetch copies (s) */
+  uint32_t peer_lists;      /* missed lists copied from a peer GPU's cache */
+  uint32_t reserved0;
+  uint64_t peer_bytes;
 } laivg_hybrid_timing;
 
 /* hybrid_search for one query. fast_out / slow_out (nullable, L entries)
@@ -314,6 +317,28 @@ int laivg_hybrid_search_batch_staged(laivg_ctx* ctx, uint32_t q0, uint32_t nq,
  * coarse quantizer filters with (never reported as results). */
 int laivg_debug_coarse_approx(laivg_ctx* ctx, const float* Q, uint32_t nq,
                               float* approx_out);
+
+/* ---- peer caches (beyond the paper's private caches) ---
+ * A miss of one GPU that another GPU of the node caches is copied from that
+ * GPU's slab over NVLink into the ring and scanned locally, instead of being
+ * scanned by the host or fetched over PCIe (batched search, miss_fetch != 0).
+ * Protocol per step, on every worker: laivg_epoch_open; publish
+ * laivg_store_offsets to the others (all-gather across processes); each
+ * worker laivg_peer_publish-es the others' offsets; serve; barrier;
+ * laivg_epoch_close. Inside an epoch a context quarantines evicted slab
+ * ranges and never compacts, so every list it published stays intact until
+ * it closes. Peers attach once: in one process from the other context
+ * (laivg_peer_attach_local, enables P2P between devices), across processes
+ * from a CUDA IPC handle of the peer's slab (laivg_slab_ipc_handle, 64 B). */
+int laivg_epoch_open(laivg_ctx* ctx);
+int laivg_epoch_close(laivg_ctx* ctx);
+/* Slab vector offset of every cluster, -1 when not resident: off_out[nc]. */
+int laivg_store_offsets(const laivg_ctx* ctx, int64_t* off_out);
+int laivg_slab_ipc_handle(laivg_ctx* ctx, void* handle_out);
+int laivg_peer_attach_ipc(laivg_ctx* ctx, uint32_t peer, const void* handle);
+int laivg_peer_attach_local(laivg_ctx* ctx, uint32_t peer, const laivg_ctx* other);
+/* The peer's published offsets for the open epoch (nullptr: none). */
+int laivg_peer_publish(laivg_ctx* ctx, uint32_t peer, const int64_t* offsets);
 
 /* ---- schedulers (sched.cpp) ---------------------------------------------- */
 /* group_microbatches (sched.cpp:39-70): order_out[n] holds the queries batch

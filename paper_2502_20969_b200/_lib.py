@@ -53,7 +53,8 @@ class HybridTimingC(C.Structure):
     _fields_ = [("t_g", f64), ("t_c", f64), ("t_2", f64), ("model_t_g", f64),
                 ("model_t_c", f64), ("model_t_2", f64), ("t_coarse", f64), ("t_scan", f64),
                 ("scanned_vectors", u64), ("scanned_bytes", u64), ("fetched_lists", u32),
-                ("cpu_lists", u32), ("fetched_bytes", u64), ("t_fetch", f64)]
+                ("cpu_lists", u32), ("fetched_bytes", u64), ("t_fetch", f64),
+                ("peer_lists", u32), ("reserved0", u32), ("peer_bytes", u64)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/laivg.h
@@ -115,6 +116,13 @@ SIGNATURES = {
     "laivg_prefetch_batch": (i32, [vp, vp, u32, vp, P(Channel), f64, vp, vp,
                                    P(TransferReportC)]),
     "laivg_group_microbatches": (i32, [vp, u64, u32, u64, vp, vp, P(u32)]),
+    "laivg_epoch_open": (i32, [vp]),
+    "laivg_epoch_close": (i32, [vp]),
+    "laivg_store_offsets": (i32, [vp, vp]),
+    "laivg_slab_ipc_handle": (i32, [vp, vp]),
+    "laivg_peer_attach_ipc": (i32, [vp, u32, vp]),
+    "laivg_peer_attach_local": (i32, [vp, u32, vp]),
+    "laivg_peer_publish": (i32, [vp, u32, vp]),
     "laivg_group_microbatches_gpu": (i32, [vp, vp, u64, u64, vp, vp, P(u32)]),
     "laivg_schedule": (i32, [vp, vp, u64, u64, i32, vp, u32, vp, vp, P(u32), vp, vp]),
     "laivg_chunk_microbatches": (i32, [u64, u64, vp, vp, P(u32)]),

@@ -339,8 +339,33 @@ struct Ctx {
   void compact();
   // TieredStore::insert + payload upload on the copy stream (no sync).
   void insert_async(uint32_t c, int tag);
+  // insert_async that, inside a peer epoch, returns false instead of
+  // compacting when the slab is too fragmented for the list
+  bool try_insert_async(uint32_t c, int tag);
   uint64_t evict(uint32_t c);
   void clear_store();
+
+  // ---- peer caches ------------------------------------
+  // During an epoch this context's resident lists are published to peers,
+  // which may copy them out of the slab: evicted ranges are quarantined (not
+  // reused) and the slab is not compacted until the epoch closes.
+  bool epoch = false;
+  std::vector<std::pair<uint64_t, uint64_t>> quarantine; // (vector offset, count)
+  uint64_t quarantined = 0;                              // reference bytes held back
+  struct Peer {
+    const float* slab = nullptr; // the peer's slab (same process or CUDA IPC)
+    void* ipc = nullptr;         // cudaIpcOpenMemHandle mapping to close
+    std::vector<int64_t> off;    // the peer's published offsets (-1 absent)
+  };
+  std::vector<Peer> peers;
+  void epoch_close() {
+    for (auto& [o, n] : quarantine) alloc.release(o, n);
+    quarantine.clear();
+    quarantined = 0;
+    for (auto& p : peers) p.off.clear();
+    epoch = false;
+  }
+  uint64_t free_bytes() const { return capacity - used - quarantined; }
 
   // ---- search --------------------------------------------------------------
   bool use_tc(uint32_t nq, uint32_t n_out) const {
@@ -372,8 +397,8 @@ struct Ctx {
     double t_g = 0, t_c = 0, t_2 = 0, t_coarse = 0, t_scan = 0;
     uint64_t vecs_gpu = 0, bytes_gpu = 0;
     // runtime fetch: misses scanned on the GPU after an on-demand H2D
-    uint32_t fetch_lists = 0, cpu_lists = 0;
-    uint64_t fetch_bytes = 0, cpu_query_bytes = 0;
+    uint32_t fetch_lists = 0, cpu_lists = 0, peer_lists = 0;
+    uint64_t fetch_bytes = 0, cpu_query_bytes = 0, peer_bytes = 0;
     double t_fetch = 0; // copy-stream time of the fetch copies
   };
   BatchResult search_batch(const float* dQ, const float* hQ, uint32_t nq, int L, int k);
@@ -527,6 +552,9 @@ Ctx::~Ctx() {
   for (void* p : {(void*)sb.q, (void*)sb.dist, (void*)sb.order, (void*)sb.off, (void*)sb.nb,
                   (void*)sb.probes, (void*)sb.resident, (void*)sb.overlap}) {
     if (p) cudaFree(p);
+  }
+  for (auto& p : peers) {
+    if (p.ipc) cudaIpcCloseMemHandle(p.ipc);
   }
   for (auto& [key, e] : graph_tab) {
     if (e.ge) cudaGraphExecDestroy(e.ge);
@@ -766,6 +794,7 @@ std::vector<Scored> Ctx::scan_result(uint32_t q, uint32_t G, int k, uint64_t V) 
 }
 
 void Ctx::compact() {
+  if (epoch) throw std::logic_error("the device slab cannot be compacted during a peer epoch");
   // Slide every resident list down to the lowest free offset (slab order),
   // through a bounce buffer so source and destination never overlap.
   copy_after_comp();
@@ -793,18 +822,26 @@ void Ctx::compact() {
 }
 
 void Ctx::insert_async(uint32_t c, int tag) {
+  if (!try_insert_async(c, tag)) {
+    throw std::runtime_error("device cache slab too fragmented inserting cluster " +
+                             std::to_string(c) + " during a peer epoch");
+  }
+}
+
+bool Ctx::try_insert_async(uint32_t c, int tag) {
   if (c >= ix->nc) throw std::invalid_argument("unknown cluster id " + std::to_string(c));
   if (resident.count(c)) {
     throw std::logic_error("cluster " + std::to_string(c) + " is already resident");
   }
   const uint64_t bytes = ix->cluster_bytes(c);
-  if (used + bytes > capacity) {
+  if (used + quarantined + bytes > capacity) {
     throw std::runtime_error("fast tier capacity exceeded inserting cluster " +
                              std::to_string(c));
   }
   const uint64_t n = ix->list_len(c);
   uint64_t off = 0;
   if (!alloc.alloc(n, off)) {
+    if (epoch) return false; // peers may be reading: no compaction now
     compact();
     if (!alloc.alloc(n, off)) {
       throw std::runtime_error("device cache slab exhausted inserting cluster " +
@@ -820,6 +857,7 @@ void Ctx::insert_async(uint32_t c, int tag) {
   used += bytes;
   h_res[c] = int64_t(off);
   res_dirty = true;
+  return true;
 }
 
 uint64_t Ctx::evict(uint32_t c) {
@@ -829,7 +867,12 @@ uint64_t Ctx::evict(uint32_t c) {
   }
   const uint64_t bytes = it->second.bytes;
   used -= bytes;
-  alloc.release(uint64_t(h_res[c]), ix->list_len(c));
+  if (epoch) { // a peer may still copy it out of the slab this epoch
+    quarantine.emplace_back(uint64_t(h_res[c]), ix->list_len(c));
+    quarantined += bytes;
+  } else {
+    alloc.release(uint64_t(h_res[c]), ix->list_len(c));
+  }
   h_res[c] = -1;
   res_dirty = true;
   resident.erase(it);
@@ -837,6 +880,12 @@ uint64_t Ctx::evict(uint32_t c) {
 }
 
 void Ctx::clear_store() {
+  if (epoch) {
+    std::vector<uint32_t> all;
+    for (auto& [c, r] : resident) all.push_back(c);
+    for (uint32_t c : all) evict(c);
+    return;
+  }
   resident.clear();
   used = 0;
   std::fill(h_res.begin(), h_res.end(), -1);
@@ -922,10 +971,29 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
     }
     r.nslow[q] = uint32_t(slow[q].size());
   }
-  // runtime fetch: the most-shared misses go to the GPU (H2D into the ring +
-  // the same scan kernel) until the modeled GPU time meets the host's
+  // Misses scanned on the GPU from the 2-slot ring: first every missed list
+  // a peer GPU holds (copied over NVLink from the peer's slab, published for
+  // this epoch), then — runtime fetch — the most-shared remaining misses
+  // copied from host memory until the modeled GPU time meets the host's.
   const uint32_t d = ix->d;
-  std::vector<std::vector<uint32_t>> chunks;
+  struct FetchItem {
+    uint32_t c;
+    const float* src;
+    bool host;
+  };
+  std::vector<std::vector<FetchItem>> chunks;
+  uint64_t fill = 0;
+  auto add_item = [&](const FetchItem& it) {
+    const uint64_t len = ix->list_len(it.c);
+    if (chunks.empty() || fill + len > ring_vecs) {
+      if (chunks.size() == kMaxFetchChunks) return false;
+      chunks.emplace_back();
+      fill = 0;
+    }
+    chunks.back().push_back(it);
+    fill += len;
+    return true;
+  };
   if (miss_fetch && any_slow) {
     std::map<uint32_t, uint32_t> share;
     for (uint32_t q = 0; q < nq; ++q) {
@@ -936,10 +1004,34 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
     std::sort(cand.begin(), cand.end(), [](auto& a, auto& b) {
       return a.first != b.first ? a.first > b.first : a.second < b.second;
     });
-    // Host model: memory-bound on the distinct missed bytes (each row is read
-    // once for all queries sharing its list) at the measured rate, scaled by
-    // the parallelism the tasks allow; GPU model: fetched bytes over the
-    // measured link rate plus a per-chunk launch cost.
+    std::vector<uint8_t> on_gpu(ix->nc, 0);
+    // 1. peer-resident misses (peer copies outrun both the host link and the
+    //    host scan)
+    if (!peers.empty()) {
+      std::vector<std::pair<uint32_t, uint32_t>> rest;
+      for (auto& [n, c] : cand) {
+        const float* src = nullptr;
+        for (auto& pr : peers) {
+          if (pr.slab && !pr.off.empty() && pr.off[c] >= 0) {
+            src = pr.slab + uint64_t(pr.off[c]) * d;
+            break;
+          }
+        }
+        if (src && ix->list_len(c) && add_item({c, src, false})) {
+          on_gpu[c] = 1;
+          ++r.peer_lists;
+          r.peer_bytes += ix->list_len(c) * d * 4;
+        } else {
+          rest.emplace_back(n, c);
+        }
+      }
+      cand.swap(rest);
+    }
+    // 2. runtime fetch from host memory. Host model: memory-bound on the
+    //    distinct missed bytes (each row is read once for all queries sharing
+    //    its list) at the measured rate, scaled by the parallelism the tasks
+    //    allow; GPU model: fetched bytes over the measured link rate plus a
+    //    per-chunk launch cost.
     const double threads = double(pool->size());
     const double cr = cpu_rate > 0 ? cpu_rate : 6e9 * threads;
     auto tasks_of = [&](uint32_t c) {
@@ -954,8 +1046,6 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
       return tasks <= 0 ? 0.0 : bytes / (cr * std::min(1.0, tasks / threads));
     };
     double gpu_t = 0;
-    std::vector<uint32_t> fetch;
-    uint64_t fill = 0;
     for (auto& [n, c] : cand) {
       const uint64_t len = ix->list_len(c);
       if (len == 0) continue;
@@ -967,21 +1057,14 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
           std::max(ng, nct) >= std::max(gpu_t, host_time(host_bytes, host_tasks))) {
         break;
       }
-      if (new_chunk) {
-        if (chunks.size() == kMaxFetchChunks) break;
-        chunks.emplace_back();
-        fill = 0;
-      }
-      chunks.back().push_back(c);
-      fill += len;
-      fetch.push_back(c);
+      if (!add_item({c, ix->vecs + ix->list_off[c] * d, true})) break;
+      on_gpu[c] = 1;
+      ++r.fetch_lists;
       gpu_t = ng;
       host_bytes -= b;
       host_tasks -= tasks_of(c);
     }
-    if (!fetch.empty()) {
-      std::vector<uint8_t> on_gpu(ix->nc, 0);
-      for (uint32_t c : fetch) on_gpu[c] = 1;
+    if (r.fetch_lists || r.peer_lists) {
       any_slow = false;
       for (uint32_t q = 0; q < nq; ++q) {
         auto& v = slow[q];
@@ -989,7 +1072,6 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
                 v.end());
         any_slow = any_slow || !v.empty();
       }
-      r.fetch_lists = uint32_t(fetch.size());
     }
   }
   if (!chunks.empty()) {
@@ -1004,28 +1086,32 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
       std::fill(hres, hres + ix->nc, int64_t(-1));
       // ring order = cluster order, so lists adjacent in the list-major host
       // store become one copy
-      std::sort(chunks[j].begin(), chunks[j].end());
+      std::sort(chunks[j].begin(), chunks[j].end(),
+                [](const FetchItem& a, const FetchItem& b) { return a.c < b.c; });
       dsts.clear();
       srcs.clear();
       sizes.clear();
+      CK(cudaStreamWaitEvent(copy, ev_freed[slot], 0));
       uint64_t off = 0;
-      for (uint32_t c : chunks[j]) {
-        const uint64_t len = ix->list_len(c);
-        hres[c] = int64_t(off);
-        const float* src = ix->vecs + ix->list_off[c] * d;
+      for (const FetchItem& it : chunks[j]) {
+        const uint64_t len = ix->list_len(it.c);
+        hres[it.c] = int64_t(off);
         float* dst = ring + off * d;
-        if (!srcs.empty() && static_cast<float*>(srcs.back()) +
-                                     sizes.back() / sizeof(float) == src) {
-          sizes.back() += len * d * sizeof(float);
+        const size_t bytes = len * d * sizeof(float);
+        if (!it.host) { // peer slab (same process or CUDA IPC): device to device
+          CK(cudaMemcpyAsync(dst, it.src, bytes, cudaMemcpyDefault, copy));
+        } else if (!srcs.empty() && static_cast<float*>(srcs.back()) +
+                                            sizes.back() / sizeof(float) == it.src) {
+          sizes.back() += bytes;
+          r.fetch_bytes += bytes;
         } else {
           dsts.push_back(dst);
-          srcs.push_back(const_cast<float*>(src));
-          sizes.push_back(len * d * sizeof(float));
+          srcs.push_back(const_cast<float*>(it.src));
+          sizes.push_back(bytes);
+          r.fetch_bytes += bytes;
         }
         off += len;
-        r.fetch_bytes += len * d * 4;
       }
-      CK(cudaStreamWaitEvent(copy, ev_freed[slot], 0));
       CK(cudaMemcpyAsync(d_res_ring[slot], hres, ix->nc * sizeof(int64_t),
                          cudaMemcpyHostToDevice, copy));
       h2d_batch(dsts, srcs, sizes, copy);
@@ -1268,6 +1354,8 @@ void fill_timing(laivg_hybrid_timing* t, const Ctx::Result& r,
   t->cpu_lists = uint32_t(r.slow.size());
   t->fetched_bytes = 0;
   t->t_fetch = 0;
+  t->peer_lists = 0;
+  t->peer_bytes = 0;
   if (cost) { // tiered.cpp:190-196
     const double miss = double(r.slow.size());
     t->model_t_c = std::ceil(miss / cost->parallel_slots) * cost->t_cc;
@@ -1311,6 +1399,8 @@ void fill_batch_timing(laivg_hybrid_timing* t, const Ctx::BatchResult& r,
   t->cpu_lists = r.cpu_lists;
   t->fetched_bytes = r.fetch_bytes;
   t->t_fetch = r.t_fetch;
+  t->peer_lists = r.peer_lists;
+  t->peer_bytes = r.peer_bytes;
   if (cost) { // tiered.cpp:190-196 summed over the batch
     double miss = 0, hit = 0;
     for (size_t q = 0; q < r.nfast.size(); ++q) {
@@ -1595,7 +1685,7 @@ int laivg_ivf_search(laivg_ctx* ctx, const float* Q, uint32_t nq, int L, int k, 
 uint64_t laivg_store_capacity_bytes(const laivg_ctx* ctx) { return ctx ? ctx->c.capacity : 0; }
 uint64_t laivg_store_used_bytes(const laivg_ctx* ctx) { return ctx ? ctx->c.used : 0; }
 uint64_t laivg_store_free_bytes(const laivg_ctx* ctx) {
-  return ctx ? ctx->c.capacity - ctx->c.used : 0;
+  return ctx ? ctx->c.free_bytes() : 0;
 }
 int laivg_store_contains(const laivg_ctx* ctx, uint32_t c) {
   return ctx && ctx->c.resident.count(c) ? 1 : 0;
@@ -1722,9 +1812,9 @@ int laivg_execute_prefetch(laivg_ctx* ctx, const uint32_t* plan, uint32_t n,
     uint32_t done = 0;
     try {
       for (uint32_t i = 0; i < n; ++i) {
-        x.insert_async(plan[i], LAIVG_TAG_PREFETCHED);
+        if (!x.try_insert_async(plan[i], LAIVG_TAG_PREFETCHED)) continue; // fragmented epoch
         bytes += x.ix->cluster_bytes(plan[i]);
-        if (transferred_out) transferred_out[i] = plan[i];
+        if (transferred_out) transferred_out[done] = plan[i];
         ++done;
       }
     } catch (...) {
@@ -1801,12 +1891,12 @@ int laivg_prefetch_batch(laivg_ctx* ctx, const float* Q_in, uint32_t nq,
       for (uint32_t q = 0; q < nq; ++q) {
         std::vector<uint32_t> plan, skipped;
         uint64_t planned = 0;
-        const uint64_t budget = std::min<uint64_t>(budgets[q], x.capacity - x.used);
+        const uint64_t budget = std::min<uint64_t>(budgets[q], x.free_bytes());
         laivg::plan_walk(*x.ix, order.data() + size_t(q) * nc,
                          [&](uint32_t c) { return x.h_res[c] >= 0; }, budget, plan, planned,
                          skipped);
         for (uint32_t c : plan) {
-          x.insert_async(c, LAIVG_TAG_PREFETCHED);
+          if (!x.try_insert_async(c, LAIVG_TAG_PREFETCHED)) continue; // fragmented epoch
           bytes += x.ix->cluster_bytes(c);
           if (transferred_out) transferred_out[done] = c;
           ++done;
@@ -2022,6 +2112,92 @@ int laivg_debug_coarse_approx(laivg_ctx* ctx, const float* Q, uint32_t nq, float
       }
       CK(cudaStreamSynchronize(c.comp));
     }
+  });
+}
+
+// ---- peer caches ---------------------------------------------------------------
+int laivg_epoch_open(laivg_ctx* ctx) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    if (ctx->c.epoch) throw std::logic_error("a peer epoch is already open");
+    ctx->c.epoch = true;
+  });
+}
+int laivg_epoch_close(laivg_ctx* ctx) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    Ctx& c = ctx->c;
+    // peer copies issued by this context must be done before its own
+    // view of the peers is dropped; its quarantine returns to the allocator
+    CK(cudaStreamSynchronize(c.copy));
+    c.epoch_close();
+  });
+}
+int laivg_store_offsets(const laivg_ctx* ctx, int64_t* off_out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(off_out, "off_out");
+    std::copy(ctx->c.h_res.begin(), ctx->c.h_res.end(), off_out);
+  });
+}
+int laivg_slab_ipc_handle(laivg_ctx* ctx, void* handle_out) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    need(handle_out, "handle_out");
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, ctx->c.d_slab));
+    std::memcpy(handle_out, &h, sizeof(h));
+  });
+}
+namespace {
+laivg::Ctx::Peer& peer_slot(Ctx& c, uint32_t peer) {
+  if (peer > 1024) throw std::invalid_argument("peer index out of range");
+  if (c.peers.size() <= peer) c.peers.resize(peer + 1);
+  return c.peers[peer];
+}
+} // namespace
+int laivg_peer_attach_ipc(laivg_ctx* ctx, uint32_t peer, const void* handle) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    need(handle, "handle");
+    auto& p = peer_slot(ctx->c, peer);
+    if (p.ipc) throw std::logic_error("peer already attached");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* ptr = nullptr;
+    CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    p.ipc = ptr;
+    p.slab = static_cast<const float*>(ptr);
+  });
+}
+int laivg_peer_attach_local(laivg_ctx* ctx, uint32_t peer, const laivg_ctx* other) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    need(other, "other");
+    if (other->c.ix->nc != ctx->c.ix->nc || other->c.ix->d != ctx->c.ix->d) {
+      throw std::invalid_argument("peer serves a different index");
+    }
+    if (other->c.dev != ctx->c.dev) {
+      int ok = 0;
+      CK(cudaDeviceCanAccessPeer(&ok, ctx->c.dev, other->c.dev));
+      if (!ok) throw laivg::CudaError("no peer access between the two devices");
+      const cudaError_t e = cudaDeviceEnablePeerAccess(other->c.dev, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+      cudaGetLastError();
+    }
+    peer_slot(ctx->c, peer).slab = other->c.d_slab;
+  });
+}
+int laivg_peer_publish(laivg_ctx* ctx, uint32_t peer, const int64_t* offsets) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (!ctx->c.epoch) {
+      throw std::logic_error("peer offsets are only valid inside an open epoch");
+    }
+    auto& p = peer_slot(ctx->c, peer);
+    if (!p.slab) throw std::logic_error("peer not attached");
+    if (offsets) p.off.assign(offsets, offsets + ctx->c.ix->nc);
+    else p.off.clear();
   });
 }
 

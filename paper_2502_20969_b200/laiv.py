@@ -321,6 +321,38 @@ class Device:
                                                      nf.ctypes.data, C.byref(t)))
         return ids, sc, cnt, nf, _timing(t)
 
+    # ---- peer caches (laivg.h, "peer caches") ----
+    def epoch_open(self) -> None:
+        check(lib().laivg_epoch_open(self.h))
+
+    def epoch_close(self) -> None:
+        check(lib().laivg_epoch_close(self.h))
+
+    def store_offsets(self) -> np.ndarray:
+        out = np.empty(self.ix.nc, np.int64)
+        check(lib().laivg_store_offsets(self.h, out.ctypes.data))
+        return out
+
+    def slab_ipc_handle(self) -> bytes:
+        buf = (C.c_char * 64)()
+        check(lib().laivg_slab_ipc_handle(self.h, buf))
+        return bytes(buf)
+
+    def peer_attach(self, peer: int, other: "Device | None" = None,
+                    ipc_handle: bytes | None = None) -> None:
+        if other is not None:
+            check(lib().laivg_peer_attach_local(self.h, peer, other.h))
+        else:
+            buf = (C.c_char * 64).from_buffer_copy(ipc_handle)
+            check(lib().laivg_peer_attach_ipc(self.h, peer, buf))
+
+    def peer_publish(self, peer: int, offsets) -> None:
+        if offsets is None:
+            check(lib().laivg_peer_publish(self.h, peer, None))
+        else:
+            o = _c(offsets, np.int64)
+            check(lib().laivg_peer_publish(self.h, peer, o.ctypes.data))
+
     def coarse_approx(self, Q) -> np.ndarray:
         """Diagnostics: raw tf32 tensor-core coarse scores [nq][nc]."""
         Q = _c(Q, np.float32).reshape(-1, self.ix.d)
@@ -456,6 +488,8 @@ class HybridTiming:                                               # tiered.hpp:8
     cpu_lists: int = 0         # distinct misses scanned by the host
     fetched_bytes: int = 0
     t_fetch: float = 0.0
+    peer_lists: int = 0        # misses copied from a peer GPU's cache (NVLink)
+    peer_bytes: int = 0
 
 
 @dataclass
@@ -469,7 +503,8 @@ class HybridResult:                                               # tiered.hpp:9
 def _timing(t: HybridTimingC) -> HybridTiming:
     return HybridTiming(t.t_g, t.t_c, t.t_2, t.model_t_g, t.model_t_c, t.model_t_2,
                         t.t_coarse, t.t_scan, int(t.scanned_vectors), int(t.scanned_bytes),
-                        int(t.fetched_lists), int(t.cpu_lists), int(t.fetched_bytes), t.t_fetch)
+                        int(t.fetched_lists), int(t.cpu_lists), int(t.fetched_bytes), t.t_fetch,
+                        int(t.peer_lists), int(t.peer_bytes))
 
 
 def plan_prefetch(dev: Device, q_in, budget_bytes: int) -> PrefetchPlan:  # tiered.hpp:100-101
