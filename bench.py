@@ -690,6 +690,25 @@ def run_ours_routed(args, cfg):
                            acc_fp64=args.acc == "fp64", scan_impl=args.scan) for w in mine}
     params = laiv.CacheParams(cache_fraction=cfg["hot_fraction"])
     hot = {w: laiv.HotnessTable(params) for w in mine}
+    # peer caches: every worker may copy another worker's cached lists
+    # (in-process contexts, or CUDA IPC handles of the other ranks' slabs)
+    peer_ids = {}  # (worker, peer worker) -> peer slot
+    if args.peers:
+        if world > 1:
+            import torch.distributed as tdist
+
+            handles = [None] * world
+            tdist.all_gather_object(handles, devs[rank].slab_ipc_handle())
+            others = [p for p in range(world) if p != rank]
+            for i, p in enumerate(others):
+                devs[rank].peer_attach(i, ipc_handle=handles[p])
+                peer_ids[(rank, p)] = i
+        else:
+            for w in mine:
+                others = [p for p in mine if p != w]
+                for i, p in enumerate(others):
+                    devs[w].peer_attach(i, other=devs[p])
+                    peer_ids[(w, p)] = i
     d0 = devs[mine[0]]
     L, k = cfg["nprobe"], cfg["k"]
     probe_plan = laiv.plan_prefetch(d0, cen[0], min(capacity, 64 * cfg["per_list"] * member))
@@ -712,7 +731,7 @@ def run_ours_routed(args, cfg):
         window), batched hybrid search, then cache maintenance."""
         dev, h = devs[w], hot[w]
         acc = dict(lat=0.0, lat_e2e=0.0, nq=0, hit=0, exposed=0.0, t_scan=0.0, bytes=0,
-                   fetched=0, t_c=0.0, same=True)
+                   fetched=0, peer=0, t_c=0.0, same=True)
         if mbs:
             dev.stage_queries(qo[np.concatenate(mbs)])
         q0 = 0
@@ -739,6 +758,7 @@ def run_ours_routed(args, cfg):
             acc["t_scan"] += tm.t_scan
             acc["bytes"] += tm.scanned_bytes
             acc["fetched"] += tm.fetched_lists
+            acc["peer"] += tm.peer_lists
             acc["t_c"] += tm.t_c
             acc["same"] = acc["same"] and bool(np.array_equal(got_ids, res.ids))
         rec_w.update(acc)
@@ -755,6 +775,18 @@ def run_ours_routed(args, cfg):
         # the host (identical on every rank: deterministic inputs)
         batches, assign, _ = laiv.schedule(d0, qi[g0:g0 + B], m, L, resident)
         t_route = time.perf_counter() - tr0
+        if args.peers:  # epoch: every worker publishes its cache for this step
+            for w in mine:
+                devs[w].epoch_open()
+            if world > 1:
+                import torch.distributed as tdist
+
+                offs = [None] * world
+                tdist.all_gather_object(offs, devs[rank].store_offsets())
+            else:
+                offs = {w: devs[w].store_offsets() for w in mine}
+            for (w, p), i in peer_ids.items():
+                devs[w].peer_publish(i, offs[p])
         per = {}
         for w in mine:
             mbs = [np.asarray([g0 + q for q in mb.queries], dtype=np.int64)
@@ -762,6 +794,11 @@ def run_ours_routed(args, cfg):
             r = {}
             serve(w, mbs, r)
             per[w] = r
+        if args.peers:
+            if dist:
+                dist.barrier()  # peers keep their lists until every rank is done
+            for w in mine:
+                devs[w].epoch_close()
         if rec is not None:
             rec.append(dict(
                 lat=max(r["lat"] for r in per.values()),
@@ -772,6 +809,7 @@ def run_ours_routed(args, cfg):
                 t_scan=sum(r["t_scan"] for r in per.values()),
                 bytes=sum(r["bytes"] for r in per.values()),
                 fetched=sum(r["fetched"] for r in per.values()),
+                peer=sum(r["peer"] for r in per.values()),
                 t_c=max(r["t_c"] for r in per.values()),
                 exposed=max(r["exposed"] for r in per.values()),
                 route=t_route,
@@ -826,6 +864,8 @@ def run_ours_routed(args, cfg):
                                                                        for r in rec]))
                                                 for w in mine},
                     "fetched_lists_mean": float(np.mean([r["fetched"] for r in rec])),
+                    "peer_lists_mean": float(np.mean([r["peer"] for r in rec])),
+                    "peer_caches": bool(args.peers),
                     "host_scan_ms_max_mean": float(np.mean([r["t_c"] for r in rec]) * 1e3),
                     "exposed_ms_mean": float(np.mean([r["exposed"] for r in rec]) * 1e3),
                     "schedule_ms_mean": float(np.mean([r["route"] for r in rec]) * 1e3),
@@ -866,6 +906,9 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=128,
                     help="queries in the reference CPU baseline sample (C2: ~20 s of CPU "
                          "work on 16 host threads)")
+    ap.add_argument("--peers", action="store_true",
+                    help="routed configs: misses cached by another worker are copied from "
+                         "that worker's HBM cache (NVLink) instead of going to the host")
     ap.add_argument("--workers", type=int, default=0,
                     help="routed configs on one process: emulate this many GPU workers "
                          "(separate contexts and caches on cuda:0, run one after another; "

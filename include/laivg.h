@@ -325,9 +325,12 @@ int laivg_debug_coarse_approx(laivg_ctx* ctx, const float* Q, uint32_t nq,
  * Protocol per step, on every worker: laivg_epoch_open; publish
  * laivg_store_offsets to the others (all-gather across processes); each
  * worker laivg_peer_publish-es the others' offsets; serve; barrier;
- * laivg_epoch_close. Inside an epoch a context quarantines evicted slab
- * ranges and never compacts, so every list it published stays intact until
- * it closes. Peers attach once: in one process from the other context
+ * laivg_epoch_close. Opening an epoch publishes (pins) the lists resident
+ * at that moment: until it closes they keep their slab ranges (an explicit
+ * eviction quarantines the range, evict_to_fraction passes over them) and
+ * the slab is not compacted; lists inserted during the epoch are not
+ * published and churn as usual. laivg_store_offsets reports the published
+ * lists while an epoch is open. Peers attach once: in one process from the other context
  * (laivg_peer_attach_local, enables P2P between devices), across processes
  * from a CUDA IPC handle of the peer's slab (laivg_slab_ipc_handle, 64 B). */
 int laivg_epoch_open(laivg_ctx* ctx);

@@ -350,6 +350,7 @@ struct Ctx {
   // which may copy them out of the slab: evicted ranges are quarantined (not
   // reused) and the slab is not compacted until the epoch closes.
   bool epoch = false;
+  std::vector<uint8_t> pinned; // the lists published at epoch open
   std::vector<std::pair<uint64_t, uint64_t>> quarantine; // (vector offset, count)
   uint64_t quarantined = 0;                              // reference bytes held back
   struct Peer {
@@ -358,13 +359,24 @@ struct Ctx {
     std::vector<int64_t> off;    // the peer's published offsets (-1 absent)
   };
   std::vector<Peer> peers;
+  // Publishes (pins) every list resident now: until the epoch closes a
+  // pinned list keeps its slab range (an eviction quarantines it, the hotness
+  // policy passes over it) and the slab is not compacted. Lists inserted
+  // during the epoch are not published and churn as usual.
+  void epoch_open() {
+    pinned.assign(ix->nc, 0);
+    for (auto& [c, r] : resident) pinned[c] = 1;
+    epoch = true;
+  }
   void epoch_close() {
     for (auto& [o, n] : quarantine) alloc.release(o, n);
     quarantine.clear();
     quarantined = 0;
     for (auto& p : peers) p.off.clear();
+    pinned.clear();
     epoch = false;
   }
+  bool is_pinned(uint32_t c) const { return epoch && !pinned.empty() && pinned[c]; }
   uint64_t free_bytes() const { return capacity - used - quarantined; }
 
   // ---- search --------------------------------------------------------------
@@ -867,9 +879,10 @@ uint64_t Ctx::evict(uint32_t c) {
   }
   const uint64_t bytes = it->second.bytes;
   used -= bytes;
-  if (epoch) { // a peer may still copy it out of the slab this epoch
+  if (is_pinned(c)) { // a peer may still copy it out of the slab this epoch
     quarantine.emplace_back(uint64_t(h_res[c]), ix->list_len(c));
     quarantined += bytes;
+    pinned[c] = 0;
   } else {
     alloc.release(uint64_t(h_res[c]), ix->list_len(c));
   }
@@ -2120,7 +2133,7 @@ int laivg_epoch_open(laivg_ctx* ctx) {
   return guard([&] {
     set_ctx_device(ctx);
     if (ctx->c.epoch) throw std::logic_error("a peer epoch is already open");
-    ctx->c.epoch = true;
+    ctx->c.epoch_open();
   });
 }
 int laivg_epoch_close(laivg_ctx* ctx) {
@@ -2137,7 +2150,10 @@ int laivg_store_offsets(const laivg_ctx* ctx, int64_t* off_out) {
   return guard([&] {
     need(ctx, "ctx");
     need(off_out, "off_out");
-    std::copy(ctx->c.h_res.begin(), ctx->c.h_res.end(), off_out);
+    const Ctx& c = ctx->c;
+    for (uint32_t i = 0; i < c.ix->nc; ++i) { // inside an epoch: the published lists
+      off_out[i] = (!c.epoch || c.is_pinned(i)) ? c.h_res[i] : -1;
+    }
   });
 }
 int laivg_slab_ipc_handle(laivg_ctx* ctx, void* handle_out) {
@@ -2463,6 +2479,7 @@ int laivg_hotness_evict_to_fraction(laivg_hotness* h, laivg_ctx* ctx, uint32_t* 
     uint32_t n = 0;
     for (uint32_t c : h->h.eviction_order(ids)) {
       if (x.used <= budget) break;
+      if (x.is_pinned(c)) continue; // published to peers for this epoch
       x.evict(c);
       h->h.forget(c);
       if (evicted_out) evicted_out[n] = c;

@@ -153,3 +153,23 @@ def test_peer_hits_across_processes_ipc(orc, laiv):
     for t in range(40):
         w = orc.ivf_search(cen, vecs, ids, off, 0, qo[t], 16, 10)
         assert_topk_parity(0, np.array(ids_[t], np.uint64), np.array(scores[t], np.float32), *w)
+
+
+def test_epoch_publishes_only_pinned_lists(laiv):
+    cen, vecs, ids, off, qi, qo, g = planted_data()
+    ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric.InnerProduct)
+    b = laiv.Device(ix, 16 * CB)
+    cache(b, range(0, 8))
+    b.epoch_open()
+    b.store.insert(30)  # during the epoch: not published
+    offs = b.store_offsets()
+    assert (offs[:8] >= 0).all() and offs[30] == -1
+    b.store.evict(30)   # unpublished: released at once
+    assert b.store.free_bytes() == 8 * CB
+    b.store.evict(3)    # published: quarantined until the epoch closes
+    assert b.store.free_bytes() == 8 * CB
+    h = laiv.HotnessTable(laiv.CacheParams(cache_fraction=0.25))
+    assert h.evict_to_fraction(b) == []  # pinned lists are passed over
+    b.epoch_close()
+    assert b.store.free_bytes() == 9 * CB
+    assert len(h.evict_to_fraction(b)) == 3  # 7 resident -> 4 (25% of 16)

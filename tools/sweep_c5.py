@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--window", type=float, default=0.15)
     ap.add_argument("--nprobe", default="32,64,128,256,512,1024")
     ap.add_argument("--cache", default="0.05,0.10,0.25,0.50")
+    ap.add_argument("--peers", action="store_true")
     a = ap.parse_args()
     sys.path.insert(0, ROOT)
     import bench
@@ -35,7 +36,7 @@ def main():
             args = argparse.Namespace(gpus=1, steps=a.steps, warmup=a.warmup, impl="ours",
                                       config="_sweep", metric="ip", window=a.window, sigma=None,
                                       cpu_sample=0, no_cpu_baseline=True, acc="fp64", scan="tma",
-                                      workers=a.workers)
+                                      workers=a.workers, peers=a.peers)
             import io
             from contextlib import redirect_stdout
 
@@ -49,6 +50,7 @@ def main():
                               "value_qps": line["value"], "p50_step_ms": line["p50_latency_ms"],
                               "hit_rate": r["hit_rate"], "exposed_h2d_ms_mean": r["exposed_ms_mean"],
                               "fetched_lists_mean": r["fetched_lists_mean"],
+                              "peer_lists_mean": r.get("peer_lists_mean", 0.0), "peers": a.peers,
                               "host_scan_ms_mean": r["host_scan_ms_max_mean"],
                               "schedule_ms_mean": r["schedule_ms_mean"],
                               "results_identical": line["value_e2e_results_identical"]}),
