@@ -394,6 +394,9 @@ struct Ctx {
     std::vector<uint32_t> fast, slow;
     double t_g = 0, t_c = 0, t_2 = 0, t_coarse = 0, t_scan = 0;
     uint64_t vecs_gpu = 0, bytes_gpu = 0;
+    uint32_t fetch_lists = 0, peer_lists = 0;
+    uint64_t fetch_bytes = 0, peer_bytes = 0;
+    double t_fetch = 0;
   };
   // One query: dq on device, hq on host (miss path). With `explicit_probe`
   // the probe is those clusters (search_clusters), otherwise the coarse
@@ -414,6 +417,20 @@ struct Ctx {
     double t_fetch = 0; // copy-stream time of the fetch copies
   };
   BatchResult search_batch(const float* dQ, const float* hQ, uint32_t nq, int L, int k);
+  // The GPU side of the miss path, shared by both searches: peer-resident
+  // misses, then runtime fetch of host lists (rate model), copied through
+  // the ring and scanned there; slow[q] loses what goes to the GPU. Returns
+  // the chunks issued (results in h_fetch_*, ev_fdone after the last scan).
+  struct FetchStats {
+    uint32_t fetch_lists = 0, peer_lists = 0;
+    uint64_t fetch_bytes = 0, peer_bytes = 0;
+    double t_fetch = 0;
+  };
+  size_t issue_fetch(std::vector<std::vector<uint32_t>>& slow, bool& any_slow, const float* dQ,
+                     uint32_t nq, uint32_t lp, const uint32_t* probe_dev, int k, int G,
+                     FetchStats& st);
+  void merge_fetch(uint32_t q, size_t nchunks, int k, std::vector<Scored>& gpu) const;
+  void finish_fetch(size_t nchunks, FetchStats& st);
 
   // ---- the coarse -> select -> scan chain as one CUDA graph per (L, k) ----
   bool use_graphs = std::getenv("LAIVG_GRAPHS") ? std::atoi(std::getenv("LAIVG_GRAPHS")) != 0 : true;
@@ -922,6 +939,195 @@ void Ctx::coarse(const float* dQ, uint32_t nq, uint32_t n_out, cudaStream_t st, 
                 /*scan_sorted=*/part && nq > 1);
 }
 
+size_t Ctx::issue_fetch(std::vector<std::vector<uint32_t>>& slow, bool& any_slow,
+                        const float* dQ, uint32_t nq, uint32_t lp, const uint32_t* probe_dev,
+                        int k, int G, FetchStats& st) {
+  // Misses scanned on the GPU from the 2-slot ring: first every missed list
+  // a peer GPU holds (copied over NVLink from the peer's slab, published for
+  // this epoch), then — runtime fetch — the most-shared remaining misses
+  // copied from host memory until the modeled GPU time meets the host's.
+  const uint32_t d = ix->d;
+  struct FetchItem {
+    uint32_t c;
+    const float* src;
+    bool host;
+  };
+  std::vector<std::vector<FetchItem>> chunks;
+  uint64_t fill = 0;
+  auto add_item = [&](const FetchItem& it) {
+    const uint64_t len = ix->list_len(it.c);
+    if (chunks.empty() || fill + len > ring_vecs) {
+      if (chunks.size() == kMaxFetchChunks) return false;
+      chunks.emplace_back();
+      fill = 0;
+    }
+    chunks.back().push_back(it);
+    fill += len;
+    return true;
+  };
+  if (miss_fetch && any_slow) {
+    std::map<uint32_t, uint32_t> share;
+    for (uint32_t q = 0; q < nq; ++q) {
+      for (uint32_t c : slow[q]) ++share[c];
+    }
+    std::vector<std::pair<uint32_t, uint32_t>> cand; // (share, list)
+    for (auto& [c, n] : share) cand.emplace_back(n, c);
+    std::sort(cand.begin(), cand.end(), [](auto& a, auto& b) {
+      return a.first != b.first ? a.first > b.first : a.second < b.second;
+    });
+    std::vector<uint8_t> on_gpu(ix->nc, 0);
+    // 1. peer-resident misses (peer copies outrun both the host link and the
+    //    host scan)
+    if (!peers.empty()) {
+      std::vector<std::pair<uint32_t, uint32_t>> rest;
+      for (auto& [n, c] : cand) {
+        const float* src = nullptr;
+        for (auto& pr : peers) {
+          if (pr.slab && !pr.off.empty() && pr.off[c] >= 0) {
+            src = pr.slab + uint64_t(pr.off[c]) * d;
+            break;
+          }
+        }
+        if (src && ix->list_len(c) && add_item({c, src, false})) {
+          on_gpu[c] = 1;
+          ++st.peer_lists;
+          st.peer_bytes += ix->list_len(c) * d * 4;
+        } else {
+          rest.emplace_back(n, c);
+        }
+      }
+      cand.swap(rest);
+    }
+    // 2. runtime fetch from host memory. Host model: memory-bound on the
+    //    distinct missed bytes (each row is read once for all queries sharing
+    //    its list) at the measured rate, scaled by the parallelism the tasks
+    //    allow; GPU model: fetched bytes over the measured link rate plus a
+    //    per-chunk launch cost.
+    const double threads = double(pool->size());
+    const double cr = cpu_rate > 0 ? cpu_rate : 6e9 * threads;
+    auto tasks_of = [&](uint32_t c) {
+      return double((ix->list_len(c) + kMissChunk - 1) / kMissChunk);
+    };
+    double host_bytes = 0, host_tasks = 0;
+    for (auto& [n, c] : cand) {
+      host_bytes += double(ix->list_len(c)) * d * 4;
+      host_tasks += tasks_of(c);
+    }
+    auto host_time = [&](double bytes, double tasks) {
+      return tasks <= 0 ? 0.0 : bytes / (cr * std::min(1.0, tasks / threads));
+    };
+    double gpu_t = 0;
+    for (auto& [n, c] : cand) {
+      const uint64_t len = ix->list_len(c);
+      if (len == 0) continue;
+      const double b = double(len) * d * 4;
+      const bool new_chunk = chunks.empty() || fill + len > ring_vecs;
+      const double ng = gpu_t + b / link_rate + (new_chunk ? 50e-6 : 0.0); // partition + scan launch
+      const double nct = host_time(host_bytes - b, host_tasks - tasks_of(c));
+      if (miss_fetch == 1 &&
+          std::max(ng, nct) >= std::max(gpu_t, host_time(host_bytes, host_tasks))) {
+        break;
+      }
+      if (!add_item({c, ix->vecs + ix->list_off[c] * d, true})) break;
+      on_gpu[c] = 1;
+      ++st.fetch_lists;
+      gpu_t = ng;
+      host_bytes -= b;
+      host_tasks -= tasks_of(c);
+    }
+    if (st.fetch_lists || st.peer_lists) {
+      any_slow = false;
+      for (uint32_t q = 0; q < nq; ++q) {
+        auto& v = slow[q];
+        v.erase(std::remove_if(v.begin(), v.end(), [&](uint32_t c) { return on_gpu[c] != 0; }),
+                v.end());
+        any_slow = any_slow || !v.empty();
+      }
+    }
+  }
+  if (!chunks.empty()) {
+    fetch_results_for(k);
+    CK(cudaEventRecord(ev_f0, copy));
+    std::vector<void*> dsts, srcs;
+    std::vector<size_t> sizes;
+    for (size_t j = 0; j < chunks.size(); ++j) {
+      const int slot = int(j & 1);
+      float* ring = d_ring + size_t(slot) * ring_vecs * d;
+      int64_t* hres = h_res_ring + j * ix->nc;
+      std::fill(hres, hres + ix->nc, int64_t(-1));
+      // ring order = cluster order, so lists adjacent in the list-major host
+      // store become one copy
+      std::sort(chunks[j].begin(), chunks[j].end(),
+                [](const FetchItem& a, const FetchItem& b) { return a.c < b.c; });
+      dsts.clear();
+      srcs.clear();
+      sizes.clear();
+      CK(cudaStreamWaitEvent(copy, ev_freed[slot], 0));
+      uint64_t off = 0;
+      for (const FetchItem& it : chunks[j]) {
+        const uint64_t len = ix->list_len(it.c);
+        hres[it.c] = int64_t(off);
+        float* dst = ring + off * d;
+        const size_t bytes = len * d * sizeof(float);
+        if (!it.host) { // peer slab (same process or CUDA IPC): device to device
+          CK(cudaMemcpyAsync(dst, it.src, bytes, cudaMemcpyDefault, copy));
+        } else if (!srcs.empty() && static_cast<float*>(srcs.back()) +
+                                            sizes.back() / sizeof(float) == it.src) {
+          sizes.back() += bytes;
+          st.fetch_bytes += bytes;
+        } else {
+          dsts.push_back(dst);
+          srcs.push_back(const_cast<float*>(it.src));
+          sizes.push_back(bytes);
+          st.fetch_bytes += bytes;
+        }
+        off += len;
+      }
+      CK(cudaMemcpyAsync(d_res_ring[slot], hres, ix->nc * sizeof(int64_t),
+                         cudaMemcpyHostToDevice, copy));
+      h2d_batch(dsts, srcs, sizes, copy);
+      CK(cudaEventRecord(ev_landed[slot], copy));
+      if (j + 1 == chunks.size()) CK(cudaEventRecord(ev_f1, copy));
+      CK(cudaStreamWaitEvent(comp, ev_landed[slot], 0));
+      fft.grid = static_cast<uint32_t>(G);
+      launch_partition(probe_dev, nq, lp, d_res_ring[slot], d_list_off, fft, comp);
+      launch_scan(dQ, nq, d, ix->metric, k, fft, ring, d_ids, fso, G, acc_fp64, scan_impl, tune,
+                  comp);
+      CK(cudaEventRecord(ev_freed[slot], comp));
+      const size_t o = j * max_batch;
+      CK(cudaMemcpyAsync(h_fetch_s + o * k, fso.out_s, size_t(nq) * k * sizeof(float),
+                         cudaMemcpyDeviceToHost, comp));
+      CK(cudaMemcpyAsync(h_fetch_id + o * k, fso.out_id, size_t(nq) * k * sizeof(uint64_t),
+                         cudaMemcpyDeviceToHost, comp));
+      CK(cudaMemcpyAsync(h_fetch_cnt + o, fso.out_count, nq * sizeof(uint32_t),
+                         cudaMemcpyDeviceToHost, comp));
+    }
+    rec(ev_fdone, comp);
+  }
+  return chunks.size();
+}
+
+void Ctx::merge_fetch(uint32_t q, size_t nchunks, int k, std::vector<Scored>& gpu) const {
+  for (size_t j = 0; j < nchunks; ++j) {
+    const size_t o = j * max_batch + q;
+    std::vector<Scored> f(h_fetch_cnt[o]);
+    for (uint32_t i = 0; i < h_fetch_cnt[o]; ++i) {
+      f[i] = {h_fetch_s[o * k + i], h_fetch_id[o * k + i]};
+    }
+    gpu = merge_topk(ix->metric, gpu, f, k);
+  }
+}
+
+void Ctx::finish_fetch(size_t nchunks, FetchStats& st) {
+  if (nchunks == 0) return;
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, ev_f0, ev_f1));
+  st.t_fetch = ms * 1e-3;
+  if (ms > 0 && st.fetch_bytes > (64ull << 20) && st.peer_lists == 0) {
+    link_rate = 0.5 * link_rate + 0.5 * double(st.fetch_bytes) / (ms * 1e-3);
+  }
+}
+
 Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq, int L,
                                    int k) {
   if (k < 1) throw std::invalid_argument("k must be >= 1");
@@ -984,168 +1190,11 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
     }
     r.nslow[q] = uint32_t(slow[q].size());
   }
-  // Misses scanned on the GPU from the 2-slot ring: first every missed list
-  // a peer GPU holds (copied over NVLink from the peer's slab, published for
-  // this epoch), then — runtime fetch — the most-shared remaining misses
-  // copied from host memory until the modeled GPU time meets the host's.
   const uint32_t d = ix->d;
-  struct FetchItem {
-    uint32_t c;
-    const float* src;
-    bool host;
-  };
-  std::vector<std::vector<FetchItem>> chunks;
-  uint64_t fill = 0;
-  auto add_item = [&](const FetchItem& it) {
-    const uint64_t len = ix->list_len(it.c);
-    if (chunks.empty() || fill + len > ring_vecs) {
-      if (chunks.size() == kMaxFetchChunks) return false;
-      chunks.emplace_back();
-      fill = 0;
-    }
-    chunks.back().push_back(it);
-    fill += len;
-    return true;
-  };
-  if (miss_fetch && any_slow) {
-    std::map<uint32_t, uint32_t> share;
-    for (uint32_t q = 0; q < nq; ++q) {
-      for (uint32_t c : slow[q]) ++share[c];
-    }
-    std::vector<std::pair<uint32_t, uint32_t>> cand; // (share, list)
-    for (auto& [c, n] : share) cand.emplace_back(n, c);
-    std::sort(cand.begin(), cand.end(), [](auto& a, auto& b) {
-      return a.first != b.first ? a.first > b.first : a.second < b.second;
-    });
-    std::vector<uint8_t> on_gpu(ix->nc, 0);
-    // 1. peer-resident misses (peer copies outrun both the host link and the
-    //    host scan)
-    if (!peers.empty()) {
-      std::vector<std::pair<uint32_t, uint32_t>> rest;
-      for (auto& [n, c] : cand) {
-        const float* src = nullptr;
-        for (auto& pr : peers) {
-          if (pr.slab && !pr.off.empty() && pr.off[c] >= 0) {
-            src = pr.slab + uint64_t(pr.off[c]) * d;
-            break;
-          }
-        }
-        if (src && ix->list_len(c) && add_item({c, src, false})) {
-          on_gpu[c] = 1;
-          ++r.peer_lists;
-          r.peer_bytes += ix->list_len(c) * d * 4;
-        } else {
-          rest.emplace_back(n, c);
-        }
-      }
-      cand.swap(rest);
-    }
-    // 2. runtime fetch from host memory. Host model: memory-bound on the
-    //    distinct missed bytes (each row is read once for all queries sharing
-    //    its list) at the measured rate, scaled by the parallelism the tasks
-    //    allow; GPU model: fetched bytes over the measured link rate plus a
-    //    per-chunk launch cost.
-    const double threads = double(pool->size());
-    const double cr = cpu_rate > 0 ? cpu_rate : 6e9 * threads;
-    auto tasks_of = [&](uint32_t c) {
-      return double((ix->list_len(c) + kMissChunk - 1) / kMissChunk);
-    };
-    double host_bytes = 0, host_tasks = 0;
-    for (auto& [n, c] : cand) {
-      host_bytes += double(ix->list_len(c)) * d * 4;
-      host_tasks += tasks_of(c);
-    }
-    auto host_time = [&](double bytes, double tasks) {
-      return tasks <= 0 ? 0.0 : bytes / (cr * std::min(1.0, tasks / threads));
-    };
-    double gpu_t = 0;
-    for (auto& [n, c] : cand) {
-      const uint64_t len = ix->list_len(c);
-      if (len == 0) continue;
-      const double b = double(len) * d * 4;
-      const bool new_chunk = chunks.empty() || fill + len > ring_vecs;
-      const double ng = gpu_t + b / link_rate + (new_chunk ? 50e-6 : 0.0); // partition + scan launch
-      const double nct = host_time(host_bytes - b, host_tasks - tasks_of(c));
-      if (miss_fetch == 1 &&
-          std::max(ng, nct) >= std::max(gpu_t, host_time(host_bytes, host_tasks))) {
-        break;
-      }
-      if (!add_item({c, ix->vecs + ix->list_off[c] * d, true})) break;
-      on_gpu[c] = 1;
-      ++r.fetch_lists;
-      gpu_t = ng;
-      host_bytes -= b;
-      host_tasks -= tasks_of(c);
-    }
-    if (r.fetch_lists || r.peer_lists) {
-      any_slow = false;
-      for (uint32_t q = 0; q < nq; ++q) {
-        auto& v = slow[q];
-        v.erase(std::remove_if(v.begin(), v.end(), [&](uint32_t c) { return on_gpu[c] != 0; }),
-                v.end());
-        any_slow = any_slow || !v.empty();
-      }
-    }
-  }
-  if (!chunks.empty()) {
-    fetch_results_for(k);
-    CK(cudaEventRecord(ev_f0, copy));
-    std::vector<void*> dsts, srcs;
-    std::vector<size_t> sizes;
-    for (size_t j = 0; j < chunks.size(); ++j) {
-      const int slot = int(j & 1);
-      float* ring = d_ring + size_t(slot) * ring_vecs * d;
-      int64_t* hres = h_res_ring + j * ix->nc;
-      std::fill(hres, hres + ix->nc, int64_t(-1));
-      // ring order = cluster order, so lists adjacent in the list-major host
-      // store become one copy
-      std::sort(chunks[j].begin(), chunks[j].end(),
-                [](const FetchItem& a, const FetchItem& b) { return a.c < b.c; });
-      dsts.clear();
-      srcs.clear();
-      sizes.clear();
-      CK(cudaStreamWaitEvent(copy, ev_freed[slot], 0));
-      uint64_t off = 0;
-      for (const FetchItem& it : chunks[j]) {
-        const uint64_t len = ix->list_len(it.c);
-        hres[it.c] = int64_t(off);
-        float* dst = ring + off * d;
-        const size_t bytes = len * d * sizeof(float);
-        if (!it.host) { // peer slab (same process or CUDA IPC): device to device
-          CK(cudaMemcpyAsync(dst, it.src, bytes, cudaMemcpyDefault, copy));
-        } else if (!srcs.empty() && static_cast<float*>(srcs.back()) +
-                                            sizes.back() / sizeof(float) == it.src) {
-          sizes.back() += bytes;
-          r.fetch_bytes += bytes;
-        } else {
-          dsts.push_back(dst);
-          srcs.push_back(const_cast<float*>(it.src));
-          sizes.push_back(bytes);
-          r.fetch_bytes += bytes;
-        }
-        off += len;
-      }
-      CK(cudaMemcpyAsync(d_res_ring[slot], hres, ix->nc * sizeof(int64_t),
-                         cudaMemcpyHostToDevice, copy));
-      h2d_batch(dsts, srcs, sizes, copy);
-      CK(cudaEventRecord(ev_landed[slot], copy));
-      if (j + 1 == chunks.size()) CK(cudaEventRecord(ev_f1, copy));
-      CK(cudaStreamWaitEvent(comp, ev_landed[slot], 0));
-      fft.grid = static_cast<uint32_t>(G);
-      launch_partition(d_order, nq, lp, d_res_ring[slot], d_list_off, fft, comp);
-      launch_scan(dQ, nq, d, ix->metric, k, fft, ring, d_ids, fso, G, acc_fp64, scan_impl, tune,
-                  comp);
-      CK(cudaEventRecord(ev_freed[slot], comp));
-      const size_t o = j * max_batch;
-      CK(cudaMemcpyAsync(h_fetch_s + o * k, fso.out_s, size_t(nq) * k * sizeof(float),
-                         cudaMemcpyDeviceToHost, comp));
-      CK(cudaMemcpyAsync(h_fetch_id + o * k, fso.out_id, size_t(nq) * k * sizeof(uint64_t),
-                         cudaMemcpyDeviceToHost, comp));
-      CK(cudaMemcpyAsync(h_fetch_cnt + o, fso.out_count, nq * sizeof(uint32_t),
-                         cudaMemcpyDeviceToHost, comp));
-    }
-    rec(ev_fdone, comp);
-  }
+  FetchStats fst;
+  const size_t nchunks = (miss_fetch && any_slow)
+                             ? issue_fetch(slow, any_slow, dQ, nq, lp, d_order, k, G, fst)
+                             : 0;
   std::vector<std::vector<Scored>> miss(nq);
   if (any_slow) {
     std::map<uint32_t, uint32_t> cl;
@@ -1172,33 +1221,24 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
     }
   }
   CK(cudaEventSynchronize(ev_c));
-  if (!chunks.empty()) CK(cudaEventSynchronize(ev_fdone));
+  if (nchunks) CK(cudaEventSynchronize(ev_fdone));
   for (uint32_t q = 0; q < nq; ++q) {
     if (h_fcount[q] != r.nfast[q]) {
       throw std::runtime_error("device residency table disagrees with the store");
     }
     std::vector<Scored> gpu = scan_result(q, uint32_t(G), k, vfast[q]);
-    for (size_t j = 0; j < chunks.size(); ++j) {
-      const size_t o = j * max_batch + q;
-      std::vector<Scored> f(h_fetch_cnt[o]);
-      for (uint32_t i = 0; i < h_fetch_cnt[o]; ++i) {
-        f[i] = {h_fetch_s[o * k + i], h_fetch_id[o * k + i]};
-      }
-      gpu = merge_topk(ix->metric, gpu, f, k);
-    }
+    merge_fetch(q, nchunks, k, gpu);
     r.top[q] = merge_topk(ix->metric, gpu, miss[q], k);
   }
   r.t_2 = secs(t0, Clock::now()); // merged results exist: timing bookkeeping follows
-  if (!chunks.empty()) {
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, ev_f0, ev_f1));
-    r.t_fetch = ms * 1e-3;
-    if (ms > 0 && r.fetch_bytes > (64ull << 20)) {
-      link_rate = 0.5 * link_rate + 0.5 * double(r.fetch_bytes) / (ms * 1e-3);
-    }
-  }
+  finish_fetch(nchunks, fst);
+  r.fetch_lists = fst.fetch_lists;
+  r.peer_lists = fst.peer_lists;
+  r.fetch_bytes = fst.fetch_bytes;
+  r.peer_bytes = fst.peer_bytes;
+  r.t_fetch = fst.t_fetch;
   float ms = 0;
-  CK(cudaEventElapsedTime(&ms, ev_a, chunks.empty() ? ev_s : ev_fdone));
+  CK(cudaEventElapsedTime(&ms, ev_a, nchunks ? ev_fdone : ev_s));
   r.t_g = ms * 1e-3;
   CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
   r.t_coarse = ms * 1e-3;
@@ -1267,14 +1307,24 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
     const uint32_t c = h_order[i];
     (h_res[c] >= 0 ? r.fast : r.slow).push_back(c);
   }
+  // The misses (r.slow keeps the reference's meaning: not cached here) go
+  // to the GPU (peer copies, runtime fetch) and/or the host scan.
+  std::vector<std::vector<uint32_t>> host(1, r.slow);
+  bool any_host = !r.slow.empty();
+  FetchStats fst;
+  const size_t nchunks =
+      (miss_fetch && any_host)
+          ? issue_fetch(host, any_host, d_Q, 1, lp, explicit_probe ? d_order : dm_order, k, G, fst)
+          : 0;
   std::vector<Scored> miss;
-  if (!r.slow.empty()) {
+  if (any_host) {
     const auto tc = Clock::now();
-    miss = miss_scan(*ix, hq, r.slow, k, *pool);
+    miss = miss_scan(*ix, hq, host[0], k, *pool);
     r.t_c = secs(tc, Clock::now());
   }
   tr.mark("split_miss");
   CK(cudaEventSynchronize(ev_c));
+  if (nchunks) CK(cudaEventSynchronize(ev_fdone));
   tr.mark("scan_wait");
   if (*h_fcount != r.fast.size()) {
     throw std::runtime_error("device residency table disagrees with the store");
@@ -1282,10 +1332,17 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
   uint64_t vfast = 0;
   for (uint32_t c : r.fast) vfast += ix->list_len(c);
   std::vector<Scored> gpu = scan_result(0, uint32_t(G), k, vfast);
+  merge_fetch(0, nchunks, k, gpu);
   r.top = merge_topk(ix->metric, gpu, miss, k);
   r.t_2 = secs(t0, Clock::now()); // the merged result exists: timing bookkeeping follows
+  finish_fetch(nchunks, fst);
+  r.fetch_lists = fst.fetch_lists;
+  r.peer_lists = fst.peer_lists;
+  r.fetch_bytes = fst.fetch_bytes;
+  r.peer_bytes = fst.peer_bytes;
+  r.t_fetch = fst.t_fetch;
   float ms = 0;
-  CK(cudaEventElapsedTime(&ms, ev_a, ev_s));
+  CK(cudaEventElapsedTime(&ms, ev_a, nchunks ? ev_fdone : ev_s));
   r.t_g = ms * 1e-3;
   CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
   r.t_coarse = ms * 1e-3;
@@ -1363,12 +1420,12 @@ void fill_timing(laivg_hybrid_timing* t, const Ctx::Result& r,
   t->t_scan = r.t_scan;
   t->scanned_vectors = r.vecs_gpu;
   t->scanned_bytes = r.bytes_gpu;
-  t->fetched_lists = 0;
-  t->cpu_lists = uint32_t(r.slow.size());
-  t->fetched_bytes = 0;
-  t->t_fetch = 0;
-  t->peer_lists = 0;
-  t->peer_bytes = 0;
+  t->fetched_lists = r.fetch_lists;
+  t->cpu_lists = uint32_t(r.slow.size()) - r.fetch_lists - r.peer_lists;
+  t->fetched_bytes = r.fetch_bytes;
+  t->t_fetch = r.t_fetch;
+  t->peer_lists = r.peer_lists;
+  t->peer_bytes = r.peer_bytes;
   if (cost) { // tiered.cpp:190-196
     const double miss = double(r.slow.size());
     t->model_t_c = std::ceil(miss / cost->parallel_slots) * cost->t_cc;
