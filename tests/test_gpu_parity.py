@@ -206,3 +206,19 @@ def test_rank_clusters_all_sort_sizes(orc, laiv, nc):
         probe = laiv.coarse_probe(dev, Q, 17)
         for t in range(3):
             assert np.array_equal(probe[t], orc.coarse_probe(cen, metric, Q[t], 17))
+
+
+@pytest.mark.parametrize("resident", [0, 1])
+def test_search_clusters_duplicate_clusters(orc, laiv, resident):
+    # score_clusters appends every member of every listed cluster, so a
+    # cluster named twice contributes its members twice (ivf.cpp:301-323)
+    cen, vecs, ids, off, qi, qo, _ = planted_data()
+    ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric.InnerProduct)
+    dev = laiv.Device(ix, BIG)
+    set_residency(dev, np.full(64, resident, np.uint8))
+    for t in range(3):
+        cl = [int(x) for x in laiv.coarse_probe(dev, qo[t], 3)]
+        cl = [cl[0], cl[1], cl[0], cl[2], cl[0]]
+        got = laiv.search_clusters(dev, qo[t], cl, 12)
+        want = orc.search_clusters(vecs, ids, off, IP, qo[t], cl, 12)
+        assert_topk_parity(IP, got.ids, got.scores, *want, exact=True)
