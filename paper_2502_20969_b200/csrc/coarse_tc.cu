@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -259,8 +260,18 @@ bool coarse_tc_supported(uint32_t nc, uint32_t d) {
   return (d % 4) == 0 && d >= 4 && nc <= kTcMaxNc && encode_fn() != nullptr;
 }
 
+// Query tile (UMMA N): LAIVG_TC_N overrides (diagnostics / tuning).
+uint32_t tc_tile_n(uint32_t nq) {
+  static const uint32_t forced = [] {
+    const char* e = std::getenv("LAIVG_TC_N");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+  }();
+  if (forced == 32 || forced == 64 || forced == 128 || forced == 256) return forced;
+  return nq <= 32 ? 32 : nq <= 64 ? 64 : nq <= 128 ? 128 : 256;
+}
+
 uint32_t coarse_tc_splits(uint32_t nq, uint32_t nc, uint32_t d, int num_sms) {
-  const uint32_t N = nq <= 32 ? 32 : nq <= 64 ? 64 : nq <= 128 ? 128 : 256;
+  const uint32_t N = tc_tile_n(nq);
   const uint32_t tiles = ((nc + kTcM - 1) / kTcM) * ((nq + N - 1) / N);
   const uint32_t nkb = (d + kTcKB - 1) / kTcKB;
   uint32_t s = tiles >= uint32_t(num_sms) ? 1u : uint32_t(num_sms) / tiles;
@@ -272,10 +283,12 @@ uint32_t launch_coarse_tc(const float* Q, uint32_t nq, const float* centroids, u
                           uint32_t d, float* approx, int num_sms, cudaStream_t st) {
   if (nq == 0 || nc == 0) return 1;
   const uint32_t S = coarse_tc_splits(nq, nc, d, num_sms);
-  if (nq <= 32) launch_tc_n<32>(Q, nq, centroids, nc, d, approx, S, st);
-  else if (nq <= 64) launch_tc_n<64>(Q, nq, centroids, nc, d, approx, S, st);
-  else if (nq <= 128) launch_tc_n<128>(Q, nq, centroids, nc, d, approx, S, st);
-  else launch_tc_n<256>(Q, nq, centroids, nc, d, approx, S, st);
+  switch (tc_tile_n(nq)) {
+    case 32: launch_tc_n<32>(Q, nq, centroids, nc, d, approx, S, st); break;
+    case 64: launch_tc_n<64>(Q, nq, centroids, nc, d, approx, S, st); break;
+    case 128: launch_tc_n<128>(Q, nq, centroids, nc, d, approx, S, st); break;
+    default: launch_tc_n<256>(Q, nq, centroids, nc, d, approx, S, st); break;
+  }
   return S;
 }
 

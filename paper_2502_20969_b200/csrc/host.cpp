@@ -178,6 +178,52 @@ __attribute__((target("avx2,fma"))) void score_rows_avx2(const float* x, const d
   }
 }
 
+template <int G, bool kIP>
+__attribute__((target("avx512f"))) void score_rows_avx512(const float* x, const double* const* q,
+                                                         uint32_t d, double* out) {
+  __m512d a0[G], a1[G];
+  for (int g = 0; g < G; ++g) {
+    a0[g] = _mm512_setzero_pd();
+    a1[g] = _mm512_setzero_pd();
+  }
+  uint32_t j = 0;
+  for (; j + 16 <= d; j += 16) {
+    const __m512d x0 = _mm512_cvtps_pd(_mm256_loadu_ps(x + j));
+    const __m512d x1 = _mm512_cvtps_pd(_mm256_loadu_ps(x + j + 8));
+    for (int g = 0; g < G; ++g) {
+      const __m512d q0 = _mm512_loadu_pd(q[g] + j), q1 = _mm512_loadu_pd(q[g] + j + 8);
+      if constexpr (kIP) {
+        a0[g] = _mm512_fmadd_pd(q0, x0, a0[g]);
+        a1[g] = _mm512_fmadd_pd(q1, x1, a1[g]);
+      } else {
+        const __m512d t0 = _mm512_sub_pd(q0, x0), t1 = _mm512_sub_pd(q1, x1);
+        a0[g] = _mm512_add_pd(a0[g], _mm512_mul_pd(t0, t0));
+        a1[g] = _mm512_add_pd(a1[g], _mm512_mul_pd(t1, t1));
+      }
+    }
+  }
+  for (int g = 0; g < G; ++g) {
+    alignas(64) double l[8];
+    _mm512_store_pd(l, _mm512_add_pd(a0[g], a1[g]));
+    double sacc = ((l[0] + l[1]) + (l[2] + l[3])) + ((l[4] + l[5]) + (l[6] + l[7]));
+    for (uint32_t t = j; t < d; ++t) {
+      const double xv = static_cast<double>(x[t]);
+      if constexpr (kIP) {
+        sacc += q[g][t] * xv;
+      } else {
+        const double u = q[g][t] - xv;
+        sacc += u * u;
+      }
+    }
+    out[g] = sacc;
+  }
+}
+
+bool host_has_avx512() {
+  static const bool ok = __builtin_cpu_supports("avx512f");
+  return ok;
+}
+
 bool host_has_avx2() {
   static const bool ok = __builtin_cpu_supports("avx2") && __builtin_cpu_supports("fma");
   return ok;
@@ -187,6 +233,16 @@ template <bool kIP>
 void score_row_blocked(const float* x, const double* const* q, uint32_t n, uint32_t d,
                        double* out) {
   uint32_t g = 0;
+  if (host_has_avx512()) {
+    for (; g + 4 <= n; g += 4) score_rows_avx512<4, kIP>(x, q + g, d, out + g);
+    switch (n - g) {
+      case 3: score_rows_avx512<3, kIP>(x, q + g, d, out + g); break;
+      case 2: score_rows_avx512<2, kIP>(x, q + g, d, out + g); break;
+      case 1: score_rows_avx512<1, kIP>(x, q + g, d, out + g); break;
+      default: break;
+    }
+    return;
+  }
   for (; g + 4 <= n; g += 4) score_rows_avx2<4, kIP>(x, q + g, d, out + g);
   switch (n - g) {
     case 3: score_rows_avx2<3, kIP>(x, q + g, d, out + g); break;
