@@ -101,6 +101,12 @@ def init_dist(world, local):
     return dist, local % n
 
 
+def host_threads(world):
+    """Host miss-scan threads per rank: the node's cores split between the
+    ranks (one process per GPU shares the host)."""
+    return max(1, (os.cpu_count() or 1) // max(1, world))
+
+
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
@@ -348,7 +354,7 @@ def run_ours(args, cfg):
     ix = laiv.IvfIndex(cen, vecs, ids, off, metric, borrow=True, trust=True)
     member = 4 * cfg["d"] + 8
     capacity = int(cfg["cache_frac"] * cfg["n_lists"]) * cfg["per_list"] * member
-    dev = laiv.Device(ix, capacity, device=gpu,
+    dev = laiv.Device(ix, capacity, device=gpu, miss_threads=host_threads(world),
                       acc_fp64=args.acc == "fp64", scan_impl=args.scan)
     L, k = cfg["nprobe"], cfg["k"]
 
@@ -520,7 +526,7 @@ def run_ours_batch(args, cfg):
     ix = laiv.IvfIndex(cen, vecs, ids, off, metric, borrow=True, trust=True)
     member = 4 * cfg["d"] + 8
     capacity = int(cfg["cache_frac"] * cfg["n_lists"]) * cfg["per_list"] * member
-    dev = laiv.Device(ix, capacity, device=gpu, max_batch=B,
+    dev = laiv.Device(ix, capacity, device=gpu, max_batch=B, miss_threads=host_threads(world),
                       acc_fp64=args.acc == "fp64", scan_impl=args.scan)
     L, k = cfg["nprobe"], cfg["k"]
     probe_plan = laiv.plan_prefetch(dev, cen[0], min(capacity, 64 * cfg["per_list"] * member))
@@ -686,7 +692,7 @@ def run_ours_routed(args, cfg):
     capacity = int(cfg["cache_frac"] * cfg["n_lists"]) * cfg["per_list"] * member
     mine = list(range(W)) if emulated or world == 1 else [rank]
     devs = {w: laiv.Device(ix, capacity, device=gpu,
-                           max_batch=max(m, 32),
+                           max_batch=max(m, 32), miss_threads=host_threads(world),
                            acc_fp64=args.acc == "fp64", scan_impl=args.scan) for w in mine}
     params = laiv.CacheParams(cache_fraction=cfg["hot_fraction"])
     hot = {w: laiv.HotnessTable(params) for w in mine}
