@@ -468,6 +468,7 @@ struct Ctx {
     cudaGraphExec_t ge = nullptr;
     cudaGraphNode_t qnode = nullptr; // the query copy, re-pointed per launch
     const float* src = nullptr;
+    uint64_t kernels = 0;            // kernel nodes (launch accounting)
   };
   std::map<uint64_t, GraphEntry> graph_tab;
   void run_coarse_path(uint32_t lp, int k, int G, const float* src) {
@@ -494,6 +495,7 @@ struct Ctx {
         capturing = false;
         ok = (cudaStreamEndCapture(comp, &e.g) == cudaSuccess) && ok && e.g != nullptr;
       }
+      e.kernels = launch_counter().load() - launched;
       launch_counter() = launched; // captured launches did not run
       if (ok) { // locate the query copy node (the one writing d_Q)
         size_t n = 0;
@@ -537,7 +539,7 @@ struct Ctx {
         e.src = src;
       }
       CK(cudaGraphLaunch(e.ge, comp));
-      launch_counter() += 4; // coarse, seg_sort, merge_runs, scan
+      launch_counter() += e.kernels;
       return;
     }
     enqueue_coarse_path(lp, k, G, src);

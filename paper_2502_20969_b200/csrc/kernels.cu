@@ -302,6 +302,53 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Single query, d % 4 == 0, d <= 1024: each warp scores kCPW centroids with
+// all of their row loads in flight (about one wave for nc = 4096). Per
+// centroid the arithmetic is exactly warp_coarse_score's, so scores are
+// bit-identical to every other coarse path.
+constexpr int kCPW = 2;
+__global__ void __launch_bounds__(256, 2)
+    coarse_scores_q1_kernel(const float* __restrict__ Q, const float* __restrict__ cen,
+                            uint32_t nc, uint32_t d, int metric, double* __restrict__ scores) {
+  __shared__ __align__(16) float sq[1024];
+  const uint32_t q = blockIdx.y;
+  for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) sq[i] = Q[static_cast<uint64_t>(q) * d + i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t c0 = (blockIdx.x * (blockDim.x >> 5) + warp) * kCPW;
+  if (c0 >= nc) return;
+  const uint32_t d4 = d >> 2;
+  float4 xs[kCPW][8];
+#pragma unroll
+  for (int u = 0; u < kCPW; ++u) {
+    const uint32_t c = c0 + u < nc ? c0 + u : c0;
+    const float4* r4 = reinterpret_cast<const float4*>(cen + static_cast<uint64_t>(c) * d);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const uint32_t j = lane + 32u * t;
+      xs[u][t] = j < d4 ? __ldg(r4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  double acc[kCPW];
+#pragma unroll
+  for (int u = 0; u < kCPW; ++u) acc[u] = 0.0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const uint32_t j = lane + 32u * t;
+    if (j < d4) {
+      const float4 qq = reinterpret_cast<const float4*>(sq)[j];
+      const double qd[4] = {qq.x, qq.y, qq.z, qq.w};
+#pragma unroll
+      for (int u = 0; u < kCPW; ++u) Acc4<true>::run(metric, qd, xs[u][t], acc[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kCPW; ++u) {
+    const double v = warp_sum(acc[u]);
+    if (lane == 0 && c0 + u < nc) scores[static_cast<uint64_t>(q) * nc + c0 + u] = v;
+  }
+}
+
 // --------------------------------------------------------------------------
 // residency split of a probe held in memory (block-wide, any blockDim <= 1024)
 // --------------------------------------------------------------------------
@@ -1613,6 +1660,10 @@ void launch_coarse_scores(const float* Q, uint32_t nq, const float* centroids,
     }
     coarse_scores_kernel<8><<<dim3((nc + warps - 1) / warps, (nq + 7) / 8), block, smem, st>>>(
         Q, nq, centroids, nc, d, metric, scores);
+  } else if ((d & 3u) == 0 && d <= 1024) {
+    const uint32_t per_cta = warps * kCPW;
+    coarse_scores_q1_kernel<<<dim3((nc + per_cta - 1) / per_cta, nq), block, 0, st>>>(
+        Q, centroids, nc, d, metric, scores);
   } else {
     const size_t smem = size_t(d) * sizeof(float);
     if (smem > 48 * 1024) {
