@@ -318,6 +318,18 @@ int laivg_hybrid_search_batch_staged(laivg_ctx* ctx, uint32_t q0, uint32_t nq,
 int laivg_debug_coarse_approx(laivg_ctx* ctx, const float* Q, uint32_t nq,
                               float* approx_out);
 
+/* ---- the slow tier on its own -------------------------------------------
+ * The host half of hybrid_search (tiered.cpp:169: the clusters not cached on
+ * the GPU are scored on the host) as a standalone call: for each query q the
+ * best-k over the members of lists[lists_off[q] .. lists_off[q+1]), scored
+ * list-major (each row read once for all queries that name its list) with
+ * the reference's fp64 arithmetic. This is the paper's CPU tier, used by the
+ * device path for cache misses; it is not a replacement for the GPU scan. */
+int laivg_slow_tier_scan(const laivg_index* ix, const float* Q, uint32_t nq,
+                         const uint32_t* lists, const uint32_t* lists_off, int k,
+                         uint32_t threads, uint64_t* ids_out, float* scores_out,
+                         uint32_t* count_out);
+
 /* ---- peer caches (beyond the paper's private caches) ---
  * A miss of one GPU that another GPU of the node caches is copied from that
  * GPU's slab over NVLink into the ring and scanned locally, instead of being

@@ -116,6 +116,7 @@ SIGNATURES = {
     "laivg_prefetch_batch": (i32, [vp, vp, u32, vp, P(Channel), f64, vp, vp,
                                    P(TransferReportC)]),
     "laivg_group_microbatches": (i32, [vp, u64, u32, u64, vp, vp, P(u32)]),
+    "laivg_slow_tier_scan": (i32, [vp, vp, u32, vp, vp, i32, u32, vp, vp, vp]),
     "laivg_epoch_open": (i32, [vp]),
     "laivg_epoch_close": (i32, [vp]),
     "laivg_store_offsets": (i32, [vp, vp]),

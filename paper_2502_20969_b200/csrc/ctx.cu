@@ -2187,6 +2187,40 @@ int laivg_debug_coarse_approx(laivg_ctx* ctx, const float* Q, uint32_t nq, float
   });
 }
 
+// ---- the slow tier on its own ---------------------------------------------------
+int laivg_slow_tier_scan(const laivg_index* ix, const float* Q, uint32_t nq,
+                         const uint32_t* lists, const uint32_t* lists_off, int k,
+                         uint32_t threads, uint64_t* ids_out, float* scores_out,
+                         uint32_t* count_out) {
+  return guard([&] {
+    need(ix, "index");
+    if (k < 1) throw std::invalid_argument("k must be >= 1");
+    if (nq) {
+      need(Q, "queries");
+      need(lists_off, "lists_off");
+      need(ids_out, "ids_out");
+      need(scores_out, "scores_out");
+    }
+    const laivg::Index& x = ix->ix;
+    std::vector<std::vector<uint32_t>> slow(nq);
+    for (uint32_t q = 0; q < nq; ++q) {
+      for (uint32_t i = lists_off[q]; i < lists_off[q + 1]; ++i) {
+        if (lists[i] >= x.nc) {
+          throw std::invalid_argument("unknown cluster id " + std::to_string(lists[i]));
+        }
+        slow[q].push_back(lists[i]);
+      }
+    }
+    if (threads == 0) threads = std::max(1u, std::thread::hardware_concurrency());
+    laivg::ThreadPool pool(threads - 1);
+    const auto top = laivg::miss_scan_batch(x, Q, nq, slow, k, pool);
+    for (uint32_t q = 0; q < nq; ++q) {
+      write_top(top[q], k, ids_out + size_t(q) * k, scores_out + size_t(q) * k,
+                count_out ? count_out + q : nullptr);
+    }
+  });
+}
+
 // ---- peer caches ---------------------------------------------------------------
 int laivg_epoch_open(laivg_ctx* ctx) {
   return guard([&] {

@@ -28,7 +28,7 @@ __all__ = [
     "HybridResult", "HybridTiming", "MicroBatch", "WorkerState", "HotnessTable",
     "CacheParams", "rank_clusters", "coarse_probe", "search_clusters", "ivf_search",
     "plan_prefetch", "execute_prefetch", "incremental_prefetch", "hybrid_search",
-    "coverage", "hybrid_search_batch", "prefetch_batch", "BatchResult", "ivf_search_batch",
+    "coverage", "hybrid_search_batch", "prefetch_batch", "slow_tier_scan", "BatchResult", "ivf_search_batch",
     "group_microbatches", "chunk_microbatches", "assign_cache_aware",
     "assign_round_robin", "assignment_overlap", "split_budget", "default_nprobe",
     "LogicError", "CudaError", "synth_centroids", "synth_lists", "synth_queries",
@@ -415,6 +415,28 @@ def ivf_search(dev: Device, q, L: int, k: int) -> TopK:           # ivf.hpp:90-9
     check(lib().laivg_ivf_search(dev.h, q.ctypes.data, 1, int(L), int(k), ids.ctypes.data,
                                  sc.ctypes.data, cnt.ctypes.data))
     return TopK(k, [ScoredId(int(ids[i]), float(sc[i])) for i in range(int(cnt[0]))])
+
+
+def slow_tier_scan(ix: IvfIndex, Q, lists_per_query, k: int, threads: int = 0) -> list[TopK]:
+    """The host (slow) tier of hybrid_search on its own: per query, the best-k
+    over the members of the given clusters, scored on the host with the
+    reference's fp64 arithmetic (tiered.cpp:169)."""
+    Q = _c(Q, np.float32).reshape(-1, ix.d)
+    nq = Q.shape[0]
+    if len(lists_per_query) != nq:
+        raise ValueError("one cluster list per query")
+    off = np.zeros(nq + 1, np.uint32)
+    for q, ls in enumerate(lists_per_query):
+        off[q + 1] = off[q] + len(ls)
+    flat = _c([c for ls in lists_per_query for c in ls] or [0], np.uint32)
+    ids = np.empty((max(nq, 1), max(k, 1)), np.uint64)
+    sc = np.empty((max(nq, 1), max(k, 1)), np.float32)
+    cnt = np.zeros(max(nq, 1), np.uint32)
+    check(lib().laivg_slow_tier_scan(ix.h, Q.ctypes.data, nq, flat.ctypes.data, off.ctypes.data,
+                                     int(k), threads, ids.ctypes.data, sc.ctypes.data,
+                                     cnt.ctypes.data))
+    return [TopK(k, [ScoredId(int(ids[q, i]), float(sc[q, i])) for i in range(int(cnt[q]))])
+            for q in range(nq)]
 
 
 def ivf_search_batch(dev: Device, Q, L: int, k: int) -> list[TopK]:
