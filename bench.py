@@ -162,6 +162,18 @@ def make_datastore(cfg, world, rank, pinned=True):
 _DATASTORES = {}
 
 
+def q_out_sigma(args, cfg, laiv, dev, vecs, L):
+    """The q_out perturbation: --sigma, else the config's value (fixed so the
+    reference arm draws the very same queries; it is what calibrate_sigma
+    returns on these seeded datastores), with the measured mean coverage."""
+    if args.sigma is not None and args.sigma < 0:  # --sigma -1: recalibrate
+        return calibrate_sigma(laiv, dev, vecs, L)
+    sigma = args.sigma or cfg.get("sigma", 0.008)
+    qi, qo, _ = laiv.synth_queries(QSEED + 1000, vecs, 32, sigma)
+    cov = float(np.mean([laiv.coverage(dev, a, b, L) for a, b in zip(qi, qo)]))
+    return sigma, cov
+
+
 def calibrate_sigma(laiv, dev, vecs, L, target=0.8, nq=32):
     """Largest q_out perturbation whose mean coverage at nprobe >= target
     (coverage in [0.6, 0.95]; acceptance.cpp:219-223)."""
@@ -292,7 +304,7 @@ def run_reference(args, cfg):
 
     cen, vecs, ids, off = make_datastore(cfg, 1, 0, pinned=False)
     metric = 0 if args.metric == "ip" else 1
-    sigma = args.sigma or 0.006
+    sigma = args.sigma or cfg.get("sigma", 0.008)  # the same queries as our arm
     qi, qo, _ = laiv.synth_queries(QSEED, vecs, 4096, sigma)
     ri = reference_index(cen, vecs, ids, off, metric)
     threads = os.cpu_count() or 1
@@ -336,6 +348,7 @@ def config_block(cfg, args, sigma):
             "dim": cfg["d"], "n_lists": cfg["n_lists"], "nprobe": cfg["nprobe"], "k": cfg["k"],
             "metric": args.metric, "batch": cfg.get("batch", 1), "window_s": args.window,
             "cache_fraction_of_lists": cfg["cache_frac"], "q_out_sigma": sigma,
+            "query_seed": QSEED,
             "l2_flush": "not needed: each query scans up to ~1 GB of lists > 126 MB L2, "
                         "and every step re-fetches its lists into a cleared cache"}
 
@@ -364,7 +377,7 @@ def run_ours(args, cfg):
     dev.store.clear()
     b_link = rep.h2d_gbps * 1e9
     budget = int(min(b_link * args.window, capacity))
-    sigma, cov = (args.sigma, None) if args.sigma else calibrate_sigma(laiv, dev, vecs, L)
+    sigma, cov = q_out_sigma(args, cfg, laiv, dev, vecs, L)
     # (one rank: extra queries of the same generator extend the CPU sample)
     nq_total = max((args.warmup + args.steps) * world + 8,
                    args.warmup + args.steps + (args.cpu_sample if world == 1 else 0))
@@ -535,7 +548,7 @@ def run_ours_batch(args, cfg):
     b_link = rep.h2d_gbps * 1e9
     budget = int(min(b_link * args.window, capacity))
     budgets = laiv.split_budget(budget, laiv.MicroBatch(list(range(B))))
-    sigma, cov = (args.sigma, None) if args.sigma else calibrate_sigma(laiv, dev, vecs, L)
+    sigma, cov = q_out_sigma(args, cfg, laiv, dev, vecs, L)
     nsteps = args.warmup + args.steps
     nq_total = nsteps * B * world
     qi, qo, _ = laiv.synth_queries(QSEED, vecs, nq_total, sigma)
@@ -722,7 +735,7 @@ def run_ours_routed(args, cfg):
     d0.store.clear()
     b_link = rep.h2d_gbps * 1e9
     budget = int(min(b_link * args.window, capacity * (1.0 - cfg["hot_fraction"])))
-    sigma = args.sigma or 0.008
+    sigma = args.sigma or cfg.get("sigma", 0.008)
     nsteps = args.warmup + args.steps
     qi, qo, _, topic = laiv.synth_queries_topical(QSEED, cen, vecs, off, nsteps * B, sigma,
                                                   cfg["topics"], cfg["zipf"], cfg["neigh"])
@@ -908,7 +921,9 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--metric", default="ip", choices=["ip", "l2"])
     ap.add_argument("--window", type=float, default=None)
-    ap.add_argument("--sigma", type=float, default=None)
+    ap.add_argument("--sigma", type=float, default=None,
+                    help="q_out noise; default the config's (0.008, coverage ~0.8); "
+                         "negative: recalibrate for coverage >= 0.8")
     ap.add_argument("--cpu-sample", type=int, default=128,
                     help="queries in the reference CPU baseline sample (C2: ~20 s of CPU "
                          "work on 16 host threads)")
