@@ -608,6 +608,86 @@ __device__ __forceinline__ void cswap_up(uint64_t* k, uint32_t* v, uint32_t a, u
   }
 }
 
+// One merge step of the prefix tree, by one warp: runs A and B (ascending by
+// (key, cluster), P = 32 * E entries each) -> the best P of A u B, ascending,
+// at `o`. C_i = min(A_i, B_{P-1-i}) holds exactly those P as a bitonic
+// sequence; a bitonic clean (strides >= E across lanes by shuffle, < E in
+// registers) sorts it. No block barrier inside.
+template <int E>
+__device__ __forceinline__ void warp_merge_best(const uint64_t* ak, const uint32_t* av,
+                                                const uint64_t* bk, const uint32_t* bv,
+                                                uint64_t* ok, uint32_t* ov) {
+  constexpr uint32_t P = 32u * E;
+  const uint32_t lane = threadIdx.x & 31u;
+  uint64_t k[E];
+  uint32_t v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t i = lane * E + e;
+    const uint64_t ka = ak[i], kb = bk[P - 1 - i];
+    const uint32_t va = av[i], vb = bv[P - 1 - i];
+    const bool take_b = kv_gt(ka, va, kb, vb);
+    k[e] = take_b ? kb : ka;
+    v[e] = take_b ? vb : va;
+  }
+#pragma unroll
+  for (uint32_t st = P / 2; st > 0; st >>= 1) {
+    if (st >= static_cast<uint32_t>(E)) {
+      const int lm = static_cast<int>(st / E);
+      const bool lower = (lane & static_cast<uint32_t>(lm)) == 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint64_t pk = __shfl_xor_sync(kFull, k[e], lm);
+        const uint32_t pv = __shfl_xor_sync(kFull, v[e], lm);
+        // the lower index keeps the smaller of the pair
+        const bool gt = kv_gt(k[e], v[e], pk, pv);
+        if (lower == gt) {
+          k[e] = pk;
+          v[e] = pv;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int pe = e ^ static_cast<int>(st);
+        if (pe > e && kv_gt(k[e], v[e], k[pe], v[pe])) {
+          const uint64_t tk = k[e];
+          k[e] = k[pe];
+          k[pe] = tk;
+          const uint32_t tv = v[e];
+          v[e] = v[pe];
+          v[pe] = tv;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    ok[lane * E + e] = k[e];
+    ov[lane * E + e] = v[e];
+  }
+}
+
+template <int E>
+__device__ void warp_merge_tree(uint64_t*& ak, uint32_t*& av, uint64_t*& bk, uint32_t*& bv,
+                                uint32_t nruns) {
+  constexpr uint32_t P = 32u * E;
+  const uint32_t warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (uint32_t lists = nruns; lists > 1; lists >>= 1) {
+    for (uint32_t pr = warp; pr < lists / 2; pr += nw) {
+      warp_merge_best<E>(ak + 2 * pr * P, av + 2 * pr * P, ak + (2 * pr + 1) * P,
+                         av + (2 * pr + 1) * P, bk + pr * P, bv + pr * P);
+    }
+    __syncthreads();
+    uint64_t* tk = ak;
+    ak = bk;
+    bk = tk;
+    uint32_t* tv = av;
+    av = bv;
+    bv = tv;
+  }
+}
+
 // nseg_pad runs of kSeg sorted entries per query (power of two, sentinel
 // padded); P = run length kept per level (power of two, <= kSeg) or kSeg with
 // `full` to keep everything.
@@ -638,7 +718,15 @@ __global__ void __launch_bounds__(1024)
     uint64_t* bk = reinterpret_cast<uint64_t*>(mv + total);
     bk = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(bk) + 7) & ~uintptr_t(7));
     uint32_t* bv = reinterpret_cast<uint32_t*>(bk + total);
-    for (uint32_t lists = nseg_pad; lists > 1; lists >>= 1) {
+    if (P >= 32 && P <= 256) {
+      // one warp per pair: min-trick + in-warp bitonic clean, one barrier
+      // per level (the merge-path search below costs ~4x more)
+      if (P == 32) warp_merge_tree<1>(ak, av, bk, bv, nseg_pad);
+      else if (P == 64) warp_merge_tree<2>(ak, av, bk, bv, nseg_pad);
+      else if (P == 128) warp_merge_tree<4>(ak, av, bk, bv, nseg_pad);
+      else warp_merge_tree<8>(ak, av, bk, bv, nseg_pad);
+    }
+    for (uint32_t lists = (P >= 32 && P <= 256) ? 1 : nseg_pad; lists > 1; lists >>= 1) {
       for (uint32_t x = threadIdx.x; x < (lists / 2) << lP; x += blockDim.x) {
         const uint32_t pr = x >> lP, p = x & (P - 1);
         const uint32_t A = 2 * pr * P, B = A + P;
@@ -1697,7 +1785,7 @@ void launch_select(const double* scores, uint32_t nq, uint32_t nc, int metric,
   const bool full = n_out > kSeg;
   uint32_t P = kSeg;
   if (!full) {
-    P = 1;
+    P = 32; // warp-merge granularity; runs hold kSeg >= 32 entries
     while (P < n_out) P <<= 1;
   }
   // prefix mode ping-pongs between two buffers
