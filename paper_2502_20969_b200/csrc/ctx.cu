@@ -129,11 +129,6 @@ class SlabAlloc {
       }
     }
   }
-  uint64_t free_total() const {
-    uint64_t s = 0;
-    for (auto& [o, n] : free_) s += n;
-    return s;
-  }
 
  private:
   uint64_t total_ = 0;

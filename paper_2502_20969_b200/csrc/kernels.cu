@@ -76,11 +76,6 @@ namespace {
 // --------------------------------------------------------------------------
 // total order (vectorstore.hpp:34-39)
 // --------------------------------------------------------------------------
-__device__ __forceinline__ bool ranks_before(int metric, float sa, uint64_t ia,
-                                             float sb, uint64_t ib) {
-  if (sa != sb) return metric == kIP ? sa > sb : sa < sb;
-  return ia < ib;
-}
 __device__ __forceinline__ float sentinel_score(int metric) {
   return metric == kIP ? -INFINITY : INFINITY;
 }
@@ -307,10 +302,11 @@ __global__ void __launch_bounds__(256)
 // centroid the arithmetic is exactly warp_coarse_score's, so scores are
 // bit-identical to every other coarse path.
 constexpr int kCPW = 2;
+template <int NCH> // float4 chunks per lane: d <= 128 * NCH
 __global__ void __launch_bounds__(256, 2)
     coarse_scores_q1_kernel(const float* __restrict__ Q, const float* __restrict__ cen,
                             uint32_t nc, uint32_t d, int metric, double* __restrict__ scores) {
-  __shared__ __align__(16) float sq[1024];
+  __shared__ __align__(16) float sq[128 * NCH];
   const uint32_t q = blockIdx.y;
   for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) sq[i] = Q[static_cast<uint64_t>(q) * d + i];
   __syncthreads();
@@ -318,13 +314,13 @@ __global__ void __launch_bounds__(256, 2)
   const uint32_t c0 = (blockIdx.x * (blockDim.x >> 5) + warp) * kCPW;
   if (c0 >= nc) return;
   const uint32_t d4 = d >> 2;
-  float4 xs[kCPW][8];
+  float4 xs[kCPW][NCH];
 #pragma unroll
   for (int u = 0; u < kCPW; ++u) {
     const uint32_t c = c0 + u < nc ? c0 + u : c0;
     const float4* r4 = reinterpret_cast<const float4*>(cen + static_cast<uint64_t>(c) * d);
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
+    for (int t = 0; t < NCH; ++t) {
       const uint32_t j = lane + 32u * t;
       xs[u][t] = j < d4 ? __ldg(r4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
@@ -333,7 +329,7 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
   for (int u = 0; u < kCPW; ++u) acc[u] = 0.0;
 #pragma unroll
-  for (int t = 0; t < 8; ++t) {
+  for (int t = 0; t < NCH; ++t) {
     const uint32_t j = lane + 32u * t;
     if (j < d4) {
       const float4 qq = reinterpret_cast<const float4*>(sq)[j];
@@ -371,12 +367,15 @@ __device__ void partition_block(const uint32_t* probe, uint32_t lp, const int64_
     const uint32_t i = t0 + threadIdx.x;
     uint32_t c = 0;
     int64_t so = -1;
-    if (i < lp) {
+    uint64_t lo0 = 0, lo1 = 0;
+    if (i < lp) { // all three loads in flight together
       c = probe[i];
       so = res_off[c];
+      lo0 = list_off[c];
+      lo1 = list_off[c + 1];
     }
     const bool fast = so >= 0;
-    const uint64_t len = fast ? list_off[c + 1] - list_off[c] : 0;
+    const uint64_t len = fast ? lo1 - lo0 : 0;
     uint32_t ic = fast ? 1u : 0u;
     uint64_t il = len;
 #pragma unroll
@@ -402,7 +401,7 @@ __device__ void partition_block(const uint32_t* probe, uint32_t lp, const int64_
     if (fast) {
       const uint32_t ex_c = pc + ic - 1u;
       ft.slab[tb + ex_c] = so;
-      ft.row[tb + ex_c] = list_off[c];
+      ft.row[tb + ex_c] = lo0;
       ft.len[tb + ex_c] = static_cast<uint32_t>(len);
       ft.cluster[tb + ex_c] = c;
       pre[ex_c] = pl + il - len;
@@ -1750,8 +1749,9 @@ void launch_coarse_scores(const float* Q, uint32_t nq, const float* centroids,
         Q, nq, centroids, nc, d, metric, scores);
   } else if ((d & 3u) == 0 && d <= 1024) {
     const uint32_t per_cta = warps * kCPW;
-    coarse_scores_q1_kernel<<<dim3((nc + per_cta - 1) / per_cta, nq), block, 0, st>>>(
-        Q, centroids, nc, d, metric, scores);
+    const dim3 grid((nc + per_cta - 1) / per_cta, nq);
+    if (d <= 768) coarse_scores_q1_kernel<6><<<grid, block, 0, st>>>(Q, centroids, nc, d, metric, scores);
+    else coarse_scores_q1_kernel<8><<<grid, block, 0, st>>>(Q, centroids, nc, d, metric, scores);
   } else {
     const size_t smem = size_t(d) * sizeof(float);
     if (smem > 48 * 1024) {
