@@ -291,3 +291,28 @@ def test_batch_single_query_and_fetch_metrics(orc, laiv):
         want = orc.ivf_search(cen, vecs, ids, off, int(metric), qo[0], 24, 10)
         assert_topk_parity(int(metric), res.topk(0).ids, res.topk(0).scores, *want)
         assert tm.fetched_lists + tm.cpu_lists == 24 - int(res.nfast[0])
+
+
+@pytest.mark.parametrize("name,metric", [("l2", L2), ("ip", IP)])
+def test_group_scan_microbatches(orc, laiv, name, metric):
+    # micro-batches of 2-4 queries stream the union of their resident lists
+    # once (list-major group scan); results must equal the single-query path
+    cen, vecs, ids, off, qi, qo, g = planted_data()
+    ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric(metric))
+    dev = laiv.Device(ix, BIG)
+    rng = np.random.default_rng(5)
+    for frac in (0.0, 1.0, 0.5):
+        set_residency(dev, (rng.random(64) < frac).astype(np.uint8))
+        for nq in (2, 3, 4):
+            for L, k in ((8, 10), (32, 32), (16, 33), (64, 1)):
+                sel = rng.choice(40, nq, replace=False)
+                res, timing = laiv.hybrid_search_batch(dev, qo[sel], L, k)
+                for i, t in enumerate(sel):
+                    single, _ = laiv.hybrid_search(dev, qo[t], L, k)
+                    got = res.topk(i)
+                    assert np.array_equal(got.ids, single.topk.ids), (nq, L, k, t)
+                    assert np.array_equal(got.scores, single.topk.scores), (nq, L, k, t)
+                    assert res.nfast[i] == len(single.fast_clusters)
+                    want = orc.ivf_search(cen, vecs, ids, off, metric, qo[t], L, k)
+                    assert_topk_parity(metric, got.ids, got.scores, *want)
+                assert timing.scanned_vectors == 300 * int(res.nfast.sum())
