@@ -242,83 +242,6 @@ struct Ctx {
   double link_rate = 50e9;       // EMA of fetch H2D bytes/s
   double cpu_rate = 0;           // EMA of the host miss scan rate on distinct list bytes
   void alloc_scan_set(FastTable& f, ScanOut& o, bool device_outputs = true);
-
-  // list-major group scan of a micro-batch: the union table, built on the
-  // host from the probes and the residency, uploaded in one copy
-  bool group_scan = true;
-  unsigned char* gt_dev = nullptr;
-  unsigned char* gt_host = nullptr;
-  size_t gt_bytes = 0;
-  void launch_group_scan(const float* dQ, uint32_t nq, uint32_t lp, int k, int G) {
-    const uint32_t nc = ix->nc;
-    std::vector<uint32_t> mask(nc, 0);
-    for (uint32_t q = 0; q < nq; ++q) {
-      for (uint32_t i = 0; i < lp; ++i) {
-        const uint32_t c = h_order[size_t(q) * lp + i];
-        if (h_res[c] >= 0) mask[c] |= 1u << q;
-      }
-    }
-    std::vector<uint32_t> uni;
-    for (uint32_t c = 0; c < nc; ++c) {
-      if (mask[c]) uni.push_back(c); // cluster order
-    }
-    const size_t U = uni.size();
-    auto al8 = [](size_t x) { return (x + 15) & ~size_t(15); };
-    const size_t o_slab = 0, o_row = al8(o_slab + U * 8), o_pre = al8(o_row + U * 8),
-                 o_len = al8(o_pre + (U + 1) * 8), o_mask = al8(o_len + U * 4),
-                 o_cnt = al8(o_mask + U * 4), o_cta = al8(o_cnt + 4),
-                 total = al8(o_cta + size_t(G) * sizeof(CtaStart));
-    if (total > gt_bytes) {
-      if (gt_dev) cudaFree(gt_dev);
-      if (gt_host) cudaFreeHost(gt_host);
-      gt_bytes = std::max(total, size_t(1) << 16);
-      gt_dev = dev_alloc<unsigned char>(gt_bytes);
-      gt_host = pin_alloc<unsigned char>(gt_bytes);
-    }
-    auto* slab_o = reinterpret_cast<int64_t*>(gt_host + o_slab);
-    auto* row_o = reinterpret_cast<uint64_t*>(gt_host + o_row);
-    auto* pre = reinterpret_cast<uint64_t*>(gt_host + o_pre);
-    auto* len = reinterpret_cast<uint32_t*>(gt_host + o_len);
-    auto* msk = reinterpret_cast<uint32_t*>(gt_host + o_mask);
-    auto* cnt = reinterpret_cast<uint32_t*>(gt_host + o_cnt);
-    auto* cta = reinterpret_cast<CtaStart*>(gt_host + o_cta);
-    uint64_t V = 0;
-    for (size_t i = 0; i < U; ++i) {
-      const uint32_t c = uni[i];
-      slab_o[i] = h_res[c];
-      row_o[i] = ix->list_off[c];
-      len[i] = uint32_t(ix->list_len(c));
-      msk[i] = mask[c];
-      pre[i] = V;
-      V += ix->list_len(c);
-    }
-    pre[U] = V;
-    *cnt = uint32_t(U);
-    // CTA b scans [V*b/G, V*(b+1)/G) of the union (the partition rule)
-    size_t li = 0;
-    for (int b = 0; b < G; ++b) {
-      const uint64_t v0 = V * uint64_t(b) / uint64_t(G), v1 = V * uint64_t(b + 1) / uint64_t(G);
-      if (v0 >= v1) {
-        cta[b] = CtaStart{0u, 0u, 0u, 0u};
-        continue;
-      }
-      while (li + 1 < U && pre[li + 1] <= v0) ++li;
-      cta[b] = CtaStart{uint32_t(li), uint32_t(v0 - pre[li]), uint32_t(v1 - v0), 0u};
-    }
-    CK(cudaMemcpyAsync(gt_dev, gt_host, total, cudaMemcpyHostToDevice, comp));
-    FastTable g{};
-    g.slab = reinterpret_cast<int64_t*>(gt_dev + o_slab);
-    g.row = reinterpret_cast<uint64_t*>(gt_dev + o_row);
-    g.pre = reinterpret_cast<uint64_t*>(gt_dev + o_pre);
-    g.len = reinterpret_cast<uint32_t*>(gt_dev + o_len);
-    g.count = reinterpret_cast<uint32_t*>(gt_dev + o_cnt);
-    g.cta = reinterpret_cast<CtaStart*>(gt_dev + o_cta);
-    g.stride = uint32_t(U);
-    g.grid = uint32_t(G);
-    launch_scan_group(dQ, nq, ix->d, ix->metric, k, g,
-                      reinterpret_cast<const uint32_t*>(gt_dev + o_mask), d_slab, d_ids, so, G,
-                      tune, comp);
-  }
   // The scan's result for query q: the device-merged top-k, or (host-final
   // mode) the k-way merge of the G CTA lists with ids looked up here.
   std::vector<Scored> scan_result(uint32_t q, uint32_t G, int k, uint64_t V) const;
@@ -653,10 +576,9 @@ Ctx::~Ctx() {
     if (e) cudaEventDestroy(e);
   }
   for (void* p : {(void*)sb.q, (void*)sb.dist, (void*)sb.order, (void*)sb.off, (void*)sb.nb,
-                  (void*)sb.probes, (void*)sb.resident, (void*)sb.overlap, (void*)gt_dev}) {
+                  (void*)sb.probes, (void*)sb.resident, (void*)sb.overlap}) {
     if (p) cudaFree(p);
   }
-  if (gt_host) cudaFreeHost(gt_host);
   for (auto& p : peers) {
     if (p.ipc) cudaIpcCloseMemHandle(p.ipc);
   }
@@ -805,7 +727,6 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   // fp64 accumulation needs no device re-score: the host merges the scan
   // CTAs' lists (saves the device grid merge chain)
   host_final = acc_fp64 && !(std::getenv("LAIVG_DEVICE_MERGE"));
-  group_scan = !(std::getenv("LAIVG_NO_GROUP_SCAN"));
   if (host_final) {
     float* ds = nullptr;
     uint64_t* dr = nullptr;
@@ -1230,15 +1151,10 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
   }
   CK(cudaStreamWaitEvent(comp, ev_copy_tail, 0));
   commit_res(comp);
-  // A micro-batch of 2-4 queries streams the union of its lists once (group
-  // scan); larger batches scan per query, each from its own fast table.
-  const bool group = host_final && scan_impl == ScanImpl::kTma && group_scan &&
-                     group_scan_ok(nq, ix->d, k, acc_fp64);
-  const int G = group ? std::max(1, std::min(scan_grid_x(1, sms, scan_impl, tune), part_cap / int(nq)))
-                      : std::max(1, std::min(scan_grid_x(nq, sms, scan_impl, tune), part_cap / int(nq)));
+  const int G = std::max(1, std::min(scan_grid_x(nq, sms, scan_impl, tune), part_cap / int(nq)));
   ft.grid = static_cast<uint32_t>(G);
   rec(ev_a, comp);
-  coarse(dQ, nq, lp, comp, /*part=*/!group);
+  coarse(dQ, nq, lp, comp, /*part=*/true);
   rec(ev_b, comp);
   CK(cudaEventRecord(ev_fork, comp));
   CK(cudaStreamWaitEvent(aux, ev_fork, 0));
@@ -1246,20 +1162,13 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
                      cudaMemcpyDeviceToHost, aux));
   rec(ev_probe, aux);
   rec(ev_p, comp);
-  if (!group) {
-    launch_scan(dQ, nq, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl,
-                tune, comp);
-    rec(ev_s, comp);
-    rec(ev_c, comp); // results are in mapped host memory
-  }
+  launch_scan(dQ, nq, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl, tune,
+              comp);
+  rec(ev_s, comp);
+  rec(ev_c, comp); // results are in mapped host memory
 
   // host: split every probe by residency and scan the misses list-major
   CK(cudaEventSynchronize(ev_probe));
-  if (group) {
-    launch_group_scan(dQ, nq, lp, k, G);
-    rec(ev_s, comp);
-    rec(ev_c, comp);
-  }
   std::vector<std::vector<uint32_t>> slow(nq);
   std::vector<uint64_t> vfast(nq, 0);
   bool any_slow = false;
@@ -1311,7 +1220,7 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
   CK(cudaEventSynchronize(ev_c));
   if (nchunks) CK(cudaEventSynchronize(ev_fdone));
   for (uint32_t q = 0; q < nq; ++q) {
-    if (!group && h_fcount[q] != r.nfast[q]) {
+    if (h_fcount[q] != r.nfast[q]) {
       throw std::runtime_error("device residency table disagrees with the store");
     }
     std::vector<Scored> gpu = scan_result(q, uint32_t(G), k, vfast[q]);

@@ -1523,179 +1523,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 }
 
 // --------------------------------------------------------------------------
-// list-major group scan: a micro-batch of up to kGroupQ queries streams the
-// UNION of its resident probed lists once; every row is scored for each query
-// whose probe holds the row's list (per-list query mask). fp64, d = 768.
-// --------------------------------------------------------------------------
-constexpr int kGroupQ = 4;
-
-template <int NCH>
-__global__ void __launch_bounds__(kTmaThreads, 1)
-    scan_group_kernel(const float* __restrict__ Q, uint32_t nq, uint32_t d, int metric, int kk,
-                      FastTable ft, const uint32_t* __restrict__ lmask,
-                      const float* __restrict__ slab, const uint64_t* __restrict__ ids_all,
-                      ScanOut out, uint32_t T, uint32_t S) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const size_t stage_floats = static_cast<size_t>(T) * d;
-  float* stage = reinterpret_cast<float*>(smem);
-  size_t off = (static_cast<size_t>(S) * stage_floats * 4 + 127) & ~size_t(127);
-  const uint32_t m = pow2_ceil(static_cast<uint32_t>(kk));
-  const size_t merge_bytes = 2 * (static_cast<size_t>(kConsumers) * m * 16 + 16);
-  if (off < merge_bytes) off = (merge_bytes + 127) & ~size_t(127);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + off);
-  uint64_t* empty = full + S;
-  uint64_t* mrow = empty + S;                                 // [S][T]
-  uint32_t* mvi = reinterpret_cast<uint32_t*>(mrow + S * T);  // [S][T]
-  uint32_t* mmask = mvi + S * T;                              // [S][T]
-  uint32_t* mn = mmask + S * T;                               // [S]
-  float* sqg = reinterpret_cast<float*>(
-      (reinterpret_cast<uintptr_t>(mn + S) + 15) & ~uintptr_t(15)); // [kGroupQ][d]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (uint32_t i = threadIdx.x; i < kGroupQ * d; i += blockDim.x) {
-    sqg[i] = i < nq * d ? Q[i] : 0.0f;
-  }
-  if (threadIdx.x == 0) {
-    for (uint32_t s = 0; s < S; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, kConsumers);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  const CtaStart cs = ft.cta[blockIdx.x];
-  const uint32_t nvec = cs.n;
-  const uint32_t ntiles = (nvec + T - 1) / T;
-  WarpTopK<1> top[kGroupQ];
-#pragma unroll
-  for (int g = 0; g < kGroupQ; ++g) {
-    top[g].ids = ids_all;
-    top[g].init(metric);
-  }
-  if (warp == 0) {
-    if (lane == 0 && ntiles) {
-      Cursor cur;
-      cur.li = cs.li;
-      cur.load(ft, 0);
-      cur.o = cs.o;
-      for (uint32_t i = 0; i < ntiles; ++i) {
-        const uint32_t s = i % S;
-        mbar_wait(empty + s, ((i / S) & 1u) ^ 1u);
-        const uint32_t tile0 = i * T;
-        const uint32_t n = min(T, nvec - tile0);
-        uint32_t j = 0;
-        Cursor c2 = cur;
-        while (true) {
-          const uint32_t take = static_cast<uint32_t>(umin64(n - j, c2.len - c2.o));
-          const uint32_t msk = lmask[c2.li];
-          for (uint32_t t = 0; t < take; ++t) {
-            mrow[s * T + j + t] = c2.row + c2.o + t;
-            mvi[s * T + j + t] = static_cast<uint32_t>(c2.slab + c2.o + t);
-            mmask[s * T + j + t] = msk;
-          }
-          j += take;
-          if (j >= n) break;
-          c2.advance(ft, 0, take);
-        }
-        mn[s] = n;
-        mbar_arrive_expect_tx(full + s, n * d * 4u);
-        j = 0;
-        while (true) {
-          const uint32_t take = static_cast<uint32_t>(umin64(n - j, cur.len - cur.o));
-          bulk_g2s(stage + s * stage_floats + static_cast<size_t>(j) * d,
-                   slab + static_cast<uint64_t>(cur.slab + static_cast<int64_t>(cur.o)) * d,
-                   take * d * 4u, full + s);
-          j += take;
-          if (tile0 + j >= nvec) break;
-          cur.advance(ft, 0, take);
-          if (j >= n) break;
-        }
-      }
-    }
-  } else {
-    const int cw = warp - 1;
-    for (uint32_t i = 0; i < ntiles; ++i) {
-      const uint32_t s = i % S;
-      mbar_wait(full + s, (i / S) & 1u);
-      const uint32_t n = mn[s];
-      const float* base = stage + s * stage_floats;
-      for (uint32_t j = cw; j < n; j += 2 * kConsumers) {
-        const uint32_t j2 = j + kConsumers;
-        const bool two = j2 < n;
-        const float4* r0 = reinterpret_cast<const float4*>(base + static_cast<size_t>(j) * d);
-        const float4* r1 =
-            reinterpret_cast<const float4*>(base + static_cast<size_t>(two ? j2 : j) * d);
-        float4 x0[NCH], x1[NCH];
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-          x0[c] = r0[c * 32 + lane];
-          x1[c] = r1[c * 32 + lane];
-        }
-        const uint32_t m0 = mmask[s * T + j], m1 = two ? mmask[s * T + j2] : 0u;
-#pragma unroll
-        for (int g = 0; g < kGroupQ; ++g) {
-          if (((m0 | m1) >> g) & 1u) { // warp-uniform
-            const float4* q4 = reinterpret_cast<const float4*>(sqg + static_cast<size_t>(g) * d);
-            double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-            for (int c = 0; c < NCH; ++c) {
-              const float4 qq = q4[c * 32 + lane];
-              const double qd[4] = {qq.x, qq.y, qq.z, qq.w};
-              Acc4<true>::run(metric, qd, x0[c], a0);
-              Acc4<true>::run(metric, qd, x1[c], a1);
-            }
-            a0 = warp_sum(a0);
-            a1 = warp_sum(a1);
-            if ((m0 >> g) & 1u) {
-              top[g].offer(metric, kk, finish_score<double>(metric, a0), mrow[s * T + j],
-                           mvi[s * T + j]);
-            }
-            if ((m1 >> g) & 1u) {
-              top[g].offer(metric, kk, finish_score<double>(metric, a1), mrow[s * T + j2],
-                           mvi[s * T + j2]);
-            }
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + s);
-    }
-  }
-  __syncthreads(); // every tile consumed: the ring is free for merging
-
-  // per query: merge the 8 consumer warps' lists, write this CTA's sorted
-  // top-kk to the host-final buffers [q][grid][kk]
-  const uint32_t cap = pow2_ceil(kConsumers) * m;
-  Cands cur = cands_at(smem, cap);
-  Cands alt = cands_at(smem + cap * 16 + 16, cap);
-  const uint32_t wl = pow2_ceil(static_cast<uint32_t>(kConsumers));
-  for (uint32_t g = 0; g < nq && g < static_cast<uint32_t>(kGroupQ); ++g) {
-    if (warp >= 1 && warp <= kConsumers) {
-      const uint32_t o = (warp - 1) * m;
-#pragma unroll
-      for (int gg = 0; gg < kGroupQ; ++gg) {
-        if (static_cast<uint32_t>(gg) == g) top[gg].store(kk, cur.s + o, cur.r + o, cur.vi + o);
-      }
-    }
-    for (uint32_t x = threadIdx.x; x < wl * m; x += blockDim.x) {
-      if ((x & (m - 1)) >= static_cast<uint32_t>(kk) || (x >> (__ffs(m) - 1)) >= static_cast<uint32_t>(kConsumers)) {
-        cur.s[x] = sentinel_score(metric);
-        cur.r[x] = ~0ull;
-        cur.vi[x] = ~0u;
-      }
-    }
-    __syncthreads();
-    Cands a = cur, b = alt;
-    merge_tree(metric, ids_all, &a, &b, wl, m);
-    const uint64_t pbase = (static_cast<uint64_t>(g) * gridDim.x + blockIdx.x) * kk;
-    for (uint32_t x = threadIdx.x; x < static_cast<uint32_t>(kk); x += blockDim.x) {
-      out.cta_s[pbase + x] = a.s[x];
-      out.cta_r[pbase + x] = a.r[x];
-    }
-    __syncthreads();
-  }
-}
-
-// --------------------------------------------------------------------------
 // LDG scan (direct 128-bit loads into registers)
 // --------------------------------------------------------------------------
 constexpr int kScanWarps = 8;
@@ -2037,27 +1864,6 @@ void launch_scan(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
     else LAIVG_D(false, 0);
   }
 #undef LAIVG_D
-}
-
-bool group_scan_ok(uint32_t nq, uint32_t d, int k, bool acc_fp64) {
-  return nq >= 2 && nq <= static_cast<uint32_t>(kGroupQ) && d == 768 && acc_fp64 &&
-         scan_kk(k, acc_fp64) <= 32;
-}
-
-void launch_scan_group(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
-                       const FastTable& ft, const uint32_t* lmask, const float* slab,
-                       const uint64_t* ids_all, const ScanOut& out, int grid_x,
-                       const ScanTune& tune, cudaStream_t st) {
-  const int kk = scan_kk(k, true);
-  const TmaGeom g = tma_geom(d, kk, static_cast<uint32_t>(grid_x), tune);
-  // + the row masks and the group's queries
-  const size_t smem = g.smem + size_t(g.S) * g.T * 4 + 16 + size_t(kGroupQ) * d * 4 + 16;
-  if (smem > 227 * 1024) throw CudaError("group scan ring does not fit shared memory");
-  auto fn = scan_group_kernel<6>;
-  ensure_dyn_smem(reinterpret_cast<const void*>(fn), smem);
-  fn<<<grid_x, kTmaThreads, smem, st>>>(Q, nq, d, metric, kk, ft, lmask, slab, ids_all, out,
-                                        g.T, g.S);
-  after_launch();
 }
 
 void launch_window(uint64_t ns, int num_sms, cudaStream_t st) {

@@ -106,16 +106,6 @@ void launch_scan(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
                  const uint64_t* ids_all, const ScanOut& out, int grid_x,
                  bool acc_fp64, ScanImpl impl, const ScanTune& tune, cudaStream_t st);
 int scan_grid_x(uint32_t nq, int num_sms, ScanImpl impl, const ScanTune& tune);
-// List-major group scan of a micro-batch (2..4 queries, d = 768, fp64, k <=
-// 32, host-final outputs): ft describes the UNION of the queries' resident
-// probed lists (query slot 0, CTA start table for grid_x CTAs), lmask[i] the
-// queries whose probe holds union list i. Writes out.cta_s/out.cta_r
-// [q][grid_x][kk] like the per-query scan in host-final mode.
-bool group_scan_ok(uint32_t nq, uint32_t d, int k, bool acc_fp64);
-void launch_scan_group(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
-                       const FastTable& ft, const uint32_t* lmask, const float* slab,
-                       const uint64_t* ids_all, const ScanOut& out, int grid_x,
-                       const ScanTune& tune, cudaStream_t st);
 // Entries each per-CTA partial list holds for a given k (k + re-score margin).
 int scan_kk(int k, bool acc_fp64);
 // ---- batched coarse quantizer on tensor cores (coarse_tc.cu) ----

@@ -294,9 +294,9 @@ def test_batch_single_query_and_fetch_metrics(orc, laiv):
 
 
 @pytest.mark.parametrize("name,metric", [("l2", L2), ("ip", IP)])
-def test_group_scan_microbatches(orc, laiv, name, metric):
-    # micro-batches of 2-4 queries stream the union of their resident lists
-    # once (list-major group scan); results must equal the single-query path
+def test_microbatches_match_single(orc, laiv, name, metric):
+    # micro-batches of 2-4 queries (the C4 micro-batch size): the batch path
+    # must equal the single-query path under every residency and k
     cen, vecs, ids, off, qi, qo, g = planted_data()
     ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric(metric))
     dev = laiv.Device(ix, BIG)
