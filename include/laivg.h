@@ -83,6 +83,20 @@ int laivg_index_create(const float* centroids, uint32_t nc, uint32_t d,
                        const uint64_t* list_off, uint32_t flags,
                        laivg_index** out);
 void laivg_index_destroy(laivg_index* ix);
+/* ivf.hpp:98 load_index: reads a LAIX file (ivf.cpp:394-458) straight into
+ * the list-major store (list rows/ids land where the devices copy them from,
+ * read by `threads` threads, 0 = all cores) and pins it in place. Errors as
+ * the reference: LAIVG_ERUNTIME for IO/format/truncation, LAIVG_EINVAL for a
+ * non-finite component or a repeated id -- the first in file order, with the
+ * reference's message. */
+int laivg_index_load(const char* path, uint32_t threads, laivg_index** out);
+/* ivf.hpp:96 save_index: writes the LAIX bytes save_index writes for the
+ * same index (ivf.cpp:351-392). */
+int laivg_index_save(const laivg_index* ix, const char* path, uint32_t threads);
+/* Read-only views of the store (any out pointer may be NULL): vecs[N][d],
+ * ids[N], list_off[nc+1], centroids[nc][d]; valid until destroy. */
+int laivg_index_store(const laivg_index* ix, const float** vecs, const uint64_t** ids,
+                      const uint64_t** list_off, const float** centroids);
 uint32_t laivg_index_num_clusters(const laivg_index* ix);
 uint32_t laivg_index_dim(const laivg_index* ix);
 int laivg_index_metric(const laivg_index* ix);

@@ -278,6 +278,9 @@ class RefLib:
         L.ref_cache_used.restype = u64
         L.ref_cache_used.argtypes = [vp]
         L.ref_cache_contains.argtypes = [vp, u32]
+        L.ref_save_index.argtypes = [vp, C.c_char_p]
+        L.ref_load_index.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.ref_index_lists.argtypes = [vp, C.c_void_p, C.c_void_p, C.c_void_p]
         L.ref_search_many.argtypes = [vp, i32, C.c_void_p, u64, i32, i32, i32, _u64p, _f32p,
                                       C.c_void_p]
 

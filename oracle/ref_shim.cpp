@@ -408,4 +408,57 @@ int ref_search_many(void* hv, int mode, const float* Q, uint64_t nq, int L,
   return failed ? -1 : 0;
 }
 
+// save_index (ivf.cpp:351-392) of an index built by ref_index_create.
+int ref_save_index(void* hv, const char* path) {
+  return guard([&] {
+    const auto* h = static_cast<RefIndex*>(hv);
+    laiv::save_index(path, h->ix, h->db);
+    return 0;
+  });
+}
+
+// load_index (ivf.cpp:394-458): 0 and a new handle in *out, or the class of
+// the exception (1 runtime_error, 2 invalid_argument, 3 logic_error, 4 other)
+// with its message in ref_last_error().
+int ref_load_index(const char* path, void** out) {
+  *out = nullptr;
+  try {
+    auto [ix, db] = laiv::load_index(path);
+    *out = new RefIndex{std::move(ix), std::move(db)};
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const std::runtime_error& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 4;
+  }
+}
+
+// The list-major store of a loaded index: list_off[nc+1], ids[N], vecs[N*d]
+// (any pointer may be NULL to skip it).
+void ref_index_lists(void* hv, uint64_t* list_off, uint64_t* ids, float* vecs) {
+  const auto* h = static_cast<RefIndex*>(hv);
+  const uint32_t d = h->ix.dim();
+  uint64_t r = 0;
+  if (list_off) list_off[0] = 0;
+  for (uint32_t c = 0; c < h->ix.num_clusters(); ++c) {
+    for (uint64_t id : h->ix.list(c)) {
+      if (ids) ids[r] = id;
+      if (vecs) {
+        const auto row = h->db.row(*h->db.row_of(id));
+        std::memcpy(vecs + r * d, row.data(), d * sizeof(float));
+      }
+      ++r;
+    }
+    if (list_off) list_off[c + 1] = r;
+  }
+}
+
 } // extern "C"

@@ -68,6 +68,9 @@ SIGNATURES = {
     "laivg_kernel_launches": (u64, []),
     "laivg_index_create": (i32, [vp, u32, u32, i32, vp, vp, vp, u32, P(vp)]),
     "laivg_index_destroy": (None, [vp]),
+    "laivg_index_load": (i32, [C.c_char_p, u32, P(vp)]),
+    "laivg_index_save": (i32, [vp, C.c_char_p, u32]),
+    "laivg_index_store": (i32, [vp, P(vp), P(vp), P(vp), P(vp)]),
     "laivg_index_num_clusters": (u32, [vp]),
     "laivg_index_dim": (u32, [vp]),
     "laivg_index_metric": (i32, [vp]),

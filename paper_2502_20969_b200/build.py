@@ -31,7 +31,7 @@ CXX_FLAGS = ["-O3", "-std=c++20", "-fPIC", "-march=x86-64-v3", "-ffp-contract=of
              "-Wall", f"-I{ROOT}/include", "-pthread"]
 
 CU = ["kernels.cu", "coarse_tc.cu", "sched.cu", "ctx.cu"]
-CPP = ["host.cpp"]
+CPP = ["host.cpp", "laix.cpp"]
 HEADERS = ["kernels.cuh", "host.hpp", "dev_common.cuh"]
 
 

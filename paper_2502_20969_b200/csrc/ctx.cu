@@ -1552,26 +1552,10 @@ int laivg_index_create(const float* centroids, uint32_t nc, uint32_t d, int metr
       need(vecs, "vecs");
       need(ids, "ids");
     }
-    if (!(flags & LAIVG_INDEX_TRUST)) { // vectorstore.cpp:66-85
-      for (size_t i = 0; i < ix.centroids.size(); ++i) {
-        if (!std::isfinite(ix.centroids[i])) {
-          throw std::invalid_argument("non-finite component in centroid " +
-                                      std::to_string(i / d));
-        }
-      }
-      for (uint64_t i = 0; i < n * d; ++i) {
-        if (!std::isfinite(vecs[i])) {
-          throw std::invalid_argument("non-finite component in row for id " +
-                                      std::to_string(ids[i / d]));
-        }
-      }
-      std::unordered_set<uint64_t> seen;
-      seen.reserve(n);
-      for (uint64_t i = 0; i < n; ++i) {
-        if (!seen.insert(ids[i]).second) {
-          throw std::invalid_argument("duplicate id " + std::to_string(ids[i]));
-        }
-      }
+    if (!(flags & LAIVG_INDEX_TRUST)) { // vectorstore.cpp:66-85, first bad row in append order
+      ix.vecs = vecs;
+      ix.ids = ids;
+      laivg::validate_store(ix, 0);
     }
     if (flags & LAIVG_INDEX_BORROW) {
       ix.vecs = vecs;
@@ -1601,9 +1585,65 @@ int laivg_index_create(const float* centroids, uint32_t nc, uint32_t d, int metr
   });
 }
 
+namespace {
+void* laix_alloc(uint64_t bytes, void* user) {
+  const size_t b = (bytes + 4095) & ~size_t(4095);
+  void* p = std::aligned_alloc(4096, b);
+  if (!p) throw std::runtime_error("host allocation failed");
+  *static_cast<size_t*>(user) = b;
+  return p;
+}
+} // namespace
+
+int laivg_index_load(const char* path, uint32_t threads, laivg_index** out) {
+  return guard([&] {
+    need(path, "path");
+    need(out, "out");
+    *out = nullptr;
+    auto h = std::make_unique<laivg_index>();
+    size_t bytes = 0;
+    try {
+      laivg::laix_load(path, threads, h->ix, laix_alloc, &bytes);
+    } catch (...) {
+      std::free(h->ix.owned_block);
+      throw;
+    }
+    h->ix.owned_pageable = true;
+    // pin the store in place (the rows are already resident): every device
+    // copies lists from it; without a driver it stays pageable
+    if (bytes && cudaHostRegister(h->ix.owned_block, bytes, cudaHostRegisterPortable) ==
+                     cudaSuccess) {
+      h->ix.owned_registered = true;
+    } else {
+      cudaGetLastError();
+    }
+    *out = h.release();
+  });
+}
+
+int laivg_index_save(const laivg_index* ix, const char* path, uint32_t threads) {
+  return guard([&] {
+    need(ix, "index");
+    need(path, "path");
+    laivg::laix_save(path, ix->ix, threads);
+  });
+}
+
+int laivg_index_store(const laivg_index* ix, const float** vecs, const uint64_t** ids,
+                      const uint64_t** list_off, const float** centroids) {
+  return guard([&] {
+    need(ix, "index");
+    if (vecs) *vecs = ix->ix.vecs;
+    if (ids) *ids = ix->ix.ids;
+    if (list_off) *list_off = ix->ix.list_off.data();
+    if (centroids) *centroids = ix->ix.centroids.data();
+  });
+}
+
 void laivg_index_destroy(laivg_index* ix) {
   if (!ix) return;
   if (ix->ix.owned_block) {
+    if (ix->ix.owned_registered) cudaHostUnregister(ix->ix.owned_block);
     if (ix->ix.owned_pageable) std::free(ix->ix.owned_block);
     else cudaFreeHost(ix->ix.owned_block);
   }

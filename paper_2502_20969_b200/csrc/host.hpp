@@ -48,6 +48,7 @@ struct Index {
   const uint64_t* ids = nullptr;    // list_off[nc]
   void* owned_block = nullptr;      // pinned allocation when copied
   bool owned_pageable = false;      // owned_block came from aligned_alloc
+  bool owned_registered = false;    // ... and is pinned in place (cudaHostRegister)
   uint64_t member_bytes() const { return 4ull * d + 8ull; } // ivf.cpp:23
   uint64_t list_len(uint32_t c) const { return list_off[c + 1] - list_off[c]; }
   uint64_t cluster_bytes(uint32_t c) const { return list_len(c) * member_bytes(); }
@@ -75,6 +76,18 @@ class ThreadPool {
   uint64_t gen_ = 0;
   bool stop_ = false;
 };
+
+// LAIX files (laix.cpp). first_invalid_row: the first row of a list-major
+// store that EmbeddingMatrix::append would reject (vectorstore.cpp:66-85),
+// n when none; validate_store throws the reference's invalid_argument for it.
+uint64_t first_invalid_row(const float* vecs, const uint64_t* ids, uint64_t n, uint32_t d,
+                           unsigned threads, bool* dup);
+void validate_store(const Index& ix, unsigned threads);
+// load_index (ivf.cpp:394-458) / save_index (ivf.cpp:351-392) against the
+// list-major store; alloc(bytes, user) provides the block for rows + ids.
+void laix_load(const std::string& path, unsigned threads, Index& ix,
+               void* (*alloc)(uint64_t bytes, void* user), void* user);
+void laix_save(const std::string& path, const Index& ix, unsigned threads);
 
 // Cache-miss path (the slow tier of hybrid_search, tiered.cpp:169): scores
 // every member of `lists` with fp64 accumulation rounded to fp32

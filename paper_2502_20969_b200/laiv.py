@@ -13,6 +13,7 @@ RuntimeError, std::logic_error -> LogicError, CUDA failures -> CudaError.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import weakref
 import enum
 from dataclasses import dataclass, field
@@ -84,6 +85,22 @@ def default_nprobe(n_clusters: int) -> int:  # ivf.cpp:264-267
     return max(1, int(np.floor(4.0 * np.sqrt(float(n_clusters)) + 0.5)))
 
 
+def _view(addr, n, dtype):
+    """numpy view of n elements of library memory at addr (no copy)."""
+    if n == 0 or not addr:
+        return np.zeros(0, dtype)
+    buf = (C.c_char * (n * np.dtype(dtype).itemsize)).from_address(addr)
+    return np.frombuffer(buf, dtype, n)
+
+
+def load_index(path, threads: int = 0) -> "IvfIndex":   # ivf.hpp:98
+    return IvfIndex.load(path, threads)
+
+
+def save_index(path, ix: "IvfIndex", threads: int = 0) -> None:   # ivf.hpp:96
+    ix.save(path, threads)
+
+
 class IvfIndex:
     """IvfIndex + EmbeddingMatrix over a list-major store (ivf.hpp:26-50).
 
@@ -135,6 +152,38 @@ class IvfIndex:
         vecs = np.asarray(db_vecs, np.float32)[rows] if len(rows) else np.zeros((0, d), np.float32)
         return cls(centroids, vecs, db_ids[rows] if len(rows) else np.zeros(0, np.uint64),
                    np.array(off, np.uint64), metric)
+
+    @classmethod
+    def load(cls, path, threads: int = 0) -> "IvfIndex":
+        """load_index (ivf.hpp:98): a LAIX file read straight into the
+        library's pinned list-major store (laivg_index_load)."""
+        h = C.c_void_p()
+        check(lib().laivg_index_load(os.fsencode(path), threads, C.byref(h)))
+        self = cls.__new__(cls)
+        self.h = h
+        self.nc = int(lib().laivg_index_num_clusters(h))
+        self.d = int(lib().laivg_index_dim(h))
+        self.metric = Metric(lib().laivg_index_metric(h))
+        v, i, o, c = (C.c_void_p() for _ in range(4))
+        check(lib().laivg_index_store(h, C.byref(v), C.byref(i), C.byref(o), C.byref(c)))
+        self.list_off = _view(o.value, self.nc + 1, np.uint64).copy()
+        self.centroids = _view(c.value, self.nc * self.d, np.float32).reshape(self.nc, self.d).copy()
+        self._vecs = None
+        self._ids = None
+        return self
+
+    def save(self, path, threads: int = 0) -> None:
+        """save_index (ivf.hpp:96): the LAIX bytes of this index."""
+        check(lib().laivg_index_save(self.h, os.fsencode(path), threads))
+
+    def store(self):
+        """Zero-copy (vecs[N, d], ids[N]) views of the library's store; valid
+        while this index lives."""
+        v, i = C.c_void_p(), C.c_void_p()
+        check(lib().laivg_index_store(self.h, C.byref(v), C.byref(i), None, None))
+        n = int(self.list_off[-1])
+        return (_view(v.value, n * self.d, np.float32).reshape(n, self.d),
+                _view(i.value, n, np.uint64))
 
     def close(self):
         if getattr(self, "h", None):
