@@ -12,6 +12,7 @@
 #include <string>
 #include <thread>
 #include <unordered_set>
+#include <sys/mman.h>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -1587,9 +1588,12 @@ int laivg_index_create(const float* centroids, uint32_t nc, uint32_t d, int metr
 
 namespace {
 void* laix_alloc(uint64_t bytes, void* user) {
-  const size_t b = (bytes + 4095) & ~size_t(4095);
-  void* p = std::aligned_alloc(4096, b);
+  // 2 MB aligned and backed by huge pages where the kernel allows: the
+  // readers fault the block in 512x fewer times
+  const size_t b = (bytes + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
+  void* p = std::aligned_alloc(size_t(2) << 20, b);
   if (!p) throw std::runtime_error("host allocation failed");
+  madvise(p, b, MADV_HUGEPAGE);
   *static_cast<size_t*>(user) = b;
   return p;
 }
@@ -1602,6 +1606,7 @@ int laivg_index_load(const char* path, uint32_t threads, laivg_index** out) {
     *out = nullptr;
     auto h = std::make_unique<laivg_index>();
     size_t bytes = 0;
+    const auto t0 = Clock::now();
     try {
       laivg::laix_load(path, threads, h->ix, laix_alloc, &bytes);
     } catch (...) {
@@ -1609,6 +1614,7 @@ int laivg_index_load(const char* path, uint32_t threads, laivg_index** out) {
       throw;
     }
     h->ix.owned_pageable = true;
+    const auto t1 = Clock::now();
     // pin the store in place (the rows are already resident): every device
     // copies lists from it; without a driver it stays pageable
     if (bytes && cudaHostRegister(h->ix.owned_block, bytes, cudaHostRegisterPortable) ==
@@ -1616,6 +1622,11 @@ int laivg_index_load(const char* path, uint32_t threads, laivg_index** out) {
       h->ix.owned_registered = true;
     } else {
       cudaGetLastError();
+    }
+    if (std::getenv("LAIVG_TRACE")) {
+      std::fprintf(stderr, "[laivg] index_load %s: read+validate %.3f s, pin %.3f s (%.2f GB)\n",
+                   path, std::chrono::duration<double>(t1 - t0).count(),
+                   std::chrono::duration<double>(Clock::now() - t1).count(), bytes / 1e9);
     }
     *out = h.release();
   });

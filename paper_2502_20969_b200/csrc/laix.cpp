@@ -20,6 +20,9 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cerrno>
 #include <cmath>
 #include <cstddef>
@@ -195,6 +198,7 @@ void validate_store(const Index& ix, unsigned threads) {
 // and ids read into one block from alloc(bytes) (the caller pins it).
 void laix_load(const std::string& path, unsigned threads, Index& ix,
                void* (*alloc)(uint64_t bytes, void* user), void* user) {
+  const auto t_start = std::chrono::steady_clock::now();
   Fd f;
   f.fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
   if (f.fd < 0) throw std::runtime_error("cannot open: " + path);
@@ -327,8 +331,15 @@ void laix_load(const std::string& path, unsigned threads, Index& ix,
   if (std::find(ok.begin(), ok.end(), 0) != ok.end()) {
     throw std::runtime_error(path + ": read failed");
   }
+  const auto t_read = std::chrono::steady_clock::now();
   bool dup = false;
   const uint64_t bad = first_invalid_row(vecs, ids, n, d, threads, &dup);
+  if (std::getenv("LAIVG_TRACE")) {
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[laivg] laix_load: read %.3f s (%u threads), validate %.3f s\n",
+                 std::chrono::duration<double>(t_read - t_start).count(), T,
+                 std::chrono::duration<double>(now - t_read).count());
+  }
   if (bad < n) {
     throw std::invalid_argument((dup ? "duplicate id " : "non-finite component in row for id ") +
                                 std::to_string(ids[bad]));
