@@ -59,18 +59,15 @@ class Bound {
     }
     ck(laivg_index_create(ix.centroids().data().data(), nc, d, int(ix.metric()), vecs.data(),
                           ids.data(), off.data(), 0, &ix_));
-    laivg_opts o;
-    laivg_opts_default(&o);
-    o.device = device;
-    o.capacity_bytes = capacity_bytes;
-    o.max_batch = max_batch;
-    const int rc = laivg_ctx_create(ix_, &o, &ctx_);
-    if (rc != LAIVG_OK) {
-      laivg_index_destroy(ix_);
-      raise(rc);
-    }
-    d_ = d;
-    nc_ = nc;
+    open_ctx(capacity_bytes, device, max_batch);
+  }
+  // Straight from a LAIX file (what load_index reads, ivf.hpp:98), without
+  // materialising the reference's EmbeddingMatrix: the library reads the
+  // lists into its pinned store in parallel (laivg_index_load).
+  Bound(const std::string& laix_path, uint64_t capacity_bytes, int device = 0,
+        uint32_t max_batch = 0, uint32_t threads = 0) {
+    ck(laivg_index_load(laix_path.c_str(), threads, &ix_));
+    open_ctx(capacity_bytes, device, max_batch);
   }
   ~Bound() {
     laivg_ctx_destroy(ctx_);
@@ -78,6 +75,11 @@ class Bound {
   }
   Bound(const Bound&) = delete;
   Bound& operator=(const Bound&) = delete;
+
+  // save_index (ivf.hpp:96) of the bound store
+  void save(const std::string& path, uint32_t threads = 0) const {
+    ck(laivg_index_save(ix_, path.c_str(), threads));
+  }
 
   laivg_ctx* ctx() const { return ctx_; }
   uint32_t dim() const { return d_; }
@@ -96,6 +98,21 @@ class Bound {
   uint64_t free_bytes() const { return laivg_store_free_bytes(ctx_); }
 
  private:
+  void open_ctx(uint64_t capacity_bytes, int device, uint32_t max_batch) {
+    laivg_opts o;
+    laivg_opts_default(&o);
+    o.device = device;
+    o.capacity_bytes = capacity_bytes;
+    o.max_batch = max_batch;
+    const int rc = laivg_ctx_create(ix_, &o, &ctx_);
+    if (rc != LAIVG_OK) {
+      laivg_index_destroy(ix_);
+      raise(rc);
+    }
+    d_ = laivg_index_dim(ix_);
+    nc_ = laivg_index_num_clusters(ix_);
+  }
+
   laivg_index* ix_ = nullptr;
   laivg_ctx* ctx_ = nullptr;
   uint32_t d_ = 0, nc_ = 0;

@@ -14,6 +14,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <string>
 #include <random>
 
 #include "laiv_gpu_shim.hpp"
@@ -91,8 +92,38 @@ int main(int argc, char** argv) {
     int e = 0;
     batch_ok += agree(batch[size_t(t)], laiv::ivf_search(ix, db, queries.row(t), L, k), e);
   }
+  // LAIX: the reference's save_index, bound straight from the file; the
+  // library's save writes the same bytes back
+  const std::string dir = argc > 2 ? argv[2] : "/tmp";
+  const std::string f1 = dir + "/shim_demo_ref.laix", f2 = dir + "/shim_demo_gpu.laix";
+  laiv::save_index(f1, ix, db);
+  int file_ok = 0;
+  {
+    laiv::gpu::Bound fromfile(f1, uint64_t(1) << 30, /*device=*/0);
+    fromfile.save(f2);
+    for (int t = 0; t < nq; ++t) {
+      int e = 0;
+      file_ok += agree(laiv::gpu::ivf_search(fromfile, queries.row(t), L, k),
+                       laiv::ivf_search(ix, db, queries.row(t), L, k), e);
+    }
+  }
+  auto slurp = [](const std::string& p) {
+    std::FILE* f = std::fopen(p.c_str(), "rb");
+    std::string s;
+    if (!f) return s;
+    char buf[1 << 16];
+    size_t n;
+    while ((n = std::fread(buf, 1, sizeof buf, f)) > 0) s.append(buf, n);
+    std::fclose(f);
+    return s;
+  };
+  const bool same_bytes = slurp(f1) == slurp(f2) && !slurp(f1).empty();
+  std::remove(f1.c_str());
+  std::remove(f2.c_str());
   std::printf("{\"metric\": \"%s\", \"queries\": %d, \"agree\": %d, \"bit_identical_pairs\": %d, "
-              "\"probe_identical\": %d, \"batch_agree\": %d}\n",
-              metric == laiv::Metric::L2 ? "l2" : "ip", nq, ok, exact, probe_eq, batch_ok);
-  return (ok == nq && batch_ok == nq && probe_eq == nq) ? 0 : 1;
+              "\"probe_identical\": %d, \"batch_agree\": %d, \"laix_agree\": %d, "
+              "\"laix_same_bytes\": %s}\n",
+              metric == laiv::Metric::L2 ? "l2" : "ip", nq, ok, exact, probe_eq, batch_ok, file_ok,
+              same_bytes ? "true" : "false");
+  return (ok == nq && batch_ok == nq && probe_eq == nq && file_ok == nq && same_bytes) ? 0 : 1;
 }

@@ -22,3 +22,6 @@ def test_cpp_shim_against_reference(metric):
     assert r.returncode == 0, r.stdout + r.stderr
     out = json.loads(r.stdout.strip().splitlines()[-1])
     assert out["agree"] == out["queries"] == out["batch_agree"] == out["probe_identical"]
+    # LAIX: reference save_index -> laivg_index_load -> same answers, and
+    # laivg_index_save writes the reference's bytes back
+    assert out["laix_agree"] == out["queries"] and out["laix_same_bytes"]
