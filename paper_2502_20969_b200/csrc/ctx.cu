@@ -293,6 +293,28 @@ struct Ctx {
   uint32_t* h_out_cnt = nullptr;
   uint32_t* h_fcount = nullptr;
   float* h_cta_s = nullptr;      // host-final grid merge input [part_cap][kMaxK]
+  unsigned long long* h_probe = nullptr; // LAIVG_SCAN_PROBE stamps [part_cap][4]
+  void print_probe(uint32_t nq, uint32_t G) const {
+    for (uint32_t q = 0; q < nq; ++q) {
+      const unsigned long long* p = h_probe + size_t(q) * G * 4;
+      unsigned long long t0 = ~0ull, e_max = 0, f_min = ~0ull, f_max = 0, l_min = ~0ull, l_max = 0,
+                         x_max = 0;
+      for (uint32_t b = 0; b < G; ++b) t0 = std::min(t0, p[b * 4]);
+      for (uint32_t b = 0; b < G; ++b) {
+        e_max = std::max(e_max, p[b * 4] - t0);
+        f_min = std::min(f_min, p[b * 4 + 1] - t0);
+        f_max = std::max(f_max, p[b * 4 + 1] - t0);
+        l_min = std::min(l_min, p[b * 4 + 2] - t0);
+        l_max = std::max(l_max, p[b * 4 + 2] - t0);
+        x_max = std::max(x_max, p[b * 4 + 3] - t0);
+      }
+      std::fprintf(stderr,
+                   "[laivg] scan probe q%u G=%u (us from first CTA entry): entry<=%.2f "
+                   "first tile %.2f..%.2f loop end %.2f..%.2f done %.2f\n",
+                   q, G, e_max / 1e3, f_min / 1e3, f_max / 1e3, l_min / 1e3, l_max / 1e3,
+                   x_max / 1e3);
+    }
+  }
   uint64_t* h_cta_r = nullptr;
   bool host_final = false;
   uint32_t* dm_order = nullptr; // device aliases of the mapped buffers above
@@ -569,7 +591,7 @@ Ctx::~Ctx() {
     if (p) cudaFree(p);
   }
   for (void* p : {(void*)h_res_ring, (void*)h_fetch_s, (void*)h_fetch_id, (void*)h_fetch_cnt,
-                  (void*)h_cta_s, (void*)h_cta_r}) {
+                  (void*)h_cta_s, (void*)h_cta_r, (void*)h_probe}) {
     if (p) cudaFreeHost(p);
   }
   for (cudaEvent_t e : {ev_landed[0], ev_landed[1], ev_freed[0], ev_freed[1], ev_f0, ev_f1,
@@ -735,6 +757,11 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
     h_cta_r = pin_alloc_mapped<uint64_t>(size_t(part_cap) * kMaxK, &dr);
     so.cta_s = ds;
     so.cta_r = dr;
+  }
+  if (std::getenv("LAIVG_SCAN_PROBE")) {
+    unsigned long long* dp = nullptr;
+    h_probe = pin_alloc_mapped<unsigned long long>(size_t(part_cap) * 4, &dp);
+    so.probe = dp;
   }
 
   unsigned threads = o.miss_threads;
@@ -1330,6 +1357,7 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
   uint64_t vfast = 0;
   for (uint32_t c : r.fast) vfast += ix->list_len(c);
   std::vector<Scored> gpu = scan_result(0, uint32_t(G), k, vfast);
+  if (h_probe) print_probe(1, uint32_t(G));
   merge_fetch(0, nchunks, k, gpu);
   r.top = merge_topk(ix->metric, gpu, miss, k);
   r.t_2 = secs(t0, Clock::now()); // the merged result exists: timing bookkeeping follows

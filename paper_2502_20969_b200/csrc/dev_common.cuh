@@ -11,6 +11,12 @@ namespace dev {
 constexpr int kIP = 0;
 constexpr unsigned kFull = 0xffffffffu;
 
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
 // --------------------------------------------------------------------------

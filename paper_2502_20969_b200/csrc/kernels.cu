@@ -1379,6 +1379,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 
   const uint32_t q = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long* probe =
+      out.probe ? out.probe + (static_cast<uint64_t>(q) * gridDim.x + blockIdx.x) * 4 : nullptr;
+  if (probe && threadIdx.x == 0) probe[0] = globaltimer();
   const float* qv = Q + static_cast<uint64_t>(q) * d;
   for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) sq[i] = qv[i];
   if (threadIdx.x == 0) {
@@ -1465,6 +1468,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     for (uint32_t i = 0; i < ntiles; ++i) {
       const uint32_t s = i % S;
       mbar_wait(full + s, (i / S) & 1u);
+      if (probe && i == 0 && cw == 0 && lane == 0) probe[1] = globaltimer();
       const uint32_t n = mn[s];
       const float* base = stage + s * stage_floats;
       for (uint32_t j = cw; j < n; j += 2 * kConsumers) {
@@ -1516,10 +1520,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     }
   }
   __syncthreads(); // every tile consumed: the stage ring is free for merging
+  if (probe && threadIdx.x == 0) probe[2] = globaltimer();
 
   const uint64_t V = pre[ft.count[q]];
   scan_epilogue<KPL>(top, metric, k, kk, !kFp64, smem, out, sq, slab, ids_all, d, V, 1,
                      kConsumers);
+  if (probe && threadIdx.x == 0) probe[3] = globaltimer();
 }
 
 // --------------------------------------------------------------------------
@@ -1643,11 +1649,6 @@ __global__ void __launch_bounds__(kScanThreads, 2)
 // --------------------------------------------------------------------------
 // generation window
 // --------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t globaltimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 __global__ void window_kernel(uint64_t ns) {
   const uint64_t t0 = globaltimer();
   while (globaltimer() - t0 < ns) {

@@ -65,6 +65,9 @@ struct ScanOut {
   // host memory) and the host merges the grid; no device grid merge
   float* cta_s = nullptr;
   uint64_t* cta_r = nullptr;
+  // diagnostics (LAIVG_SCAN_PROBE): per CTA globaltimer stamps [nq][grid][4]
+  // = entry, first tile landed, last tile consumed, epilogue done
+  unsigned long long* probe = nullptr;
 };
 
 enum class ScanImpl : int {
