@@ -1,0 +1,78 @@
+"""The pipeline caller (pipeline.cpp:293-617) on the GPU:
+run_batch replays the reference's own synthesized traces (six pipeline
+shapes) under four configs (lookahead on/off, hotness cache, similarity
+grouping, cache-aware routing, 1-3 workers) with every retrieval, prefetch
+plan and cache decision executed by the B200 path. On the simulated clock
+the record must equal the one the unmodified reference's run_batch wrote
+(tests/golden/pipeline/, tests/golden/make_golden.py) field for field:
+result ids, fast/slow splits, coverage, transfers, modeled phase times,
+routing decisions, hotness snapshots, makespan."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from common import accept1_case
+
+pytestmark = pytest.mark.gpu
+G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "pipeline")
+SHAPES = ["HyDE", "SubQ", "Iter", "IRG", "FLARE", "SRAG"]
+
+
+def records(path):
+    out = []
+    with open(path) as f:
+        for line in f:
+            if line.strip():
+                out.append(json.loads(line))
+    return out
+
+
+@pytest.fixture(scope="module")
+def index(orc, laiv):
+    case, *_ = accept1_case(orc)
+    return laiv.IvfIndex(case.centroids, case.vecs, case.ids, case.list_off, laiv.Metric.L2)
+
+
+@pytest.mark.parametrize("cfg", ["a", "b", "c", "d"])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_run_batch_matches_reference(tmp_path, index, shape, cfg):
+    from paper_2502_20969_b200 import pipeline as P
+
+    traces = P.load_traces(os.path.join(G, f"traces_{shape}.jsonl"))
+    side = np.load(os.path.join(G, "sidecars.npz"))[shape]
+    conf = P.load_config(os.path.join(G, f"cfg_{cfg}.conf"))
+    rec = P.run_batch(traces, side, index, conf)
+    out = tmp_path / "rec.jsonl"
+    P.save_records(out, rec)
+    got, want = records(out), records(os.path.join(G, f"rec_{shape}_{cfg}.jsonl"))
+    assert rec.assertions_ok, rec.assertion_failures
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        assert g == w
+
+
+def test_measured_clock_replay(index):
+    # the same replay on measured times: copies under a window kernel, timed
+    # hybrid searches; results are clock-independent
+    from paper_2502_20969_b200 import laiv
+    from paper_2502_20969_b200 import pipeline as P
+
+    traces = P.load_traces(os.path.join(G, "traces_Iter.jsonl"))
+    side = np.load(os.path.join(G, "sidecars.npz"))["Iter"]
+    conf = P.load_config(os.path.join(G, "cfg_b.conf"))
+    sim = P.run_batch(traces, side, index, conf)
+    conf.mode = laiv.ChannelMode.Device
+    conf.time_scale = 1e-3  # 0.5 s generation stages run as 0.5 ms windows
+    meas = P.run_batch(traces, side, index, conf)
+    assert meas.assertions_ok
+    assert [[rr.result_ids for rr in r.retrievals] for r in meas.rows] == \
+        [[rr.result_ids for rr in r.retrievals] for r in sim.rows]
+    assert [r.transfer_bytes for r in meas.rows] == [r.transfer_bytes for r in sim.rows]
+    for r in meas.rows:
+        assert r.total_s > 0 and r.retrieve_s > 0
+        for t in r.transfers:
+            assert t.t_p > 0  # measured copy time
+    agg = P.aggregate(meas.rows, meas.makespan_s)
+    assert agg.traces == len(meas.rows) and agg.throughput_qps > 0

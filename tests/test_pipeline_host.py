@@ -1,0 +1,99 @@
+"""Host side of the pipeline caller (pipeline.py): trace / config / record
+file formats and the trace decomposition, against the reference's files
+(tests/golden/pipeline/) and the rules of trace.cpp / pipeline.cpp."""
+import json
+import os
+
+import pytest
+
+from paper_2502_20969_b200 import laiv
+from paper_2502_20969_b200 import pipeline as P
+
+G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "pipeline")
+
+
+@pytest.mark.parametrize("shape", ["HyDE", "SubQ", "Iter", "IRG", "FLARE", "SRAG"])
+def test_trace_files_round_trip(tmp_path, shape):
+    src = os.path.join(G, f"traces_{shape}.jsonl")
+    traces = P.load_traces(src)
+    assert len(traces) == 16
+    out = tmp_path / "t.jsonl"
+    P.save_traces(out, traces)
+    a = [json.loads(x) for x in open(src)]
+    b = [json.loads(x) for x in open(out)]
+    assert a == b
+    for t in traces:
+        walk = P.decompose_trace(t)
+        assert walk.phases, t
+        for ph in walk.phases:
+            assert ph.predictor_ref >= 0 and ph.query_refs
+
+
+def test_decompose_rules():
+    S, K = P.Stage, P.StageKind
+    t = P.QueryTrace(1, P.PipelineKind.Custom, [
+        S(K.Generate, 0, 0.0), S(K.Generate, 1, 0.4), S(K.Retrieve, 1, 0.0, 2),
+        S(K.Generate, -1, 0.3), S(K.Judge, 5, 0.2), S(K.Retrieve, 6, 0.0), S(K.Generate, -1, 0.7)])
+    w = P.decompose_trace(t)
+    assert len(w.phases) == 2
+    # phase 0: window = the Generate right before (0.4 s); predictor = the
+    # latest ref BEFORE the window stage (a Generate's ref is its output)
+    assert w.phases[0].window_s == 0.4 and w.phases[0].plain_before_s == 0.0
+    assert w.phases[0].predictor_ref == 0 and w.phases[0].query_refs == [1, 2]
+    # phase 1: a Judge window counts its own (input) ref
+    assert w.phases[1].plain_before_s == 0.3 and w.phases[1].window_s == 0.2
+    assert w.phases[1].predictor_ref == 5 and w.phases[1].query_refs == [6]
+    assert w.tail_s == 0.7
+
+
+def test_validate_traces_errors():
+    S, K = P.Stage, P.StageKind
+    with pytest.raises(RuntimeError, match="dangles past sidecar"):
+        P.validate_traces([P.QueryTrace(3, stages=[S(K.Generate, 9, 0.0, 2)])], 10)
+    with pytest.raises(RuntimeError, match="Retrieve stage has no query"):
+        P.validate_traces([P.QueryTrace(3, stages=[S(K.Generate, 0), S(K.Retrieve, -1)])], 10)
+    with pytest.raises(RuntimeError, match="no preceding stage"):
+        P.validate_traces([P.QueryTrace(3, stages=[S(K.Retrieve, 0)])], 10)
+
+
+def test_load_config_and_clamp(tmp_path, monkeypatch):
+    c = P.load_config(os.path.join(G, "cfg_d.conf"))
+    assert (c.n_probe, c.top_k, c.workers, c.micro_batch) == (16, 10, 3, 2)
+    assert c.flags.cache_on and c.flags.prefetch_sched_on and not c.flags.cache_sched_on
+    assert c.cost.parallel_slots == 4 and c.h_inc == 0.5 and c.decay == 3.0
+    w = c.validate_and_clamp()
+    assert "clamping" in w and c.prefetch_budget_bytes == 100000
+    monkeypatch.setenv("LAIV_TOP_K", "7")
+    assert P.load_config(os.path.join(G, "cfg_d.conf")).top_k == 7
+    bad = tmp_path / "bad.conf"
+    bad.write_text("n_probe = 4\nnope = 1\n")
+    with pytest.raises(RuntimeError, match="bad.conf:2: unknown config key 'nope'"):
+        P.load_config(bad)
+    bad.write_text("cache_on = maybe\n")
+    with pytest.raises(RuntimeError, match="expected a boolean"):
+        P.load_config(bad)
+    c = P.RunConfig(workers=0)
+    with pytest.raises(ValueError):
+        c.validate_and_clamp()
+
+
+def test_load_traces_errors(tmp_path):
+    p = tmp_path / "t.jsonl"
+    p.write_text('{"schema_version": 2, "trace_id": 0, "pipeline": "HyDE", "stages": []}\n')
+    with pytest.raises(RuntimeError, match="t.jsonl:1: schema_version 2 does not match"):
+        P.load_traces(p)
+    p.write_text('{"schema_version": 1, "trace_id": 0, "pipeline": "Nope", "stages": []}\n')
+    with pytest.raises(RuntimeError, match="unknown pipeline: Nope"):
+        P.load_traces(p)
+    with pytest.raises(RuntimeError, match="cannot open"):
+        P.load_traces(tmp_path / "missing.jsonl")
+
+
+def test_aggregate():
+    rows = [P.TraceRow(total_s=2.0, gen_plain_s=1.0, overlap_s=0.5, retrieve_s=0.5,
+                       retrievals=[P.RetrievalRow(hit_rate=0.5, coverage=1.0)]),
+            P.TraceRow(total_s=4.0, retrieve_s=1.0,
+                       retrievals=[P.RetrievalRow(hit_rate=1.0, coverage=0.5)])]
+    a = P.aggregate(rows, 2.0)
+    assert a.mean_latency_s == 3.0 and a.mean_hit_rate == 0.75 and a.throughput_qps == 1.0
+    assert laiv.ChannelMode.Device == 2
