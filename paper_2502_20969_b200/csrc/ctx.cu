@@ -40,11 +40,11 @@ using Clock = std::chrono::steady_clock;
 // printed to stderr (diagnostics for the latency budget; off by default).
 struct PhaseTrace {
   bool on = std::getenv("LAIVG_TRACE") != nullptr;
-  Clock::time_point t[12];
-  const char* name[12];
+  Clock::time_point t[16];
+  const char* name[16];
   int n = 0;
   void mark(const char* nm) {
-    if (!on || n >= 12) return;
+    if (!on || n >= 16) return;
     t[n] = Clock::now();
     name[n++] = nm;
   }
@@ -287,6 +287,8 @@ struct Ctx {
   }
   int part_cap = 0; // partial top-k rows available (CTAs x queries)
   float* h_Q = nullptr;
+  const float* volatile* h_qslot = nullptr; // staged-query source of the captured chain (mapped)
+  const float* const* dm_qslot = nullptr;
   uint32_t* h_order = nullptr;
   float* h_out_s = nullptr;
   uint64_t* h_out_id = nullptr;
@@ -464,37 +466,39 @@ struct Ctx {
   // mapped host memory; completion (event synchronize) orders those writes
   // before the host reads them.
   void enqueue_results(int) { rec(ev_c, comp); }
-  // Query in `src` (device or pinned host): copied into d_Q by the chain's
-  // first node, then coarse scores, ranking + residency split, scan,
-  // results; the probe goes to the host on the aux stream as soon as it
-  // exists.
+  // The chain's first node, a one-CTA kernel, copies the query into d_Q:
+  // from the pinned staging row h_Q (a fixed argument), or from whatever a
+  // mapped pointer slot holds (staged HBM rows, which change per call). Both
+  // graphs keep fixed parameters: a memcpy node costs 2-4 us more launch and
+  // re-pointing a node per call ~4 us plus a slower launch. Then coarse
+  // scores, ranking + residency split, scan, results; the probe lands in
+  // mapped host memory as soon as it exists.
   void enqueue_coarse_path(uint32_t lp, int k, int G, const float* src) {
-    CK(cudaMemcpyAsync(d_Q, src, ix->d * sizeof(float), cudaMemcpyDefault, comp));
+    if (src == h_Q) {
+      launch_fetch_query(h_Q, nullptr, d_Q, ix->d, comp);
+    } else {
+      *h_qslot = src;
+      launch_fetch_query(nullptr, dm_qslot, d_Q, ix->d, comp);
+    }
     rec(ev_a, comp);
     launch_coarse_scores(d_Q, 1, d_cen, ix->nc, ix->d, ix->metric, d_scores, comp);
-    // the ranking prefix lands directly in host memory (mapped)
     launch_select(d_scores, 1, ix->nc, ix->metric, lp, dm_order, d_run_k, d_run_v, d_res,
                   d_list_off, &ft, comp);
     rec(ev_b, comp);
     launch_scan(d_Q, 1, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl,
                 tune, comp);
-    rec(ev_s, comp);
-    enqueue_results(k);
+    rec(ev_s, comp); // also marks the results in mapped host memory complete
   }
   struct GraphEntry {
     cudaGraph_t g = nullptr;
     cudaGraphExec_t ge = nullptr;
-    cudaGraphNode_t qnode = nullptr; // the query copy, re-pointed per launch
-    const float* src = nullptr;
-    uint64_t kernels = 0;            // kernel nodes (launch accounting)
+    uint64_t kernels = 0; // kernel nodes (launch accounting)
   };
   std::map<uint64_t, GraphEntry> graph_tab;
-  void run_coarse_path(uint32_t lp, int k, int G, const float* src) {
-    cudaPointerAttributes pa{};
-    const bool dev_src = cudaPointerGetAttributes(&pa, src) == cudaSuccess &&
-                         pa.type == cudaMemoryTypeDevice;
-    cudaGetLastError();
-    const uint64_t key = (uint64_t(lp) << 33) | (uint64_t(uint32_t(k)) << 1) | (dev_src ? 1 : 0);
+  void run_coarse_path(uint32_t lp, int k, int G, const float* src, PhaseTrace* tr = nullptr) {
+    const bool staged = src != h_Q;
+    if (staged) *h_qslot = src; // read by the chain's first kernel
+    const uint64_t key = (uint64_t(lp) << 33) | (uint64_t(uint32_t(k)) << 1) | (staged ? 1 : 0);
     auto it = graph_tab.find(key);
     if (it == graph_tab.end() && use_graphs) {
       // first call for this shape runs eagerly (sets kernel attributes), then
@@ -515,28 +519,10 @@ struct Ctx {
       }
       e.kernels = launch_counter().load() - launched;
       launch_counter() = launched; // captured launches did not run
-      if (ok) { // locate the query copy node (the one writing d_Q)
-        size_t n = 0;
-        ok = cudaGraphGetNodes(e.g, nullptr, &n) == cudaSuccess;
-        std::vector<cudaGraphNode_t> nodes(n);
-        ok = ok && cudaGraphGetNodes(e.g, nodes.data(), &n) == cudaSuccess;
-        for (size_t i = 0; ok && i < n; ++i) {
-          cudaGraphNodeType t;
-          if (cudaGraphNodeGetType(nodes[i], &t) != cudaSuccess || t != cudaGraphNodeTypeMemcpy) {
-            continue;
-          }
-          cudaMemcpy3DParms mp{};
-          if (cudaGraphMemcpyNodeGetParams(nodes[i], &mp) == cudaSuccess &&
-              mp.dstPtr.ptr == static_cast<void*>(d_Q)) {
-            e.qnode = nodes[i];
-          }
-        }
-        ok = ok && e.qnode != nullptr;
-      }
       ok = ok && cudaGraphInstantiate(&e.ge, e.g, 0) == cudaSuccess;
+      ok = ok && cudaGraphUpload(e.ge, comp) == cudaSuccess;
       cudaGetLastError();
       if (ok) {
-        e.src = src;
         graph_tab[key] = e;
       } else {
         if (e.g) cudaGraphDestroy(e.g);
@@ -545,24 +531,15 @@ struct Ctx {
       return;
     }
     if (it != graph_tab.end()) {
-      GraphEntry& e = it->second;
-      if (e.src != src) {
-        if (cudaGraphExecMemcpyNodeSetParams1D(e.ge, e.qnode, d_Q, src, ix->d * sizeof(float),
-                                               cudaMemcpyDefault) != cudaSuccess) {
-          cudaGetLastError();
-          use_graphs = false;
-          enqueue_coarse_path(lp, k, G, src);
-          return;
-        }
-        e.src = src;
-      }
-      CK(cudaGraphLaunch(e.ge, comp));
-      launch_counter() += e.kernels;
+      if (tr) tr->mark("glookup");
+      CK(cudaGraphLaunch(it->second.ge, comp));
+      launch_counter() += it->second.kernels;
       return;
     }
     enqueue_coarse_path(lp, k, G, src);
   }
 };
+
 
 Ctx::~Ctx() {
   if (comp) cudaStreamSynchronize(comp);
@@ -577,7 +554,7 @@ Ctx::~Ctx() {
                   (void*)d_staged, (void*)d_approx, (void*)d_cnorm}) {
     if (p) cudaFree(p);
   }
-  for (void* p : {(void*)res_stage[0], (void*)res_stage[1], (void*)h_Q,
+  for (void* p : {(void*)res_stage[0], (void*)res_stage[1], (void*)h_Q, (void*)h_qslot,
                   (void*)h_order, (void*)h_out_s, (void*)h_out_id,
                   (void*)h_out_cnt, (void*)h_fcount}) {
     if (p) cudaFreeHost(p);
@@ -737,6 +714,11 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   }
   h_Q = pin_alloc<float>(size_t(max_batch) * d);
   h_order = pin_alloc_mapped<uint32_t>(size_t(max_batch) * std::max(nc, 1u), &dm_order);
+  {
+    const float** dslot = nullptr;
+    h_qslot = pin_alloc_mapped<const float*>(1, &dslot);
+    dm_qslot = dslot;
+  }
   h_out_s = pin_alloc_mapped<float>(size_t(max_batch) * kMaxK, &dm_out_s);
   h_out_id = pin_alloc_mapped<uint64_t>(size_t(max_batch) * kMaxK, &dm_out_id);
   h_out_cnt = pin_alloc_mapped<uint32_t>(max_batch, &dm_out_cnt);
@@ -803,47 +785,42 @@ std::vector<Scored> Ctx::scan_result(uint32_t q, uint32_t G, int k, uint64_t V) 
     }
     return g;
   }
-  // k-way merge of G sorted lists (score, then id: vectorstore.hpp:34-39);
-  // ids are looked up only to break an exact score tie and for the output
+  // Best `want` of G sorted lists (score, then id: vectorstore.hpp:34-39):
+  // one pass over the lists with a sorted buffer; a list is left at its
+  // first entry that does not beat the buffer's last (the lists are sorted),
+  // so most lists cost one read. Ids are looked up only to break an exact
+  // score tie and for the output.
   const size_t base = size_t(q) * G * kk;
-  struct Head {
-    float s;
-    uint64_t row;
-    uint32_t list, pos;
-  };
   const int metric = ix->metric;
   const uint64_t* idt = ix->ids;
-  auto worse = [&](const Head& a, const Head& b) { // a ranks after b
-    if (a.s != b.s) return metric == kMetricIP ? a.s < b.s : a.s > b.s;
-    return idt[a.row] > idt[b.row];
+  struct E {
+    float s;
+    uint64_t row;
   };
-  std::vector<Head> heap;
-  heap.reserve(G);
-  auto entry = [&](uint32_t l, uint32_t p, Head& h) {
-    const size_t o = base + size_t(l) * kk + p;
-    if (p >= uint32_t(kk) || h_cta_r[o] == ~0ull) return false;
-    h = {h_cta_s[o], h_cta_r[o], l, p};
-    return true;
+  auto before = [&](const E& a, const E& b) { // a ranks before b
+    if (a.s != b.s) return metric == kMetricIP ? a.s > b.s : a.s < b.s;
+    return idt[a.row] < idt[b.row];
   };
-  for (uint32_t l = 0; l < G; ++l) {
-    Head h;
-    if (entry(l, 0, h)) heap.push_back(h);
-  }
-  std::make_heap(heap.begin(), heap.end(), worse);
-  std::vector<Scored> out;
   const size_t want = size_t(std::min<uint64_t>(V, uint64_t(k)));
-  out.reserve(want);
-  while (out.size() < want && !heap.empty()) {
-    std::pop_heap(heap.begin(), heap.end(), worse);
-    const Head h = heap.back();
-    heap.pop_back();
-    out.push_back({h.s, idt[h.row]});
-    Head nx;
-    if (entry(h.list, h.pos + 1, nx)) {
-      heap.push_back(nx);
-      std::push_heap(heap.begin(), heap.end(), worse);
+  E best[kMaxK + 1];
+  size_t n = 0;
+  for (uint32_t l = 0; l < G && want; ++l) {
+    const float* ls = h_cta_s + base + size_t(l) * kk;
+    const uint64_t* lr = h_cta_r + base + size_t(l) * kk;
+    for (int p = 0; p < kk; ++p) {
+      const E e{ls[p], lr[p]};
+      if (e.row == ~0ull) break;
+      if (n == want && !before(e, best[n - 1])) break;
+      size_t i = n < want ? n++ : n - 1; // drop the last when full
+      while (i > 0 && before(e, best[i - 1])) {
+        best[i] = best[i - 1];
+        --i;
+      }
+      best[i] = e;
     }
   }
+  std::vector<Scored> out(n);
+  for (size_t i = 0; i < n; ++i) out[i] = {best[i].s, idt[best[i].row]};
   return out;
 }
 
@@ -1320,7 +1297,7 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
     enqueue_results(k);
   } else {
     // the query always runs from d_Q so one captured graph serves every call
-    run_coarse_path(lp, k, G, dq);
+    run_coarse_path(lp, k, G, dq, &tr);
   }
   tr.mark("launch");
 
@@ -1348,7 +1325,7 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
     r.t_c = secs(tc, Clock::now());
   }
   tr.mark("split_miss");
-  CK(cudaEventSynchronize(ev_c));
+  CK(cudaEventSynchronize(explicit_probe ? ev_c : ev_s));
   if (nchunks) CK(cudaEventSynchronize(ev_fdone));
   tr.mark("scan_wait");
   if (*h_fcount != r.fast.size()) {
@@ -1357,11 +1334,14 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
   uint64_t vfast = 0;
   for (uint32_t c : r.fast) vfast += ix->list_len(c);
   std::vector<Scored> gpu = scan_result(0, uint32_t(G), k, vfast);
+  tr.mark("scanres");
   if (h_probe) print_probe(1, uint32_t(G));
   merge_fetch(0, nchunks, k, gpu);
   r.top = merge_topk(ix->metric, gpu, miss, k);
   r.t_2 = secs(t0, Clock::now()); // the merged result exists: timing bookkeeping follows
+  tr.mark("mtopk");
   finish_fetch(nchunks, fst);
+  tr.mark("fetchfin");
   r.fetch_lists = fst.fetch_lists;
   r.peer_lists = fst.peer_lists;
   r.fetch_bytes = fst.fetch_bytes;

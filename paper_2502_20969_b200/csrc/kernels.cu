@@ -1649,6 +1649,24 @@ __global__ void __launch_bounds__(kScanThreads, 2)
 // --------------------------------------------------------------------------
 // generation window
 // --------------------------------------------------------------------------
+// First node of the captured single-query chain: copies the query into d_Q
+// from `src` (the pinned staging row: a fixed argument) or, when `slot` is
+// set, from the pointer the host left in that mapped word (a staged HBM row
+// that changes per call). Both are device-addressable under UVA; neither
+// needs the graph node re-pointed (that costs ~4 us + a slower launch).
+__global__ void __launch_bounds__(256) fetch_query_kernel(const float* src,
+                                                          const float* const* slot, float* dQ,
+                                                          uint32_t d) {
+  if (slot != nullptr) src = *reinterpret_cast<const float* const volatile*>(slot);
+  if ((d & 3u) == 0 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+    for (uint32_t i = threadIdx.x; i < d / 4; i += blockDim.x) {
+      reinterpret_cast<float4*>(dQ)[i] = reinterpret_cast<const float4*>(src)[i];
+    }
+  } else {
+    for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) dQ[i] = src[i];
+  }
+}
+
 __global__ void window_kernel(uint64_t ns) {
   const uint64_t t0 = globaltimer();
   while (globaltimer() - t0 < ns) {
@@ -1865,6 +1883,12 @@ void launch_scan(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
     else LAIVG_D(false, 0);
   }
 #undef LAIVG_D
+}
+
+void launch_fetch_query(const float* src, const float* const* slot, float* dQ, uint32_t d,
+                        cudaStream_t st) {
+  fetch_query_kernel<<<1, 256, 0, st>>>(src, slot, dQ, d);
+  after_launch();
 }
 
 void launch_window(uint64_t ns, int num_sms, cudaStream_t st) {

@@ -150,6 +150,8 @@ void launch_overlap(const uint32_t* probes, uint32_t L, const uint64_t* order,
                     const uint64_t* off, uint32_t nb, const unsigned long long* resident,
                     uint32_t nw, uint32_t words, unsigned long long* overlap, cudaStream_t st);
 // Generation-window stand-in: one CTA per SM spins on %globaltimer for ns.
+void launch_fetch_query(const float* src, const float* const* slot, float* dQ, uint32_t d,
+                        cudaStream_t st);
 void launch_window(uint64_t ns, int num_sms, cudaStream_t st);
 
 } // namespace laivg
