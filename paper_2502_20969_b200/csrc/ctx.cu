@@ -1348,12 +1348,18 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
   r.peer_bytes = fst.peer_bytes;
   r.t_fetch = fst.t_fetch;
   float ms = 0;
-  CK(cudaEventElapsedTime(&ms, ev_a, nchunks ? ev_fdone : ev_s));
-  r.t_g = ms * 1e-3;
   CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
   r.t_coarse = ms * 1e-3;
+  tr.mark("ev1");
   CK(cudaEventElapsedTime(&ms, explicit_probe ? ev_p : ev_b, ev_s));
   r.t_scan = ms * 1e-3;
+  tr.mark("ev2");
+  if (nchunks || explicit_probe) {
+    CK(cudaEventElapsedTime(&ms, ev_a, nchunks ? ev_fdone : ev_s));
+    r.t_g = ms * 1e-3;
+  } else {
+    r.t_g = r.t_coarse + r.t_scan; // one query: a -> b -> s back to back
+  }
   for (uint32_t c : r.fast) {
     r.vecs_gpu += ix->list_len(c);
     r.bytes_gpu += ix->cluster_bytes(c);
