@@ -653,3 +653,107 @@ def aggregate_by_pipeline(rows: list[TraceRow]) -> dict[str, Aggregates]:  # pip
     for r in rows:
         grouped.setdefault(pipeline_name(r.pipeline), []).append(r)
     return {k: aggregate(v, 0.0) for k, v in sorted(grouped.items())}
+
+
+def _fmt_full(v: float) -> str:                                     # pipeline.cpp:29-33
+    return "%.17g" % v
+
+
+_GETTERS = {  # key -> value text (pipeline.cpp:57-127, same order as _FIELDS)
+    "n_probe": lambda c: str(c.n_probe),
+    "top_k": lambda c: str(c.top_k),
+    "prefetch_budget_bytes": lambda c: str(c.prefetch_budget_bytes),
+    "capacity_bytes": lambda c: str(c.capacity_bytes),
+    "cache_fraction": lambda c: _fmt_full(c.cache_fraction),
+    "bandwidth_bytes_per_s": lambda c: _fmt_full(c.cost.bandwidth_bytes_per_s),
+    "t_cc": lambda c: _fmt_full(c.cost.t_cc),
+    "t_gc": lambda c: _fmt_full(c.cost.t_gc),
+    "parallel_slots": lambda c: str(c.cost.parallel_slots),
+    "workers": lambda c: str(c.workers),
+    "micro_batch": lambda c: str(c.micro_batch),
+    "mode": lambda c: {laiv.ChannelMode.SimulatedClock: "simulated",
+                       laiv.ChannelMode.Measured: "measured",
+                       laiv.ChannelMode.Device: "device"}[laiv.ChannelMode(c.mode)],
+    "lookahead_on": lambda c: "true" if c.flags.lookahead_on else "false",
+    "prefetch_sched_on": lambda c: "true" if c.flags.prefetch_sched_on else "false",
+    "cache_sched_on": lambda c: "true" if c.flags.cache_sched_on else "false",
+    "cache_on": lambda c: "true" if c.flags.cache_on else "false",
+    "h_init": lambda c: _fmt_full(c.h_init),
+    "h_inc": lambda c: _fmt_full(c.h_inc),
+    "decay": lambda c: _fmt_full(c.decay),
+    "warmup_traces": lambda c: str(c.warmup_traces),
+    "validate_exactness": lambda c: "true" if c.validate_exactness else "false",
+    "seed": lambda c: str(c.seed),
+    "time_scale": lambda c: _fmt_full(c.time_scale),
+}
+
+
+def save_config(path, cfg: RunConfig) -> None:                     # pipeline.cpp:215-226
+    try:
+        f = open(path, "w")
+    except OSError:
+        raise RuntimeError(f"cannot open for writing: {path}") from None
+    with f:
+        for key, get in _GETTERS.items():
+            f.write(f"{key} = {get(cfg)}\n")
+
+
+def load_records(path) -> RunRecord:                                # pipeline.cpp:824-901
+    try:
+        f = open(path)
+    except OSError:
+        raise RuntimeError(f"cannot open: {path}") from None
+    rec, have_meta = RunRecord(), False
+    with f:
+        for lineno, line in enumerate(f, 1):
+            line = line.rstrip("\n")
+            if not line:
+                continue
+            try:
+                j = json.loads(line)
+                t = j["type"]
+                if t == "meta":
+                    if int(j["schema_version"]) != 1:
+                        raise ValueError(f"unsupported record schema version {j['schema_version']}")
+                    rec.makespan_s = float(j["makespan_s"])
+                    rec.workers = int(j["workers"])
+                    rec.assertions_ok = bool(j["assertions_ok"])
+                    rec.assertion_failures = list(j["assertion_failures"])
+                    have_meta = True
+                elif t == "trace":
+                    row = TraceRow(int(j["trace_id"]), pipeline_from_name(j["pipeline"]),
+                                   int(j["worker"]), int(j["batch"]), float(j["total_s"]),
+                                   float(j["gen_plain_s"]), float(j["overlap_s"]),
+                                   float(j["retrieve_s"]), float(j["tail_s"]),
+                                   float(j["transfer_s"]), int(j["transfer_bytes"]))
+                    row.retrievals = [RetrievalRow(**r) for r in j["retrievals"]]
+                    row.transfers = [TransferRow(**x) for x in j["transfers"]]
+                    rec.rows.append(row)
+                elif t == "decision":
+                    rec.decisions.append(BatchDecision(int(j["batch"]), int(j["worker"]),
+                                                       int(j["overlap"])))
+                elif t == "hotness":
+                    rec.hotness.append((int(j["worker"]),
+                                        {int(c): float(np.float32(v)) for c, v in j["entries"]}))
+                else:
+                    raise ValueError(f"unknown record type '{t}'")
+            except Exception as e:  # noqa: BLE001 - the reference wraps every error
+                raise RuntimeError(f"{path}:{lineno}: {e}") from None
+    if not have_meta:
+        raise RuntimeError(f"{path}: missing meta record")
+    return rec
+
+
+def run_single(trace: QueryTrace, sidecar, worker: Worker, cfg: RunConfig,
+               failures: list[str] | None = None) -> TraceRow:      # pipeline.cpp:478-496
+    """Replays one trace against a worker's cache (and hotness table) and
+    advances them; run_batch with one worker and micro-batch 1."""
+    import copy
+
+    local = copy.deepcopy(cfg)
+    local.capacity_bytes = worker.dev.store.capacity_bytes()
+    local.validate_and_clamp()
+    sidecar = np.ascontiguousarray(sidecar, np.float32)
+    _, rows = serve_microbatch([trace], [local.prefetch_budget_bytes], sidecar, local, worker,
+                               failures)
+    return rows[0]

@@ -76,3 +76,20 @@ def test_measured_clock_replay(index):
             assert t.t_p > 0  # measured copy time
     agg = P.aggregate(meas.rows, meas.makespan_s)
     assert agg.traces == len(meas.rows) and agg.throughput_qps > 0
+
+
+def test_run_single_matches_run_batch(index):
+    # run_single == run_batch with one worker and micro-batch 1 (pipeline.hpp:184-190):
+    # replaying config a (no cache) trace by trace on one worker reproduces
+    # the reference's records row for row
+    from paper_2502_20969_b200 import pipeline as P
+
+    traces = P.load_traces(os.path.join(G, "traces_SubQ.jsonl"))
+    side = np.load(os.path.join(G, "sidecars.npz"))["SubQ"]
+    conf = P.load_config(os.path.join(G, "cfg_a.conf"))
+    want = P.load_records(os.path.join(G, "rec_SubQ_a.jsonl"))
+    w = P.Worker(index, conf)
+    for t, wr in zip(traces, want.rows):
+        row = P.run_single(t, side, w, conf)
+        row.worker, row.batch = wr.worker, wr.batch
+        assert row == wr

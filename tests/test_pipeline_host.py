@@ -97,3 +97,25 @@ def test_aggregate():
     a = P.aggregate(rows, 2.0)
     assert a.mean_latency_s == 3.0 and a.mean_hit_rate == 0.75 and a.throughput_qps == 1.0
     assert laiv.ChannelMode.Device == 2
+
+
+def test_records_and_config_round_trip(tmp_path):
+    # load_records of the reference's own record files, save_records back:
+    # the same JSON objects (pipeline.cpp:765-901)
+    for name in ("rec_HyDE_b.jsonl", "rec_SubQ_d.jsonl"):
+        src = os.path.join(G, name)
+        rec = P.load_records(src)
+        out = tmp_path / name
+        P.save_records(out, rec)
+        assert [json.loads(x) for x in open(src)] == [json.loads(x) for x in open(out)]
+    c = P.load_config(os.path.join(G, "cfg_b.conf"))
+    P.save_config(tmp_path / "c.conf", c)
+    c2 = P.load_config(tmp_path / "c.conf")
+    assert c2 == c
+    bad = tmp_path / "r.jsonl"
+    bad.write_text('{"type": "trace"}\n')
+    with pytest.raises(RuntimeError, match="r.jsonl:1"):
+        P.load_records(bad)
+    bad.write_text("")
+    with pytest.raises(RuntimeError, match="missing meta record"):
+        P.load_records(bad)
