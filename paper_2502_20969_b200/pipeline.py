@@ -757,3 +757,23 @@ def run_single(trace: QueryTrace, sidecar, worker: Worker, cfg: RunConfig,
     _, rows = serve_microbatch([trace], [local.prefetch_budget_bytes], sidecar, local, worker,
                                failures)
     return rows[0]
+
+
+def calibrate_budget(traces: list[QueryTrace], pipeline: PipelineKind | None,
+                     bandwidth_bytes_per_s: float) -> float:        # budget.cpp:159-182
+    """Prefetch budget = mean duration of the stage right before each
+    Retrieve x link bandwidth (the paper's B_link * t_LLM rule)."""
+    if bandwidth_bytes_per_s <= 0.0:
+        raise ValueError("bandwidth must be positive")
+    total, count = 0.0, 0
+    for t in traces:
+        if pipeline is not None and t.pipeline != pipeline:
+            continue
+        for i in range(1, len(t.stages)):
+            if t.stages[i].kind == StageKind.Retrieve and \
+                    t.stages[i - 1].kind != StageKind.Retrieve:
+                total += t.stages[i - 1].duration_s
+                count += 1
+    if count == 0:
+        raise RuntimeError("no pre-retrieval stage found in the calibration traces")
+    return (total / count) * bandwidth_bytes_per_s

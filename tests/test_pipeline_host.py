@@ -119,3 +119,18 @@ def test_records_and_config_round_trip(tmp_path):
     bad.write_text("")
     with pytest.raises(RuntimeError, match="missing meta record"):
         P.load_records(bad)
+
+
+def test_calibrate_budget():
+    # budget.cpp:159-182: mean duration of the stage before each Retrieve x B
+    traces = P.load_traces(os.path.join(G, "traces_Iter.jsonl"))
+    durs = [t.stages[i - 1].duration_s for t in traces for i in range(1, len(t.stages))
+            if t.stages[i].kind == P.StageKind.Retrieve
+            and t.stages[i - 1].kind != P.StageKind.Retrieve]
+    want = (sum(durs) / len(durs)) * 64e9
+    assert P.calibrate_budget(traces, None, 64e9) == want
+    assert P.calibrate_budget(traces, P.PipelineKind.Iter, 64e9) == want
+    with pytest.raises(RuntimeError, match="no pre-retrieval stage"):
+        P.calibrate_budget(traces, P.PipelineKind.HyDE, 64e9)
+    with pytest.raises(ValueError):
+        P.calibrate_budget(traces, None, 0.0)
