@@ -127,7 +127,10 @@ def test_calibrate_budget():
     durs = [t.stages[i - 1].duration_s for t in traces for i in range(1, len(t.stages))
             if t.stages[i].kind == P.StageKind.Retrieve
             and t.stages[i - 1].kind != P.StageKind.Retrieve]
-    want = (sum(durs) / len(durs)) * 64e9
+    acc = 0.0
+    for x in durs:  # sequential, as the reference adds (Python's sum() compensates)
+        acc += x
+    want = (acc / len(durs)) * 64e9
     assert P.calibrate_budget(traces, None, 64e9) == want
     assert P.calibrate_budget(traces, P.PipelineKind.Iter, 64e9) == want
     with pytest.raises(RuntimeError, match="no pre-retrieval stage"):
