@@ -1407,6 +1407,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   if (warp == 0) {
     // ---------------- producer: one lane drives the bulk copies ----------
     if (lane == 0 && ntiles) {
+      const uint64_t pol = l2_evict_first_policy();
       Cursor cur;
       cur.li = cs.li;
       cur.load(ft, tb);
@@ -1434,9 +1435,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         j = 0;
         while (true) {
           const uint32_t take = static_cast<uint32_t>(umin64(n - j, cur.len - cur.o));
-          bulk_g2s(stage + s * stage_floats + static_cast<size_t>(j) * d,
-                   slab + static_cast<uint64_t>(cur.slab + static_cast<int64_t>(cur.o)) * d,
-                   take * d * 4u, full + s);
+          bulk_g2s_hint(stage + s * stage_floats + static_cast<size_t>(j) * d,
+                        slab + static_cast<uint64_t>(cur.slab + static_cast<int64_t>(cur.o)) * d,
+                        take * d * 4u, full + s, pol);
           j += take;
           if (tile0 + j >= nvec) break;
           cur.advance(ft, tb, take);
