@@ -4,8 +4,8 @@ infrastructure: the oracle is the checker). Each trial draws an index shape
 (lists of ragged sizes incl. empty ones, odd dimensions, duplicated rows for
 exact ties), a metric, a residency, a miss mode, nprobe and k (incl. k above
 the candidate count), and checks single-query hybrid_search, the batch path
-and the scan-only search_clusters against the oracle with the §8c rule, plus
-batch == single bit for bit.
+and the scan-only search_clusters against the oracle with the §8c rule,
+batch == single bit for bit, and the prefetch planner and coverage exactly.
 
     python tools/fuzz_parity.py --trials 200 --seed 1
 """
@@ -75,6 +75,19 @@ def main():
                 sc = laiv.search_clusters(dev, Q[q], probe, k)
                 want2 = orc.search_clusters(vecs, ids, off, metric, Q[q], probe, k)
                 assert_topk_parity(metric, sc.ids, sc.scores, *want2)
+            # planner + coverage (tiered.cpp:67-84, 200-211), exact
+            member = 4 * d + 8
+            cb = sizes.astype(np.uint64) * np.uint64(member)
+            resident = dev.store.resident_mask(nc).astype(np.uint8)
+            budget = int(rng.integers(0, int(cb.sum()) + 2))
+            plan = laiv.plan_prefetch(dev, Q[0], budget)
+            order = orc.rank_clusters(cen, metric, Q[0])
+            wp, wpb, wsk = orc.plan_prefetch(order, cb, resident, budget)
+            assert list(plan.clusters) == list(wp) and plan.planned_bytes == wpb, "plan"
+            assert list(plan.skipped) == list(wsk), "plan skipped"
+            if L > 0 and nq > 1:
+                assert laiv.coverage(dev, Q[0], Q[1], L) == \
+                    orc.coverage(cen, metric, Q[0], Q[1], L), "coverage"
             del dev, ix
         except Exception as e:  # noqa: BLE001 - report and continue
             fails.append(dict(cfg, error=repr(e)[:300]))
