@@ -310,11 +310,15 @@ struct Ctx {
         l_max = std::max(l_max, p[b * 4 + 2] - t0);
         x_max = std::max(x_max, p[b * 4 + 3] - t0);
       }
+      std::vector<unsigned long long> epi(G);
+      for (uint32_t b = 0; b < G; ++b) epi[b] = p[b * 4 + 3] - p[b * 4 + 2];
+      std::sort(epi.begin(), epi.end());
       std::fprintf(stderr,
                    "[laivg] scan probe q%u G=%u (us from first CTA entry): entry<=%.2f "
-                   "first tile %.2f..%.2f loop end %.2f..%.2f done %.2f\n",
+                   "first tile %.2f..%.2f loop end %.2f..%.2f done %.2f epilogue p50 %.2f max "
+                   "%.2f\n",
                    q, G, e_max / 1e3, f_min / 1e3, f_max / 1e3, l_min / 1e3, l_max / 1e3,
-                   x_max / 1e3);
+                   x_max / 1e3, epi[G / 2] / 1e3, epi[G - 1] / 1e3);
     }
   }
   uint64_t* h_cta_r = nullptr;

@@ -1379,9 +1379,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 
   const uint32_t q = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // probe stamps stay on chip until the end: a store to mapped host memory
+  // stalls the issuing warp for microseconds
   unsigned long long* probe =
       out.probe ? out.probe + (static_cast<uint64_t>(q) * gridDim.x + blockIdx.x) * 4 : nullptr;
-  if (probe && threadIdx.x == 0) probe[0] = globaltimer();
+  __shared__ unsigned long long s_first_tile;
+  const unsigned long long t_entry = probe ? globaltimer() : 0ull;
   const float* qv = Q + static_cast<uint64_t>(q) * d;
   for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) sq[i] = qv[i];
   if (threadIdx.x == 0) {
@@ -1469,7 +1472,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     for (uint32_t i = 0; i < ntiles; ++i) {
       const uint32_t s = i % S;
       mbar_wait(full + s, (i / S) & 1u);
-      if (probe && i == 0 && cw == 0 && lane == 0) probe[1] = globaltimer();
+      if (probe && i == 0 && cw == 0 && lane == 0) s_first_tile = globaltimer();
       const uint32_t n = mn[s];
       const float* base = stage + s * stage_floats;
       for (uint32_t j = cw; j < n; j += 2 * kConsumers) {
@@ -1521,12 +1524,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     }
   }
   __syncthreads(); // every tile consumed: the stage ring is free for merging
-  if (probe && threadIdx.x == 0) probe[2] = globaltimer();
+  const unsigned long long t_loop = probe ? globaltimer() : 0ull;
 
   const uint64_t V = pre[ft.count[q]];
   scan_epilogue<KPL>(top, metric, k, kk, !kFp64, smem, out, sq, slab, ids_all, d, V, 1,
                      kConsumers);
-  if (probe && threadIdx.x == 0) probe[3] = globaltimer();
+  if (probe && threadIdx.x == 0) {
+    const unsigned long long t_done = globaltimer();
+    probe[0] = t_entry;
+    probe[1] = s_first_tile;
+    probe[2] = t_loop;
+    probe[3] = t_done;
+  }
 }
 
 // --------------------------------------------------------------------------
