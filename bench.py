@@ -115,21 +115,25 @@ def dist_env():
 # --------------------------------------------------------------------------
 # datastore
 # --------------------------------------------------------------------------
-def make_datastore(cfg, world, rank, pinned=True):
+def make_datastore(cfg, world, rank, pinned=True, gen=None):
     """Planted-cluster list-major datastore. One process: pinned allocation.
     Several ranks: rank 0 fills a /dev/shm file that every rank maps and pins
-    (one host copy shared by all GPUs)."""
-    from paper_2502_20969_b200 import laiv
+    (one host copy shared by all GPUs). `gen` draws it: the product's
+    laivg_synth_* (our arm) or oracle/libsynth.so, the same generator source
+    built alone (the reference arm, which must not load liblaivg.so)."""
+    if gen is None:
+        from paper_2502_20969_b200 import laiv as gen
+    laiv = gen
 
     nc, per, d = cfg["n_lists"], cfg["per_list"], cfg["d"]
     n = nc * per
-    key = (nc, per, d, pinned)
+    key = (nc, per, d, pinned, getattr(gen, "__name__", ""))
     if world == 1 and key in _DATASTORES:  # sweeps reuse one datastore
         return _DATASTORES[key]
     cen = laiv.synth_centroids(SEED, nc, d)
     t0 = time.time()
     if world == 1:
-        vecs = laiv.pinned_empty((n, d), np.float32) if pinned else np.empty((n, d), np.float32)
+        vecs = gen.pinned_empty((n, d), np.float32) if pinned else np.empty((n, d), np.float32)
         ids = np.empty(n, np.uint64)
         laiv.synth_lists(SEED, cen, per, SPREAD, vecs=vecs, ids=ids)
     else:
@@ -300,12 +304,13 @@ def run_reference(args, cfg):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0  # the reference arm is one host process on rank 0
-    from paper_2502_20969_b200 import laiv
+    # workload from oracle/libsynth.so: the product library is never loaded here
+    from oracle import synth
 
-    cen, vecs, ids, off = make_datastore(cfg, 1, 0, pinned=False)
+    cen, vecs, ids, off = make_datastore(cfg, 1, 0, pinned=False, gen=synth)
     metric = 0 if args.metric == "ip" else 1
     sigma = args.sigma or cfg.get("sigma", 0.008)  # the same queries as our arm
-    qi, qo, _ = laiv.synth_queries(QSEED, vecs, 4096, sigma)
+    qi, qo, _ = synth.synth_queries(QSEED, vecs, 4096, sigma)
     ri = reference_index(cen, vecs, ids, off, metric)
     threads = os.cpu_count() or 1
     per_step = threads
@@ -413,7 +418,8 @@ def run_ours(args, cfg):
         a[1] = qo_c[qidx].ctypes.data
         t = time.perf_counter()
         check(e_fn(*a))
-        return time.perf_counter() - t, e_ids[: e_cnt.value].copy()
+        return (time.perf_counter() - t, e_ids[: e_cnt.value].copy(), e_sc[: e_cnt.value].copy(),
+                e_tm.h2d_bytes, e_tm.d2h_bytes)
 
     def step(j, rec):
         qidx = mine[j]
@@ -422,17 +428,26 @@ def run_ours(args, cfg):
         plan = laiv.plan_prefetch(dev, qi[qidx], budget)
         rp = laiv.execute_prefetch(dev, plan, chan, args.window)
         t1 = time.perf_counter()
-        got_ids, got_sc, nfast, tm = dev.hybrid_search_staged(j, L, k)  # value path
-        t_e2e, e_got = e2e_call(qidx)                                      # e2e path
+        # the value path (query staged in HBM) and the e2e path (host buffers
+        # through the C ABI) alternate which runs first, so neither always
+        # sees the other's warm L2 / centroids
+        if j % 2 == 0:
+            got_ids, got_sc, nfast, tm = dev.hybrid_search_staged(j, L, k)
+            t_e2e, e_got, _, e_h2d, e_d2h = e2e_call(qidx)
+        else:
+            t_e2e, e_got, _, e_h2d, e_d2h = e2e_call(qidx)
+            got_ids, got_sc, nfast, tm = dev.hybrid_search_staged(j, L, k)
         if rec is not None:
-            nvec = sum(cfg["per_list"] for _ in plan.clusters)
             rec.append(dict(
                 exposed=rp.overshoot_s, t_p=rp.t_p, window=rp.window_s, h2d_gbps=rp.h2d_gbps,
                 lat_value=rp.overshoot_s + tm.t_2, lat_e2e=rp.overshoot_s + t_e2e,
                 t_scan=tm.t_scan, t_coarse=tm.t_coarse, t_g=tm.t_g, t_c=tm.t_c,
                 bytes=tm.scanned_bytes, hit=nfast / L, plan_s=t1 - t0,
-                h2d_bytes=2 * 4 * cfg["d"] + nvec * 4 * cfg["d"] + cfg["n_lists"] * 8,
-                d2h_bytes=cfg["n_lists"] * 4 + L * 4 + k * 12 + 8,
+                # inside the e2e call's timed region (counted by the library)
+                h2d_bytes=e_h2d, d2h_bytes=e_d2h,
+                # the lookahead copies run during the window; only the part
+                # past its end (`exposed`) is in the retrieval latency
+                prefetch_bytes=rp.bytes // member * 4 * cfg["d"],
                 same=bool(np.array_equal(got_ids, e_got))))
 
     for j in range(args.warmup):
@@ -490,7 +505,16 @@ def run_ours(args, cfg):
         "e2e": {"value": n_total / sum_e, "unit": "queries/s",
                 "p50_latency_ms": float(np.median(lat_e) * 1e3),
                 "h2d_bytes_per_step": int(np.mean([r["h2d_bytes"] for r in rec])),
-                "d2h_bytes_per_step": int(np.mean([r["d2h_bytes"] for r in rec]))},
+                "d2h_bytes_per_step": int(np.mean([r["d2h_bytes"] for r in rec])),
+                "bytes_note": "host-link bytes inside the timed e2e call, counted by the "
+                              "library (laivg_hybrid_timing.h2d_bytes/d2h_bytes): query row, "
+                              "residency table, runtime-fetched missed lists; probe + result "
+                              "lists read back",
+                "prefetch_h2d_bytes_per_step": int(np.mean([r["prefetch_bytes"] for r in rec])),
+                "prefetch_note": "lookahead copies during the generation window (outside the "
+                                 "call); only the exposed part past the window end is in the "
+                                 "latency",
+                "order": "value and e2e calls alternate which runs first each step"},
         "value_e2e_results_identical": all(r["same"] for r in rec),
         "gpu_launches": int(launches),
         "clocks": clk,
@@ -501,11 +525,12 @@ def run_ours(args, cfg):
         sample = args.cpu_sample
         # the timed queries first, then more of the same generator
         cb = cpu_baseline(ri, qo[args.warmup:args.warmup + sample], L, k, threads, sample)
-        # parity of the timed queries with the reference on the same inputs
-        npar = min(sample, args.steps)
+        # parity with the reference on the same inputs: every query of the
+        # CPU sample (the timed ones first), through the C-ABI e2e call
+        npar = sample
         eq = 0
         for j in range(npar):
-            got_ids, got_sc, _, _ = dev.hybrid_search_staged(args.warmup + j, L, k)
+            _, got_ids, got_sc, _, _ = e2e_call(args.warmup + j)
             eq += bool(np.array_equal(got_ids, cb["ids"][j]) and
                        np.array_equal(got_sc, cb["scores"][j]))
         line["cpu_baseline"] = {"value": cb["qps"], "unit": "queries/s", "cores": threads,

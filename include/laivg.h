@@ -284,6 +284,12 @@ typedef struct {
   uint32_t peer_lists;      /* missed lists copied from a peer GPU's cache */
   uint32_t reserved0;
   uint64_t peer_bytes;
+  /* bytes this call moved across the host link, counted from the copies it
+     issued: h2d = query rows (host-buffer entry points) + the residency
+     table when it changed + runtime-fetched lists; d2h = probes and partial
+     / final result lists read back (mapped or copied) */
+  uint64_t h2d_bytes;
+  uint64_t d2h_bytes;
 } laivg_hybrid_timing;
 
 /* hybrid_search for one query. fast_out / slow_out (nullable, L entries)

@@ -31,8 +31,8 @@ CXX_FLAGS = ["-O3", "-std=c++20", "-fPIC", "-march=x86-64-v3", "-ffp-contract=of
              "-Wall", f"-I{ROOT}/include", "-pthread"]
 
 CU = ["kernels.cu", "coarse_tc.cu", "sched.cu", "ctx.cu"]
-CPP = ["host.cpp", "laix.cpp"]
-HEADERS = ["kernels.cuh", "host.hpp", "dev_common.cuh"]
+CPP = ["host.cpp", "laix.cpp", "synth.cpp"]
+HEADERS = ["kernels.cuh", "host.hpp", "dev_common.cuh", "synth.hpp"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:

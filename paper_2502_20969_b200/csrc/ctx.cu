@@ -246,6 +246,17 @@ struct Ctx {
   // The scan's result for query q: the device-merged top-k, or (host-final
   // mode) the k-way merge of the G CTA lists with ids looked up here.
   std::vector<Scored> scan_result(uint32_t q, uint32_t G, int k, uint64_t V) const;
+  // Host-link bytes of the scan results of nq queries (G CTAs each): the
+  // per-CTA lists (host-final mode) or the device-merged top-k, read from
+  // mapped host memory; and of the fetch chunks' result lists.
+  uint64_t result_bytes(uint32_t nq, uint32_t G, int k) const {
+    const uint64_t e = sizeof(float) + sizeof(uint64_t);
+    return host_final ? uint64_t(nq) * G * scan_kk(k, acc_fp64) * e
+                      : uint64_t(nq) * (k * e + sizeof(uint32_t));
+  }
+  uint64_t fetch_result_bytes(size_t nchunks, uint32_t nq, int k) const {
+    return uint64_t(nchunks) * nq * (k * (sizeof(float) + sizeof(uint64_t)) + sizeof(uint32_t));
+  }
 
   // GPU schedulers (sched.cu): grown on demand, freed with the context
   struct SchedBufs {
@@ -343,8 +354,9 @@ struct Ctx {
   void init(const Index* index, const laivg_opts& o);
 
   // ---- residency -----------------------------------------------------------
-  void commit_res(cudaStream_t st) {
-    if (!res_dirty) return;
+  // Uploads the residency table if it changed; returns the bytes copied.
+  uint64_t commit_res(cudaStream_t st) {
+    if (!res_dirty) return 0;
     const int s = res_slot;
     res_slot ^= 1;
     CK(cudaEventSynchronize(res_ev[s]));
@@ -353,6 +365,7 @@ struct Ctx {
                        cudaMemcpyHostToDevice, st));
     CK(cudaEventRecord(res_ev[s], st));
     res_dirty = false;
+    return h_res.size() * sizeof(int64_t);
   }
   // Copy-stream work issued after this point is ordered after all compute
   // work issued so far (scans may still read slab regions being reused).
@@ -421,6 +434,7 @@ struct Ctx {
     uint32_t fetch_lists = 0, peer_lists = 0;
     uint64_t fetch_bytes = 0, peer_bytes = 0;
     double t_fetch = 0;
+    uint64_t h2d_bytes = 0, d2h_bytes = 0; // host-link bytes of this call
   };
   // One query: dq on device, hq on host (miss path). With `explicit_probe`
   // the probe is those clusters (search_clusters), otherwise the coarse
@@ -439,6 +453,7 @@ struct Ctx {
     uint32_t fetch_lists = 0, cpu_lists = 0, peer_lists = 0;
     uint64_t fetch_bytes = 0, cpu_query_bytes = 0, peer_bytes = 0;
     double t_fetch = 0; // copy-stream time of the fetch copies
+    uint64_t h2d_bytes = 0, d2h_bytes = 0; // host-link bytes of this call
   };
   BatchResult search_batch(const float* dQ, const float* hQ, uint32_t nq, int L, int k);
   // The GPU side of the miss path, shared by both searches: peer-resident
@@ -1159,7 +1174,7 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
     return r;
   }
   CK(cudaStreamWaitEvent(comp, ev_copy_tail, 0));
-  commit_res(comp);
+  r.h2d_bytes += commit_res(comp);
   const int G = std::max(1, std::min(scan_grid_x(nq, sms, scan_impl, tune), part_cap / int(nq)));
   ft.grid = static_cast<uint32_t>(G);
   rec(ev_a, comp);
@@ -1243,6 +1258,9 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
   r.fetch_bytes = fst.fetch_bytes;
   r.peer_bytes = fst.peer_bytes;
   r.t_fetch = fst.t_fetch;
+  r.h2d_bytes += fst.fetch_bytes;
+  r.d2h_bytes += uint64_t(nq) * lp * sizeof(uint32_t) + uint64_t(nq) * sizeof(uint32_t) +
+                 result_bytes(nq, uint32_t(G), k) + fetch_result_bytes(nchunks, nq, k);
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, ev_a, nchunks ? ev_fdone : ev_s));
   r.t_g = ms * 1e-3;
@@ -1281,7 +1299,7 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
   // Retrieval is ordered after every prefetch copy issued so far, then sees
   // the residency table of the host store state.
   CK(cudaStreamWaitEvent(comp, ev_copy_tail, 0));
-  commit_res(comp);
+  r.h2d_bytes += commit_res(comp);
   tr.mark("commit");
   const int G = std::min(scan_grid_x(1, sms, scan_impl, tune), part_cap);
   ft.grid = static_cast<uint32_t>(G); // the partition step lays out G scan CTAs
@@ -1351,6 +1369,9 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
   r.fetch_bytes = fst.fetch_bytes;
   r.peer_bytes = fst.peer_bytes;
   r.t_fetch = fst.t_fetch;
+  r.h2d_bytes += fst.fetch_bytes + (explicit_probe ? uint64_t(lp) * sizeof(uint32_t) : 0);
+  r.d2h_bytes += uint64_t(lp) * sizeof(uint32_t) + sizeof(uint32_t) +
+                 result_bytes(1, uint32_t(G), k) + fetch_result_bytes(nchunks, 1, k);
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
   r.t_coarse = ms * 1e-3;
@@ -1442,6 +1463,8 @@ void fill_timing(laivg_hybrid_timing* t, const Ctx::Result& r,
   t->t_fetch = r.t_fetch;
   t->peer_lists = r.peer_lists;
   t->peer_bytes = r.peer_bytes;
+  t->h2d_bytes = r.h2d_bytes;
+  t->d2h_bytes = r.d2h_bytes;
   if (cost) { // tiered.cpp:190-196
     const double miss = double(r.slow.size());
     t->model_t_c = std::ceil(miss / cost->parallel_slots) * cost->t_cc;
@@ -1487,6 +1510,8 @@ void fill_batch_timing(laivg_hybrid_timing* t, const Ctx::BatchResult& r,
   t->t_fetch = r.t_fetch;
   t->peer_lists = r.peer_lists;
   t->peer_bytes = r.peer_bytes;
+  t->h2d_bytes = r.h2d_bytes;
+  t->d2h_bytes = r.d2h_bytes;
   if (cost) { // tiered.cpp:190-196 summed over the batch
     double miss = 0, hit = 0;
     for (size_t q = 0; q < r.nfast.size(); ++q) {
@@ -2112,6 +2137,7 @@ int laivg_hybrid_search(laivg_ctx* ctx, const float* q_out, int L, int k,
     Ctx& c = ctx->c;
     stage_query(c, q_out);
     auto r = c.search(c.h_Q, q_out, L, k, nullptr);
+    r.h2d_bytes += uint64_t(c.ix->d) * sizeof(float); // the query row
     write_top(r.top, k, ids_out, scores_out, count_out);
     if (fast_out) std::copy(r.fast.begin(), r.fast.end(), fast_out);
     if (slow_out) std::copy(r.slow.begin(), r.slow.end(), slow_out);
@@ -2194,6 +2220,7 @@ int laivg_hybrid_search_batch(laivg_ctx* ctx, const float* Q, uint32_t nq, int L
     if (nq > c.max_batch) throw std::invalid_argument("batch exceeds the context's max_batch");
     stage_batch(c, Q, nq);
     auto r = c.search_batch(c.d_Q, Q, nq, L, k);
+    r.h2d_bytes += uint64_t(nq) * c.ix->d * sizeof(float); // the query rows
     for (uint32_t i = 0; i < nq; ++i) {
       write_top(r.top[i], k, ids_out + size_t(i) * k, scores_out + size_t(i) * k,
                 count_out ? count_out + i : nullptr);

@@ -561,6 +561,8 @@ class HybridTiming:                                               # tiered.hpp:8
     t_fetch: float = 0.0
     peer_lists: int = 0        # misses copied from a peer GPU's cache (NVLink)
     peer_bytes: int = 0
+    h2d_bytes: int = 0         # host-link bytes the call moved (counted by the library)
+    d2h_bytes: int = 0
 
 
 @dataclass
@@ -575,7 +577,8 @@ def _timing(t: HybridTimingC) -> HybridTiming:
     return HybridTiming(t.t_g, t.t_c, t.t_2, t.model_t_g, t.model_t_c, t.model_t_2,
                         t.t_coarse, t.t_scan, int(t.scanned_vectors), int(t.scanned_bytes),
                         int(t.fetched_lists), int(t.cpu_lists), int(t.fetched_bytes), t.t_fetch,
-                        int(t.peer_lists), int(t.peer_bytes))
+                        int(t.peer_lists), int(t.peer_bytes), int(t.h2d_bytes),
+                        int(t.d2h_bytes))
 
 
 def plan_prefetch(dev: Device, q_in, budget_bytes: int) -> PrefetchPlan:  # tiered.hpp:100-101
