@@ -101,6 +101,8 @@ uint32_t laivg_index_num_clusters(const laivg_index* ix);
 uint32_t laivg_index_dim(const laivg_index* ix);
 int laivg_index_metric(const laivg_index* ix);
 uint64_t laivg_index_total_vectors(const laivg_index* ix);
+/* |list c| (ivf.hpp:38 IvfIndex::list(c).size()) */
+uint64_t laivg_index_list_len(const laivg_index* ix, uint32_t c);
 /* ivf.hpp:40 IvfIndex::cluster_bytes */
 uint64_t laivg_index_cluster_bytes(const laivg_index* ix, uint32_t c);
 /* ivf.hpp:41 IvfIndex::total_payload_bytes */
@@ -160,7 +162,8 @@ int laivg_coarse_probe(laivg_ctx* ctx, const float* Q, uint32_t nq, int L,
  * Results: ids_out[nq*k], scores_out[nq*k], count_out[nq] (= min(k,
  * candidates)), best-first. Resident clusters are scanned on the GPU, the rest
  * by the host miss path; the merged result equals the monolithic search
- * whatever the residency (tiered.hpp:120-124). */
+ * whatever the residency (tiered.hpp:120-124). Any k >= 1: k <= 256 runs the
+ * register top-k scans, larger k a radix sort of every candidate. */
 /* search_clusters (ivf.hpp:85-87) for one query over an explicit cluster
  * list. */
 int laivg_search_clusters(laivg_ctx* ctx, const float* q,
@@ -172,7 +175,28 @@ int laivg_ivf_search(laivg_ctx* ctx, const float* Q, uint32_t nq, int L,
                      int k, uint64_t* ids_out, float* scores_out,
                      uint32_t* count_out);
 
-/* ---- tiered store = the GPU cluster cache (tiered.hpp:22-56) ------------- */
+/* score_clusters (ivf.hpp:75-81, ivf.cpp:301-324): every member of
+ * clusters[0..n) scored against q without ranking or truncation, in the
+ * reference's order (clusters in the given order, duplicates included; each
+ * list in its member order). Resident lists are scored on the GPU, the rest
+ * by the host. cap = entries ids_out / scores_out hold (the sum of the lists'
+ * lengths is needed: laivg_index_list_len); *count_out gets that sum.
+ * LAIVG_EINVAL for an unknown cluster id or too small a buffer. */
+int laivg_score_clusters(laivg_ctx* ctx, const float* q, const uint32_t* clusters, uint32_t n,
+                         uint64_t cap, uint64_t* ids_out, float* scores_out,
+                         uint64_t* count_out);
+/* exact_search (vectorstore.hpp:94-98, vectorstore.cpp:117-139) over the
+ * index's datastore for nq queries and any k >= 1: the best k of every row
+ * (the union of the lists), ties by ascending id. */
+int laivg_exact_search(laivg_ctx* ctx, const float* Q, uint32_t nq, int k, uint64_t* ids_out,
+                       float* scores_out, uint32_t* count_out);
+/* pairwise_l2 (vectorstore.hpp:100-102, vectorstore.cpp:141-153): out[i*nb+j]
+ * = f32(sqrt(l2_sq_d(a_i, b_j))) with the reference's serial fp64
+ * accumulation (bit-identical), computed on the context's GPU. */
+int laivg_pairwise_l2(laivg_ctx* ctx, const float* a, uint64_t na, const float* b, uint64_t nb,
+                      uint32_t d, float* out);
+
+/* ---- tiered store = the GPU cluster cache (tiered.hpp:22-56) ------------- *//* ---- tiered store = the GPU cluster cache (tiered.hpp:22-56) ------------- */
 uint64_t laivg_store_capacity_bytes(const laivg_ctx* ctx);
 uint64_t laivg_store_used_bytes(const laivg_ctx* ctx);
 uint64_t laivg_store_free_bytes(const laivg_ctx* ctx);

@@ -250,6 +250,9 @@ class RefLib:
         L.ref_search_clusters.argtypes = [vp, _f32p, _u32p, u32, i32, _u64p, _f32p]
         L.ref_ivf_search.argtypes = [vp, _f32p, i32, i32, _u64p, _f32p]
         L.ref_exact_search.argtypes = [vp, _f32p, i32, _u64p, _f32p]
+        L.ref_score_clusters.restype = C.c_int64
+        L.ref_score_clusters.argtypes = [vp, _f32p, _u32p, u32, u64, _u64p, _f32p]
+        L.ref_pairwise_l2.argtypes = [_f32p, u64, _f32p, u64, u32, _f32p]
         L.ref_hybrid_search.argtypes = [vp, _u8p, _f32p, i32, i32, _u64p, _f32p, _u32p,
                                         C.POINTER(u32), _u32p, C.POINTER(u32),
                                         C.POINTER(C.c_double)]
@@ -295,6 +298,13 @@ class RefLib:
         if rc < 0:
             raise RuntimeError(self.err())
         return rc
+
+    def pairwise_l2(self, a, b):
+        A, B = _c(a, np.float32), _c(b, np.float32)
+        out = np.empty(A.shape[0] * B.shape[0], np.float32)
+        self.check(self.L.ref_pairwise_l2(A.reshape(-1), A.shape[0], B.reshape(-1), B.shape[0],
+                                          A.shape[1], out))
+        return out
 
     def rng_gaussians(self, seed, n):
         out = np.empty(n, np.float64)
@@ -385,6 +395,16 @@ class RefIndex:
         osc = np.empty(max(k, 1), np.float32)
         n = self.lib.check(self.lib.L.ref_ivf_search(self.h, _c(q, np.float32), int(L),
                                                      int(k), oid, osc))
+        return oid[:n].copy(), osc[:n].copy()
+
+    def score_clusters(self, q, clusters):
+        cl = _c(clusters, np.uint32)
+        cap = int(sum(int(self._off[c + 1] - self._off[c]) for c in cl if c < self.nc))
+        oid = np.empty(max(cap, 1), np.uint64)
+        osc = np.empty(max(cap, 1), np.float32)
+        n = self.lib.L.ref_score_clusters(self.h, _c(q, np.float32), cl, cl.size, cap, oid, osc)
+        if n < 0:
+            raise ValueError(self.lib.err())
         return oid[:n].copy(), osc[:n].copy()
 
     def exact_search(self, q, k):

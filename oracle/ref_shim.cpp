@@ -167,6 +167,40 @@ int ref_exact_search(void* hv, const float* q, int k, uint64_t* ids,
   });
 }
 
+// score_clusters: the raw candidate list (returns its length; -1 on a throw).
+int64_t ref_score_clusters(void* hv, const float* q, const uint32_t* clusters, uint32_t n,
+                           uint64_t cap, uint64_t* ids, float* scores) {
+  auto* h = static_cast<RefIndex*>(hv);
+  try {
+    auto v = laiv::score_clusters(h->ix, h->db, {q, h->ix.dim()}, {clusters, n});
+    if (v.size() > cap) {
+      g_err = "capacity";
+      return -1;
+    }
+    for (size_t i = 0; i < v.size(); ++i) {
+      ids[i] = v[i].id;
+      scores[i] = v[i].score;
+    }
+    return static_cast<int64_t>(v.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// pairwise_l2 over two row-major matrices (ids 0..n-1).
+int ref_pairwise_l2(const float* a, uint64_t na, const float* b, uint64_t nb, uint32_t d,
+                    float* out) {
+  return guard([&] {
+    laiv::EmbeddingMatrix A(d), B(d);
+    for (uint64_t i = 0; i < na; ++i) A.append(i, {a + i * d, d});
+    for (uint64_t i = 0; i < nb; ++i) B.append(i, {b + i * d, d});
+    auto v = laiv::pairwise_l2(A, B);
+    std::memcpy(out, v.data(), v.size() * sizeof(float));
+    return 0;
+  });
+}
+
 // hybrid_search with a store holding exactly the clusters marked resident.
 int ref_hybrid_search(void* hv, const uint8_t* resident, const float* q, int L,
                       int k, uint64_t* ids, float* scores, uint32_t* fast,

@@ -78,6 +78,10 @@ SIGNATURES = {
     "laivg_index_total_vectors": (u64, [vp]),
     "laivg_index_cluster_bytes": (u64, [vp, u32]),
     "laivg_index_total_payload_bytes": (u64, [vp]),
+    "laivg_index_list_len": (u64, [vp, u32]),
+    "laivg_score_clusters": (i32, [vp, vp, vp, u32, u64, vp, vp, P(u64)]),
+    "laivg_exact_search": (i32, [vp, vp, u32, i32, vp, vp, vp]),
+    "laivg_pairwise_l2": (i32, [vp, vp, u64, vp, u64, u32, vp]),
     "laivg_opts_default": (None, [P(Opts)]),
     "laivg_ctx_create": (i32, [vp, P(Opts), P(vp)]),
     "laivg_ctx_destroy": (None, [vp]),

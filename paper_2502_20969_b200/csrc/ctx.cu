@@ -224,19 +224,20 @@ struct Ctx {
   int64_t* h_res_ring = nullptr; // pinned [kMaxFetchChunks][nc] staging
   FastTable fft{};
   ScanOut fso{};
-  float* h_fetch_s = nullptr;    // pinned [kMaxFetchChunks][max_batch][kMaxK]
+  float* h_fetch_s = nullptr;    // pinned [chunk][fetch_nq][k] chunk results
   uint64_t* h_fetch_id = nullptr;
-  uint32_t* h_fetch_cnt = nullptr;
-  int fetch_k = 0;               // k the chunk result buffers are sized for
-  void fetch_results_for(int k) {
-    if (k <= fetch_k) return;
+  uint32_t* h_fetch_cnt = nullptr; // [chunk][max_batch]
+  size_t fetch_cap = 0;          // entries h_fetch_s / h_fetch_id hold
+  uint32_t fetch_nq = 0;         // queries of the call the chunk results belong to
+  void fetch_results_for(size_t entries) {
+    if (entries <= fetch_cap) return;
     if (h_fetch_s) cudaFreeHost(h_fetch_s);
     if (h_fetch_id) cudaFreeHost(h_fetch_id);
     h_fetch_s = nullptr;
     h_fetch_id = nullptr;
-    h_fetch_s = pin_alloc<float>(size_t(kMaxFetchChunks) * max_batch * k);
-    h_fetch_id = pin_alloc<uint64_t>(size_t(kMaxFetchChunks) * max_batch * k);
-    fetch_k = k;
+    fetch_cap = std::max(entries, fetch_cap + fetch_cap / 2);
+    h_fetch_s = pin_alloc<float>(fetch_cap);
+    h_fetch_id = pin_alloc<uint64_t>(fetch_cap);
   }
   cudaEvent_t ev_landed[2] = {nullptr, nullptr}, ev_freed[2] = {nullptr, nullptr};
   cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr, ev_fdone = nullptr;
@@ -251,6 +252,7 @@ struct Ctx {
   // mapped host memory; and of the fetch chunks' result lists.
   uint64_t result_bytes(uint32_t nq, uint32_t G, int k) const {
     const uint64_t e = sizeof(float) + sizeof(uint64_t);
+    if (k > kMaxK) return uint64_t(nq) * (k * e + sizeof(uint32_t));
     return host_final ? uint64_t(nq) * G * scan_kk(k, acc_fp64) * e
                       : uint64_t(nq) * (k * e + sizeof(uint32_t));
   }
@@ -295,6 +297,59 @@ struct Ctx {
     sb.n = std::max(sb.n, n);
     sb.L = std::max(sb.L, L);
     sb.nw = std::max(sb.nw, nw);
+  }
+  // ---- size-unbounded paths (wide.cu) ----
+  // k > kMaxK: every fast-list member of a query becomes one 64-bit key
+  // (score key, datastore-id rank); a radix sort orders them exactly as the
+  // reference's partial_sort (ivf.cpp:336-341). Also score_clusters' raw list.
+  uint32_t* d_rank_of_row = nullptr; // built on first use
+  uint32_t* d_row_of_rank = nullptr;
+  uint64_t* d_wkeys = nullptr;
+  uint64_t* d_wkeys_alt = nullptr;
+  uint64_t wcap = 0;
+  void* d_wtmp = nullptr;
+  size_t wtmp_bytes = 0;
+  float* d_wout_s = nullptr; // [max_batch][wk] device top-k of the wide scan
+  uint64_t* d_wout_id = nullptr;
+  uint32_t* d_wout_cnt = nullptr;
+  float* h_wout_s = nullptr; // pinned copies the host merges from
+  uint64_t* h_wout_id = nullptr;
+  uint32_t* h_wout_cnt = nullptr;
+  int wk = 0;
+  float* d_wraw_s = nullptr; // score_clusters raw candidates
+  uint64_t* d_wraw_id = nullptr;
+  float* h_wraw_s = nullptr;
+  uint64_t* h_wraw_id = nullptr;
+  uint64_t wraw_cap = 0;
+  // nc > kMaxSortNc: ranking by a multi-CTA radix sort per query
+  RankScratch rs{};
+  bool large_nc() const { return ix->nc > kMaxSortNc; }
+  void wide_reserve(uint64_t V, int k);
+  void wide_raw_reserve(uint64_t V);
+  // Top-k of nq queries over their fast lists (table f over `slab`, V[q]
+  // members each) for any k: results to d_wout_* [q * k], fcount_out[q]
+  // (nullable) gets the partition's fast-list count.
+  void scan_wide(const float* dQ, uint32_t nq, const FastTable& f, const float* slab,
+                 const std::vector<uint64_t>& V, int k, uint32_t* fcount_out, cudaStream_t st);
+  // score_clusters (ivf.cpp:301-324): the raw candidate list of one query
+  // over `cl` in order; resident lists scored on the GPU, the rest by the
+  // host at the same time. Returns the candidate count.
+  uint64_t score_clusters(const float* hq, const uint32_t* cl, uint32_t n, uint64_t cap,
+                          float* s_out, uint64_t* id_out);
+  // d_wout_* of nq queries -> the pinned h_wout_* scan_result reads.
+  void wide_results(uint32_t nq, int k, cudaStream_t st);
+  // First n_out entries of each query's coarse ranking into `order` (device),
+  // with the residency split into ft when `part`.
+  void select_order(const double* scores, uint32_t nq, uint32_t n_out, uint32_t* order, bool part,
+                    cudaStream_t st, bool scan_sorted) {
+    if (!large_nc()) {
+      launch_select(scores, nq, ix->nc, ix->metric, n_out, order, d_run_k, d_run_v,
+                    part ? d_res : nullptr, part ? d_list_off : nullptr, part ? &ft : nullptr, st,
+                    scan_sorted);
+      return;
+    }
+    launch_rank_large(scores, nq, ix->nc, ix->metric, n_out, order, rs, st);
+    if (part) launch_partition(order, nq, n_out, d_res, d_list_off, ft, st);
   }
   int part_cap = 0; // partial top-k rows available (CTAs x queries)
   float* h_Q = nullptr;
@@ -501,8 +556,14 @@ struct Ctx {
     }
     rec(ev_a, comp);
     launch_coarse_scores(d_Q, 1, d_cen, ix->nc, ix->d, ix->metric, d_scores, comp);
-    launch_select(d_scores, 1, ix->nc, ix->metric, lp, dm_order, d_run_k, d_run_v, d_res,
-                  d_list_off, &ft, comp);
+    if (large_nc()) {
+      select_order(d_scores, 1, lp, d_order, /*part=*/true, comp, false);
+      CK(cudaMemcpyAsync(h_order, d_order, size_t(lp) * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                         comp));
+    } else {
+      launch_select(d_scores, 1, ix->nc, ix->metric, lp, dm_order, d_run_k, d_run_v, d_res,
+                    d_list_off, &ft, comp);
+    }
     rec(ev_b, comp);
     launch_scan(d_Q, 1, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl,
                 tune, comp);
@@ -598,6 +659,16 @@ Ctx::~Ctx() {
                   (void*)sb.probes, (void*)sb.resident, (void*)sb.overlap}) {
     if (p) cudaFree(p);
   }
+  for (void* p : {(void*)d_rank_of_row, (void*)d_row_of_rank, (void*)d_wkeys, (void*)d_wkeys_alt,
+                  (void*)d_wtmp, (void*)d_wout_s, (void*)d_wout_id, (void*)d_wout_cnt,
+                  (void*)d_wraw_s, (void*)d_wraw_id, (void*)rs.keys, (void*)rs.keys_alt,
+                  (void*)rs.vals, (void*)rs.vals_alt, rs.tmp}) {
+    if (p) cudaFree(p);
+  }
+  for (void* p : {(void*)h_wout_s, (void*)h_wout_id, (void*)h_wout_cnt, (void*)h_wraw_s,
+                  (void*)h_wraw_id}) {
+    if (p) cudaFreeHost(p);
+  }
   for (auto& p : peers) {
     if (p.ipc) cudaIpcCloseMemHandle(p.ipc);
   }
@@ -640,10 +711,6 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   tune.stages = o.tma_stages;
   tune.ctas_per_sm = o.ctas_per_sm;
   if (o.ctas_per_sm > 6) throw std::invalid_argument("ctas_per_sm must be <= 6");
-  if (ix->nc > kMaxSortNc) {
-    throw std::invalid_argument("device coarse ranking supports up to " +
-                                std::to_string(kMaxSortNc) + " clusters");
-  }
   CK(cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
@@ -707,8 +774,18 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   }
   d_scores = dev_alloc<double>(size_t(max_batch) * nc);
   d_order = dev_alloc<uint32_t>(size_t(max_batch) * std::max(nc, 1u));
-  d_run_k = dev_alloc<uint64_t>(select_scratch_entries(max_batch, nc));
-  d_run_v = dev_alloc<uint32_t>(select_scratch_entries(max_batch, nc));
+  if (!large_nc()) {
+    d_run_k = dev_alloc<uint64_t>(select_scratch_entries(max_batch, nc));
+    d_run_v = dev_alloc<uint32_t>(select_scratch_entries(max_batch, nc));
+  } else {
+    const size_t n = size_t(max_batch) * nc;
+    rs.keys = dev_alloc<uint64_t>(n);
+    rs.keys_alt = dev_alloc<uint64_t>(n);
+    rs.vals = dev_alloc<uint32_t>(n);
+    rs.vals_alt = dev_alloc<uint32_t>(n);
+    rs.tmp_bytes = rank_large_temp_bytes(nc);
+    rs.tmp = dev_alloc<unsigned char>(rs.tmp_bytes);
+  }
   const int per_sm = std::max<int>(2, int(tune.ctas_per_sm));
   part_cap = std::max<int>(per_sm * sms, int(max_batch)) + per_sm * sms;
   alloc_scan_set(ft, so, /*device_outputs=*/false);
@@ -795,7 +872,22 @@ void Ctx::alloc_scan_set(FastTable& f, ScanOut& o, bool device_outputs) {
   }
 }
 
+void Ctx::wide_results(uint32_t nq, int k, cudaStream_t st) {
+  CK(cudaMemcpyAsync(h_wout_s, d_wout_s, size_t(nq) * k * sizeof(float), cudaMemcpyDeviceToHost,
+                     st));
+  CK(cudaMemcpyAsync(h_wout_id, d_wout_id, size_t(nq) * k * sizeof(uint64_t),
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h_wout_cnt, d_wout_cnt, nq * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+}
+
 std::vector<Scored> Ctx::scan_result(uint32_t q, uint32_t G, int k, uint64_t V) const {
+  if (k > kMaxK) { // wide path (wide_results copied them)
+    std::vector<Scored> g(h_wout_cnt[q]);
+    for (uint32_t i = 0; i < h_wout_cnt[q]; ++i) {
+      g[i] = {h_wout_s[size_t(q) * k + i], h_wout_id[size_t(q) * k + i]};
+    }
+    return g;
+  }
   const int kk = scan_kk(k, acc_fp64);
   if (!host_final) {
     std::vector<Scored> g(h_out_cnt[q]);
@@ -841,6 +933,125 @@ std::vector<Scored> Ctx::scan_result(uint32_t q, uint32_t G, int k, uint64_t V) 
   std::vector<Scored> out(n);
   for (size_t i = 0; i < n; ++i) out[i] = {best[i].s, idt[best[i].row]};
   return out;
+}
+
+void Ctx::wide_reserve(uint64_t V, int k) {
+  if (!d_rank_of_row) {
+    const uint64_t n = ix->total();
+    d_rank_of_row = dev_alloc<uint32_t>(n);
+    d_row_of_rank = dev_alloc<uint32_t>(n);
+    build_id_rank(d_ids, n, d_rank_of_row, d_row_of_rank, comp);
+  }
+  if (V > wcap) {
+    for (void* p : {(void*)d_wkeys, (void*)d_wkeys_alt, d_wtmp}) {
+      if (p) cudaFree(p);
+    }
+    // one allocation serves later calls: grow by 1.5x
+    wcap = std::max<uint64_t>(V, wcap + wcap / 2);
+    d_wkeys = dev_alloc<uint64_t>(wcap);
+    d_wkeys_alt = dev_alloc<uint64_t>(wcap);
+    wtmp_bytes = wide_sort_temp_bytes(wcap);
+    d_wtmp = dev_alloc<unsigned char>(wtmp_bytes);
+  }
+  if (k > wk) {
+    for (void* p : {(void*)d_wout_s, (void*)d_wout_id, (void*)d_wout_cnt}) {
+      if (p) cudaFree(p);
+    }
+    for (void* p : {(void*)h_wout_s, (void*)h_wout_id, (void*)h_wout_cnt}) {
+      if (p) cudaFreeHost(p);
+    }
+    wk = k;
+    d_wout_s = dev_alloc<float>(size_t(max_batch) * wk);
+    d_wout_id = dev_alloc<uint64_t>(size_t(max_batch) * wk);
+    d_wout_cnt = dev_alloc<uint32_t>(max_batch);
+    h_wout_s = pin_alloc<float>(size_t(max_batch) * wk);
+    h_wout_id = pin_alloc<uint64_t>(size_t(max_batch) * wk);
+    h_wout_cnt = pin_alloc<uint32_t>(max_batch);
+  }
+}
+
+void Ctx::wide_raw_reserve(uint64_t V) {
+  if (V <= wraw_cap) return;
+  for (void* p : {(void*)d_wraw_s, (void*)d_wraw_id}) {
+    if (p) cudaFree(p);
+  }
+  for (void* p : {(void*)h_wraw_s, (void*)h_wraw_id}) {
+    if (p) cudaFreeHost(p);
+  }
+  wraw_cap = std::max<uint64_t>(V, wraw_cap + wraw_cap / 2);
+  d_wraw_s = dev_alloc<float>(wraw_cap);
+  d_wraw_id = dev_alloc<uint64_t>(wraw_cap);
+  h_wraw_s = pin_alloc<float>(wraw_cap);
+  h_wraw_id = pin_alloc<uint64_t>(wraw_cap);
+}
+
+void Ctx::scan_wide(const float* dQ, uint32_t nq, const FastTable& f, const float* slab,
+                    const std::vector<uint64_t>& V, int k, uint32_t* fcount_out, cudaStream_t st) {
+  uint64_t vmax = 0;
+  for (uint32_t q = 0; q < nq; ++q) vmax = std::max(vmax, V[q]);
+  wide_reserve(vmax, k);
+  for (uint32_t q = 0; q < nq; ++q) {
+    launch_score_all(dQ + size_t(q) * ix->d, q, ix->d, ix->metric, f, slab, d_rank_of_row, d_ids,
+                     V[q], d_wkeys, nullptr, nullptr, sms, st);
+    launch_wide_topk(d_wkeys, d_wkeys_alt, V[q], k, ix->metric, d_wtmp, wtmp_bytes,
+                     d_row_of_rank, d_ids, d_wout_s + size_t(q) * k, d_wout_id + size_t(q) * k,
+                     d_wout_cnt + q, f.count, fcount_out ? fcount_out + q : nullptr, q, st);
+  }
+}
+
+uint64_t Ctx::score_clusters(const float* hq, const uint32_t* cl, uint32_t n, uint64_t cap,
+                             float* s_out, uint64_t* id_out) {
+  std::vector<uint64_t> base(size_t(n) + 1, 0);
+  for (uint32_t i = 0; i < n; ++i) {
+    if (cl[i] >= ix->nc) throw std::invalid_argument("unknown cluster id " + std::to_string(cl[i]));
+    base[i + 1] = base[i] + ix->list_len(cl[i]);
+  }
+  const uint64_t total = base[n];
+  if (total > cap) {
+    throw std::invalid_argument("score_clusters: " + std::to_string(total) +
+                                " candidates exceed the output capacity " + std::to_string(cap));
+  }
+  if (n == 0 || total == 0) return total;
+  if (n > max_probe) {
+    throw std::invalid_argument("score_clusters over " + std::to_string(n) +
+                                " clusters exceeds the context's max_probe " +
+                                std::to_string(max_probe));
+  }
+  CK(cudaStreamWaitEvent(comp, ev_copy_tail, 0));
+  commit_res(comp);
+  std::memcpy(h_Q, hq, ix->d * sizeof(float));
+  CK(cudaMemcpyAsync(d_Q, h_Q, ix->d * sizeof(float), cudaMemcpyHostToDevice, comp));
+  std::memcpy(h_order, cl, n * sizeof(uint32_t));
+  CK(cudaMemcpyAsync(d_order, h_order, n * sizeof(uint32_t), cudaMemcpyHostToDevice, comp));
+  ft.grid = 1;
+  launch_partition(d_order, 1, n, d_res, d_list_off, ft, comp);
+  uint64_t vf = 0;
+  std::vector<std::pair<uint32_t, uint64_t>> host_items;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (h_res[cl[i]] >= 0) vf += ix->list_len(cl[i]);
+    else host_items.emplace_back(cl[i], base[i]);
+  }
+  if (vf) {
+    wide_raw_reserve(vf);
+    launch_score_all(d_Q, 0, ix->d, ix->metric, ft, d_slab, nullptr, d_ids, vf, nullptr, d_wraw_s,
+                     d_wraw_id, sms, comp);
+    CK(cudaMemcpyAsync(h_wraw_s, d_wraw_s, vf * sizeof(float), cudaMemcpyDeviceToHost, comp));
+    CK(cudaMemcpyAsync(h_wraw_id, d_wraw_id, vf * sizeof(uint64_t), cudaMemcpyDeviceToHost, comp));
+  }
+  CK(cudaEventRecord(ev_c, comp));
+  if (!host_items.empty()) score_lists(*ix, hq, host_items, s_out, id_out, *pool);
+  CK(cudaEventSynchronize(ev_c));
+  // the GPU's list is the resident entries in probe order: place each at
+  // its position in the full candidate list
+  uint64_t g = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (h_res[cl[i]] < 0) continue;
+    const uint64_t len = ix->list_len(cl[i]);
+    std::memcpy(s_out + base[i], h_wraw_s + g, len * sizeof(float));
+    std::memcpy(id_out + base[i], h_wraw_id + g, len * sizeof(uint64_t));
+    g += len;
+  }
+  return total;
 }
 
 void Ctx::compact() {
@@ -955,9 +1166,8 @@ void Ctx::coarse(const float* dQ, uint32_t nq, uint32_t n_out, cudaStream_t st, 
     return;
   }
   launch_coarse_scores(dQ, nq, d_cen, ix->nc, ix->d, ix->metric, d_scores, st);
-  launch_select(d_scores, nq, ix->nc, ix->metric, n_out, d_order, d_run_k, d_run_v,
-                part ? d_res : nullptr, part ? d_list_off : nullptr, f, st,
-                /*scan_sorted=*/part && nq > 1);
+  (void)f;
+  select_order(d_scores, nq, n_out, d_order, part, st, /*scan_sorted=*/part && nq > 1);
 }
 
 size_t Ctx::issue_fetch(std::vector<std::vector<uint32_t>>& slow, bool& any_slow,
@@ -1067,7 +1277,9 @@ size_t Ctx::issue_fetch(std::vector<std::vector<uint32_t>>& slow, bool& any_slow
     }
   }
   if (!chunks.empty()) {
-    fetch_results_for(k);
+    fetch_results_for(chunks.size() * nq * size_t(k));
+    fetch_nq = nq;
+    const bool wide = k > kMaxK;
     CK(cudaEventRecord(ev_f0, copy));
     std::vector<void*> dsts, srcs;
     std::vector<size_t> sizes;
@@ -1112,15 +1324,32 @@ size_t Ctx::issue_fetch(std::vector<std::vector<uint32_t>>& slow, bool& any_slow
       CK(cudaStreamWaitEvent(comp, ev_landed[slot], 0));
       fft.grid = static_cast<uint32_t>(G);
       launch_partition(probe_dev, nq, lp, d_res_ring[slot], d_list_off, fft, comp);
-      launch_scan(dQ, nq, d, ix->metric, k, fft, ring, d_ids, fso, G, acc_fp64, scan_impl, tune,
-                  comp);
+      const float* rs_s = fso.out_s;
+      const uint64_t* rs_id = fso.out_id;
+      const uint32_t* rs_cnt = fso.out_count;
+      if (wide) { // members per query in this chunk, from the host copy of the probe
+        std::vector<uint64_t> V(nq, 0);
+        for (uint32_t q = 0; q < nq; ++q) {
+          for (uint32_t i = 0; i < lp; ++i) {
+            const uint32_t c = h_order[size_t(q) * lp + i];
+            if (hres[c] >= 0) V[q] += ix->list_len(c);
+          }
+        }
+        scan_wide(dQ, nq, fft, ring, V, k, nullptr, comp);
+        rs_s = d_wout_s;
+        rs_id = d_wout_id;
+        rs_cnt = d_wout_cnt;
+      } else {
+        launch_scan(dQ, nq, d, ix->metric, k, fft, ring, d_ids, fso, G, acc_fp64, scan_impl, tune,
+                    comp);
+      }
       CK(cudaEventRecord(ev_freed[slot], comp));
-      const size_t o = j * max_batch;
-      CK(cudaMemcpyAsync(h_fetch_s + o * k, fso.out_s, size_t(nq) * k * sizeof(float),
+      const size_t o = j * nq;
+      CK(cudaMemcpyAsync(h_fetch_s + o * k, rs_s, size_t(nq) * k * sizeof(float),
                          cudaMemcpyDeviceToHost, comp));
-      CK(cudaMemcpyAsync(h_fetch_id + o * k, fso.out_id, size_t(nq) * k * sizeof(uint64_t),
+      CK(cudaMemcpyAsync(h_fetch_id + o * k, rs_id, size_t(nq) * k * sizeof(uint64_t),
                          cudaMemcpyDeviceToHost, comp));
-      CK(cudaMemcpyAsync(h_fetch_cnt + o, fso.out_count, nq * sizeof(uint32_t),
+      CK(cudaMemcpyAsync(h_fetch_cnt + j * max_batch, rs_cnt, nq * sizeof(uint32_t),
                          cudaMemcpyDeviceToHost, comp));
     }
     rec(ev_fdone, comp);
@@ -1130,9 +1359,10 @@ size_t Ctx::issue_fetch(std::vector<std::vector<uint32_t>>& slow, bool& any_slow
 
 void Ctx::merge_fetch(uint32_t q, size_t nchunks, int k, std::vector<Scored>& gpu) const {
   for (size_t j = 0; j < nchunks; ++j) {
-    const size_t o = j * max_batch + q;
-    std::vector<Scored> f(h_fetch_cnt[o]);
-    for (uint32_t i = 0; i < h_fetch_cnt[o]; ++i) {
+    const uint32_t n = h_fetch_cnt[j * max_batch + q];
+    const size_t o = j * fetch_nq + q;
+    std::vector<Scored> f(n);
+    for (uint32_t i = 0; i < n; ++i) {
       f[i] = {h_fetch_s[o * k + i], h_fetch_id[o * k + i]};
     }
     gpu = merge_topk(ix->metric, gpu, f, k);
@@ -1152,10 +1382,7 @@ void Ctx::finish_fetch(size_t nchunks, FetchStats& st) {
 Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq, int L,
                                    int k) {
   if (k < 1) throw std::invalid_argument("k must be >= 1");
-  if (k > kMaxK) {
-    throw std::invalid_argument("k = " + std::to_string(k) +
-                                " exceeds the device top-k limit " + std::to_string(kMaxK));
-  }
+  const bool wide = k > kMaxK; // top-k by radix sort of every candidate (wide.cu)
   if (nq > max_batch) throw std::invalid_argument("batch exceeds the context's max_batch");
   const auto t0 = Clock::now();
   BatchResult r;
@@ -1186,10 +1413,12 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
                      cudaMemcpyDeviceToHost, aux));
   rec(ev_probe, aux);
   rec(ev_p, comp);
-  launch_scan(dQ, nq, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl, tune,
-              comp);
-  rec(ev_s, comp);
-  rec(ev_c, comp); // results are in mapped host memory
+  if (!wide) {
+    launch_scan(dQ, nq, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl, tune,
+                comp);
+    rec(ev_s, comp);
+    rec(ev_c, comp); // results are in mapped host memory
+  }
 
   // host: split every probe by residency and scan the misses list-major
   CK(cudaEventSynchronize(ev_probe));
@@ -1210,6 +1439,12 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
       }
     }
     r.nslow[q] = uint32_t(slow[q].size());
+  }
+  if (wide) { // the candidate sort is sized by the probe split
+    scan_wide(dQ, nq, ft, d_slab, vfast, k, dm_fcount, comp);
+    wide_results(nq, k, comp);
+    rec(ev_s, comp);
+    rec(ev_c, comp);
   }
   const uint32_t d = ix->d;
   FetchStats fst;
@@ -1274,10 +1509,7 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
 Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
                         const std::vector<uint32_t>* explicit_probe) {
   if (k < 1) throw std::invalid_argument("k must be >= 1");
-  if (k > kMaxK) {
-    throw std::invalid_argument("k = " + std::to_string(k) +
-                                " exceeds the device top-k limit " + std::to_string(kMaxK));
-  }
+  const bool wide = k > kMaxK; // top-k by radix sort of every candidate (wide.cu)
   const auto t0 = Clock::now();
   PhaseTrace tr;
   tr.mark("start");
@@ -1313,8 +1545,36 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
     CK(cudaEventRecord(ev_b, comp));
     launch_partition(d_order, 1, lp, d_res, d_list_off, ft, comp);
     CK(cudaEventRecord(ev_p, comp));
-    launch_scan(d_Q, 1, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl,
-                tune, comp);
+    if (wide) {
+      std::vector<uint64_t> V(1, 0);
+      for (uint32_t c : *explicit_probe) {
+        if (h_res[c] >= 0) V[0] += ix->list_len(c);
+      }
+      scan_wide(d_Q, 1, ft, d_slab, V, k, dm_fcount, comp);
+      wide_results(1, k, comp);
+    } else {
+      launch_scan(d_Q, 1, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl,
+                  tune, comp);
+    }
+    CK(cudaEventRecord(ev_s, comp));
+    enqueue_results(k);
+  } else if (wide) {
+    // eager chain: query -> coarse -> ranking + residency split; the host
+    // needs the probe to size the candidate sort
+    CK(cudaMemcpyAsync(d_Q, dq, ix->d * sizeof(float), cudaMemcpyDefault, comp));
+    CK(cudaEventRecord(ev_a, comp));
+    coarse(d_Q, 1, lp, comp, /*part=*/true);
+    if (lp) {
+      CK(cudaMemcpyAsync(h_order, d_order, lp * sizeof(uint32_t), cudaMemcpyDeviceToHost, comp));
+    }
+    CK(cudaEventRecord(ev_b, comp));
+    CK(cudaEventSynchronize(ev_b));
+    std::vector<uint64_t> V(1, 0);
+    for (uint32_t i = 0; i < lp; ++i) {
+      if (h_res[h_order[i]] >= 0) V[0] += ix->list_len(h_order[i]);
+    }
+    scan_wide(d_Q, 1, ft, d_slab, V, k, dm_fcount, comp);
+    wide_results(1, k, comp);
     CK(cudaEventRecord(ev_s, comp));
     enqueue_results(k);
   } else {
@@ -1338,7 +1598,8 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
   FetchStats fst;
   const size_t nchunks =
       (miss_fetch && any_host)
-          ? issue_fetch(host, any_host, d_Q, 1, lp, explicit_probe ? d_order : dm_order, k, G, fst)
+          ? issue_fetch(host, any_host, d_Q, 1, lp, (explicit_probe || wide) ? d_order : dm_order,
+                        k, G, fst)
           : 0;
   std::vector<Scored> miss;
   if (any_host) {
@@ -1347,7 +1608,7 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
     r.t_c = secs(tc, Clock::now());
   }
   tr.mark("split_miss");
-  CK(cudaEventSynchronize(explicit_probe ? ev_c : ev_s));
+  CK(cudaEventSynchronize((explicit_probe || wide) ? ev_c : ev_s));
   if (nchunks) CK(cudaEventSynchronize(ev_fdone));
   tr.mark("scan_wait");
   if (*h_fcount != r.fast.size()) {
@@ -1379,7 +1640,7 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
   CK(cudaEventElapsedTime(&ms, explicit_probe ? ev_p : ev_b, ev_s));
   r.t_scan = ms * 1e-3;
   tr.mark("ev2");
-  if (nchunks || explicit_probe) {
+  if (nchunks || explicit_probe || wide) {
     CK(cudaEventElapsedTime(&ms, ev_a, nchunks ? ev_fdone : ev_s));
     r.t_g = ms * 1e-3;
   } else {
@@ -1710,6 +1971,9 @@ uint64_t laivg_index_total_vectors(const laivg_index* ix) { return ix ? ix->ix.t
 uint64_t laivg_index_cluster_bytes(const laivg_index* ix, uint32_t c) {
   return (ix && c < ix->ix.nc) ? ix->ix.cluster_bytes(c) : 0;
 }
+uint64_t laivg_index_list_len(const laivg_index* ix, uint32_t c) {
+  return (ix && c < ix->ix.nc) ? ix->ix.list_len(c) : 0;
+}
 uint64_t laivg_index_total_payload_bytes(const laivg_index* ix) {
   return ix ? ix->ix.total() * ix->ix.member_bytes() : 0;
 }
@@ -1839,6 +2103,82 @@ int laivg_ivf_search(laivg_ctx* ctx, const float* Q, uint32_t nq, int L, int k, 
                   count_out ? count_out + q0 + i : nullptr);
       }
     }
+  });
+}
+
+int laivg_score_clusters(laivg_ctx* ctx, const float* q, const uint32_t* clusters, uint32_t n,
+                         uint64_t cap, uint64_t* ids_out, float* scores_out, uint64_t* count_out) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    need(q, "query");
+    if (n) need(clusters, "clusters");
+    if (cap) {
+      need(ids_out, "ids_out");
+      need(scores_out, "scores_out");
+    }
+    const uint64_t m = ctx->c.score_clusters(q, clusters, n, cap, scores_out, ids_out);
+    if (count_out) *count_out = m;
+  });
+}
+
+int laivg_exact_search(laivg_ctx* ctx, const float* Q, uint32_t nq, int k, uint64_t* ids_out,
+                       float* scores_out, uint32_t* count_out) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    if (k < 1) throw std::invalid_argument("k must be >= 1");
+    if (nq) {
+      need(Q, "queries");
+      need(ids_out, "ids_out");
+      need(scores_out, "scores_out");
+    }
+    Ctx& c = ctx->c;
+    // every row of the datastore is a member of exactly one list: the union
+    // of all lists is the datastore (test_ivf.cpp:213-222)
+    std::vector<uint32_t> all(c.ix->nc);
+    for (uint32_t i = 0; i < c.ix->nc; ++i) all[i] = i;
+    for (uint32_t i = 0; i < nq; ++i) {
+      const float* q = Q + size_t(i) * c.ix->d;
+      stage_query(c, q);
+      auto r = c.search(c.h_Q, q, 0, k, &all);
+      write_top(r.top, k, ids_out + size_t(i) * k, scores_out + size_t(i) * k,
+                count_out ? count_out + i : nullptr);
+    }
+  });
+}
+
+int laivg_pairwise_l2(laivg_ctx* ctx, const float* a, uint64_t na, const float* b, uint64_t nb,
+                      uint32_t d, float* out) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    if (na == 0 || nb == 0) return;
+    need(a, "a");
+    need(b, "b");
+    need(out, "out");
+    if (d == 0) throw std::invalid_argument("pairwise_l2: dimension must be > 0");
+    Ctx& c = ctx->c;
+    // rows of a in chunks so one chunk's output stays <= 256 MB of HBM
+    const uint64_t rows = std::max<uint64_t>(1, std::min<uint64_t>(na, (64ull << 20) / nb));
+    float* dA = laivg::dev_alloc<float>(rows * d);
+    float* dB = laivg::dev_alloc<float>(nb * d);
+    float* dO = laivg::dev_alloc<float>(rows * nb);
+    try {
+      CK(cudaMemcpyAsync(dB, b, nb * d * sizeof(float), cudaMemcpyDefault, c.comp));
+      for (uint64_t r0 = 0; r0 < na; r0 += rows) {
+        const uint64_t m = std::min(rows, na - r0);
+        CK(cudaMemcpyAsync(dA, a + r0 * d, m * d * sizeof(float), cudaMemcpyDefault, c.comp));
+        laivg::launch_pairwise_l2(dA, m, dB, nb, d, dO, nullptr, c.comp);
+        CK(cudaMemcpyAsync(out + r0 * nb, dO, m * nb * sizeof(float), cudaMemcpyDefault, c.comp));
+      }
+      CK(cudaStreamSynchronize(c.comp));
+    } catch (...) {
+      cudaFree(dA);
+      cudaFree(dB);
+      cudaFree(dO);
+      throw;
+    }
+    cudaFree(dA);
+    cudaFree(dB);
+    cudaFree(dO);
   });
 }
 

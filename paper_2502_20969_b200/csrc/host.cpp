@@ -304,6 +304,48 @@ std::vector<Scored> miss_scan(const Index& ix, const float* q,
   return std::move(all.e);
 }
 
+void score_lists(const Index& ix, const float* q,
+                 const std::vector<std::pair<uint32_t, uint64_t>>& items, float* s_out,
+                 uint64_t* id_out, ThreadPool& pool) {
+  struct Task {
+    uint64_t r0, r1, out;
+  };
+  std::vector<Task> tasks;
+  for (const auto& [c, o] : items) {
+    const uint64_t b = ix.list_off[c], e = ix.list_off[c + 1];
+    for (uint64_t r = b; r < e; r += kMissChunk) {
+      tasks.push_back({r, std::min(r + kMissChunk, e), o + (r - b)});
+    }
+  }
+  const uint32_t d = ix.d;
+  const bool fast = host_has_avx2();
+  std::vector<double> qd(fast ? d : 0);
+  for (uint32_t j = 0; fast && j < d; ++j) qd[j] = q[j];
+  const double* qp = qd.data();
+  pool.parallel_for(tasks.size(), [&](size_t t, unsigned) {
+    uint64_t o = tasks[t].out;
+    for (uint64_t r = tasks[t].r0; r < tasks[t].r1; ++r, ++o) {
+      const float* x = ix.vecs + r * d;
+      float sc;
+      if (fast) { // the miss scan's arithmetic
+        double v;
+        if (ix.metric == kMetricIP) {
+          score_row_blocked<true>(x, &qp, 1, d, &v);
+          sc = static_cast<float>(v);
+        } else {
+          score_row_blocked<false>(x, &qp, 1, d, &v);
+          sc = static_cast<float>(std::sqrt(v));
+        }
+      } else {
+        sc = ix.metric == kMetricIP ? static_cast<float>(dot_f64(q, x, d))
+                                    : static_cast<float>(std::sqrt(l2sq_f64(q, x, d)));
+      }
+      s_out[o] = sc;
+      id_out[o] = ix.ids[r];
+    }
+  });
+}
+
 std::vector<std::vector<Scored>> miss_scan_batch(const Index& ix, const float* Q, uint32_t nq,
                                                  const std::vector<std::vector<uint32_t>>& slow,
                                                  int k, ThreadPool& pool) {

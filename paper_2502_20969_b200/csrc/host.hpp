@@ -98,6 +98,13 @@ std::vector<Scored> miss_scan(const Index& ix, const float* q,
                               const std::vector<uint32_t>& lists, int k,
                               ThreadPool& pool);
 
+// score_clusters' host half (ivf.cpp:301-324): every row of list c scored
+// (the miss scan's arithmetic) into s_out / id_out starting at offset o, for
+// each (c, o) of items.
+void score_lists(const Index& ix, const float* q,
+                 const std::vector<std::pair<uint32_t, uint64_t>>& items, float* s_out,
+                 uint64_t* id_out, ThreadPool& pool);
+
 // Batched miss path: slow[q] are the missed lists of query q (rows of Q).
 // List-major: each missed list is read once and scored for every query that
 // misses it. Returns each query's best-k, best-first.

@@ -149,6 +149,42 @@ void launch_group(const double* dist, uint32_t n, uint32_t m, uint64_t* order, u
 void launch_overlap(const uint32_t* probes, uint32_t L, const uint64_t* order,
                     const uint64_t* off, uint32_t nb, const unsigned long long* resident,
                     uint32_t nw, uint32_t words, unsigned long long* overlap, cudaStream_t st);
+// ---- size-unbounded paths (wide.cu) ----
+// Datastore id ranks: rank_of_row[r] = rank of ids[r] among all ids,
+// row_of_rank its inverse (n < 2^32).
+void build_id_rank(const uint64_t* ids, uint64_t n, uint32_t* rank_of_row, uint32_t* row_of_rank,
+                   cudaStream_t st);
+// Scores the V fast-list members of query qi (fast table ft, query vector q
+// on the device): keys[v] = (score key << 32) | rank_of_row[row] (keys set),
+// or raw (score, id) in candidate order (raw_s / raw_id set).
+void launch_score_all(const float* q, uint32_t qi, uint32_t d, int metric, const FastTable& ft,
+                      const float* slab, const uint32_t* rank_of_row, const uint64_t* ids,
+                      uint64_t V, uint64_t* keys, float* raw_s, uint64_t* raw_id, int num_sms,
+                      cudaStream_t st);
+size_t wide_sort_temp_bytes(uint64_t n);
+// Sorts keys[0, V) into keys_alt and writes the first min(k, V) as (score,
+// id) to out_s / out_id, out_count[0]; fcount_out[0] = fcount_in[qi].
+void launch_wide_topk(uint64_t* keys, uint64_t* keys_alt, uint64_t V, int k, int metric,
+                      void* tmp, size_t tmp_bytes, const uint32_t* row_of_rank,
+                      const uint64_t* ids, float* out_s, uint64_t* out_id, uint32_t* out_count,
+                      const uint32_t* fcount_in, uint32_t* fcount_out, uint32_t qi,
+                      cudaStream_t st);
+// Coarse ranking prefix for any nc (multi-CTA radix sort per query).
+struct RankScratch {
+  uint64_t* keys = nullptr;
+  uint64_t* keys_alt = nullptr;
+  uint32_t* vals = nullptr;
+  uint32_t* vals_alt = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+};
+size_t rank_large_temp_bytes(uint32_t nc);
+void launch_rank_large(const double* scores, uint32_t nq, uint32_t nc, int metric, uint32_t n_out,
+                       uint32_t* order, RankScratch& rs, cudaStream_t st);
+// pairwise_l2 (vectorstore.cpp:141-153): out[i * nb + j] = f32(sqrt(serial
+// fp64 l2_sq_d(A_i, B_j))), or the fp64 squared distances into out_sq.
+void launch_pairwise_l2(const float* A, uint64_t na, const float* B, uint64_t nb, uint32_t d,
+                        float* out, double* out_sq, cudaStream_t st);
 // Generation-window stand-in: one CTA per SM spins on %globaltimer for ns.
 void launch_fetch_query(const float* src, const float* const* slot, float* dQ, uint32_t d,
                         cudaStream_t st);

@@ -187,6 +187,10 @@ class IvfIndex:
 
     def close(self):
         if getattr(self, "h", None):
+            live = [d for d in getattr(self, "_devices", ()) if getattr(d, "h", None)]
+            if live:
+                raise LogicError(f"IvfIndex.close() while {len(live)} Device(s) still use it: "
+                                 "close them first (their contexts copy lists from this store)")
             lib().laivg_index_destroy(self.h)
             self.h = None
 
@@ -321,6 +325,9 @@ class Device:
         check(L.laivg_ctx_create(ix.h, C.byref(o), C.byref(h)))
         self.h = h
         self.ix = ix
+        if not hasattr(ix, "_devices"):
+            ix._devices = weakref.WeakSet()
+        ix._devices.add(self)
         self.store = TieredStore(self)
 
     def close(self):
@@ -454,6 +461,65 @@ def search_clusters(dev: Device, q, clusters, k: int) -> TopK:    # ivf.hpp:85-8
     check(lib().laivg_search_clusters(dev.h, q.ctypes.data, cl.ctypes.data, cl.size, int(k),
                                       ids.ctypes.data, sc.ctypes.data, C.byref(cnt)))
     return TopK(k, [ScoredId(int(ids[i]), float(sc[i])) for i in range(cnt.value)])
+
+
+def score_clusters(dev: Device, q, clusters) -> list[ScoredId]:   # ivf.hpp:75-81
+    """Every member of ``clusters`` (in order, duplicates included) scored
+    against q, unranked (ivf.cpp:301-324); resident lists on the GPU."""
+    q = _check_q(dev, q)
+    cl = _c(clusters, np.uint32).reshape(-1)
+    if cl.size and int(cl.max()) >= dev.ix.nc:
+        bad = int(cl[np.argmax(cl >= dev.ix.nc)])
+        raise ValueError(f"unknown cluster id {bad}")
+    n = int(sum(dev.ix.list_len(int(c)) for c in cl))
+    ids = np.empty(max(n, 1), np.uint64)
+    sc = np.empty(max(n, 1), np.float32)
+    got = C.c_uint64()
+    check(lib().laivg_score_clusters(dev.h, q.ctypes.data, _ptr(cl if cl.size else None), cl.size,
+                                     n, ids.ctypes.data, sc.ctypes.data, C.byref(got)))
+    return [ScoredId(int(ids[i]), float(sc[i])) for i in range(got.value)]
+
+
+def score_clusters_arrays(dev: Device, q, clusters):
+    """score_clusters as (ids[n], scores[n]) arrays."""
+    q = _check_q(dev, q)
+    cl = _c(clusters, np.uint32).reshape(-1)
+    n = int(sum(dev.ix.list_len(int(c)) for c in cl if 0 <= int(c) < dev.ix.nc))
+    ids = np.empty(max(n, 1), np.uint64)
+    sc = np.empty(max(n, 1), np.float32)
+    got = C.c_uint64()
+    check(lib().laivg_score_clusters(dev.h, q.ctypes.data, _ptr(cl if cl.size else None), cl.size,
+                                     n, ids.ctypes.data, sc.ctypes.data, C.byref(got)))
+    return ids[: got.value], sc[: got.value]
+
+
+def exact_search(dev: Device, q, k: int) -> TopK:                 # vectorstore.hpp:94-98
+    """Brute force over every row of the index's datastore (the union of its
+    lists), any k >= 1; ties by ascending id (vectorstore.cpp:117-139)."""
+    q = _check_q(dev, q)
+    ids = np.empty(max(k, 1), np.uint64)
+    sc = np.empty(max(k, 1), np.float32)
+    cnt = np.zeros(1, np.uint32)
+    check(lib().laivg_exact_search(dev.h, q.ctypes.data, 1, int(k), ids.ctypes.data,
+                                   sc.ctypes.data, cnt.ctypes.data))
+    return TopK(k, [ScoredId(int(ids[i]), float(sc[i])) for i in range(int(cnt[0]))])
+
+
+def pairwise_l2(dev: Device, a, b) -> np.ndarray:                 # vectorstore.hpp:100-102
+    """Dense a.count() x b.count() Euclidean distances (row-major f32), the
+    reference's serial fp64 arithmetic on the device's GPU (bit-identical)."""
+    A = np.ascontiguousarray(np.asarray(a, np.float32))
+    B = np.ascontiguousarray(np.asarray(b, np.float32))
+    if A.ndim != 2 or B.ndim != 2:
+        raise ValueError("pairwise_l2: matrices must be 2-D")
+    if A.shape[1] != B.shape[1]:
+        raise ValueError("pairwise_l2: dim mismatch")
+    out = np.empty((A.shape[0], B.shape[0]), np.float32)
+    if out.size == 0:
+        return out.reshape(-1)
+    check(lib().laivg_pairwise_l2(dev.h, A.ctypes.data, A.shape[0], B.ctypes.data, B.shape[0],
+                                  A.shape[1], out.ctypes.data))
+    return out.reshape(-1)
 
 
 def ivf_search(dev: Device, q, L: int, k: int) -> TopK:           # ivf.hpp:90-91
