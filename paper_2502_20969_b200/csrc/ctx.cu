@@ -272,17 +272,39 @@ struct Ctx {
     unsigned long long* overlap = nullptr;
     uint64_t n = 0, L = 0, nw = 0;
   } sb;
+  GroupScratch gs{};
+  uint64_t dist_n = 0;
   void sched_reserve(uint64_t n, uint64_t L, uint64_t nw) {
     const uint32_t words = (ix->nc + 63) / 64;
     if (n > sb.n) {
-      for (void* p : {(void*)sb.q, (void*)sb.dist, (void*)sb.order, (void*)sb.off, (void*)sb.nb}) {
+      for (void* p : {(void*)sb.q, (void*)sb.order, (void*)sb.off, (void*)sb.nb}) {
         if (p) cudaFree(p);
       }
       sb.q = dev_alloc<float>(n * ix->d);
-      sb.dist = dev_alloc<double>(n * n);
       sb.order = dev_alloc<uint64_t>(n);
       sb.off = dev_alloc<uint64_t>(n + 1);
       sb.nb = dev_alloc<uint32_t>(1);
+    }
+    // grouping scratch: the n x n pair matrix up to group_max_queries(), the
+    // streaming kernel's O(n) state above
+    if (n <= group_max_queries()) {
+      if (n > dist_n) {
+        if (sb.dist) cudaFree(sb.dist);
+        sb.dist = dev_alloc<double>(n * n);
+        dist_n = n;
+      }
+    } else if (n > gs.n) {
+      for (void* p : {(void*)gs.taken, (void*)gs.dist_row}) {
+        if (p) cudaFree(p);
+      }
+      gs.taken = dev_alloc<unsigned char>(n);
+      gs.dist_row = dev_alloc<double>(n);
+      if (!gs.slot_d) {
+        gs.slot_d = dev_alloc<double>(2 * kGroupLargeMaxGrid);
+        gs.slot_i = dev_alloc<uint32_t>(2 * kGroupLargeMaxGrid);
+        gs.bar = dev_alloc<uint64_t>(1);
+      }
+      gs.n = n;
     }
     if (n * L > sb.n * sb.L || sb.probes == nullptr) {
       if (sb.probes) cudaFree(sb.probes);
@@ -656,7 +678,8 @@ Ctx::~Ctx() {
     if (e) cudaEventDestroy(e);
   }
   for (void* p : {(void*)sb.q, (void*)sb.dist, (void*)sb.order, (void*)sb.off, (void*)sb.nb,
-                  (void*)sb.probes, (void*)sb.resident, (void*)sb.overlap}) {
+                  (void*)sb.probes, (void*)sb.resident, (void*)sb.overlap, (void*)gs.taken,
+                  (void*)gs.dist_row, (void*)gs.slot_d, (void*)gs.slot_i, gs.bar}) {
     if (p) cudaFree(p);
   }
   for (void* p : {(void*)d_rank_of_row, (void*)d_row_of_rank, (void*)d_wkeys, (void*)d_wkeys_alt,
@@ -2815,8 +2838,15 @@ namespace {
 // off on the host.
 uint32_t group_on_device(Ctx& c, uint64_t n, uint64_t m, std::vector<uint64_t>& order,
                          std::vector<uint64_t>& off) {
-  laivg::launch_pair_dist(c.sb.q, uint32_t(n), c.ix->d, c.sb.dist, c.comp);
-  laivg::launch_group(c.sb.dist, uint32_t(n), uint32_t(m), c.sb.order, c.sb.off, c.sb.nb, c.comp);
+  if (n >= (1ull << 32) || m >= (1ull << 32)) throw std::invalid_argument("too many queries");
+  if (n <= laivg::group_max_queries()) {
+    laivg::launch_pair_dist(c.sb.q, uint32_t(n), c.ix->d, c.sb.dist, c.comp);
+    laivg::launch_group(c.sb.dist, uint32_t(n), uint32_t(m), c.sb.order, c.sb.off, c.sb.nb,
+                        c.comp);
+  } else {
+    laivg::launch_group_large(c.sb.q, uint32_t(n), c.ix->d, uint32_t(m), c.gs, c.sb.order,
+                              c.sb.off, c.sb.nb, c.sms, c.comp);
+  }
   uint32_t nb = 0;
   CK(cudaMemcpyAsync(&nb, c.sb.nb, sizeof(uint32_t), cudaMemcpyDeviceToHost, c.comp));
   CK(cudaStreamSynchronize(c.comp));
@@ -2841,10 +2871,6 @@ int laivg_group_microbatches_gpu(laivg_ctx* ctx, const float* queries, uint64_t 
     set_ctx_device(ctx);
     if (m < 1) throw std::invalid_argument("micro-batch size must be >= 1");
     Ctx& c = ctx->c;
-    if (n > laivg::group_max_queries()) {
-      throw std::invalid_argument("GPU grouping supports up to " +
-                                  std::to_string(laivg::group_max_queries()) + " queries");
-    }
     if (n == 0) {
       if (batch_off_out) batch_off_out[0] = 0;
       if (nb_out) *nb_out = 0;
@@ -2870,10 +2896,6 @@ int laivg_schedule(laivg_ctx* ctx, const float* queries, uint64_t n, uint64_t m,
     if (m < 1) throw std::invalid_argument("micro-batch size must be >= 1");
     if (nw == 0) throw std::invalid_argument("need at least one worker");
     Ctx& c = ctx->c;
-    if (n > laivg::group_max_queries()) {
-      throw std::invalid_argument("GPU scheduling supports up to " +
-                                  std::to_string(laivg::group_max_queries()) + " queries");
-    }
     if (n == 0) {
       if (batch_off_out) batch_off_out[0] = 0;
       if (nb_out) *nb_out = 0;

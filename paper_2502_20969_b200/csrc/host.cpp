@@ -485,25 +485,52 @@ void group_microbatches(const float* q, uint64_t n, uint32_t d, uint64_t m,
                         std::vector<uint64_t>& order,
                         std::vector<uint64_t>& off, ThreadPool* pool) {
   if (m < 1) throw std::invalid_argument("micro-batch size must be >= 1");
-  // Pairwise fp64 L2^2 with the reference's serial accumulation (the
-  // distance is symmetric bit for bit: (a-b)^2 == (b-a)^2), rows in parallel.
-  std::vector<double> dist(n * n, 0.0);
-  auto row = [&](size_t i, unsigned) {
-    for (uint64_t j = i + 1; j < n; ++j) dist[i * n + j] = l2sq_serial(q + i * d, q + j * d, d);
-  };
-  if (pool) pool->parallel_for(n, row);
-  else for (size_t i = 0; i < n; ++i) row(i, 0);
+  // fp64 L2^2 with the reference's serial accumulation (symmetric bit for
+  // bit: (a-b)^2 == (b-a)^2). Small n: the whole upper triangle at once, rows
+  // in parallel. Larger n: each seed's row over its unassigned later queries
+  // only (what sched.cpp:52-56 computes), so memory stays O(n).
+  constexpr uint64_t kMatrixMax = 2048; // 32 MB of pair distances
+  const bool matrix = n <= kMatrixMax;
+  std::vector<double> dist(matrix ? n * n : n, 0.0);
+  if (matrix) {
+    auto row = [&](size_t i, unsigned) {
+      for (uint64_t j = i + 1; j < n; ++j) dist[i * n + j] = l2sq_serial(q + i * d, q + j * d, d);
+    };
+    if (pool) pool->parallel_for(n, row);
+    else for (size_t i = 0; i < n; ++i) row(i, 0);
+  }
   order.clear();
   off.assign(1, 0);
   std::vector<char> assigned(n, 0);
   std::vector<std::pair<double, uint64_t>> cand;
+  std::vector<uint64_t> open;
   for (uint64_t seed = 0; seed < n; ++seed) {
     if (assigned[seed]) continue;
     order.push_back(seed);
     assigned[seed] = 1;
     cand.clear();
-    for (uint64_t j = seed + 1; j < n; ++j) {
-      if (!assigned[j]) cand.emplace_back(dist[seed * n + j], j);
+    if (m > 1) {
+      if (matrix) {
+        for (uint64_t j = seed + 1; j < n; ++j) {
+          if (!assigned[j]) cand.emplace_back(dist[seed * n + j], j);
+        }
+      } else {
+        open.clear();
+        for (uint64_t j = seed + 1; j < n; ++j) {
+          if (!assigned[j]) open.push_back(j);
+        }
+        constexpr size_t kChunk = 256;
+        auto part = [&](size_t c, unsigned) {
+          const size_t e = std::min(open.size(), (c + 1) * kChunk);
+          for (size_t x = c * kChunk; x < e; ++x) {
+            dist[open[x]] = l2sq_serial(q + seed * d, q + open[x] * d, d);
+          }
+        };
+        const size_t nch = (open.size() + kChunk - 1) / kChunk;
+        if (pool && nch > 1) pool->parallel_for(nch, part);
+        else for (size_t c = 0; c < nch; ++c) part(c, 0);
+        for (uint64_t j : open) cand.emplace_back(dist[j], j);
+      }
     }
     const size_t take = std::min<size_t>(m - 1, cand.size());
     std::partial_sort(cand.begin(), cand.begin() + take, cand.end());

@@ -145,6 +145,20 @@ void launch_pair_dist(const float* Q, uint32_t n, uint32_t d, double* dist, cuda
 uint32_t group_max_queries();
 void launch_group(const double* dist, uint32_t n, uint32_t m, uint64_t* order, uint64_t* off,
                   uint32_t* nb, cudaStream_t st);
+// group_microbatches for any n without the n x n matrix: one persistent
+// (cooperative) grid walks the seeds; bit-identical to launch_group.
+struct GroupScratch {
+  unsigned char* taken = nullptr; // [n]
+  double* dist_row = nullptr;     // [n]
+  double* slot_d = nullptr;       // [2 * max grid]
+  uint32_t* slot_i = nullptr;
+  void* bar = nullptr;            // grid barrier (2 words)
+  uint64_t n = 0;
+};
+constexpr uint32_t kGroupLargeMaxGrid = 1024;
+void launch_group_large(const float* Q, uint32_t n, uint32_t d, uint32_t m, GroupScratch& gs,
+                        uint64_t* order, uint64_t* off, uint32_t* nb, int num_sms,
+                        cudaStream_t st);
 // overlap[b][w] = |probe union of batch b  ∩  resident bitset of worker w|.
 void launch_overlap(const uint32_t* probes, uint32_t L, const uint64_t* order,
                     const uint64_t* off, uint32_t nb, const unsigned long long* resident,

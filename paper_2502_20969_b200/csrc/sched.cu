@@ -16,7 +16,9 @@
 // The greedy assignment over the nb x nw overlap matrix stays on the host
 // (greedy_assign, host.cpp): it is O(nb^2 nw) on a few hundred entries.
 #include <cstdint>
+#include <algorithm>
 #include <stdexcept>
+#include <string>
 
 #include "dev_common.cuh"
 #include "host.hpp"
@@ -141,6 +143,160 @@ __global__ void __launch_bounds__(kGroupThreads)
   if (threadIdx.x == 0) *nb_out = nb;
 }
 
+// ---------------------------------------------------------------------------
+// group_microbatches for any n (no n x n matrix): one persistent grid, every
+// CTA co-resident (cooperative launch), walking the seeds in order. Thread t
+// owns queries j = t, t + T, ... (T = grid threads). Per seed s: each owner
+// computes l2_sq_d(q_s, q_j) for its unassigned j > s (serial, the
+// reference's order), then m-1 rounds pick the (distance, index)-smallest
+// unassigned j: thread -> warp -> CTA minimum into a per-CTA slot, one grid
+// barrier, then every CTA reduces the slots itself (no second barrier); the
+// owner of the pick marks it taken. A barrier ends each seed so every CTA
+// sees the same taken flags.
+// ---------------------------------------------------------------------------
+struct GridBar {
+  unsigned count;
+  unsigned gen;
+};
+
+__device__ __forceinline__ void grid_barrier(GridBar* b, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = &b->gen;
+    const unsigned g = *vgen;
+    __threadfence();
+    if (atomicAdd(&b->count, 1u) == nblocks - 1) {
+      b->count = 0;
+      __threadfence();
+      atomicAdd(&b->gen, 1u);
+    } else {
+      while (*vgen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+constexpr int kGLThreads = 256;
+__global__ void __launch_bounds__(kGLThreads)
+    group_large_kernel(const float* __restrict__ Q, uint32_t n, uint32_t d, uint32_t m,
+                       unsigned char* taken, double* dist_row, double* slot_d, uint32_t* slot_i,
+                       GridBar* bar, uint64_t* __restrict__ order_out,
+                       uint64_t* __restrict__ off_out, uint32_t* __restrict__ nb_out) {
+  extern __shared__ float sseed[];
+  __shared__ double wd[kGLThreads / 32];
+  __shared__ uint32_t wi[kGLThreads / 32];
+  const unsigned G = gridDim.x;
+  const uint32_t T = G * blockDim.x, t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  volatile unsigned char* vt = taken;
+  uint64_t pos = 0;
+  uint32_t nb = 0, round = 0;
+  if (t == 0) off_out[0] = 0;
+  for (uint32_t s = 0; s < n; ++s) {
+    if (vt[s]) continue; // uniform: read after the last barrier
+    if (t == 0) order_out[pos] = s;
+    ++pos;
+    if (m > 1 && s + 1 < n) {
+      for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) sseed[i] = Q[static_cast<uint64_t>(s) * d + i];
+      __syncthreads();
+      for (uint32_t j = t; j < n; j += T) {
+        if (j <= s || vt[j]) continue;
+        const float* b = Q + static_cast<uint64_t>(j) * d;
+        double acc = 0.0;
+        for (uint32_t e = 0; e < d; ++e) { // serial, separately rounded (l2_sq_d)
+          const double u = __dsub_rn(static_cast<double>(sseed[e]), static_cast<double>(__ldg(b + e)));
+          acc = __dadd_rn(acc, __dmul_rn(u, u));
+        }
+        dist_row[j] = acc;
+      }
+      for (uint32_t r = 1; r < m; ++r, ++round) {
+        double bd = INFINITY;
+        uint32_t bi = 0xffffffffu;
+        for (uint32_t j = t; j < n; j += T) {
+          if (j <= s || vt[j]) continue;
+          const double dj = dist_row[j];
+          if (pair_less(dj, j, bd, bi)) {
+            bd = dj;
+            bi = j;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+          const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (pair_less(od, oi, bd, bi)) {
+            bd = od;
+            bi = oi;
+          }
+        }
+        if (lane == 0) {
+          wd[warp] = bd;
+          wi[warp] = bi;
+        }
+        __syncthreads();
+        const uint32_t par = (round & 1u) * G;
+        if (threadIdx.x == 0) {
+          double cd = wd[0];
+          uint32_t ci = wi[0];
+          for (int w = 1; w < kGLThreads / 32; ++w) {
+            if (pair_less(wd[w], wi[w], cd, ci)) {
+              cd = wd[w];
+              ci = wi[w];
+            }
+          }
+          slot_d[par + blockIdx.x] = cd;
+          slot_i[par + blockIdx.x] = ci;
+        }
+        grid_barrier(bar, G);
+        // every CTA reduces the slots: same answer everywhere
+        bd = INFINITY;
+        bi = 0xffffffffu;
+        for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) {
+          const double od = __ldcg(slot_d + par + g);
+          const uint32_t oi = __ldcg(slot_i + par + g);
+          if (pair_less(od, oi, bd, bi)) {
+            bd = od;
+            bi = oi;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+          const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (pair_less(od, oi, bd, bi)) {
+            bd = od;
+            bi = oi;
+          }
+        }
+        __syncthreads();
+        if (lane == 0) {
+          wd[warp] = bd;
+          wi[warp] = bi;
+        }
+        __syncthreads();
+        bd = wd[0];
+        bi = wi[0];
+        for (int w = 1; w < kGLThreads / 32; ++w) {
+          if (pair_less(wd[w], wi[w], bd, bi)) {
+            bd = wd[w];
+            bi = wi[w];
+          }
+        }
+        __syncthreads();
+        if (bi == 0xffffffffu) break; // fewer than m-1 unassigned remain
+        if (bi % T == t) taken[bi] = 1; // the owner: only it reads taken[bi] this seed
+        if (t == 0) order_out[pos] = bi;
+        ++pos;
+      }
+    }
+    ++nb;
+    if (t == 0) off_out[nb] = pos;
+    grid_barrier(bar, G); // every owner's taken flags visible before the next seed
+  }
+  if (t == 0) *nb_out = nb;
+}
+
 // One CTA per micro-batch. probes[q * L + i]; members of batch b are
 // order[off[b] .. off[b + 1]); resident bitsets [nw][words].
 __global__ void __launch_bounds__(256)
@@ -184,6 +340,38 @@ void launch_group(const double* dist, uint32_t n, uint32_t m, uint64_t* order, u
                   uint32_t* nb, cudaStream_t st) {
   if (n > group_max_queries()) throw std::invalid_argument("too many queries for GPU grouping");
   group_kernel<<<1, kGroupThreads, n, st>>>(dist, n, m, order, off, nb);
+  after_launch();
+}
+
+void launch_group_large(const float* Q, uint32_t n, uint32_t d, uint32_t m, GroupScratch& gs,
+                        uint64_t* order, uint64_t* off, uint32_t* nb, int num_sms,
+                        cudaStream_t st) {
+  if (n == 0) return;
+  const size_t smem = size_t(d) * sizeof(float);
+  auto fn = group_large_kernel;
+  if (smem > 48 * 1024) ensure_dyn_smem(reinterpret_cast<const void*>(fn), smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGLThreads, smem);
+  if (per_sm < 1) throw std::runtime_error("group_large_kernel does not fit an SM");
+  unsigned G = static_cast<unsigned>(std::min(per_sm, 2) * num_sms);
+  // at least ~16 queries per thread before adding CTAs
+  const unsigned want = static_cast<unsigned>((uint64_t(n) + 16 * kGLThreads - 1) / (16 * kGLThreads));
+  if (want < G) G = want < 1 ? 1 : want;
+  cudaMemsetAsync(gs.taken, 0, n, st);
+  cudaMemsetAsync(gs.bar, 0, sizeof(GridBar), st);
+  const float* q = Q;
+  unsigned char* tk = gs.taken;
+  double* dr = gs.dist_row;
+  double* sd = gs.slot_d;
+  uint32_t* si = gs.slot_i;
+  GridBar* b = reinterpret_cast<GridBar*>(gs.bar);
+  void* args[] = {(void*)&q, (void*)&n, (void*)&d, (void*)&m, (void*)&tk, (void*)&dr, (void*)&sd,
+                  (void*)&si, (void*)&b, (void*)&order, (void*)&off, (void*)&nb};
+  const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(G),
+                                                    dim3(kGLThreads), args, smem, st);
+  if (e != cudaSuccess) {
+    throw CudaError(std::string("group_large_kernel launch: ") + cudaGetErrorString(e));
+  }
   after_launch();
 }
 

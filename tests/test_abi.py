@@ -74,6 +74,21 @@ def test_group_microbatches_matches_oracle_random(orc, laiv):
         assert [b.queries for b in laiv.group_microbatches(q, m)] == orc.group_microbatches(q, m)
 
 
+def test_group_microbatches_streaming_matches_reference(laiv):
+    """n above the pair-matrix threshold (2048): per-seed rows, O(n) memory
+    (ADVICE r01), bit-identical to the unmodified reference."""
+    from oracle.oracle import RefLib
+
+    if not RefLib.available():
+        pytest.skip("oracle/_ref/libref.so not built")
+    rng = np.random.default_rng(9)
+    q = rng.standard_normal((3001, 24)).astype(np.float32)
+    q[100:110] = q[7]  # exact distance ties: broken by index
+    for m in (1, 4, 9):
+        got = [b.queries for b in laiv.group_microbatches(q, m)]
+        assert got == RefLib().group_microbatches(q, m)
+
+
 def test_chunk_and_round_robin(laiv):
     assert [b.queries for b in laiv.chunk_microbatches(5, 2)] == [[0, 1], [2, 3], [4]]
     assert laiv.assign_round_robin(8, 3) == [b % 3 for b in range(8)]

@@ -255,6 +255,25 @@ def test_group_microbatches_gpu_matches_host(laiv, n, m, d):
     assert [b.queries for b in got] == [b.queries for b in want]
 
 
+@pytest.mark.parametrize("n,m,d", [(8193, 4, 16), (12000, 3, 64), (9000, 1, 8)])
+def test_group_microbatches_gpu_streaming(laiv, n, m, d):
+    """n above the one-CTA kernel's 8192: the persistent streaming grouping
+    (no n x n matrix) equals the host scheduler bit for bit."""
+    rng = np.random.default_rng(n + m)
+    q = rng.standard_normal((n, d)).astype(np.float32)
+    q[n // 3: n // 3 + 7] = q[11]  # exact ties
+    cen = rng.standard_normal((8, d)).astype(np.float32)
+    ix = laiv.IvfIndex(cen, cen.copy(), np.arange(8, dtype=np.uint64),
+                       np.arange(9, dtype=np.uint64), laiv.Metric.L2)
+    dev = laiv.Device(ix, 1 << 20)
+    got = laiv.group_microbatches_gpu(dev, q, m)
+    want = laiv.group_microbatches(q, m)
+    assert [b.queries for b in got] == [b.queries for b in want]
+    # and the smaller path still works on the same context afterwards
+    got = laiv.group_microbatches_gpu(dev, q[:300], m)
+    assert [b.queries for b in got] == [b.queries for b in laiv.group_microbatches(q[:300], m)]
+
+
 @pytest.mark.parametrize("nw", [1, 2, 3, 8])
 def test_schedule_matches_oracle(orc, laiv, nw):
     from paper_2502_20969_b200 import shard
