@@ -1880,6 +1880,10 @@ void launch_scan(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
                  const FastTable& ft, const float* slab_vecs,
                  const uint64_t* ids_all, const ScanOut& out, int grid_x,
                  bool acc_fp64, ScanImpl impl, const ScanTune& tune, cudaStream_t st) {
+  // fp32 accumulation keeps k + kRerankMargin survivors for the exact
+  // re-score; where that margin no longer fits the register top-k, every
+  // candidate is accumulated in fp64 instead (no survivor cut to get wrong)
+  if (!acc_fp64 && k + kRerankMargin > kMaxK) acc_fp64 = true;
   const int kk = scan_kk(k, acc_fp64);
   const bool tma = impl == ScanImpl::kTma && (d % 4) == 0;
   const bool d768 = d == 768;

@@ -475,6 +475,46 @@ def _modeled_t2(slow: int, fast: int, cost: laiv.CostModel) -> float:  # tiered.
     return max(math.ceil(slow / cost.parallel_slots) * cost.t_cc, fast * cost.t_gc)
 
 
+def _device_retrievals(dev, walks, act, r, sidecar, cfg, rows, used, traces, failures) -> float:
+    """Device mode: the round's retrievals of every active trace as batched
+    hybrid searches (laivg_hybrid_search_batch: one coarse + one scan launch
+    per max_batch queries, the misses list-major on the host or fetched
+    through the HBM ring); results per query equal hybrid_search's. Returns
+    the measured phase time."""
+    refs = [(i, walks[i].phases[r].predictor_ref, ref)
+            for i in act for ref in walks[i].phases[r].query_refs]
+    if not refs:
+        return 0.0
+    Q = np.stack([sidecar[ref] for _, _, ref in refs])
+    probes = laiv.coarse_probe(dev, Q, cfg.n_probe).reshape(len(refs), -1)
+    probed = probes.shape[1]
+    t2 = 0.0
+    step = 256
+    for q0 in range(0, len(refs), step):
+        res, tm = laiv.hybrid_search_batch(dev, Q[q0:q0 + step], cfg.n_probe, cfg.top_k, cfg.cost)
+        t2 += tm.t_2
+        for j in range(res.counts.shape[0]):
+            i, pred, ref = refs[q0 + j]
+            rr = RetrievalRow(round=r, coverage=laiv.coverage(dev, sidecar[pred], Q[q0 + j],
+                                                              cfg.n_probe))
+            rr.t_c, rr.t_g = tm.t_c, tm.t_g  # the batch's phase times
+            rr.fast = int(res.nfast[j])
+            rr.probed = probed
+            rr.slow = probed - rr.fast
+            rr.hit_rate = rr.fast / probed if probed else 0.0
+            top = res.topk(j)
+            rr.result_ids = [e.id for e in top.entries]
+            used.update(int(c) for c in probes[q0 + j])
+            if cfg.validate_exactness and failures is not None:
+                want = laiv.ivf_search(dev, Q[q0 + j], cfg.n_probe, cfg.top_k)
+                if [(e.id, e.score) for e in want.entries] != \
+                        [(e.id, e.score) for e in top.entries]:
+                    failures.append(f"trace {traces[i].trace_id}: hybrid top-k differs "
+                                    "from the monolithic search")
+            rows[i].retrievals.append(rr)
+    return t2
+
+
 def serve_microbatch(traces: list[QueryTrace], budgets: list[int], sidecar: np.ndarray,
                      cfg: RunConfig, worker: Worker, failures: list[str] | None):
     """One micro-batch of traces on one worker, round by round: the rounds'
@@ -489,12 +529,37 @@ def serve_microbatch(traces: list[QueryTrace], budgets: list[int], sidecar: np.n
                                 else laiv.ChannelMode.SimulatedClock)
     used: set[int] = set()
     batch_time = 0.0
+    # Device mode runs on one clock: every trace-second (plain generation,
+    # windows, tail) is scaled by time_scale next to the measured copy and
+    # retrieval times
+    scale = cfg.time_scale if measured else 1.0
     for r in range(max((len(w.phases) for w in walks), default=0)):
         act = [i for i, w in enumerate(walks) if r < len(w.phases)]
-        plain_r = max(walks[i].phases[r].plain_before_s for i in act)
+        plain_r = max(walks[i].phases[r].plain_before_s for i in act) * scale
         window_r = max(walks[i].phases[r].window_s for i in act)
         t_p_total = 0.0
-        if cfg.flags.lookahead_on:
+        if measured and cfg.flags.lookahead_on:
+            # the round's prefetches as one batch: one coarse pass, the
+            # sequential plans against the filling store, ONE generation
+            # window for all their copies (laivg_prefetch_batch)
+            q_in = np.stack([sidecar[walks[i].phases[r].predictor_ref] for i in act])
+            bud = np.array([budgets[i] for i in act], np.uint64)
+            rep, nplan = laiv.prefetch_batch(dev, q_in, bud, chan, window_r * scale)
+            t_p_total = rep.t_p
+            k0 = 0
+            for j, i in enumerate(act):
+                mine = rep.transferred[k0:k0 + int(nplan[j])]
+                k0 += int(nplan[j])
+                b = sum(dev.ix.cluster_bytes(c) for c in mine)
+                tp = rep.t_p * b / rep.bytes if rep.bytes else 0.0
+                if cfg.flags.cache_on:
+                    for c in mine:
+                        worker.hot.on_fetch(c)
+                if b > 0 or mine:
+                    rows[i].transfers.append(TransferRow(r, b, tp, len(mine)))
+                rows[i].transfer_s += tp
+                rows[i].transfer_bytes += b
+        elif cfg.flags.lookahead_on:
             for i in act:
                 ph = walks[i].phases[r]
                 budget = min(budgets[i], dev.store.free_bytes())
@@ -510,10 +575,13 @@ def serve_microbatch(traces: list[QueryTrace], budgets: list[int], sidecar: np.n
                                                          len(rep.transferred)))
                 rows[i].transfer_s += rep.t_p
                 rows[i].transfer_bytes += rep.bytes
-        t1_r = max(window_r * (cfg.time_scale if measured else 1.0), t_p_total)
+        t1_r = max(window_r * scale, t_p_total)
         tot_fast = tot_slow = tot_probed = 0
         t2_meas = 0.0
-        for i in act:
+        if measured and cfg.flags.lookahead_on:
+            t2_meas = _device_retrievals(dev, walks, act, r, sidecar, cfg, rows, used,
+                                         traces, failures)
+        for i in act if not (measured and cfg.flags.lookahead_on) else ():
             ph = walks[i].phases[r]
             pred = sidecar[ph.predictor_ref]
             for ref in ph.query_refs:
@@ -563,9 +631,9 @@ def serve_microbatch(traces: list[QueryTrace], budgets: list[int], sidecar: np.n
         batch_time += plain_r + t1_r + t2_r
     tail_r = 0.0
     for w, row in zip(walks, rows):
-        row.tail_s = w.tail_s
+        row.tail_s = w.tail_s * scale
         row.total_s = row.gen_plain_s + row.overlap_s + row.retrieve_s + row.tail_s
-        tail_r = max(tail_r, w.tail_s)
+        tail_r = max(tail_r, row.tail_s)
     batch_time += tail_r
     # cache maintenance between batches (pipeline.cpp:462-472)
     if cfg.flags.cache_on:
@@ -688,6 +756,13 @@ _GETTERS = {  # key -> value text (pipeline.cpp:57-127, same order as _FIELDS)
 }
 
 
+# keys only this port writes; each is written only when it differs from the
+# reference's behaviour, so a config saved here for a reference-expressible
+# run loads in the reference's load_config (which rejects unknown keys,
+# pipeline.cpp:170-212)
+_EXTENSION_KEYS = {"time_scale": lambda c: c.time_scale != 1.0}
+
+
 def save_config(path, cfg: RunConfig) -> None:                     # pipeline.cpp:215-226
     try:
         f = open(path, "w")
@@ -695,6 +770,8 @@ def save_config(path, cfg: RunConfig) -> None:                     # pipeline.cp
         raise RuntimeError(f"cannot open for writing: {path}") from None
     with f:
         for key, get in _GETTERS.items():
+            if key in _EXTENSION_KEYS and not _EXTENSION_KEYS[key](cfg):
+                continue
             f.write(f"{key} = {get(cfg)}\n")
 
 

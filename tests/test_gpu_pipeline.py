@@ -70,6 +70,17 @@ def test_measured_clock_replay(index):
     assert [[rr.result_ids for rr in r.retrievals] for r in meas.rows] == \
         [[rr.result_ids for rr in r.retrievals] for r in sim.rows]
     assert [r.transfer_bytes for r in meas.rows] == [r.transfer_bytes for r in sim.rows]
+    # the batched Device round (one window per round, batched hybrid search)
+    # makes the same per-trace decisions as the reference's per-trace loops
+    assert [[(rr.fast, rr.slow, rr.probed, rr.coverage) for rr in r.retrievals]
+            for r in meas.rows] == \
+        [[(rr.fast, rr.slow, rr.probed, rr.coverage) for rr in r.retrievals] for r in sim.rows]
+    assert [[(t.round, t.bytes, t.clusters) for t in r.transfers] for r in meas.rows] == \
+        [[(t.round, t.bytes, t.clusters) for t in r.transfers] for r in sim.rows]
+    # one clock: trace-seconds scaled like the windows
+    for rm, rs in zip(meas.rows, sim.rows):
+        assert rm.tail_s == pytest.approx(rs.tail_s * 1e-3)
+        assert rm.gen_plain_s == pytest.approx(rs.gen_plain_s * 1e-3)
     for r in meas.rows:
         assert r.total_s > 0 and r.retrieve_s > 0
         for t in r.transfers:

@@ -112,6 +112,17 @@ def test_records_and_config_round_trip(tmp_path):
     P.save_config(tmp_path / "c.conf", c)
     c2 = P.load_config(tmp_path / "c.conf")
     assert c2 == c
+    # exactly the reference's keys, in its order (pipeline.cpp:57-127), when
+    # no extension is in use: the file loads in the reference's load_config
+    keys = [ln.split(" = ")[0] for ln in open(tmp_path / "c.conf")]
+    assert keys == ["n_probe", "top_k", "prefetch_budget_bytes", "capacity_bytes",
+                    "cache_fraction", "bandwidth_bytes_per_s", "t_cc", "t_gc", "parallel_slots",
+                    "workers", "micro_batch", "mode", "lookahead_on", "prefetch_sched_on",
+                    "cache_sched_on", "cache_on", "h_init", "h_inc", "decay", "warmup_traces",
+                    "validate_exactness", "seed"]
+    c.time_scale = 0.5
+    P.save_config(tmp_path / "c2.conf", c)
+    assert P.load_config(tmp_path / "c2.conf").time_scale == 0.5
     bad = tmp_path / "r.jsonl"
     bad.write_text('{"type": "trace"}\n')
     with pytest.raises(RuntimeError, match="r.jsonl:1"):
