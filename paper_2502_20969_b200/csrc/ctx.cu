@@ -138,24 +138,10 @@ class SlabAlloc {
 
 constexpr uint32_t kMaxFetchChunks = 128;
 
-// Enqueues many host->device copies with one cudaMemcpyBatchAsync call
-// (CUDA 12.8+), falling back to one cudaMemcpyAsync per copy.
+// Enqueues host->device copies, one cudaMemcpyAsync per (already coalesced)
+// run of adjacent lists.
 void h2d_batch(std::vector<void*>& dst, std::vector<void*>& src, std::vector<size_t>& size,
                cudaStream_t st) {
-  if (dst.empty()) return;
-  static bool batch_ok = true;
-  if (batch_ok) {
-    cudaMemcpyAttributes attr;
-    std::memset(&attr, 0, sizeof(attr));
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-    size_t idx = 0, fail = 0;
-    const cudaError_t e = cudaMemcpyBatchAsync(dst.data(), src.data(), size.data(), dst.size(),
-                                               &attr, &idx, 1, &fail, st);
-    if (e == cudaSuccess) return;
-    cudaGetLastError();
-    batch_ok = false;
-  }
   for (size_t i = 0; i < dst.size(); ++i) {
     CK(cudaMemcpyAsync(dst[i], src[i], size[i], cudaMemcpyHostToDevice, st));
   }
