@@ -75,6 +75,15 @@ CONFIGS = {
                 n_lists=4096, per_list=2442, d=768, nprobe=256, k=10, window_s=0.15,
                 cache_frac=0.10, batch=256, routed=True, micro=4, topics=32, zipf=1.0,
                 neigh=16, hot_fraction=0.5),
+    # C2 where prefetch hiding can fail: a 50 ms window
+    # (copy time ~ window at the calibrate_budget rule, budget uncapped by the
+    # 25% cache) that streams a 16 GB "weights" buffer like a memory-bound
+    # decode at ~5 TB/s, so the copies share HBM with it
+    "c2h": dict(workload="synthetic IVF-Flat 10M x 768 fp32, 4096 lists, nprobe=128, k=10, "
+                         "single-query lookahead prefetch, 50 ms decode-like window (16 GB "
+                         "streamed at 5 TB/s), cache 25% of lists",
+                n_lists=4096, per_list=2442, d=768, nprobe=128, k=10, window_s=0.05,
+                cache_frac=0.25, window_load_gbps=5000.0, window_buffer_gb=16.0),
     "small": dict(workload="synthetic IVF-Flat 100K x 768 fp32, 256 lists, nprobe=16, k=10",
                   n_lists=256, per_list=400, d=768, nprobe=16, k=10, window_s=0.005,
                   cache_frac=0.25),
@@ -244,18 +253,21 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def profiled_traffic(kernel_prefix: str):
-    """dram read+write bytes per launch of the scan kernel from the committed
-    `ncu --set full` summary of the C2 workload (profiles/rNN/), or None."""
+def profiled_traffic(kernel_prefix: str, config: str = "c2"):
+    """dram read+write bytes per launch of the dominant kernel from the newest
+    committed `ncu --set full` summary of this workload (profiles/rNN/
+    ncu_*full*_summary.json; a summary without a "config" key is C2), or None."""
     import glob
 
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*",
-                                              "ncu_scan_full_summary.json")), reverse=True):
+    paths = glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_*full*summary.json"))
+    for path in sorted(paths, reverse=True):
         try:
             with open(path) as f:
-                ks = json.load(f)["kernels"]
+                doc = json.load(f)
+            if doc.get("config", "c2") != config:
+                continue
             vals = []
-            for k in ks:
+            for k in doc["kernels"]:
                 if kernel_prefix in k["name"]:
                     rd = float(k["dram__bytes_read.sum"].split()[0])
                     wr = float(k["dram__bytes_write.sum"].split()[0])
@@ -354,6 +366,9 @@ def config_block(cfg, args, sigma):
             "metric": args.metric, "batch": cfg.get("batch", 1), "window_s": args.window,
             "cache_fraction_of_lists": cfg["cache_frac"], "q_out_sigma": sigma,
             "query_seed": QSEED,
+            "window_kind": (f"decode-like: {args.window_buffer_gb:g} GB streamed per token at "
+                            f"{args.window_load:g} GB/s target" if args.window_load > 0
+                            else "idle (%globaltimer spin)"),
             "l2_flush": "not needed: each query scans up to ~1 GB of lists > 126 MB L2, "
                         "and every step re-fetches its lists into a cleared cache"}
 
@@ -373,8 +388,13 @@ def run_ours(args, cfg):
     member = 4 * cfg["d"] + 8
     capacity = int(cfg["cache_frac"] * cfg["n_lists"]) * cfg["per_list"] * member
     dev = laiv.Device(ix, capacity, device=gpu, miss_threads=host_threads(world),
-                      acc_fp64=args.acc == "fp64", scan_impl=args.scan)
+                      acc_fp64=args.acc == "fp64", scan_impl=args.scan,
+                      single_query=args.single)
     L, k = cfg["nprobe"], cfg["k"]
+    if args.window_load > 0:
+        dev.window_load(int(args.window_buffer_gb * 1e9), args.window_load)
+    # independent host-link peak: one large pinned copy per direction
+    link_h2d, link_d2h = dev.link_peak(1 << 30)
 
     # link bandwidth for the calibrate_budget rule, measured on this box
     probe_plan = laiv.plan_prefetch(dev, cen[0], min(capacity, 64 * cfg["per_list"] * member))
@@ -440,8 +460,10 @@ def run_ours(args, cfg):
         if rec is not None:
             rec.append(dict(
                 exposed=rp.overshoot_s, t_p=rp.t_p, window=rp.window_s, h2d_gbps=rp.h2d_gbps,
+                window_read_gbps=rp.window_read_gbps,
                 lat_value=rp.overshoot_s + tm.t_2, lat_e2e=rp.overshoot_s + t_e2e,
                 t_scan=tm.t_scan, t_coarse=tm.t_coarse, t_g=tm.t_g, t_c=tm.t_c,
+                t_kernel=tm.t_kernel,
                 bytes=tm.scanned_bytes, hit=nfast / L, plan_s=t1 - t0,
                 # inside the e2e call's timed region (counted by the library)
                 h2d_bytes=e_h2d, d2h_bytes=e_d2h,
@@ -474,12 +496,23 @@ def run_ours(args, cfg):
     n_total = args.steps * world
     bytes_scan = sum(r["bytes"] for r in rec)
     t_scan = sum(r["t_scan"] for r in rec)
+    t_kernel = sum(r["t_kernel"] for r in rec)
     peak, peak_kind = measured_peaks()
-    achieved = bytes_scan / t_scan / 1e9 if t_scan > 0 else 0.0
+    fused = t_kernel > 0
+    if fused:
+        # one kernel per query: its algorithmic bytes are the probed resident
+        # lists (reference accounting n*(4d+8)) plus the centroid matrix the
+        # coarse phase reads, over its event-timed duration
+        cen_bytes = cfg["n_lists"] * cfg["d"] * 4
+        bytes_kernel = bytes_scan + cen_bytes * len(rec)
+        kname, t_dom = "fused_query_kernel", t_kernel
+    else:
+        bytes_kernel, kname, t_dom = bytes_scan, f"scan_{args.scan}_kernel", t_scan
+    achieved = bytes_kernel / t_dom / 1e9 if t_dom > 0 else 0.0
     exposed = np.array([r["exposed"] for r in rec])
     t_p = np.array([r["t_p"] for r in rec])
-    traffic, traffic_src = (profiled_traffic("scan_tma_kernel")
-                            if args.config == "c2" and args.scan == "tma" else (None, None))
+    traffic, traffic_src = (profiled_traffic(kname, args.config)
+                            if args.scan == "tma" else (None, None))
     line = {
         "metric": METRIC, "value": n_total / sum_v, "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum_v / args.steps * 1e3,
@@ -489,14 +522,26 @@ def run_ours(args, cfg):
         "p99_latency_ms": float(np.percentile(lat_v, 99) * 1e3),
         "pipeline_ms_per_step": wall / args.steps * 1e3,
         "config": config_block(cfg, args, sigma),
-        "roofline": {"kernel": f"scan_{args.scan}_kernel", "bound": "hbm", "achieved": achieved,
+        "roofline": {"kernel": kname, "bound": "hbm", "achieved": achieved,
                      "peak": peak, "peak_kind": f"{peak_kind} copy (MEASURED_PEAKS.json hbm_gbs)",
                      "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_source": traffic_src,
-                     "algorithmic_bytes_per_launch": bytes_scan / max(len(rec), 1),
-                     "avg_launch_ms": t_scan / max(len(rec), 1) * 1e3},
+                     "algorithmic_bytes_per_launch": bytes_kernel / max(len(rec), 1),
+                     "avg_launch_ms": t_dom / max(len(rec), 1) * 1e3,
+                     **({"bytes_note": "probed resident lists n*(4d+8) + centroids nc*d*4",
+                         "scan_phase": {
+                             "achieved": bytes_scan / t_scan / 1e9 if t_scan > 0 else 0.0,
+                             "avg_ms": t_scan / max(len(rec), 1) * 1e3,
+                             "note": "kernel time minus CTA 0's coarse + selection phase"}}
+                        if fused else {})},
         "prefetch": {"h2d_gbps": float(np.mean([r["h2d_gbps"] for r in rec])),
                      "b_link_gbps": b_link / 1e9, "budget_gb": budget / 1e9,
+                     "link_peak_h2d_gbps": link_h2d, "link_peak_d2h_gbps": link_d2h,
+                     "h2d_frac_of_link_peak": float(np.mean([r["h2d_gbps"] for r in rec])) / link_h2d
+                                              if link_h2d > 0 else None,
+                     "copy_ms_mean": float(t_p.mean() * 1e3),
+                     "window_ms_mean": float(np.mean([r["window"] for r in rec]) * 1e3),
+                     "window_read_gbps": float(np.mean([r["window_read_gbps"] for r in rec])),
                      "hidden_frac": float(1.0 - exposed.sum() / t_p.sum()) if t_p.sum() else 1.0,
                      "exposed_ms_mean": float(exposed.mean() * 1e3),
                      "hit_rate": float(np.mean([r["hit"] for r in rec]))},
@@ -599,6 +644,7 @@ def run_ours_batch(args, cfg):
             nhit = int(nfast.sum())
             rec.append(dict(
                 exposed=rp.overshoot_s, t_p=rp.t_p, window=rp.window_s, h2d_gbps=rp.h2d_gbps,
+                window_read_gbps=rp.window_read_gbps,
                 lat_value=rp.overshoot_s + tm.t_2, lat_e2e=rp.overshoot_s + (t3 - t2),
                 t_scan=tm.t_scan, t_coarse=tm.t_coarse, t_g=tm.t_g, t_c=tm.t_c, t_2=tm.t_2,
                 bytes=tm.scanned_bytes, hit=nhit / (B * L), plan_s=t1 - t0,
@@ -965,10 +1011,22 @@ def main():
                          "(default) or fp32 FMA + exact fp64 re-score of the survivors")
     ap.add_argument("--scan", default="tma", choices=["tma", "ldg"],
                     help="scan kernel: TMA bulk-copy staged (default) or direct LDG")
+    ap.add_argument("--window-load", type=float, default=None,
+                    help="decode-like window: GB/s target read rate of the streamed "
+                         "buffer (default: the config's, 0 = idle window)")
+    ap.add_argument("--window-buffer-gb", type=float, default=None,
+                    help="decode-like window: streamed buffer size in GB")
+    ap.add_argument("--single", default="fused", choices=["fused", "chain"],
+                    help="single-query search: one fused cooperative kernel (default) or "
+                         "the multi-kernel chain")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.window is None:
         args.window = cfg["window_s"]
+    if args.window_load is None:
+        args.window_load = cfg.get("window_load_gbps", 0.0)
+    if args.window_buffer_gb is None:
+        args.window_buffer_gb = cfg.get("window_buffer_gb", 16.0)
     if args.impl == "reference":
         return run_reference(args, cfg)
     if cfg.get("routed"):

@@ -136,7 +136,10 @@ typedef struct {
                               rest, split by measured rates; 2 = every miss
                               the ring can take goes to the GPU */
   uint32_t fetch_chunk_mb; /* ring slot size in MiB; 0 = 512 */
-  uint32_t reserved[1];
+  uint32_t single_chain;   /* single-query search: 0 (default) = one fused
+                              cooperative kernel (query fetch, coarse scores,
+                              top-L, residency split, TMA scan) where the shape
+                              fits shared memory; 1 = the multi-kernel chain */
 } laivg_opts;
 void laivg_opts_default(laivg_opts* o);
 typedef struct laivg_ctx laivg_ctx;
@@ -245,6 +248,8 @@ typedef struct {
   uint32_t n_transferred;
   double window_s;     /* measured duration of the generation-window kernel */
   double h2d_gbps;     /* achieved host->device GB/s of this transfer */
+  double window_read_gbps; /* HBM read rate of a decode-like window
+                              (laivg_window_load), 0 for the idle window */
 } laivg_transfer_report;
 
 /* execute_prefetch (tiered.cpp:86-136): inserts the planned clusters
@@ -280,6 +285,15 @@ int laivg_prefetch_batch(laivg_ctx* ctx, const float* Q_in, uint32_t nq,
 /* Runs only the generation-window kernel (seconds) on the compute stream and
  * returns its measured duration. */
 int laivg_window(laivg_ctx* ctx, double seconds, double* measured_s);
+/* Makes every later generation window decode-like: it streams a device buffer
+ * of buffer_bytes (the "weights") once per token period at full speed, the
+ * token period being buffer_bytes / read_gbps, so the lookahead copies share
+ * HBM, L2 and the SMs with a memory-bound decode. read_gbps = 0 (or
+ * buffer_bytes = 0) restores the idle %globaltimer window. */
+int laivg_window_load(laivg_ctx* ctx, uint64_t buffer_bytes, double read_gbps);
+/* Pinned host <-> device copy rate of this context's GPU, measured with one
+ * large cudaMemcpyAsync per direction (independent of the prefetch path). */
+int laivg_link_peak(laivg_ctx* ctx, uint64_t bytes, double* h2d_gbps, double* d2h_gbps);
 
 /* ---- hybrid search (tiered.cpp:148-198) ---------------------------------- */
 typedef struct {
@@ -314,6 +328,10 @@ typedef struct {
      / final result lists read back (mapped or copied) */
   uint64_t h2d_bytes;
   uint64_t d2h_bytes;
+  /* single query on the fused kernel: its device-event duration (s); t_coarse
+     is then its coarse + selection phase (CTA 0's globaltimer) and t_scan the
+     rest. 0 when the multi-kernel chain ran. */
+  double t_kernel;
 } laivg_hybrid_timing;
 
 /* hybrid_search for one query. fast_out / slow_out (nullable, L entries)

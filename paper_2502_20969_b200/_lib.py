@@ -32,7 +32,7 @@ class Opts(C.Structure):
                 ("max_batch", u32), ("max_probe", u32), ("acc_fp64", u32),
                 ("scan_impl", u32), ("tma_tile", u32), ("tma_stages", u32),
                 ("ctas_per_sm", u32), ("coarse_impl", u32), ("miss_fetch", u32),
-                ("fetch_chunk_mb", u32), ("reserved", u32 * 1)]
+                ("fetch_chunk_mb", u32), ("single_chain", u32)]
 
 
 class Channel(C.Structure):
@@ -41,7 +41,7 @@ class Channel(C.Structure):
 
 class TransferReportC(C.Structure):
     _fields_ = [("t_p", f64), ("bytes", u64), ("overshoot_s", f64), ("n_transferred", u32),
-                ("window_s", f64), ("h2d_gbps", f64)]
+                ("window_s", f64), ("h2d_gbps", f64), ("window_read_gbps", f64)]
 
 
 class CostModelC(C.Structure):
@@ -55,7 +55,7 @@ class HybridTimingC(C.Structure):
                 ("scanned_vectors", u64), ("scanned_bytes", u64), ("fetched_lists", u32),
                 ("cpu_lists", u32), ("fetched_bytes", u64), ("t_fetch", f64),
                 ("peer_lists", u32), ("reserved0", u32), ("peer_bytes", u64),
-                ("h2d_bytes", u64), ("d2h_bytes", u64)]
+                ("h2d_bytes", u64), ("d2h_bytes", u64), ("t_kernel", f64)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/laivg.h
@@ -108,6 +108,8 @@ SIGNATURES = {
     "laivg_incremental_prefetch": (i32, [vp, vp, u64, P(Channel), f64, vp,
                                          P(TransferReportC)]),
     "laivg_window": (i32, [vp, f64, P(f64)]),
+    "laivg_window_load": (i32, [vp, u64, f64]),
+    "laivg_link_peak": (i32, [vp, u64, P(f64), P(f64)]),
     "laivg_hybrid_search": (i32, [vp, vp, i32, i32, P(CostModelC), vp, vp, P(u32), vp,
                                   P(u32), vp, P(u32), P(f64), P(HybridTimingC)]),
     "laivg_coverage": (i32, [vp, vp, vp, i32, P(f64)]),

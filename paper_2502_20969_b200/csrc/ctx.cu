@@ -493,6 +493,7 @@ struct Ctx {
     std::vector<Scored> top;
     std::vector<uint32_t> fast, slow;
     double t_g = 0, t_c = 0, t_2 = 0, t_coarse = 0, t_scan = 0;
+    double t_kernel = 0; // fused single-query kernel (events), 0 for the chain
     uint64_t vecs_gpu = 0, bytes_gpu = 0;
     uint32_t fetch_lists = 0, peer_lists = 0;
     uint64_t fetch_bytes = 0, peer_bytes = 0;
@@ -534,6 +535,74 @@ struct Ctx {
   void merge_fetch(uint32_t q, size_t nchunks, int k, std::vector<Scored>& gpu) const;
   void finish_fetch(size_t nchunks, FetchStats& st);
 
+  // ---- generation window (execute_prefetch / prefetch_batch / window) ----
+  // With a load buffer set (laivg_window_load), the window streams it like a
+  // memory-bound decode (one full read per token period) instead of idling.
+  float* d_wbuf = nullptr;
+  uint64_t wbuf_bytes = 0;
+  double w_rate = 0;                       // target read rate, bytes/s
+  float* d_wsink = nullptr;
+  unsigned long long* d_wread = nullptr;   // bytes the last window read
+  void launch_window_any(double seconds) {
+    if (!(seconds > 0)) return;
+    if (d_wbuf && w_rate > 0) {
+      CK(cudaMemsetAsync(d_wread, 0, sizeof(unsigned long long), comp));
+      const uint64_t period = uint64_t(double(wbuf_bytes) / w_rate * 1e9);
+      launch_window_stream(d_wbuf, wbuf_bytes, uint64_t(seconds * 1e9), std::max<uint64_t>(1, period),
+                           sms, d_wsink, d_wread, comp);
+    } else {
+      launch_window(uint64_t(seconds * 1e9), sms, comp);
+    }
+  }
+  // Read rate of the last window (after it completed), GB/s.
+  double window_read_gbps(double window_s) {
+    if (!d_wbuf || !(w_rate > 0) || !(window_s > 0)) return 0.0;
+    unsigned long long b = 0;
+    CK(cudaMemcpy(&b, d_wread, sizeof(b), cudaMemcpyDeviceToHost));
+    return double(b) / window_s / 1e9;
+  }
+
+  // ---- fused single-query kernel (one cooperative launch per query) ----
+  bool fused_on = true;               // opts.single_chain == 0
+  uint64_t* d_keys = nullptr;         // [nc] order keys of the coarse scores
+  unsigned* d_ctl = nullptr;          // [2] grid barrier word, call sequence
+  unsigned* h_flag = nullptr;         // mapped: sequence number once the probe is out
+  unsigned* dm_flag = nullptr;
+  unsigned long long* h_stamps = nullptr; // mapped [6] phase stamps of CTA 0
+  unsigned long long* dm_stamps = nullptr;
+  unsigned long long* h_cta_stamps = nullptr; // LAIVG_SCAN_PROBE: [sms][3]
+  unsigned long long* dm_cta_stamps = nullptr;
+  unsigned fused_seq = 0;             // launches of the fused kernel executed
+  bool last_fused = false;            // the last single-query chain was fused
+  std::map<uint64_t, size_t> fused_fit; // (L, k) -> smem (0: does not fit)
+  bool use_fused(uint32_t lp, int k, int G) {
+    if (!fused_on || large_nc() || scan_impl != ScanImpl::kTma || G > sms || k > kMaxK) {
+      return false;
+    }
+    const uint64_t key = (uint64_t(lp) << 32) | uint32_t(k);
+    auto it = fused_fit.find(key);
+    if (it == fused_fit.end()) {
+      it = fused_fit.emplace(key, fused_query_smem(ix->nc, ix->d, lp, k, acc_fp64, uint32_t(G),
+                                                   tune)).first;
+    }
+    return it->second != 0;
+  }
+  // Waits until the fused kernel of call `seq` has published its probe.
+  void wait_probe_flag(unsigned seq) {
+    const volatile unsigned* f = h_flag;
+    uint32_t spins = 0;
+    while (*f != seq) {
+      if ((++spins & 0x3fffu) == 0) {
+        const cudaError_t e = cudaStreamQuery(comp);
+        if (e == cudaSuccess) {
+          if (*f == seq) break;
+          throw std::runtime_error("fused query kernel finished without publishing its probe");
+        }
+        if (e != cudaErrorNotReady) throw CudaError(cudaGetErrorString(e));
+      }
+    }
+  }
+
   // ---- the coarse -> select -> scan chain as one CUDA graph per (L, k) ----
   bool use_graphs = std::getenv("LAIVG_GRAPHS") ? std::atoi(std::getenv("LAIVG_GRAPHS")) != 0 : true;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr; // capture-internal fork/join
@@ -556,6 +625,37 @@ struct Ctx {
   // scores, ranking + residency split, scan, results; the probe lands in
   // mapped host memory as soon as it exists.
   void enqueue_coarse_path(uint32_t lp, int k, int G, const float* src) {
+    if (use_fused(lp, k, G)) {
+      // launched directly (not captured): the query row is a kernel
+      // argument. A staged row (HBM) is read by every CTA; the pinned host
+      // row once by CTA 0 (a read of mapped host memory costs microseconds).
+      FusedQuery fq;
+      fq.src = src;
+      fq.qdirect = src != h_Q || std::getenv("LAIVG_FUSED_QDIRECT") ? 1 : 0;
+      fq.dQ = d_Q;
+      fq.cen = d_cen;
+      fq.nc = ix->nc;
+      fq.d = ix->d;
+      fq.L = lp;
+      fq.metric = ix->metric;
+      fq.k = k;
+      fq.keys = d_keys;
+      fq.res_off = d_res;
+      fq.list_off = d_list_off;
+      fq.order_out = dm_order;
+      fq.fcount_out = dm_fcount;
+      fq.flag_out = dm_flag;
+      fq.ctl = d_ctl;
+      fq.stamps = dm_stamps;
+      fq.cta_stamps = dm_cta_stamps;
+      fq.slab = d_slab;
+      fq.ids = d_ids;
+      fq.grid = uint32_t(G);
+      rec(ev_a, comp);
+      launch_fused_query(fq, so, acc_fp64, tune, comp);
+      rec(ev_s, comp); // also marks the results in mapped host memory complete
+      return;
+    }
     if (src == h_Q) {
       launch_fetch_query(h_Q, nullptr, d_Q, ix->d, comp);
     } else {
@@ -585,6 +685,13 @@ struct Ctx {
   std::map<uint64_t, GraphEntry> graph_tab;
   void run_coarse_path(uint32_t lp, int k, int G, const float* src, PhaseTrace* tr = nullptr) {
     const bool staged = src != h_Q;
+    last_fused = use_fused(lp, k, G);
+    if (last_fused) {
+      // one kernel: a direct launch costs less host time than a graph launch
+      ++fused_seq; // this call executes one fused launch
+      enqueue_coarse_path(lp, k, G, src);
+      return;
+    }
     if (staged) *h_qslot = src; // read by the chain's first kernel
     const uint64_t key = (uint64_t(lp) << 33) | (uint64_t(uint32_t(k)) << 1) | (staged ? 1 : 0);
     auto it = graph_tab.find(key);
@@ -639,12 +746,14 @@ Ctx::~Ctx() {
                   (void*)ft.cluster, (void*)ft.pre, (void*)ft.count, (void*)ft.cta,
                   (void*)so.part_s, (void*)so.part_id, (void*)so.part_vi, (void*)so.ticket,
                   (void*)so.gpart_s, (void*)so.gpart_id, (void*)so.gpart_vi,
-                  (void*)d_staged, (void*)d_approx, (void*)d_cnorm}) {
+                  (void*)d_staged, (void*)d_approx, (void*)d_cnorm, (void*)d_keys,
+                  (void*)d_ctl, (void*)d_wbuf, (void*)d_wsink, (void*)d_wread}) {
     if (p) cudaFree(p);
   }
   for (void* p : {(void*)res_stage[0], (void*)res_stage[1], (void*)h_Q, (void*)h_qslot,
                   (void*)h_order, (void*)h_out_s, (void*)h_out_id,
-                  (void*)h_out_cnt, (void*)h_fcount}) {
+                  (void*)h_out_cnt, (void*)h_fcount, (void*)h_flag, (void*)h_stamps,
+                  (void*)h_cta_stamps}) {
     if (p) cudaFreeHost(p);
   }
   for (void* p : {(void*)fft.slab, (void*)fft.row, (void*)fft.len, (void*)fft.cluster,
@@ -828,6 +937,16 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   h_out_id = pin_alloc_mapped<uint64_t>(size_t(max_batch) * kMaxK, &dm_out_id);
   h_out_cnt = pin_alloc_mapped<uint32_t>(max_batch, &dm_out_cnt);
   h_fcount = pin_alloc_mapped<uint32_t>(max_batch, &dm_fcount);
+  fused_on = o.single_chain == 0 && !std::getenv("LAIVG_CHAIN");
+  d_keys = dev_alloc<uint64_t>(std::max(nc, 1u));
+  d_ctl = dev_alloc<unsigned>(2);
+  CK(cudaMemset(d_ctl, 0, 2 * sizeof(unsigned)));
+  h_flag = pin_alloc_mapped<unsigned>(1, &dm_flag);
+  *h_flag = 0;
+  h_stamps = pin_alloc_mapped<unsigned long long>(32, &dm_stamps);
+  if (std::getenv("LAIVG_SCAN_PROBE")) {
+    h_cta_stamps = pin_alloc_mapped<unsigned long long>(size_t(sms) * 4, &dm_cta_stamps);
+  }
   // the main scan writes its results straight into host memory
   so.out_s = dm_out_s;
   so.out_id = dm_out_id;
@@ -1594,7 +1713,9 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
 
   // Host: split the probe by residency (tiered.cpp:155-161) and scan the
   // misses while the GPU scans the hits.
-  if (!explicit_probe && lp) CK(cudaEventSynchronize(ev_b));
+  const bool fused = !explicit_probe && !wide && last_fused;
+  if (fused && lp) wait_probe_flag(fused_seq);
+  else if (!explicit_probe && lp) CK(cudaEventSynchronize(ev_b));
   tr.mark("probe_wait");
   for (uint32_t i = 0; i < lp; ++i) {
     const uint32_t c = h_order[i];
@@ -1643,11 +1764,60 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
   r.d2h_bytes += uint64_t(lp) * sizeof(uint32_t) + sizeof(uint32_t) +
                  result_bytes(1, uint32_t(G), k) + fetch_result_bytes(nchunks, 1, k);
   float ms = 0;
-  CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
-  r.t_coarse = ms * 1e-3;
-  tr.mark("ev1");
-  CK(cudaEventElapsedTime(&ms, explicit_probe ? ev_p : ev_b, ev_s));
-  r.t_scan = ms * 1e-3;
+  if (fused) {
+    // one kernel: its event time; the coarse + selection phase from CTA 0's
+    // globaltimer stamps (entry -> scan ranges ready)
+    CK(cudaEventElapsedTime(&ms, ev_a, ev_s));
+    r.t_kernel = ms * 1e-3;
+    r.t_coarse = std::min(r.t_kernel, double(h_stamps[5] - h_stamps[0]) * 1e-9);
+    r.t_scan = r.t_kernel - r.t_coarse;
+    if (tr.on) {
+      std::fprintf(stderr,
+                   "[laivg fused] us from CTA 0 entry: query %.2f keys %.2f loaded %.2f "
+                   "selected %.2f ranges %.2f loop end %.2f done %.2f | kernel (events) %.2f\n",
+                   (h_stamps[1] - h_stamps[0]) * 1e-3, (h_stamps[2] - h_stamps[0]) * 1e-3,
+                   (h_stamps[3] - h_stamps[0]) * 1e-3, (h_stamps[4] - h_stamps[0]) * 1e-3,
+                   (h_stamps[5] - h_stamps[0]) * 1e-3, (h_stamps[6] - h_stamps[0]) * 1e-3,
+                   (h_stamps[7] - h_stamps[0]) * 1e-3, r.t_kernel * 1e6);
+      std::string sel = "[laivg fused] select us from keys loaded:";
+      for (int i = 8; i < 19; ++i) {
+        if (h_stamps[i] >= h_stamps[3]) {
+          sel += " " + std::to_string(i - 8) + ":" + std::to_string((h_stamps[i] - h_stamps[3]) * 1e-3);
+        }
+      }
+      sel += " passes " + std::to_string(h_stamps[19]);
+      std::fprintf(stderr, "%s\n", sel.c_str());
+      std::fprintf(stderr, "[laivg fused] CTA 0: query copied %.2f, CTA merge done %.2f\n",
+                   (h_stamps[21] - h_stamps[0]) * 1e-3, (h_stamps[22] - h_stamps[0]) * 1e-3);
+      if (h_cta_stamps) {
+        unsigned long long e0 = ~0ull, e1 = 0, b1a = ~0ull, b1b = 0, b2a = ~0ull, b2b = 0,
+                           da = ~0ull, db = 0;
+        for (int b = 0; b < sms; ++b) {
+          const unsigned long long* p = h_cta_stamps + 4 * b;
+          e0 = std::min(e0, p[0]);
+          e1 = std::max(e1, p[0]);
+          b1a = std::min(b1a, p[1]);
+          b1b = std::max(b1b, p[1]);
+          b2a = std::min(b2a, p[2]);
+          b2b = std::max(b2b, p[2]);
+          da = std::min(da, p[3]);
+          db = std::max(db, p[3]);
+        }
+        std::fprintf(stderr,
+                     "[laivg fused] CTAs (us from first entry): entry <= %.2f, barrier 1 exit "
+                     "%.2f..%.2f, barrier 2 exit %.2f..%.2f, done %.2f..%.2f (CTA 0 %.2f)\n",
+                     (e1 - e0) * 1e-3, (b1a - e0) * 1e-3, (b1b - e0) * 1e-3, (b2a - e0) * 1e-3,
+                     (b2b - e0) * 1e-3, (da - e0) * 1e-3, (db - e0) * 1e-3,
+                     (h_cta_stamps[3] - e0) * 1e-3);
+      }
+    }
+  } else {
+    CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
+    r.t_coarse = ms * 1e-3;
+    tr.mark("ev1");
+    CK(cudaEventElapsedTime(&ms, explicit_probe ? ev_p : ev_b, ev_s));
+    r.t_scan = ms * 1e-3;
+  }
   tr.mark("ev2");
   if (nchunks || explicit_probe || wide) {
     CK(cudaEventElapsedTime(&ms, ev_a, nchunks ? ev_fdone : ev_s));
@@ -1725,6 +1895,7 @@ void fill_timing(laivg_hybrid_timing* t, const Ctx::Result& r,
   t->t_2 = r.t_2;
   t->t_coarse = r.t_coarse;
   t->t_scan = r.t_scan;
+  t->t_kernel = r.t_kernel;
   t->scanned_vectors = r.vecs_gpu;
   t->scanned_bytes = r.bytes_gpu;
   t->fetched_lists = r.fetch_lists;
@@ -1772,6 +1943,7 @@ void fill_batch_timing(laivg_hybrid_timing* t, const Ctx::BatchResult& r,
   t->t_2 = r.t_2;
   t->t_coarse = r.t_coarse;
   t->t_scan = r.t_scan;
+  t->t_kernel = 0.0;
   t->scanned_vectors = r.vecs_gpu;
   t->scanned_bytes = r.bytes_gpu;
   t->fetched_lists = r.fetch_lists;
@@ -2316,7 +2488,7 @@ int laivg_execute_prefetch(laivg_ctx* ctx, const uint32_t* plan, uint32_t n,
     CK(cudaEventRecord(x.ev_base, x.comp));
     CK(cudaStreamWaitEvent(x.copy, x.ev_base, 0));
     const bool win = mode == LAIVG_CHAN_DEVICE && overlap_window_s > 0;
-    if (win) laivg::launch_window(uint64_t(overlap_window_s * 1e9), x.sms, x.comp);
+    if (win) x.launch_window_any(overlap_window_s);
     CK(cudaEventRecord(x.ev_win, x.comp));
     CK(cudaEventRecord(x.ev_cp0, x.copy));
     uint32_t done = 0;
@@ -2349,6 +2521,7 @@ int laivg_execute_prefetch(laivg_ctx* ctx, const uint32_t* plan, uint32_t n,
     r.n_transferred = done;
     r.window_s = win ? ms_win * 1e-3 : 0.0;
     r.h2d_gbps = ms_cp > 0 ? double(bytes) / (ms_cp * 1e-3) / 1e9 : 0.0;
+    r.window_read_gbps = win ? x.window_read_gbps(r.window_s) : 0.0;
     if (mode == LAIVG_CHAN_SIMULATED) {
       r.t_p = double(bytes) / chan->bandwidth_bytes_per_s; // tiered.cpp:131
       r.overshoot_s = std::max(0.0, r.t_p - overlap_window_s);
@@ -2389,7 +2562,7 @@ int laivg_prefetch_batch(laivg_ctx* ctx, const float* Q_in, uint32_t nq,
     CK(cudaEventRecord(x.ev_base, x.comp));
     CK(cudaStreamWaitEvent(x.copy, x.ev_base, 0));
     const bool win = overlap_window_s > 0;
-    if (win) laivg::launch_window(uint64_t(overlap_window_s * 1e9), x.sms, x.comp);
+    if (win) x.launch_window_any(overlap_window_s);
     CK(cudaEventRecord(x.ev_win, x.comp));
     CK(cudaEventRecord(x.ev_cp0, x.copy));
     uint64_t bytes = 0;
@@ -2433,6 +2606,7 @@ int laivg_prefetch_batch(laivg_ctx* ctx, const float* Q_in, uint32_t nq,
     r.n_transferred = done;
     r.window_s = win ? ms_win * 1e-3 : 0.0;
     r.h2d_gbps = ms_cp > 0 ? double(bytes) / (ms_cp * 1e-3) / 1e9 : 0.0;
+    r.window_read_gbps = win ? x.window_read_gbps(r.window_s) : 0.0;
     r.t_p = ms_cp * 1e-3;
     r.overshoot_s = std::max(0.0, double(ms_end - (win ? ms_win : 0.0f)) * 1e-3);
     if (rep) *rep = r;
@@ -2463,12 +2637,73 @@ int laivg_window(laivg_ctx* ctx, double seconds, double* measured_s) {
     set_ctx_device(ctx);
     Ctx& x = ctx->c;
     CK(cudaEventRecord(x.ev_base, x.comp));
-    if (seconds > 0) laivg::launch_window(uint64_t(seconds * 1e9), x.sms, x.comp);
+    x.launch_window_any(seconds);
     CK(cudaEventRecord(x.ev_win, x.comp));
     CK(cudaEventSynchronize(x.ev_win));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, x.ev_base, x.ev_win));
     if (measured_s) *measured_s = ms * 1e-3;
+  });
+}
+
+int laivg_window_load(laivg_ctx* ctx, uint64_t buffer_bytes, double read_gbps) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    Ctx& x = ctx->c;
+    if (read_gbps < 0) throw std::invalid_argument("read_gbps must be >= 0");
+    CK(cudaStreamSynchronize(x.comp));
+    if (x.d_wbuf && (buffer_bytes == 0 || buffer_bytes != x.wbuf_bytes)) {
+      CK(cudaFree(x.d_wbuf));
+      x.d_wbuf = nullptr;
+      x.wbuf_bytes = 0;
+    }
+    buffer_bytes &= ~uint64_t(63);
+    if (buffer_bytes && !x.d_wbuf) {
+      x.d_wbuf = laivg::dev_alloc<float>(buffer_bytes / sizeof(float));
+      CK(cudaMemset(x.d_wbuf, 0, buffer_bytes));
+      x.wbuf_bytes = buffer_bytes;
+      if (!x.d_wsink) x.d_wsink = laivg::dev_alloc<float>(1);
+      if (!x.d_wread) x.d_wread = laivg::dev_alloc<unsigned long long>(1);
+    }
+    x.w_rate = read_gbps * 1e9;
+  });
+}
+
+int laivg_link_peak(laivg_ctx* ctx, uint64_t bytes, double* h2d_gbps, double* d2h_gbps) {
+  return guard([&] {
+    set_ctx_device(ctx);
+    Ctx& x = ctx->c;
+    if (bytes == 0) throw std::invalid_argument("bytes must be > 0");
+    void* h = nullptr;
+    void* d = nullptr;
+    CK(cudaHostAlloc(&h, bytes, cudaHostAllocPortable));
+    try {
+      std::memset(h, 1, bytes);
+      d = laivg::dev_alloc<unsigned char>(bytes);
+      cudaStream_t st = x.aux;
+      auto timed = [&](cudaMemcpyKind kind) {
+        void* dst = kind == cudaMemcpyHostToDevice ? d : h;
+        const void* src = kind == cudaMemcpyHostToDevice ? h : d;
+        CK(cudaMemcpyAsync(dst, src, bytes, kind, st)); // warm the path
+        CK(cudaEventRecord(x.ev_cp0, st));
+        for (int i = 0; i < 3; ++i) CK(cudaMemcpyAsync(dst, src, bytes, kind, st));
+        CK(cudaEventRecord(x.ev_cp1, st));
+        CK(cudaEventSynchronize(x.ev_cp1));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, x.ev_cp0, x.ev_cp1));
+        return 3.0 * double(bytes) / (ms * 1e-3) / 1e9;
+      };
+      const double a = timed(cudaMemcpyHostToDevice);
+      const double b = timed(cudaMemcpyDeviceToHost);
+      if (h2d_gbps) *h2d_gbps = a;
+      if (d2h_gbps) *d2h_gbps = b;
+    } catch (...) {
+      if (d) cudaFree(d);
+      cudaFreeHost(h);
+      throw;
+    }
+    CK(cudaFree(d));
+    CK(cudaFreeHost(h));
   });
 }
 

@@ -1208,7 +1208,8 @@ template <int KPL>
 __device__ void scan_epilogue(WarpTopK<KPL>& top, int metric, int k, int kk, bool rerank,
                               unsigned char* scratch, const ScanOut& out, const float* sq,
                               const float* __restrict__ slab, const uint64_t* __restrict__ ids,
-                              uint32_t d, uint64_t V, int first, int nw) {
+                              uint32_t d, uint64_t V, int first, int nw,
+                              unsigned long long* t_merged = nullptr) {
   __shared__ bool last;
   const int warp = threadIdx.x >> 5;
   const uint32_t q = blockIdx.y, G = gridDim.x;
@@ -1235,6 +1236,7 @@ __device__ void scan_epilogue(WarpTopK<KPL>& top, int metric, int k, int kk, boo
   }
   __syncthreads();
   merge_tree(metric, ids, &cur, &alt, wl, m);
+  if (t_merged && threadIdx.x == 0) *t_merged = globaltimer();
   const uint64_t pbase = static_cast<uint64_t>(q) * G * kk;
   if (out.cta_s != nullptr && !rerank) {
     // host-final mode: the host merges the grid's sorted lists
@@ -1356,50 +1358,23 @@ struct Cursor {
 constexpr int kConsumers = 8;
 constexpr int kTmaThreads = 32 * (kConsumers + 1);
 
+// One CTA's share of a query's TMA scan: the range `cs` of the query's
+// flattened fast-list vector space (V vectors in all), tiles streamed through
+// the ring at `stage` (S stages of T rows), then the CTA merge and the
+// epilogue. sq: the query in shared memory. Shared by scan_tma_kernel and
+// fused_query_kernel. Returns the time the last tile was consumed when
+// `probe` stamps are on.
 template <bool kFp64, int KPL, int NCH>
-__global__ void __launch_bounds__(kTmaThreads, 1)
-    scan_tma_kernel(const float* __restrict__ Q, uint32_t d, int metric, int k, int kk,
-                    FastTable ft, const float* __restrict__ slab,
-                    const uint64_t* __restrict__ ids_all, ScanOut out, uint32_t T, uint32_t S) {
+__device__ __forceinline__ unsigned long long scan_tma_cta(
+    const float* sq, uint32_t d, int metric, int k, int kk, const FastTable& ft, uint64_t tb,
+    CtaStart cs, uint64_t V, const float* __restrict__ slab, const uint64_t* __restrict__ ids_all,
+    const ScanOut& out, uint32_t T, uint32_t S, unsigned char* smem, uint64_t* full,
+    uint64_t* empty, uint64_t* mrow, uint32_t* mvi, uint32_t* mn, bool probe,
+    unsigned long long* s_first_tile, unsigned long long* t_merged = nullptr) {
   using ACC = typename std::conditional<kFp64, double, float>::type;
-  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t stage_floats = static_cast<size_t>(T) * d;
   float* stage = reinterpret_cast<float*>(smem);
-  // the stage ring doubles as the epilogue's scratch once every tile is used
-  size_t off = (static_cast<size_t>(S) * stage_floats * 4 + 127) & ~size_t(127);
-  const size_t merge_bytes = epilogue_scratch(kConsumers, kk, gridDim.x);
-  if (off < merge_bytes) off = (merge_bytes + 127) & ~size_t(127);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + off);
-  uint64_t* empty = full + S;
-  uint64_t* mrow = empty + S;                                 // [S][T]
-  uint32_t* mvi = reinterpret_cast<uint32_t*>(mrow + S * T);  // [S][T]
-  uint32_t* mn = mvi + S * T;                                 // [S]
-  float* sq = reinterpret_cast<float*>(
-      (reinterpret_cast<uintptr_t>(mn + S) + 15) & ~uintptr_t(15));
-
-  const uint32_t q = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // probe stamps stay on chip until the end: a store to mapped host memory
-  // stalls the issuing warp for microseconds
-  unsigned long long* probe =
-      out.probe ? out.probe + (static_cast<uint64_t>(q) * gridDim.x + blockIdx.x) * 4 : nullptr;
-  __shared__ unsigned long long s_first_tile;
-  const unsigned long long t_entry = probe ? globaltimer() : 0ull;
-  const float* qv = Q + static_cast<uint64_t>(q) * d;
-  for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) sq[i] = qv[i];
-  if (threadIdx.x == 0) {
-    for (uint32_t s = 0; s < S; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, kConsumers);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  const uint64_t tb = static_cast<uint64_t>(q) * ft.stride;
-  const uint64_t* pre = ft.pre + static_cast<uint64_t>(q) * (ft.stride + 1);
-  // this CTA's range, precomputed by the partition step (no search here)
-  const CtaStart cs = ft.cta[static_cast<uint64_t>(q) * gridDim.x + blockIdx.x];
   const uint32_t nvec = cs.n;
   const uint32_t ntiles = (nvec + T - 1) / T;
 
@@ -1448,7 +1423,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         }
       }
     }
-  } else {
+  } else if (warp <= kConsumers) { // (the fused kernel's host I/O warp idles)
     // ---------------- consumers ----------------
     const int cw = warp - 1;
     float qf[NCH > 0 ? NCH * 4 : 1];
@@ -1472,7 +1447,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     for (uint32_t i = 0; i < ntiles; ++i) {
       const uint32_t s = i % S;
       mbar_wait(full + s, (i / S) & 1u);
-      if (probe && i == 0 && cw == 0 && lane == 0) s_first_tile = globaltimer();
+      if (probe && i == 0 && cw == 0 && lane == 0) *s_first_tile = globaltimer();
       const uint32_t n = mn[s];
       const float* base = stage + s * stage_floats;
       for (uint32_t j = cw; j < n; j += 2 * kConsumers) {
@@ -1525,16 +1500,698 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   }
   __syncthreads(); // every tile consumed: the stage ring is free for merging
   const unsigned long long t_loop = probe ? globaltimer() : 0ull;
-
-  const uint64_t V = pre[ft.count[q]];
   scan_epilogue<KPL>(top, metric, k, kk, !kFp64, smem, out, sq, slab, ids_all, d, V, 1,
-                     kConsumers);
+                     kConsumers, t_merged);
+  return t_loop;
+}
+
+// Shared-memory layout of the TMA ring (scan_tma_kernel, fused_query_kernel):
+// [S stages of T rows | >= the epilogue's merge scratch] [full[S] empty[S]]
+// [mrow[S][T]] [mvi[S][T]] [mn[S]] [sq[d]] — then the fused kernel's tables.
+struct RingSmem {
+  uint64_t* full;
+  uint64_t* empty;
+  uint64_t* mrow;
+  uint32_t* mvi;
+  uint32_t* mn;
+  float* sq;
+  unsigned char* end; // first byte after sq[d]
+};
+__device__ __forceinline__ RingSmem ring_smem(unsigned char* smem, uint32_t T, uint32_t S,
+                                              uint32_t d, int kk) {
+  RingSmem r;
+  const size_t stage_floats = static_cast<size_t>(T) * d;
+  size_t off = (static_cast<size_t>(S) * stage_floats * 4 + 127) & ~size_t(127);
+  const size_t merge_bytes = epilogue_scratch(kConsumers, kk, gridDim.x);
+  if (off < merge_bytes) off = (merge_bytes + 127) & ~size_t(127);
+  r.full = reinterpret_cast<uint64_t*>(smem + off);
+  r.empty = r.full + S;
+  r.mrow = r.empty + S;                                  // [S][T]
+  r.mvi = reinterpret_cast<uint32_t*>(r.mrow + S * T);   // [S][T]
+  r.mn = r.mvi + S * T;                                  // [S]
+  r.sq = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(r.mn + S) + 15) & ~uintptr_t(15));
+  r.end = reinterpret_cast<unsigned char*>(r.sq + d);
+  return r;
+}
+
+__device__ __forceinline__ void ring_init(const RingSmem& r, uint32_t S) {
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < S; ++s) {
+      mbar_init(r.full + s, 1);
+      mbar_init(r.empty + s, kConsumers);
+    }
+    fence_mbar_init();
+  }
+}
+
+template <bool kFp64, int KPL, int NCH>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    scan_tma_kernel(const float* __restrict__ Q, uint32_t d, int metric, int k, int kk,
+                    FastTable ft, const float* __restrict__ slab,
+                    const uint64_t* __restrict__ ids_all, ScanOut out, uint32_t T, uint32_t S) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const RingSmem rs = ring_smem(smem, T, S, d, kk);
+  const uint32_t q = blockIdx.y;
+  // probe stamps stay on chip until the end: a store to mapped host memory
+  // stalls the issuing warp for microseconds
+  unsigned long long* probe =
+      out.probe ? out.probe + (static_cast<uint64_t>(q) * gridDim.x + blockIdx.x) * 4 : nullptr;
+  __shared__ unsigned long long s_first_tile;
+  const unsigned long long t_entry = probe ? globaltimer() : 0ull;
+  const float* qv = Q + static_cast<uint64_t>(q) * d;
+  for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) rs.sq[i] = qv[i];
+  ring_init(rs, S);
+  __syncthreads();
+
+  const uint64_t tb = static_cast<uint64_t>(q) * ft.stride;
+  const uint64_t* pre = ft.pre + static_cast<uint64_t>(q) * (ft.stride + 1);
+  // this CTA's range, precomputed by the partition step (no search here)
+  const CtaStart cs = ft.cta[static_cast<uint64_t>(q) * gridDim.x + blockIdx.x];
+  const uint64_t V = pre[ft.count[q]];
+  const unsigned long long t_loop = scan_tma_cta<kFp64, KPL, NCH>(
+      rs.sq, d, metric, k, kk, ft, tb, cs, V, slab, ids_all, out, T, S, smem, rs.full, rs.empty,
+      rs.mrow, rs.mvi, rs.mn, probe != nullptr, &s_first_tile);
   if (probe && threadIdx.x == 0) {
     const unsigned long long t_done = globaltimer();
     probe[0] = t_entry;
     probe[1] = s_first_tile;
     probe[2] = t_loop;
     probe[3] = t_done;
+  }
+}
+
+// --------------------------------------------------------------------------
+// fused single-query kernel: query fetch -> coarse scores -> top-L selection
+// -> residency split -> TMA scan, one cooperative launch (ivf.cpp:269-343,
+// tiered.cpp:148-185). The multi-kernel chain pays a launch gap per kernel and
+// ranks on one SM; here every CTA scores a slice of the centroids, two grid
+// barriers publish the query and the scores, and every CTA then ranks all nc
+// keys itself (radix select in shared memory), splits the probe by residency
+// and derives its own scan range, so the scan starts with no further barrier.
+// --------------------------------------------------------------------------
+constexpr int kFusedWarps = kConsumers + 2; // producer, 8 consumers, host I/O
+constexpr int kFusedThreads = 32 * kFusedWarps;
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid-wide barrier of a cooperative launch (every CTA co-resident). The
+// word's top bit flips once all gridDim.x CTAs have arrived (CTA 0 adds
+// 2^31 - (G - 1), the others 1), so it needs no reset between barriers or
+// launches. A watchdog turns a broken barrier into a launch error instead
+// of a hung device.
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned add = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
+    __threadfence();
+    const unsigned old = atomicAdd(bar, add);
+    const uint64_t t0 = globaltimer();
+    while (((old ^ ld_acquire_gpu(bar)) & 0x80000000u) == 0u) {
+      if (globaltimer() - t0 > 4000000000ull) __trap();
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+struct FusedArgs {
+  const float* src;             // query row (pinned host or HBM), unless
+  const float* const* slot;     // set: mapped word holding the row pointer
+  float* dQ;                    // HBM copy of the query, read by every CTA
+  const float* cen;
+  uint32_t nc, d, L;
+  int metric;
+  uint64_t* keys;               // [nc] order keys of the coarse scores
+  const int64_t* res_off;
+  const uint64_t* list_off;
+  uint32_t* order_out;          // [L] the probe (mapped host memory)
+  uint32_t* fcount_out;         // fast-list count (mapped)
+  unsigned* flag_out;           // mapped: call sequence number, probe is out
+  unsigned* ctl;                // [0] grid barrier word, [1] call sequence
+  unsigned long long* stamps;   // [32] phase stamps of CTA 0 (mapped), nullable
+  unsigned long long* cta_stamps; // [G][4] entry, query ready, keys ready, done; nullable
+  int qdirect;                  // every CTA reads a host row itself (diagnostics)
+  const float* slab;
+  const uint64_t* ids;
+  ScanOut out;
+  uint32_t T, S;
+  int k, kk;
+};
+
+// Shared memory of the fused kernel beyond the ring (host and device agree):
+// fast table (slab, row, pre, len, cluster) for L lists + G scan starts.
+__host__ __device__ inline size_t fused_tables_bytes(uint32_t L, uint32_t G) {
+  return 16 + static_cast<size_t>(L) * (8 + 8 + 4 + 4) + (static_cast<size_t>(L) + 1) * 8 +
+         static_cast<size_t>(G) * sizeof(CtaStart) + 16;
+}
+// Selection scratch, aliased onto the ring before the scan starts.
+__host__ __device__ inline size_t fused_select_bytes(uint32_t nc, uint32_t L) {
+  return 2 * (static_cast<size_t>(nc) * 12 + 16) + static_cast<size_t>(L) * (8 + 4 + 4) + 64;
+}
+
+template <int R, int NCHC>
+__device__ __forceinline__ void fused_load_rows(const float* __restrict__ cen, uint32_t nc,
+                                                uint32_t d4, uint32_t c0, int lane,
+                                                float4 (&xs)[R][NCHC]) {
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    const uint32_t c = c0 + u < nc ? c0 + u : 0u;
+    const float4* r4 = reinterpret_cast<const float4*>(cen + static_cast<uint64_t>(c) * d4 * 4);
+#pragma unroll
+    for (int t = 0; t < NCHC; ++t) {
+      const uint32_t j = lane + 32u * t;
+      xs[u][t] = (c0 + u < nc && j < d4) ? __ldg(r4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+}
+
+// Scores of rows c0..c0+R-1 with exactly warp_coarse_score's sequence
+// (lane-strided fp64 terms, then the butterfly), stored as order keys.
+template <int R, int NCHC>
+__device__ __forceinline__ void fused_score_rows(const float* sq, uint32_t nc, uint32_t d4,
+                                                 uint32_t c0, int lane, int metric,
+                                                 const float4 (&xs)[R][NCHC], uint64_t* keys) {
+  double acc[R];
+#pragma unroll
+  for (int u = 0; u < R; ++u) acc[u] = 0.0;
+#pragma unroll
+  for (int t = 0; t < NCHC; ++t) {
+    const uint32_t j = lane + 32u * t;
+    if (j < d4) {
+      const float4 qq = reinterpret_cast<const float4*>(sq)[j];
+      const double qd[4] = {qq.x, qq.y, qq.z, qq.w};
+#pragma unroll
+      for (int u = 0; u < R; ++u) Acc4<true>::run(metric, qd, xs[u][t], acc[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    const double v = warp_sum(acc[u]);
+    if (lane == 0 && c0 + u < nc) __stcg(reinterpret_cast<unsigned long long*>(keys) + c0 + u,
+                                         static_cast<unsigned long long>(order_key(v, metric)));
+  }
+}
+
+// ---- top-L selection inside one CTA -------------------------------------
+// The ranking order is (key, cluster id) ascending (ivf.cpp:282-289), i.e.
+// the unique 96-bit composite key:id. A radix select walks its digits from
+// the highest bit where the keys differ; each pass histograms the current
+// group (the entries sharing the resolved prefix), moves the entries of lower
+// bins to the selection and keeps the boundary bin as the next, much smaller
+// group. It stops when the boundary bin is taken whole or the group is small
+// enough to rank directly. The selected L entries are then ordered by rank
+// counting.
+constexpr uint32_t kRankCap = 64;
+
+__device__ __forceinline__ bool comp_less(uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
+  return ka < kb || (ka == kb && va < vb);
+}
+// Bits [shift, shift + w) of the composite (key << 32 | id), w <= 8.
+__device__ __forceinline__ uint32_t comp_digit(uint64_t key, uint32_t id, int shift, uint32_t mask) {
+  const uint64_t v = shift >= 32 ? (key >> (shift - 32))
+                                 : ((key << (32 - shift)) | (static_cast<uint64_t>(id) >> shift));
+  return static_cast<uint32_t>(v) & mask;
+}
+
+struct SelectScratch {
+  uint64_t* gk[2]; // group keys, ping-pong (nc entries each)
+  uint32_t* gv[2]; // group ids
+  uint64_t* sel_k; // the L selected
+  uint32_t* sel_v;
+};
+
+// The first L (L <= nc) of the ranking of sk[0, nc) into probe[0, L). va /
+// vo / kmin: the AND, OR and minimum of all keys (computed while loading
+// them). sk may be overwritten (its space backs group buffer 1).
+//
+// Fast path: warp 0 ranks 64 evenly spaced keys; the one of rank ~3L*64/nc
+// is a threshold with about 3L keys below it. One pass histograms only the
+// keys at or below it (few, so the shared-memory atomics hardly collide) into
+// 256 bins relative to kmin; the lower bins go to the selection and the
+// boundary bin becomes the group. If fewer than L keys fall below the
+// threshold (an unlucky sample) the selection restarts on the general path:
+// radix passes over the composite bits from the highest differing one.
+__device__ void block_select_topL(const uint64_t* sk, uint32_t nc, uint32_t L,
+                                  unsigned long long va, unsigned long long vo,
+                                  unsigned long long kmin, const SelectScratch& sc,
+                                  uint32_t* probe, unsigned long long* dbg = nullptr) {
+  // dbg (thread 0, diagnostics): [0] start, [1..8] after each pass,
+  // [9] selected, [10] ranked, [11] passes run
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t s_nsel, s_ng, s_need, s_m, s_dsel, s_before, s_flag;
+  __shared__ unsigned long long s_test, s_and, s_or, w_ka[32], w_ko[32], w_ia[32], w_io[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  if (L == 0) return;
+  if (dbg && threadIdx.x == 0) dbg[0] = globaltimer();
+  uint64_t* gk[2] = {sc.gk[0], sc.gk[1]};
+  uint32_t* gv[2] = {sc.gv[0], sc.gv[1]};
+  uint64_t* selk = sc.sel_k;
+  uint32_t* selv = sc.sel_v;
+  int npass = 0;
+
+  // the boundary bin of a histogram (warp 0): s_dsel, s_before (entries in
+  // lower bins), s_m (boundary bin size), s_flag = 1 if it is taken whole,
+  // 2 if the histogram holds fewer than `need` entries
+  auto find_boundary = [&](uint32_t need) {
+    uint32_t h[8], sum = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      h[e] = hist[lane * 8 + e];
+      sum += h[e];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
+    }
+    uint32_t before = incl - sum;
+    if (before < need && need <= incl) {
+      int e = 0;
+      while (before + h[e] < need) before += h[e++];
+      s_dsel = static_cast<uint32_t>(lane * 8 + e);
+      s_before = before;
+      s_flag = h[e] == need - before ? 1u : 0u;
+      s_m = h[e];
+    }
+    if (lane == 31 && incl < need) s_flag = 2u;
+    if (lane == 0) s_ng = 0;
+  };
+
+  if (L >= nc) {
+    for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
+      selk[i] = sk[i];
+      selv[i] = i;
+    }
+  } else {
+    if (threadIdx.x == 0) {
+      s_nsel = 0;
+      s_need = L;
+      s_test = ~0ull;
+    }
+    // ---- threshold from a 64-key sample -------------------------------
+    const uint32_t rs = static_cast<uint32_t>((3ull * L * 64 + nc - 1) / nc);
+    const bool sampled = rs < 48 && nc >= 512;
+    if (sampled) {
+      // rank of each sample among the 64 (ties by sample index): every
+      // thread compares one sample with a slice of the others
+      __shared__ uint32_t srank[64];
+      __shared__ unsigned long long sval[64];
+      if (threadIdx.x < 64) {
+        srank[threadIdx.x] = 0;
+        sval[threadIdx.x] = sk[static_cast<uint64_t>(threadIdx.x) * nc / 64];
+      }
+      __syncthreads();
+      const uint32_t parts = max(1u, blockDim.x / 64u);
+      if (threadIdx.x < parts * 64u) {
+        const uint32_t si = threadIdx.x & 63u, part = threadIdx.x >> 6;
+        const unsigned long long v = sval[si];
+        uint32_t r = 0;
+        for (uint32_t j = part * 64u / parts; j < (part + 1) * 64u / parts; ++j) {
+          const unsigned long long b = sval[j];
+          r += (b < v || (b == v && j < si)) ? 1u : 0u;
+        }
+        atomicAdd(&srank[si], r);
+      }
+      __syncthreads();
+      if (threadIdx.x < 64 && srank[threadIdx.x] == rs) s_test = sval[threadIdx.x];
+    }
+    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const unsigned long long T = s_test;
+    int cur = -1; // -1: the group is sk with ids 0..nc-1
+    bool done = false, general = T == ~0ull;
+    if (!general) {
+      const unsigned long long span = T - kmin;
+      const int sh = span ? max(0, 64 - __clzll(static_cast<long long>(span)) - 8) : 0;
+      for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
+        const unsigned long long k = sk[i];
+        if (k <= T) atomicAdd(&hist[static_cast<uint32_t>((k - kmin) >> sh)], 1u);
+      }
+      __syncthreads();
+      if (warp == 0) find_boundary(L);
+      __syncthreads();
+      if (s_flag == 2u) {
+        general = true; // fewer than L keys at or below the sample threshold
+      } else {
+        const uint32_t dsel = s_dsel, whole = s_flag;
+        for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
+          const unsigned long long k = sk[i];
+          if (k > T) continue;
+          const uint32_t bn = static_cast<uint32_t>((k - kmin) >> sh);
+          if (bn < dsel || (bn == dsel && whole)) {
+            const uint32_t p = atomicAdd(&s_nsel, 1u);
+            selk[p] = k;
+            selv[p] = i;
+          } else if (bn == dsel) {
+            const uint32_t p = atomicAdd(&s_ng, 1u);
+            gk[0][p] = k;
+            gv[0][p] = i;
+          }
+        }
+        ++npass;
+        __syncthreads();
+        if (dbg && threadIdx.x == 0) dbg[npass] = globaltimer();
+        if (whole) {
+          done = true;
+        } else {
+          if (threadIdx.x == 0) s_need = L - s_before;
+          cur = 0;
+        }
+      }
+    }
+    int top = 0;
+    if (!done) {
+      if (general) {
+        const unsigned long long diff = va ^ vo;
+        top = diff ? 32 + (63 - __clzll(static_cast<long long>(diff)))
+                   : (nc > 1 ? 31 - __clz(static_cast<int>(nc - 1)) : 0);
+        if (threadIdx.x == 0) {
+          s_nsel = 0;
+          s_need = L;
+          s_m = nc;
+        }
+        __syncthreads();
+      } else if (s_m > kRankCap) {
+        // the group shares the bits above the highest one its composites
+        // differ in
+        unsigned long long ka = ~0ull, ko = 0ull, ia = ~0ull, io = 0ull;
+        for (uint32_t i = threadIdx.x; i < s_m; i += blockDim.x) {
+          ka &= gk[0][i];
+          ko |= gk[0][i];
+          ia &= gv[0][i];
+          io |= gv[0][i];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          ka &= __shfl_xor_sync(kFull, ka, o);
+          ko |= __shfl_xor_sync(kFull, ko, o);
+          ia &= __shfl_xor_sync(kFull, ia, o);
+          io |= __shfl_xor_sync(kFull, io, o);
+        }
+        if (lane == 0) {
+          w_ka[warp] = ka;
+          w_ko[warp] = ko;
+          w_ia[warp] = ia;
+          w_io[warp] = io;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          unsigned long long a1 = ~0ull, o1 = 0ull, a2 = ~0ull, o2 = 0ull;
+          for (int w = 0; w < nwarps; ++w) {
+            a1 &= w_ka[w];
+            o1 |= w_ko[w];
+            a2 &= w_ia[w];
+            o2 |= w_io[w];
+          }
+          s_and = a1 ^ o1; // bits the group's keys differ in
+          s_or = a2 ^ o2;  // ... and its ids
+        }
+        __syncthreads();
+        const unsigned long long dk = s_and, di = s_or;
+        top = dk ? 32 + (63 - __clzll(static_cast<long long>(dk)))
+                 : (di ? 63 - __clzll(static_cast<long long>(di)) : 0);
+      }
+    }
+    while (!done) {
+      if (cur >= 0 && s_m <= kRankCap) {
+        // rank the small group directly; composites are unique
+        const uint32_t gm = s_m, need = s_need;
+        for (uint32_t e = threadIdx.x; e < gm; e += blockDim.x) {
+          const uint64_t ke = gk[cur][e];
+          const uint32_t ve = gv[cur][e];
+          uint32_t r = 0;
+          for (uint32_t j = 0; j < gm; ++j) r += comp_less(gk[cur][j], gv[cur][j], ke, ve);
+          if (r < need) {
+            const uint32_t p = atomicAdd(&s_nsel, 1u);
+            selk[p] = ke;
+            selv[p] = ve;
+          }
+        }
+        break;
+      }
+      const int w = top >= 7 ? 8 : top + 1;
+      const int shift = top + 1 - w;
+      const uint32_t dmask = (1u << w) - 1u;
+      const uint32_t m = s_m;
+      const uint64_t* ck = cur < 0 ? sk : gk[cur];
+      const uint32_t* cv = cur < 0 ? nullptr : gv[cur];
+      for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        atomicAdd(&hist[comp_digit(ck[i], cv ? cv[i] : i, shift, dmask)], 1u);
+      }
+      __syncthreads();
+      if (warp == 0) find_boundary(s_need);
+      __syncthreads();
+      const uint32_t dsel = s_dsel, whole = s_flag == 1u;
+      const int nxt = cur < 0 ? 0 : cur ^ 1;
+      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const uint64_t key = ck[i];
+        const uint32_t id = cv ? cv[i] : i;
+        const uint32_t dg = comp_digit(key, id, shift, dmask);
+        if (dg < dsel || (dg == dsel && whole)) {
+          const uint32_t p = atomicAdd(&s_nsel, 1u);
+          selk[p] = key;
+          selv[p] = id;
+        } else if (dg == dsel) {
+          const uint32_t p = atomicAdd(&s_ng, 1u);
+          gk[nxt][p] = key;
+          gv[nxt][p] = id;
+        }
+      }
+      __syncthreads();
+      ++npass;
+      if (dbg && threadIdx.x == 0 && npass <= 8) dbg[npass] = globaltimer();
+      if (whole) break;
+      if (threadIdx.x == 0) s_need = s_need - s_before;
+      cur = nxt;
+      top = shift - 1;
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  if (dbg && threadIdx.x == 0) dbg[9] = globaltimer();
+  // order the L selected by rank counting, every thread one (entry, slice
+  // of the others) pair; the counters reuse group buffer 0
+  {
+    uint32_t* rank = gv[0];
+    for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) rank[i] = 0;
+    __syncthreads();
+    const uint32_t parts = max(1u, blockDim.x / L);
+    for (uint32_t t = threadIdx.x; t < parts * L; t += blockDim.x) {
+      const uint32_t e = t % L, part = t / L;
+      const uint64_t ke = selk[e];
+      const uint32_t ve = selv[e];
+      uint32_t r = 0;
+      const uint32_t j1 = (part + 1) * L / parts;
+#pragma unroll 4
+      for (uint32_t j = part * L / parts; j < j1; ++j) r += comp_less(selk[j], selv[j], ke, ve);
+      atomicAdd(&rank[e], r);
+    }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < L; e += blockDim.x) probe[rank[e]] = selv[e];
+  }
+  __syncthreads();
+  if (dbg && threadIdx.x == 0) {
+    dbg[10] = globaltimer();
+    dbg[11] = static_cast<unsigned long long>(npass);
+  }
+}
+
+template <bool kFp64, int KPL, int NCH>
+__global__ void __launch_bounds__(kFusedThreads, 1) fused_query_kernel(FusedArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const RingSmem rs = ring_smem(smem, a.T, a.S, a.d, a.kk);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t d4 = a.d >> 2, L = a.L, G = gridDim.x;
+  const bool stamp = a.stamps != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  __shared__ unsigned long long s_dbg[12];
+  const unsigned long long t_in = a.cta_stamps ? globaltimer() : 0ull;
+  if (stamp) st[0] = globaltimer();
+
+  // fast table of this query (shared memory after the ring's sq)
+  unsigned char* tp = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(rs.end) + 15) & ~uintptr_t(15));
+  int64_t* f_slab = reinterpret_cast<int64_t*>(tp);
+  uint64_t* f_row = reinterpret_cast<uint64_t*>(f_slab + L);
+  uint64_t* f_pre = f_row + L;
+  CtaStart* f_cta = reinterpret_cast<CtaStart*>(f_pre + L + 1);
+  uint32_t* f_len = reinterpret_cast<uint32_t*>(f_cta + G);
+  uint32_t* f_clu = f_len + L;
+  __shared__ uint32_t f_count;
+  FastTable ft;
+  ft.slab = f_slab;
+  ft.row = f_row;
+  ft.len = f_len;
+  ft.cluster = f_clu;
+  ft.pre = f_pre;
+  ft.count = &f_count;
+  ft.cta = f_cta;
+  ft.stride = L;
+  ft.grid = G;
+
+  // ---- 0. the query -> HBM; meanwhile the first centroid rows load --------
+  constexpr int NCHC = NCH > 0 ? NCH : 8; // float4 chunks per lane (d <= 1024)
+  constexpr int R = NCH > 0 ? 4 : 2;      // centroid rows per warp per round
+  const uint32_t gw = blockIdx.x * kFusedWarps + warp, GW = G * kFusedWarps;
+  // A staged query (HBM row named by the mapped slot) is read by every CTA
+  // straight into shared memory; a host row (pinned, PCIe) is copied to HBM
+  // once by CTA 0 behind a grid barrier.
+  unsigned long long q_st[3] = {0, 0, 0};
+  const bool direct = a.slot != nullptr || a.qdirect;
+  const float* src = nullptr;
+  if (direct || blockIdx.x == 0) {
+    src = a.slot ? *reinterpret_cast<const float* const volatile*>(a.slot) : a.src;
+  }
+  float4 xs[R][NCHC];
+  fused_load_rows<R, NCHC>(a.cen, a.nc, d4, gw * R, lane, xs);
+  if (direct) {
+    if ((reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+      for (uint32_t i = threadIdx.x; i < d4; i += blockDim.x) {
+        reinterpret_cast<float4*>(rs.sq)[i] = reinterpret_cast<const float4*>(src)[i];
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < a.d; i += blockDim.x) rs.sq[i] = src[i];
+    }
+    if (stamp) q_st[1] = globaltimer();
+    ring_init(rs, a.S);
+    __syncthreads();
+  } else {
+    if (blockIdx.x == 0) {
+      if ((reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+        for (uint32_t i = threadIdx.x; i < d4; i += blockDim.x) {
+          reinterpret_cast<float4*>(a.dQ)[i] = reinterpret_cast<const float4*>(src)[i];
+        }
+      } else {
+        for (uint32_t i = threadIdx.x; i < a.d; i += blockDim.x) a.dQ[i] = src[i];
+      }
+      if (stamp) q_st[1] = globaltimer();
+    }
+    ring_init(rs, a.S);
+    if (stamp) q_st[2] = globaltimer();
+    grid_sync(a.ctl);
+    for (uint32_t i = threadIdx.x; i < d4; i += blockDim.x) {
+      reinterpret_cast<float4*>(rs.sq)[i] = __ldcg(reinterpret_cast<const float4*>(a.dQ) + i);
+    }
+    __syncthreads();
+  }
+  if (stamp) st[1] = globaltimer();
+  const unsigned long long t_b1 = a.cta_stamps ? globaltimer() : 0ull;
+
+  // ---- 1. coarse scores of this CTA's centroid rows -> order keys ---------
+  for (uint32_t c0 = gw * R; c0 < a.nc; c0 += GW * R) {
+    if (c0 != gw * R) fused_load_rows<R, NCHC>(a.cen, a.nc, d4, c0, lane, xs);
+    fused_score_rows<R, NCHC>(rs.sq, a.nc, d4, c0, lane, a.metric, xs, a.keys);
+  }
+  grid_sync(a.ctl);
+  if (stamp) st[2] = globaltimer();
+  if (a.cta_stamps && threadIdx.x == 0) {
+    unsigned long long* cs3 = a.cta_stamps + 4ull * blockIdx.x;
+    cs3[0] = t_in;
+    cs3[1] = t_b1;
+    cs3[2] = globaltimer();
+  }
+
+  // ---- 2. every CTA ranks all nc keys (scratch aliased on the ring) -------
+  // [keys / group 1: nc x 12 B][group 0: nc x 12 B][selection: L x 12 B][probe]
+  uint64_t* sk = reinterpret_cast<uint64_t*>(smem);
+  SelectScratch sc;
+  sc.gk[1] = sk;
+  sc.gv[1] = reinterpret_cast<uint32_t*>(sk + a.nc);
+  sc.gk[0] = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(sc.gv[1] + a.nc) + 15) & ~uintptr_t(15));
+  sc.gv[0] = reinterpret_cast<uint32_t*>(sc.gk[0] + a.nc);
+  sc.sel_k = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(sc.gv[0] + a.nc) + 15) & ~uintptr_t(15));
+  sc.sel_v = reinterpret_cast<uint32_t*>(sc.sel_k + L);
+  uint32_t* probe = sc.sel_v + L;
+  unsigned long long va = ~0ull, vo = 0ull, vmin = ~0ull;
+  {
+    const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(a.keys);
+    for (uint32_t i = threadIdx.x; i < a.nc / 2; i += blockDim.x) {
+      const ulonglong2 v = __ldcg(k2 + i);
+      sk[2 * i] = v.x;
+      sk[2 * i + 1] = v.y;
+      va &= v.x & v.y;
+      vo |= v.x | v.y;
+      vmin = min(vmin, min(v.x, v.y));
+    }
+    if ((a.nc & 1u) && threadIdx.x == 0) {
+      const unsigned long long v = __ldcg(reinterpret_cast<const unsigned long long*>(a.keys) + a.nc - 1);
+      sk[a.nc - 1] = v;
+      va &= v;
+      vo |= v;
+      vmin = min(vmin, v);
+    }
+  }
+  {
+    __shared__ unsigned long long w_and[32], w_or[32], w_min[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      va &= __shfl_xor_sync(kFull, va, o);
+      vo |= __shfl_xor_sync(kFull, vo, o);
+      vmin = min(vmin, __shfl_xor_sync(kFull, vmin, o));
+    }
+    if (lane == 0) {
+      w_and[warp] = va;
+      w_or[warp] = vo;
+      w_min[warp] = vmin;
+    }
+    __syncthreads();
+    va = ~0ull;
+    vo = 0ull;
+    vmin = ~0ull;
+    for (int w = 0; w < kFusedWarps; ++w) {
+      va &= w_and[w];
+      vo |= w_or[w];
+      vmin = min(vmin, w_min[w]);
+    }
+  }
+  if (stamp) st[3] = globaltimer();
+  block_select_topL(sk, a.nc, L, va, vo, vmin, sc, probe,
+                    a.stamps && blockIdx.x == 0 ? s_dbg : nullptr);
+  if (stamp) st[4] = globaltimer();
+  // residency split + this query's scan-CTA start table (partition step)
+  partition_block(probe, L, a.res_off, a.list_off, ft, 0);
+  __syncthreads();
+  if (blockIdx.x == 0 && warp == kFusedWarps - 1) {
+    // host I/O warp: the probe and the fast count go out, then the flag
+    for (uint32_t i = lane; i < L; i += 32) a.order_out[i] = probe[i];
+    if (lane == 0) {
+      *a.fcount_out = f_count;
+      const unsigned s = a.ctl[1] + 1u;
+      a.ctl[1] = s;
+      __threadfence_system();
+      *reinterpret_cast<volatile unsigned*>(a.flag_out) = s;
+    }
+  }
+  if (stamp) st[5] = globaltimer();
+  // the scratch was written through the generic proxy; the ring's bulk
+  // copies write the same bytes through the async proxy
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+
+  // ---- 3. scan of this CTA's range of the fast lists ----------------------
+  const uint64_t V = f_pre[f_count];
+  const CtaStart cs = (L > 0 && f_count > 0) ? f_cta[blockIdx.x] : CtaStart{0u, 0u, 0u, 0u};
+  __shared__ unsigned long long s_first_tile;
+  const unsigned long long t_loop = scan_tma_cta<kFp64, KPL, NCH>(
+      rs.sq, a.d, a.metric, a.k, a.kk, ft, 0, cs, V, a.slab, a.ids, a.out, a.T, a.S, smem, rs.full,
+      rs.empty, rs.mrow, rs.mvi, rs.mn, stamp, &s_first_tile, stamp ? &q_st[2] : nullptr);
+  if (a.cta_stamps && threadIdx.x == 0) a.cta_stamps[4ull * blockIdx.x + 3] = globaltimer();
+  if (stamp) {
+    st[6] = t_loop;
+    st[7] = globaltimer();
+    for (int i = 0; i < 8; ++i) a.stamps[i] = st[i];
+    for (int i = 0; i < 12; ++i) a.stamps[8 + i] = s_dbg[i];
+    for (int i = 0; i < 3; ++i) a.stamps[20 + i] = q_st[i];
   }
 }
 
@@ -1682,6 +2339,47 @@ __global__ void window_kernel(uint64_t ns) {
   while (globaltimer() - t0 < ns) {
     __nanosleep(2000);
   }
+}
+
+// Decode-like generation window: for `ns` nanoseconds, one "token" every
+// period_ns streams the whole buffer (an LLM decode step reads every weight
+// once) at full speed, then idles until the next token is due. The HBM,
+// L2 and SM load of a memory-bound decode thus share the device with the
+// lookahead copies. Bytes read are counted into *bytes_read.
+__global__ void __launch_bounds__(512) window_stream_kernel(const float4* __restrict__ buf,
+                                                            uint64_t n16, uint64_t ns,
+                                                            uint64_t period_ns, float* sink,
+                                                            unsigned long long* bytes_read) {
+  const uint64_t t0 = globaltimer();
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  float acc = 0.f;
+  uint64_t mine = 0;
+  for (uint64_t tok = 0;; ++tok) {
+    const uint64_t due = tok * period_ns;
+    uint64_t now = globaltimer() - t0;
+    if (now >= ns) break;
+    while (now < due) {
+      __nanosleep(1000);
+      now = globaltimer() - t0;
+      if (now >= ns) break;
+    }
+    if (now >= ns) break;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n16;
+         i += 4 * stride) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint64_t j = i + u * stride;
+        v[u] = j < n16 ? ldg_stream(buf + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+      mine += 4;
+    }
+  }
+  if (acc == 1234.5f) *sink = acc; // keeps the loads; never true for the zeroed buffer
+  const uint64_t tot = __reduce_add_sync(kFull, static_cast<unsigned>(mine));
+  if ((threadIdx.x & 31) == 0 && tot) atomicAdd(bytes_read, static_cast<unsigned long long>(tot) * 16ull);
 }
 
 // --------------------------------------------------------------------------
@@ -1899,6 +2597,95 @@ void launch_scan(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
 #undef LAIVG_D
 }
 
+size_t fused_query_smem(uint32_t nc, uint32_t d, uint32_t L, int k, bool acc_fp64, uint32_t G,
+                        const ScanTune& tune) {
+  if (!acc_fp64 && k + kRerankMargin > kMaxK) acc_fp64 = true;
+  const int kk = scan_kk(k, acc_fp64);
+  if (k > kMaxK || (d % 4) != 0 || d > 1024 || nc == 0) return 0;
+  const TmaGeom g = tma_geom(d, kk, G, tune);
+  // the selection scratch lives in the ring region (ring or merge scratch)
+  size_t region = (size_t(g.S) * g.T * d * 4 + 127) & ~size_t(127);
+  const size_t merge = epilogue_scratch(kConsumers, kk, G);
+  if (region < merge) region = (merge + 127) & ~size_t(127);
+  if (fused_select_bytes(nc, L) > region) return 0;
+  const size_t smem = g.smem + fused_tables_bytes(L, G);
+  return smem > 227 * 1024 ? 0 : smem;
+}
+
+template <bool kFp64, int KPL, int NCH>
+void launch_fused_t(const FusedArgs& a, uint32_t G, size_t smem, cudaStream_t st) {
+  auto fn = fused_query_kernel<kFp64, KPL, NCH>;
+  ensure_dyn_smem(reinterpret_cast<const void*>(fn), smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(kFusedThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, a);
+  if (e != cudaSuccess) {
+    throw CudaError(std::string("fused query launch failed: ") + cudaGetErrorString(e));
+  }
+  after_launch();
+}
+
+void launch_fused_query(const FusedQuery& q, const ScanOut& out, bool acc_fp64,
+                        const ScanTune& tune, cudaStream_t st) {
+  if (!acc_fp64 && q.k + kRerankMargin > kMaxK) acc_fp64 = true;
+  const int kk = scan_kk(q.k, acc_fp64);
+  const size_t smem = fused_query_smem(q.nc, q.d, q.L, q.k, acc_fp64, q.grid, tune);
+  if (smem == 0) throw CudaError("fused query kernel: shape does not fit shared memory");
+  const TmaGeom g = tma_geom(q.d, kk, q.grid, tune);
+  FusedArgs a;
+  a.src = q.src;
+  a.slot = q.slot;
+  a.dQ = q.dQ;
+  a.cen = q.cen;
+  a.nc = q.nc;
+  a.d = q.d;
+  a.L = q.L;
+  a.metric = q.metric;
+  a.keys = q.keys;
+  a.res_off = q.res_off;
+  a.list_off = q.list_off;
+  a.order_out = q.order_out;
+  a.fcount_out = q.fcount_out;
+  a.flag_out = q.flag_out;
+  a.ctl = q.ctl;
+  a.stamps = q.stamps;
+  a.cta_stamps = q.cta_stamps;
+  a.qdirect = q.qdirect;
+  a.slab = q.slab;
+  a.ids = q.ids;
+  a.out = out;
+  a.out.fcount_out = nullptr; // the I/O warp publishes the fast count
+  a.out.fcount_in = nullptr;
+  a.out.probe = nullptr;
+  a.T = g.T;
+  a.S = g.S;
+  a.k = q.k;
+  a.kk = kk;
+#define LAIVG_FUSED(F64, NCH)                                   \
+  do {                                                          \
+    if (kk <= 32) launch_fused_t<F64, 1, NCH>(a, q.grid, smem, st);  \
+    else if (kk <= 64) launch_fused_t<F64, 2, NCH>(a, q.grid, smem, st); \
+    else if (kk <= 128) launch_fused_t<F64, 4, NCH>(a, q.grid, smem, st); \
+    else launch_fused_t<F64, 8, NCH>(a, q.grid, smem, st);       \
+  } while (0)
+  if (acc_fp64) {
+    if (q.d == 768) LAIVG_FUSED(true, 6);
+    else LAIVG_FUSED(true, 0);
+  } else {
+    if (q.d == 768) LAIVG_FUSED(false, 6);
+    else LAIVG_FUSED(false, 0);
+  }
+#undef LAIVG_FUSED
+}
+
 void launch_fetch_query(const float* src, const float* const* slot, float* dQ, uint32_t d,
                         cudaStream_t st) {
   fetch_query_kernel<<<1, 256, 0, st>>>(src, slot, dQ, d);
@@ -1907,6 +2694,14 @@ void launch_fetch_query(const float* src, const float* const* slot, float* dQ, u
 
 void launch_window(uint64_t ns, int num_sms, cudaStream_t st) {
   window_kernel<<<num_sms, 32, 0, st>>>(ns);
+  after_launch();
+}
+
+void launch_window_stream(const float* buf, uint64_t bytes, uint64_t ns, uint64_t period_ns,
+                          int num_sms, float* sink, unsigned long long* bytes_read,
+                          cudaStream_t st) {
+  window_stream_kernel<<<num_sms * 2, 512, 0, st>>>(reinterpret_cast<const float4*>(buf),
+                                                    bytes / 16, ns, period_ns, sink, bytes_read);
   after_launch();
 }
 

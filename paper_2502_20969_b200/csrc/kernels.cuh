@@ -111,6 +111,41 @@ void launch_scan(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
 int scan_grid_x(uint32_t nq, int num_sms, ScanImpl impl, const ScanTune& tune);
 // Entries each per-CTA partial list holds for a given k (k + re-score margin).
 int scan_kk(int k, bool acc_fp64);
+// ---- fused single-query kernel (kernels.cu) ----
+// query fetch -> coarse scores -> top-L -> residency split -> TMA scan in one
+// cooperative launch of `grid` CTAs (one per SM). Results as launch_scan's
+// (host-final or device-merged per `out`); the probe and the fast-list count
+// land in mapped memory followed by the call's sequence number in *flag_out.
+struct FusedQuery {
+  const float* src = nullptr;          // query row (pinned host or HBM), or
+  const float* const* slot = nullptr;  // mapped word holding the row pointer
+  float* dQ = nullptr;
+  const float* cen = nullptr;
+  uint32_t nc = 0, d = 0, L = 0;
+  int metric = 0, k = 0;
+  uint64_t* keys = nullptr;            // [nc] device scratch
+  const int64_t* res_off = nullptr;
+  const uint64_t* list_off = nullptr;
+  uint32_t* order_out = nullptr;       // [L] (device-visible, mapped)
+  uint32_t* fcount_out = nullptr;
+  unsigned* flag_out = nullptr;
+  unsigned* ctl = nullptr;             // [2] device: barrier word, sequence (zeroed)
+  // [8] CTA 0 globaltimer stamps (mapped), nullable: entry, query ready,
+  // keys ready, keys loaded, top-L selected, scan ranges ready, last tile
+  // consumed, done
+  unsigned long long* stamps = nullptr;   // [32]; [8..19] selection stamps
+  unsigned long long* cta_stamps = nullptr; // [grid][4] per CTA (diagnostics), nullable
+  int qdirect = 0;                     // host row read by every CTA (diagnostics)
+  const float* slab = nullptr;
+  const uint64_t* ids = nullptr;
+  uint32_t grid = 0;
+};
+// Dynamic shared memory of the fused kernel for this shape, 0 if it does not
+// fit (the caller then runs the multi-kernel chain).
+size_t fused_query_smem(uint32_t nc, uint32_t d, uint32_t L, int k, bool acc_fp64, uint32_t G,
+                        const ScanTune& tune);
+void launch_fused_query(const FusedQuery& q, const ScanOut& out, bool acc_fp64,
+                        const ScanTune& tune, cudaStream_t st);
 // ---- batched coarse quantizer on tensor cores (coarse_tc.cu) ----
 // Used for batches of >= kTcMinBatch queries when nc <= kTcMaxNc and d % 4 == 0.
 constexpr uint32_t kTcMinBatch = 16; // measured crossover (profiles/r01/coarse_bench.jsonl)
@@ -203,5 +238,11 @@ void launch_pairwise_l2(const float* A, uint64_t na, const float* B, uint64_t nb
 void launch_fetch_query(const float* src, const float* const* slot, float* dQ, uint32_t d,
                         cudaStream_t st);
 void launch_window(uint64_t ns, int num_sms, cudaStream_t st);
+// Decode-like window: every period_ns the grid streams `bytes` of buf (the
+// "weights") once at full speed, for ns nanoseconds; bytes read are added to
+// *bytes_read.
+void launch_window_stream(const float* buf, uint64_t bytes, uint64_t ns, uint64_t period_ns,
+                          int num_sms, float* sink, unsigned long long* bytes_read,
+                          cudaStream_t st);
 
 } // namespace laivg

@@ -298,7 +298,8 @@ class Device:
                  miss_threads: int = 0, max_batch: int = 0, max_probe: int = 0,
                  acc_fp64: bool = True, scan_impl: str = "tma", tma_tile: int = 0,
                  tma_stages: int = 0, ctas_per_sm: int = 0, coarse_impl: str = "auto",
-                 miss_fetch: str = "auto", fetch_chunk_mb: int = 0):
+                 miss_fetch: str = "auto", fetch_chunk_mb: int = 0,
+                 single_query: str = "fused"):
         L = lib()
         o = Opts()
         L.laivg_opts_default(C.byref(o))
@@ -321,6 +322,9 @@ class Device:
             raise ValueError("miss_fetch must be 'off', 'auto' or 'all'")
         o.miss_fetch = fetches[miss_fetch]
         o.fetch_chunk_mb = fetch_chunk_mb
+        if single_query not in ("fused", "chain"):
+            raise ValueError("single_query must be 'fused' or 'chain'")
+        o.single_chain = 0 if single_query == "fused" else 1
         h = C.c_void_p()
         check(L.laivg_ctx_create(ix.h, C.byref(o), C.byref(h)))
         self.h = h
@@ -348,6 +352,17 @@ class Device:
         out = C.c_double()
         check(lib().laivg_window(self.h, seconds, C.byref(out)))
         return out.value
+
+    def window_load(self, buffer_bytes: int, read_gbps: float) -> None:
+        """Decode-like generation windows: stream `buffer_bytes` of HBM once per
+        token period (buffer_bytes / read_gbps); 0 restores the idle window."""
+        check(lib().laivg_window_load(self.h, int(buffer_bytes), float(read_gbps)))
+
+    def link_peak(self, nbytes: int = 1 << 30) -> tuple[float, float]:
+        """Pinned H2D / D2H GB/s of this GPU's host link (one large copy each)."""
+        a, b = C.c_double(), C.c_double()
+        check(lib().laivg_link_peak(self.h, int(nbytes), C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def stage_queries(self, Q) -> None:
         Q = _c(Q, np.float32).reshape(-1, self.ix.d)
@@ -594,6 +609,7 @@ class TransferReport:                                             # tiered.hpp:7
     overshoot_s: float = 0.0
     window_s: float = 0.0
     h2d_gbps: float = 0.0
+    window_read_gbps: float = 0.0  # HBM read rate of a decode-like window (0: idle window)
 
 
 @dataclass
@@ -629,6 +645,7 @@ class HybridTiming:                                               # tiered.hpp:8
     peer_bytes: int = 0
     h2d_bytes: int = 0         # host-link bytes the call moved (counted by the library)
     d2h_bytes: int = 0
+    t_kernel: float = 0.0      # fused single-query kernel duration (0: multi-kernel chain)
 
 
 @dataclass
@@ -644,7 +661,7 @@ def _timing(t: HybridTimingC) -> HybridTiming:
                         t.t_coarse, t.t_scan, int(t.scanned_vectors), int(t.scanned_bytes),
                         int(t.fetched_lists), int(t.cpu_lists), int(t.fetched_bytes), t.t_fetch,
                         int(t.peer_lists), int(t.peer_bytes), int(t.h2d_bytes),
-                        int(t.d2h_bytes))
+                        int(t.d2h_bytes), t.t_kernel)
 
 
 def plan_prefetch(dev: Device, q_in, budget_bytes: int) -> PrefetchPlan:  # tiered.hpp:100-101
@@ -660,7 +677,7 @@ def plan_prefetch(dev: Device, q_in, budget_bytes: int) -> PrefetchPlan:  # tier
 
 def _report(r: TransferReportC, transferred) -> TransferReport:
     return TransferReport(r.t_p, list(transferred), int(r.bytes), r.overshoot_s, r.window_s,
-                          r.h2d_gbps)
+                          r.h2d_gbps, r.window_read_gbps)
 
 
 def execute_prefetch(dev: Device, plan: PrefetchPlan, chan: TransferChannel,

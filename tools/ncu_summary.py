@@ -1,7 +1,11 @@
 #!/usr/bin/env python
 """Summarise an ncu report (--set full) into a small JSON for profiles/.
 
-    python tools/ncu_summary.py gpurun_out/x/prof.ncu-rep "<source command>" > profiles/rNN/x.json
+    python tools/ncu_summary.py gpurun_out/x/prof.ncu-rep "<source command>" [config] \
+        > profiles/rNN/x.json
+
+`config` (the bench workload, e.g. c1 / c2) lets bench.py pick the summary for
+its `roofline.traffic`.
 """
 import csv
 import io
@@ -26,6 +30,7 @@ METRICS = [
 
 def main():
     rep, src = sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else ""
+    config = sys.argv[3] if len(sys.argv) > 3 else None
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -33,6 +38,8 @@ def main():
     stall = [h for h in hdr if h.startswith("smsp__average_warp_latency_issue_stalled_")
              or h.startswith("smsp__pcsamp_warps_issue_stalled_")]
     out = {"source": src, "kernels": []}
+    if config:
+        out["config"] = config
     for r in rows[2:]:
         k = {"name": r[hdr.index("Kernel Name")]}
         for m in METRICS:
