@@ -1787,7 +1787,7 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
       }
       sel += " passes " + std::to_string(h_stamps[19]);
       std::fprintf(stderr, "%s\n", sel.c_str());
-      std::fprintf(stderr, "[laivg fused] CTA 0: query copied %.2f, CTA merge done %.2f\n",
+      std::fprintf(stderr, "[laivg fused] CTA 0 epilogue: lists stored %.2f, CTA merge done %.2f\n",
                    (h_stamps[21] - h_stamps[0]) * 1e-3, (h_stamps[22] - h_stamps[0]) * 1e-3);
       if (h_cta_stamps) {
         unsigned long long e0 = ~0ull, e1 = 0, b1a = ~0ull, b1b = 0, b2a = ~0ull, b2b = 0,

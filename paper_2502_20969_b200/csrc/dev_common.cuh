@@ -13,7 +13,7 @@ constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : : "memory");
   return t;
 }
 
