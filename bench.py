@@ -116,6 +116,18 @@ def host_threads(world):
     return max(1, (os.cpu_count() or 1) // max(1, world))
 
 
+def pin_rank_cores(rank, world):
+    """One process per GPU: rank r runs (and spawns its miss-scan threads) on
+    its own slice of the node's cores, so N ranks never share a core."""
+    if world <= 1 or not hasattr(os, "sched_setaffinity"):
+        return None
+    cores = sorted(os.sched_getaffinity(0))
+    per = max(1, len(cores) // world)
+    mine = cores[rank * per:(rank + 1) * per] or cores[-per:]
+    os.sched_setaffinity(0, mine)
+    return mine
+
+
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
@@ -382,6 +394,7 @@ def run_ours(args, cfg):
     rank, world, local = dist_env()
     dist = None
     dist, gpu = init_dist(world, local)
+    pin_rank_cores(rank, world)
     cen, vecs, ids, off = make_datastore(cfg, world, rank)
     metric = laiv.Metric.InnerProduct if args.metric == "ip" else laiv.Metric.L2
     ix = laiv.IvfIndex(cen, vecs, ids, off, metric, borrow=True, trust=True)
@@ -603,6 +616,7 @@ def run_ours_batch(args, cfg):
     rank, world, local = dist_env()
     dist = None
     dist, gpu = init_dist(world, local)
+    pin_rank_cores(rank, world)
     B = cfg["batch"]
     cen, vecs, ids, off = make_datastore(cfg, world, rank)
     metric = laiv.Metric.InnerProduct if args.metric == "ip" else laiv.Metric.L2
@@ -768,6 +782,7 @@ def run_ours_routed(args, cfg):
     dist, gpu = init_dist(world, local)
     emulated = world == 1 and args.workers > 1
     W = world if world > 1 else max(1, args.workers)
+    pin_rank_cores(rank, world)
     B, m = cfg["batch"], cfg["micro"]
     cen, vecs, ids, off = make_datastore(cfg, world, rank)
     metric = laiv.Metric.InnerProduct if args.metric == "ip" else laiv.Metric.L2
@@ -775,8 +790,10 @@ def run_ours_routed(args, cfg):
     member = 4 * cfg["d"] + 8
     capacity = int(cfg["cache_frac"] * cfg["n_lists"]) * cfg["per_list"] * member
     mine = list(range(W)) if emulated or world == 1 else [rank]
+    # emulated workers get the host share a real W-GPU node would give each
+    # rank (cores / W), not the whole host
     devs = {w: laiv.Device(ix, capacity, device=gpu,
-                           max_batch=max(m, 32), miss_threads=host_threads(world),
+                           max_batch=max(m, 32), miss_threads=host_threads(W),
                            acc_fp64=args.acc == "fp64", scan_impl=args.scan) for w in mine}
     params = laiv.CacheParams(cache_fraction=cfg["hot_fraction"])
     hot = {w: laiv.HotnessTable(params) for w in mine}

@@ -455,6 +455,7 @@ struct Ctx {
   uint64_t quarantined = 0;                              // reference bytes held back
   struct Peer {
     const float* slab = nullptr; // the peer's slab (same process or CUDA IPC)
+    int dev = -1;                // CUDA ordinal the slab lives on
     void* ipc = nullptr;         // cudaIpcOpenMemHandle mapping to close
     std::vector<int64_t> off;    // the peer's published offsets (-1 absent)
   };
@@ -1310,6 +1311,7 @@ size_t Ctx::issue_fetch(std::vector<std::vector<uint32_t>>& slow, bool& any_slow
     uint32_t c;
     const float* src;
     bool host;
+    int dev = -1; // device of a peer slab
   };
   std::vector<std::vector<FetchItem>> chunks;
   uint64_t fill = 0;
@@ -1341,13 +1343,15 @@ size_t Ctx::issue_fetch(std::vector<std::vector<uint32_t>>& slow, bool& any_slow
       std::vector<std::pair<uint32_t, uint32_t>> rest;
       for (auto& [n, c] : cand) {
         const float* src = nullptr;
+        int sdev = -1;
         for (auto& pr : peers) {
           if (pr.slab && !pr.off.empty() && pr.off[c] >= 0) {
             src = pr.slab + uint64_t(pr.off[c]) * d;
+            sdev = pr.dev;
             break;
           }
         }
-        if (src && ix->list_len(c) && add_item({c, src, false})) {
+        if (src && ix->list_len(c) && add_item({c, src, false, sdev})) {
           on_gpu[c] = 1;
           ++st.peer_lists;
           st.peer_bytes += ix->list_len(c) * d * 4;
@@ -1430,8 +1434,9 @@ size_t Ctx::issue_fetch(std::vector<std::vector<uint32_t>>& slow, bool& any_slow
         hres[it.c] = int64_t(off);
         float* dst = ring + off * d;
         const size_t bytes = len * d * sizeof(float);
-        if (!it.host) { // peer slab (same process or CUDA IPC): device to device
-          CK(cudaMemcpyAsync(dst, it.src, bytes, cudaMemcpyDefault, copy));
+        if (!it.host) { // peer slab (same process or CUDA IPC): over NVLink when the
+                        // peer is another device (peer access enabled at attach)
+          CK(cudaMemcpyPeerAsync(dst, dev, it.src, it.dev >= 0 ? it.dev : dev, bytes, copy));
         } else if (!srcs.empty() && static_cast<float*>(srcs.back()) +
                                             sizes.back() / sizeof(float) == it.src) {
           sizes.back() += bytes;
@@ -2952,6 +2957,9 @@ int laivg_peer_attach_ipc(laivg_ctx* ctx, uint32_t peer, const void* handle) {
     CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
     p.ipc = ptr;
     p.slab = static_cast<const float*>(ptr);
+    cudaPointerAttributes at{};
+    CK(cudaPointerGetAttributes(&at, ptr));
+    p.dev = at.device;
   });
 }
 int laivg_peer_attach_local(laivg_ctx* ctx, uint32_t peer, const laivg_ctx* other) {
@@ -2970,6 +2978,7 @@ int laivg_peer_attach_local(laivg_ctx* ctx, uint32_t peer, const laivg_ctx* othe
       cudaGetLastError();
     }
     peer_slot(ctx->c, peer).slab = other->c.d_slab;
+    peer_slot(ctx->c, peer).dev = other->c.dev;
   });
 }
 int laivg_peer_publish(laivg_ctx* ctx, uint32_t peer, const int64_t* offsets) {
