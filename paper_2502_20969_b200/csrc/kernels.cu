@@ -831,6 +831,8 @@ __device__ __forceinline__ void tc_bounds(int metric, double a, double qn, doubl
 // bounds[nc], upper bounds[nc], candidate keys/ids[cap] (cap = pow2 >= nc,
 // so every centroid fits).
 constexpr int kSelThreads = 1024;
+// LAIVG_TC_PROBE diagnostics: query 0's CTA stamps its phases here
+__device__ unsigned long long g_tc_dbg[8];
 __global__ void __launch_bounds__(kSelThreads)
     tc_select_kernel(const float* __restrict__ approx, uint32_t splits,
                      const float* __restrict__ Q, uint32_t d,
@@ -838,7 +840,7 @@ __global__ void __launch_bounds__(kSelThreads)
                      uint32_t nc, int metric, uint32_t n_out, uint32_t cap,
                      uint32_t* __restrict__ order, const int64_t* res_off,
                      const uint64_t* list_off, FastTable ft, bool do_partition,
-                     bool scan_sorted) {
+                     bool scan_sorted, bool probe_on) {
   extern __shared__ __align__(16) unsigned char sm[];
   float* sq = reinterpret_cast<float*>(sm);
   uint32_t* lok = reinterpret_cast<uint32_t*>(sm + ((static_cast<size_t>(d) * 4 + 15) & ~size_t(15)));
@@ -855,6 +857,8 @@ __global__ void __launch_bounds__(kSelThreads)
   const float* qv = Q + static_cast<uint64_t>(q) * d;
   const float* aq = approx + static_cast<uint64_t>(q) * nc;
   const uint64_t plane = static_cast<uint64_t>(gridDim.x) * nc; // split-K partial planes
+  const bool dbg = probe_on && q == 0 && threadIdx.x == 0;
+  if (dbg) g_tc_dbg[0] = globaltimer();
 
   // ||q||^2 in fp64
   double part = 0.0;
@@ -902,6 +906,8 @@ __global__ void __launch_bounds__(kSelThreads)
       }
     }
   }
+  __syncthreads();
+  if (dbg) g_tc_dbg[1] = globaltimer();
   // radix select: the (n_out-1)-th smallest key, 8 bits at a time
   uint32_t mask = 0;
   for (int shift = 24; shift >= 0; shift -= 8) {
@@ -949,12 +955,14 @@ __global__ void __launch_bounds__(kSelThreads)
     __syncthreads();
   }
   const float T = order_float(~s_prefix); // the n_out-th best lower bound
+  if (dbg) g_tc_dbg[2] = globaltimer();
 
   // candidates: upper bound reaches T (includes every exact top-n_out member)
   for (uint32_t c = threadIdx.x; c < nc; c += blockDim.x) {
     if (hik[c] >= T) cv[atomicAdd(&s_count, 1u)] = c;
   }
   __syncthreads();
+  if (dbg) g_tc_dbg[3] = globaltimer();
   const uint32_t n = s_count;
   uint32_t m = 2;
   while (m < n) m <<= 1;
@@ -970,6 +978,10 @@ __global__ void __launch_bounds__(kSelThreads)
     cv[i] = ~0u;
   }
   __syncthreads();
+  if (dbg) {
+    g_tc_dbg[4] = globaltimer();
+    g_tc_dbg[7] = n;
+  }
   // bitonic sort on (key, cluster id)
   for (uint32_t kk = 2; kk <= m; kk <<= 1) {
     for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
@@ -990,6 +1002,7 @@ __global__ void __launch_bounds__(kSelThreads)
       __syncthreads();
     }
   }
+  if (dbg) g_tc_dbg[5] = globaltimer();
   uint32_t* out = order + static_cast<uint64_t>(q) * n_out;
   for (uint32_t i = threadIdx.x; i < n_out; i += blockDim.x) out[i] = cv[i];
   if (do_partition) {
@@ -997,6 +1010,7 @@ __global__ void __launch_bounds__(kSelThreads)
     if (scan_sorted) sort_ids_block(cv, n_out);
     partition_block(cv, n_out, res_off, list_off, ft, q);
   }
+  if (dbg) g_tc_dbg[6] = globaltimer();
 }
 
 // --------------------------------------------------------------------------
@@ -2550,11 +2564,22 @@ void launch_tc_select(const float* approx, uint32_t splits, const float* Q, uint
   if (smem > 227 * 1024) throw CudaError("tc_select: shared memory exceeds 227 KB");
   ensure_dyn_smem(reinterpret_cast<const void*>(tc_select_kernel), smem);
   const FastTable f = ft ? *ft : FastTable{};
+  static const bool probe = std::getenv("LAIVG_TC_PROBE") != nullptr;
   tc_select_kernel<<<nq, kSelThreads, smem, st>>>(approx, splits, Q, d, centroids, cnorm, nc, metric,
                                            n_out,
                                            cap, order, res_off, list_off, f, ft != nullptr,
-                                           scan_sorted);
+                                           scan_sorted, probe);
   after_launch();
+  if (probe) {
+    unsigned long long t[8];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(t, g_tc_dbg, sizeof(t));
+    std::fprintf(stderr,
+                 "[laivg tc_select] q0 us: bounds %.2f radix %.2f collect %.2f rescore %.2f "
+                 "sort %.2f out+partition %.2f (candidates %llu, nq %u, L %u)\n",
+                 (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3,
+                 (t[4] - t[3]) * 1e-3, (t[5] - t[4]) * 1e-3, (t[6] - t[5]) * 1e-3, t[7], nq, n_out);
+  }
 }
 
 void launch_partition(const uint32_t* probe, uint32_t nq, uint32_t lp,
