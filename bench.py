@@ -378,6 +378,7 @@ def config_block(cfg, args, sigma):
             "metric": args.metric, "batch": cfg.get("batch", 1), "window_s": args.window,
             "cache_fraction_of_lists": cfg["cache_frac"], "q_out_sigma": sigma,
             "query_seed": QSEED,
+            "budget_scale": args.budget_scale,
             "window_kind": (f"decode-like: {args.window_buffer_gb:g} GB streamed per token at "
                             f"{args.window_load:g} GB/s target" if args.window_load > 0
                             else "idle (%globaltimer spin)"),
@@ -414,7 +415,7 @@ def run_ours(args, cfg):
     rep = laiv.execute_prefetch(dev, probe_plan, laiv.TransferChannel(1, laiv.ChannelMode.Device))
     dev.store.clear()
     b_link = rep.h2d_gbps * 1e9
-    budget = int(min(b_link * args.window, capacity))
+    budget = int(min(b_link * args.window * args.budget_scale, capacity))
     sigma, cov = q_out_sigma(args, cfg, laiv, dev, vecs, L)
     # (one rank: extra queries of the same generator extend the CPU sample)
     nq_total = max((args.warmup + args.steps) * world + 8,
@@ -630,7 +631,7 @@ def run_ours_batch(args, cfg):
     rep = laiv.execute_prefetch(dev, probe_plan, laiv.TransferChannel(1, laiv.ChannelMode.Device))
     dev.store.clear()
     b_link = rep.h2d_gbps * 1e9
-    budget = int(min(b_link * args.window, capacity))
+    budget = int(min(b_link * args.window * args.budget_scale, capacity))
     budgets = laiv.split_budget(budget, laiv.MicroBatch(list(range(B))))
     sigma, cov = q_out_sigma(args, cfg, laiv, dev, vecs, L)
     nsteps = args.warmup + args.steps
@@ -1028,6 +1029,9 @@ def main():
                          "(default) or fp32 FMA + exact fp64 re-score of the survivors")
     ap.add_argument("--scan", default="tma", choices=["tma", "ldg"],
                     help="scan kernel: TMA bulk-copy staged (default) or direct LDG")
+    ap.add_argument("--budget-scale", type=float, default=1.0,
+                    help="lookahead budget = scale x B_link x window (capped by the cache); "
+                         "above 1 the copies outlast the window (prefetch-hiding stress)")
     ap.add_argument("--window-load", type=float, default=None,
                     help="decode-like window: GB/s target read rate of the streamed "
                          "buffer (default: the config's, 0 = idle window)")
