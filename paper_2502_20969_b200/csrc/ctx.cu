@@ -228,6 +228,23 @@ struct Ctx {
   cudaEvent_t ev_landed[2] = {nullptr, nullptr}, ev_freed[2] = {nullptr, nullptr};
   cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr, ev_fdone = nullptr;
   double link_rate = 50e9;       // EMA of fetch H2D bytes/s
+  double scan_rate = 6e12;       // EMA of the GPU scan's vector bytes/s
+  uint64_t fast_vecs(const std::vector<uint32_t>& fast) const {
+    uint64_t v = 0;
+    for (uint32_t c : fast) v += ix->list_len(c);
+    return v;
+  }
+  // Modeled seconds the batched / single hit scan of these vectors takes.
+  double busy_of(const std::vector<uint64_t>& v) const {
+    uint64_t t = 0;
+    for (uint64_t x : v) t += x;
+    return double(t) * ix->d * 4 / scan_rate;
+  }
+  void note_scan(uint64_t vecs, double t_scan) {
+    if (vecs > 0 && t_scan > 0) {
+      scan_rate = 0.8 * scan_rate + 0.2 * (double(vecs) * ix->d * 4 / t_scan);
+    }
+  }
   double cpu_rate = 0;           // EMA of the host miss scan rate on distinct list bytes
   void alloc_scan_set(FastTable& f, ScanOut& o, bool device_outputs = true);
   // The scan's result for query q: the device-merged top-k, or (host-final
@@ -530,7 +547,10 @@ struct Ctx {
     uint64_t fetch_bytes = 0, peer_bytes = 0;
     double t_fetch = 0;
   };
-  size_t issue_fetch(std::vector<std::vector<uint32_t>>& slow, bool& any_slow, const float* dQ,
+  // gpu_busy: modeled seconds the GPU still spends scanning the hits once the
+  // probe is known (the host scans misses for free during that time)
+  size_t issue_fetch(std::vector<std::vector<uint32_t>>& slow, bool& any_slow, double gpu_busy,
+                     const float* dQ,
                      uint32_t nq, uint32_t lp, const uint32_t* probe_dev, int k, int G,
                      FetchStats& st);
   void merge_fetch(uint32_t q, size_t nchunks, int k, std::vector<Scored>& gpu) const;
@@ -625,7 +645,8 @@ struct Ctx {
   // re-pointing a node per call ~4 us plus a slower launch. Then coarse
   // scores, ranking + residency split, scan, results; the probe lands in
   // mapped host memory as soon as it exists.
-  void enqueue_coarse_path(uint32_t lp, int k, int G, const float* src) {
+  void enqueue_coarse_path(uint32_t lp, int k, int G, const float* src,
+                           PhaseTrace* tr = nullptr) {
     if (use_fused(lp, k, G)) {
       // launched directly (not captured): the query row is a kernel
       // argument. A staged row (HBM) is read by every CTA; the pinned host
@@ -652,8 +673,11 @@ struct Ctx {
       fq.slab = d_slab;
       fq.ids = d_ids;
       fq.grid = uint32_t(G);
+      if (tr) tr->mark("prep");
       rec(ev_a, comp);
+      if (tr) tr->mark("ev_a");
       launch_fused_query(fq, so, acc_fp64, tune, comp);
+      if (tr) tr->mark("kernel");
       rec(ev_s, comp); // also marks the results in mapped host memory complete
       return;
     }
@@ -690,7 +714,7 @@ struct Ctx {
     if (last_fused) {
       // one kernel: a direct launch costs less host time than a graph launch
       ++fused_seq; // this call executes one fused launch
-      enqueue_coarse_path(lp, k, G, src);
+      enqueue_coarse_path(lp, k, G, src, tr);
       return;
     }
     if (staged) *h_qslot = src; // read by the chain's first kernel
@@ -1300,7 +1324,7 @@ void Ctx::coarse(const float* dQ, uint32_t nq, uint32_t n_out, cudaStream_t st, 
 }
 
 size_t Ctx::issue_fetch(std::vector<std::vector<uint32_t>>& slow, bool& any_slow,
-                        const float* dQ, uint32_t nq, uint32_t lp, const uint32_t* probe_dev,
+                        double gpu_busy, const float* dQ, uint32_t nq, uint32_t lp, const uint32_t* probe_dev,
                         int k, int G, FetchStats& st) {
   // Misses scanned on the GPU from the 2-slot ring: first every missed list
   // a peer GPU holds (copied over NVLink from the peer's slab, published for
@@ -1379,22 +1403,35 @@ size_t Ctx::issue_fetch(std::vector<std::vector<uint32_t>>& slow, bool& any_slow
     auto host_time = [&](double bytes, double tasks) {
       return tasks <= 0 ? 0.0 : bytes / (cr * std::min(1.0, tasks / threads));
     };
-    double gpu_t = 0;
+    // GPU side: the hit scan keeps the GPU busy for gpu_busy; fetched lists
+    // are copied meanwhile and their chunks scanned after it (a launch of
+    // partition + scan per chunk). Host side: the host scan, which runs
+    // during the hit scan. A list moves to the GPU only if that lowers the
+    // later of the two finishes.
+    double copy_t = 0, over_t = double(chunks.size()) * 50e-6;
+    bool gpu_any = !chunks.empty();
+    auto gpu_end = [&](double cp, double ov, bool any) {
+      return any ? std::max(gpu_busy, cp) + ov : gpu_busy;
+    };
     for (auto& [n, c] : cand) {
       const uint64_t len = ix->list_len(c);
       if (len == 0) continue;
       const double b = double(len) * d * 4;
       const bool new_chunk = chunks.empty() || fill + len > ring_vecs;
-      const double ng = gpu_t + b / link_rate + (new_chunk ? 50e-6 : 0.0); // partition + scan launch
+      const double ncp = copy_t + b / link_rate;
+      const double nov = over_t + (new_chunk ? 50e-6 : 0.0) + b / scan_rate;
       const double nct = host_time(host_bytes - b, host_tasks - tasks_of(c));
       if (miss_fetch == 1 &&
-          std::max(ng, nct) >= std::max(gpu_t, host_time(host_bytes, host_tasks))) {
+          std::max(gpu_end(ncp, nov, true), nct) >=
+              std::max(gpu_end(copy_t, over_t, gpu_any), host_time(host_bytes, host_tasks))) {
         break;
       }
       if (!add_item({c, ix->vecs + ix->list_off[c] * d, true})) break;
       on_gpu[c] = 1;
       ++st.fetch_lists;
-      gpu_t = ng;
+      copy_t = ncp;
+      over_t = nov;
+      gpu_any = true;
       host_bytes -= b;
       host_tasks -= tasks_of(c);
     }
@@ -1582,7 +1619,8 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
   const uint32_t d = ix->d;
   FetchStats fst;
   const size_t nchunks = (miss_fetch && any_slow)
-                             ? issue_fetch(slow, any_slow, dQ, nq, lp, d_order, k, G, fst)
+                             ? issue_fetch(slow, any_slow, busy_of(vfast), dQ, nq, lp, d_order, k,
+                                           G, fst)
                              : 0;
   std::vector<std::vector<Scored>> miss(nq);
   if (any_slow) {
@@ -1636,6 +1674,11 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
   r.t_coarse = ms * 1e-3;
   CK(cudaEventElapsedTime(&ms, ev_p, ev_s));
   r.t_scan = ms * 1e-3;
+  {
+    uint64_t v = 0;
+    for (uint64_t x : vfast) v += x;
+    note_scan(v, r.t_scan);
+  }
   return r;
 }
 
@@ -1733,8 +1776,8 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
   FetchStats fst;
   const size_t nchunks =
       (miss_fetch && any_host)
-          ? issue_fetch(host, any_host, d_Q, 1, lp, (explicit_probe || wide) ? d_order : dm_order,
-                        k, G, fst)
+          ? issue_fetch(host, any_host, busy_of(std::vector<uint64_t>(1, fast_vecs(r.fast))), d_Q,
+                        1, lp, (explicit_probe || wide) ? d_order : dm_order, k, G, fst)
           : 0;
   std::vector<Scored> miss;
   if (any_host) {
@@ -1834,6 +1877,7 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
     r.vecs_gpu += ix->list_len(c);
     r.bytes_gpu += ix->cluster_bytes(c);
   }
+  note_scan(r.vecs_gpu, r.t_scan);
   tr.mark("merge");
   tr.dump();
   return r;
