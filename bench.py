@@ -442,18 +442,27 @@ def run_ours(args, cfg):
     e_tm = HybridTimingC()
     e_cm = CostModelC(32e9, 1e-3, 1e-5, 1)
     e_fn = laiv.lib().laivg_hybrid_search
+    # the plain user call: no timing struct (the library then skips its
+    # device-event queries); host-link bytes from the library's counters
     e_args = (dev.h, None, L, k, C.byref(e_cm), e_ids.ctypes.data, e_sc.ctypes.data,
               C.byref(e_cnt), e_fast.ctypes.data, C.byref(e_nf), e_slow.ctypes.data,
-              C.byref(e_ns), C.byref(e_hr), C.byref(e_tm))
+              C.byref(e_ns), C.byref(e_hr), None)
     qo_c = np.ascontiguousarray(qo, np.float32)
+    lb_h, lb_d = C.c_uint64(), C.c_uint64()
+
+    def link_bytes():
+        check(laiv.lib().laivg_link_bytes(dev.h, C.byref(lb_h), C.byref(lb_d)))
+        return lb_h.value, lb_d.value
 
     def e2e_call(qidx):
         a = list(e_args)
         a[1] = qo_c[qidx].ctypes.data
+        h0, d0 = link_bytes()
         t = time.perf_counter()
         check(e_fn(*a))
-        return (time.perf_counter() - t, e_ids[: e_cnt.value].copy(), e_sc[: e_cnt.value].copy(),
-                e_tm.h2d_bytes, e_tm.d2h_bytes)
+        dt = time.perf_counter() - t
+        h1, d1 = link_bytes()
+        return (dt, e_ids[: e_cnt.value].copy(), e_sc[: e_cnt.value].copy(), h1 - h0, d1 - d0)
 
     def step(j, rec):
         qidx = mine[j]

@@ -294,6 +294,11 @@ int laivg_window_load(laivg_ctx* ctx, uint64_t buffer_bytes, double read_gbps);
 /* Pinned host <-> device copy rate of this context's GPU, measured with one
  * large cudaMemcpyAsync per direction (independent of the prefetch path). */
 int laivg_link_peak(laivg_ctx* ctx, uint64_t bytes, double* h2d_gbps, double* d2h_gbps);
+/* Host-link bytes moved by this context's single-query searches so far
+ * (query rows, residency tables, fetched lists; probes and results read
+ * back) — the per-call counts of laivg_hybrid_timing, cumulative, for
+ * callers that pass no timing struct. */
+int laivg_link_bytes(const laivg_ctx* ctx, uint64_t* h2d_bytes, uint64_t* d2h_bytes);
 
 /* ---- hybrid search (tiered.cpp:148-198) ---------------------------------- */
 typedef struct {

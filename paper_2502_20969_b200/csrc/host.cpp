@@ -262,8 +262,8 @@ std::vector<Scored> miss_scan(const Index& ix, const float* q,
   };
   std::vector<Task> tasks;
   for (uint32_t c : lists) {
-    for (uint64_t r = ix.list_off[c]; r < ix.list_off[c + 1]; r += kMissChunk) {
-      tasks.push_back({r, std::min(r + kMissChunk, ix.list_off[c + 1])});
+    for (uint64_t r = ix.list_off[c]; r < ix.list_off[c + 1]; r += kMissChunkSingle) {
+      tasks.push_back({r, std::min(r + kMissChunkSingle, ix.list_off[c + 1])});
     }
   }
   std::vector<TopList> per(pool.size(), TopList{ix.metric, k, {}});

@@ -22,7 +22,10 @@ namespace laivg {
 
 constexpr int kMetricIP = 0;
 constexpr int kMetricL2 = 1;
-constexpr uint64_t kMissChunk = 512; // vectors per host miss-scan task
+constexpr uint64_t kMissChunk = 512; // vectors per host miss-scan task (batched scan)
+// single query: a missed list is usually the only host work and must finish
+// inside the GPU's hit scan, so it is cut finer to occupy every host thread
+constexpr uint64_t kMissChunkSingle = 128;
 
 // CUDA failures map to LAIVG_ECUDA at the ABI.
 struct CudaError : std::runtime_error {

@@ -158,3 +158,40 @@ def test_fused_large_nc_shapes(orc, laiv):
                 probe = orc.coarse_probe(cen, metric, q, L)
                 got = sorted(a[0].fast_clusters + a[0].slow_clusters)
                 assert got == sorted(int(c) for c in probe)
+
+
+def test_plain_call_without_timing(laiv):
+    # laivg_hybrid_search with no timing struct (the library skips its event
+    # queries) returns the same result; the cumulative link counters count
+    # the call's host-link bytes (laivg_link_bytes)
+    import ctypes as C
+
+    from paper_2502_20969_b200._lib import CostModelC, check
+
+    cen, vecs, ids, off, qi, qo, _ = planted_data()
+    ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric.InnerProduct)
+    dev = laiv.Device(ix, BIG)
+    set_res((dev,), np.arange(64) % 2)
+    k, L = 10, 16
+    e_ids = np.empty(k, np.uint64)
+    e_sc = np.empty(k, np.float32)
+    fast = np.empty(64, np.uint32)
+    slow = np.empty(64, np.uint32)
+    cnt, nf, ns, hr = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_double()
+    cm = CostModelC(32e9, 1e-3, 1e-5, 1)
+    h, d = C.c_uint64(), C.c_uint64()
+    for t in range(6):
+        q = np.ascontiguousarray(qo[t], np.float32)
+        check(laiv.lib().laivg_link_bytes(dev.h, C.byref(h), C.byref(d)))
+        h0, d0 = h.value, d.value
+        check(laiv.lib().laivg_hybrid_search(dev.h, q.ctypes.data, L, k, C.byref(cm),
+                                             e_ids.ctypes.data, e_sc.ctypes.data, C.byref(cnt),
+                                             fast.ctypes.data, C.byref(nf), slow.ctypes.data,
+                                             C.byref(ns), C.byref(hr), None))
+        check(laiv.lib().laivg_link_bytes(dev.h, C.byref(h), C.byref(d)))
+        assert h.value - h0 >= 768 * 4 and d.value > d0
+        res, tm = laiv.hybrid_search(dev, q, L, k)
+        assert np.array_equal(res.topk.ids, e_ids[: cnt.value])
+        assert np.array_equal(res.topk.scores, e_sc[: cnt.value])
+        assert res.fast_clusters == fast[: nf.value].tolist()
+        assert tm.t_kernel > 0.0
