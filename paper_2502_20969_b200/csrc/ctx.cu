@@ -953,7 +953,15 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
     alloc_scan_set(fft, fso);
     h_fetch_cnt = pin_alloc<uint32_t>(size_t(kMaxFetchChunks) * max_batch);
   }
-  h_Q = pin_alloc<float>(size_t(max_batch) * d);
+  {
+    // the query staging rows: written by the host, read only by the GPU (a
+    // kernel or a copy), so write-combined (PCIe reads need no CPU snoop)
+    void* p = nullptr;
+    const unsigned fl = std::getenv("LAIVG_HQ_NOWC") ? cudaHostAllocPortable
+                                                    : (cudaHostAllocPortable | cudaHostAllocWriteCombined);
+    CK(cudaHostAlloc(&p, std::max<size_t>(1, size_t(max_batch) * d) * sizeof(float), fl));
+    h_Q = static_cast<float*>(p);
+  }
   h_order = pin_alloc_mapped<uint32_t>(size_t(max_batch) * std::max(nc, 1u), &dm_order);
   {
     const float** dslot = nullptr;
