@@ -2079,6 +2079,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_query_kernel(FusedArgs
     if (stamp) q_st[1] = globaltimer();
     ring_init(rs, a.S);
     __syncthreads();
+    // the row also lands in dQ: the miss path's chunk scans that follow this
+    // kernel on the stream (runtime fetch, peer copies) read the query there
+    if (blockIdx.x == 0) {
+      for (uint32_t i = threadIdx.x; i < a.d; i += blockDim.x) a.dQ[i] = rs.sq[i];
+    }
   } else {
     if (blockIdx.x == 0) {
       if ((reinterpret_cast<uintptr_t>(src) & 15u) == 0) {

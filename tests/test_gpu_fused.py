@@ -112,6 +112,25 @@ def test_fused_empty_lists_and_no_resident(orc, laiv):
         assert laiv.ivf_search(fused, q, 0, 5).entries == []
 
 
+@pytest.mark.parametrize("miss_fetch", ["off", "auto", "all"])
+def test_fused_staged_misses_every_path(orc, laiv, miss_fetch):
+    # staged rows with a third of the lists missing: the misses go to the
+    # host, to the runtime fetch ring (chunk scans after the fused kernel read
+    # the query from dQ), or are split between them; every path is exact
+    cen, vecs, ids, off, qi, qo, _ = planted_data()
+    ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric.InnerProduct)
+    dev = laiv.Device(ix, BIG, miss_fetch=miss_fetch, fetch_chunk_mb=4)
+    set_res((dev,), np.arange(64) % 3 != 0)
+    dev.stage_queries(qo)
+    for t in range(40):
+        want = orc.ivf_search(cen, vecs, ids, off, IP, qo[t], 16, 10)
+        i, s, n, tm = dev.hybrid_search_staged(t, 16, 10)
+        assert tm.t_kernel > 0.0
+        assert_topk_parity(IP, i, s, *want)
+        res, _ = laiv.hybrid_search(dev, qo[t], 16, 10)
+        assert_topk_parity(IP, res.topk.ids, res.topk.scores, *want)
+
+
 def test_fused_staged_queries_and_repeats(laiv):
     # the staged-row entry (mapped slot) and back-to-back calls: the grid
     # barrier word and the probe sequence number carry across launches
