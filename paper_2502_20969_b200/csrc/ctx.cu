@@ -610,9 +610,10 @@ struct Ctx {
     }
     return it->second != 0;
   }
-  // Waits until the fused kernel of call `seq` has published its probe.
-  void wait_probe_flag(unsigned seq) {
-    const volatile unsigned* f = h_flag;
+  // Waits until the fused kernel of call `seq` has published its probe
+  // (word 0) or all of its results (word 1).
+  void wait_probe_flag(unsigned seq, int word = 0) {
+    const volatile unsigned* f = h_flag + word;
     uint32_t spins = 0;
     while (*f != seq) {
       if ((++spins & 0x3fffu) == 0) {
@@ -669,6 +670,7 @@ struct Ctx {
       fq.order_out = dm_order;
       fq.fcount_out = dm_fcount;
       fq.flag_out = dm_flag;
+      fq.done_out = dm_flag + 1;
       fq.ctl = d_ctl;
       fq.stamps = dm_stamps;
       fq.cta_stamps = dm_cta_stamps;
@@ -974,10 +976,10 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   h_fcount = pin_alloc_mapped<uint32_t>(max_batch, &dm_fcount);
   fused_on = o.single_chain == 0 && !std::getenv("LAIVG_CHAIN");
   d_keys = dev_alloc<uint64_t>(std::max(nc, 1u));
-  d_ctl = dev_alloc<unsigned>(2);
-  CK(cudaMemset(d_ctl, 0, 2 * sizeof(unsigned)));
-  h_flag = pin_alloc_mapped<unsigned>(1, &dm_flag);
-  *h_flag = 0;
+  d_ctl = dev_alloc<unsigned>(3);
+  CK(cudaMemset(d_ctl, 0, 3 * sizeof(unsigned)));
+  h_flag = pin_alloc_mapped<unsigned>(2, &dm_flag); // [0] probe out, [1] results out
+  h_flag[0] = h_flag[1] = 0;
   h_stamps = pin_alloc_mapped<unsigned long long>(32, &dm_stamps);
   if (std::getenv("LAIVG_SCAN_PROBE")) {
     h_cta_stamps = pin_alloc_mapped<unsigned long long>(size_t(sms) * 4, &dm_cta_stamps);
@@ -1797,7 +1799,8 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
     r.t_c = secs(tc, Clock::now());
   }
   tr.mark("split_miss");
-  CK(cudaEventSynchronize((explicit_probe || wide) ? ev_c : ev_s));
+  if (fused) wait_probe_flag(fused_seq, 1); // results out (before the kernel's teardown)
+  else CK(cudaEventSynchronize((explicit_probe || wide) ? ev_c : ev_s));
   if (nchunks) CK(cudaEventSynchronize(ev_fdone));
   tr.mark("scan_wait");
   if (*h_fcount != r.fast.size()) {
@@ -1839,6 +1842,7 @@ Ctx::Result Ctx::search(const float* dq, const float* hq, int L, int k,
   if (fused) {
     // one kernel: its event time; the coarse + selection phase from CTA 0's
     // globaltimer stamps (entry -> scan ranges ready)
+    CK(cudaEventSynchronize(ev_s)); // the host only waited for the results flag
     CK(cudaEventElapsedTime(&ms, ev_a, ev_s));
     r.t_kernel = ms * 1e-3;
     r.t_coarse = std::min(r.t_kernel, double(h_stamps[5] - h_stamps[0]) * 1e-9);

@@ -1647,7 +1647,8 @@ struct FusedArgs {
   uint32_t* order_out;          // [L] the probe (mapped host memory)
   uint32_t* fcount_out;         // fast-list count (mapped)
   unsigned* flag_out;           // mapped: call sequence number, probe is out
-  unsigned* ctl;                // [0] grid barrier word, [1] call sequence
+  unsigned* done_out;           // mapped: call sequence number, results are out
+  unsigned* ctl;                // [0] grid barrier word, [1] call sequence, [2] done ticket
   unsigned long long* stamps;   // [32] phase stamps of CTA 0 (mapped), nullable
   unsigned long long* cta_stamps; // [G][4] entry, query ready, keys ready, done; nullable
   int qdirect;                  // every CTA reads a host row itself (diagnostics)
@@ -2214,6 +2215,19 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_query_kernel(FusedArgs
     for (int i = 0; i < 12; ++i) a.stamps[8 + i] = s_dbg[i];
     for (int i = 0; i < 3; ++i) a.stamps[20 + i] = q_st[i];
   }
+  // completion: the last CTA to finish publishes the call's sequence number
+  // after every CTA's results (mapped host memory) are visible, so the host
+  // need not wait for the kernel's teardown and its event
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    if (atomicAdd(a.ctl + 2, 1u) == gridDim.x - 1) {
+      a.ctl[2] = 0u;
+      const unsigned s = *reinterpret_cast<volatile unsigned*>(a.ctl + 1);
+      __threadfence_system();
+      *reinterpret_cast<volatile unsigned*>(a.done_out) = s;
+    }
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -2687,6 +2701,7 @@ void launch_fused_query(const FusedQuery& q, const ScanOut& out, bool acc_fp64,
   a.order_out = q.order_out;
   a.fcount_out = q.fcount_out;
   a.flag_out = q.flag_out;
+  a.done_out = q.done_out;
   a.ctl = q.ctl;
   a.stamps = q.stamps;
   a.cta_stamps = q.cta_stamps;

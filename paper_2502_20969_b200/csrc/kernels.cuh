@@ -129,7 +129,8 @@ struct FusedQuery {
   uint32_t* order_out = nullptr;       // [L] (device-visible, mapped)
   uint32_t* fcount_out = nullptr;
   unsigned* flag_out = nullptr;
-  unsigned* ctl = nullptr;             // [2] device: barrier word, sequence (zeroed)
+  unsigned* done_out = nullptr;        // mapped: sequence number once every CTA's results are out
+  unsigned* ctl = nullptr;             // [3] device: barrier word, sequence, done ticket (zeroed)
   // [8] CTA 0 globaltimer stamps (mapped), nullable: entry, query ready,
   // keys ready, keys loaded, top-L selected, scan ranges ready, last tile
   // consumed, done
