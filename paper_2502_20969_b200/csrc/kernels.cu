@@ -830,10 +830,14 @@ __device__ __forceinline__ void tc_bounds(int metric, double a, double qn, doubl
 // One CTA (1024 threads) per query. smem: q[d], 32-bit keys of the lower
 // bounds[nc], upper bounds[nc], candidate keys/ids[cap] (cap = pow2 >= nc,
 // so every centroid fits).
+// Threads per query CTA: 1024 for small batches; 512 (two CTAs per SM) once
+// the batch exceeds the SM count, so a 256-query batch runs in one wave
+// (1024-thread CTAs are held to one per SM by the register file)
 constexpr int kSelThreads = 1024;
 // LAIVG_TC_PROBE diagnostics: query 0's CTA stamps its phases here
 __device__ unsigned long long g_tc_dbg[8];
-__global__ void __launch_bounds__(kSelThreads)
+template <int NT>
+__global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1)
     tc_select_kernel(const float* __restrict__ approx, uint32_t splits,
                      const float* __restrict__ Q, uint32_t d,
                      const float* __restrict__ cen, const float* __restrict__ cnorm,
@@ -2137,13 +2141,28 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_query_kernel(FusedArgs
   unsigned long long va = ~0ull, vo = 0ull, vmin = ~0ull;
   {
     const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(a.keys);
-    for (uint32_t i = threadIdx.x; i < a.nc / 2; i += blockDim.x) {
-      const ulonglong2 v = __ldcg(k2 + i);
-      sk[2 * i] = v.x;
-      sk[2 * i + 1] = v.y;
-      va &= v.x & v.y;
-      vo |= v.x | v.y;
-      vmin = min(vmin, min(v.x, v.y));
+    // eight 16-byte loads per thread in flight per round (the stores to
+    // shared memory would otherwise serialise them behind each other)
+    constexpr int kB = 8;
+    const uint32_t n2 = a.nc / 2;
+    for (uint32_t base = 0; base < n2; base += kB * blockDim.x) {
+      ulonglong2 v[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const uint32_t i = base + u * blockDim.x + threadIdx.x;
+        v[u] = i < n2 ? __ldcg(k2 + i) : make_ulonglong2(~0ull, ~0ull);
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const uint32_t i = base + u * blockDim.x + threadIdx.x;
+        if (i < n2) {
+          sk[2 * i] = v[u].x;
+          sk[2 * i + 1] = v[u].y;
+          va &= v[u].x & v[u].y;
+          vo |= v[u].x | v[u].y;
+          vmin = min(vmin, min(v[u].x, v[u].y));
+        }
+      }
     }
     if ((a.nc & 1u) && threadIdx.x == 0) {
       const unsigned long long v = __ldcg(reinterpret_cast<const unsigned long long*>(a.keys) + a.nc - 1);
@@ -2581,10 +2600,18 @@ void launch_tc_select(const float* approx, uint32_t splits, const float* Q, uint
   while (cap < nc) cap <<= 1;
   const size_t smem = tc_select_smem(nc, d);
   if (smem > 227 * 1024) throw CudaError("tc_select: shared memory exceeds 227 KB");
-  ensure_dyn_smem(reinterpret_cast<const void*>(tc_select_kernel), smem);
+  int nsm = 148;
+  {
+    int dv = 0;
+    cudaGetDevice(&dv);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dv);
+  }
+  const bool half = nq > uint32_t(nsm);
+  auto kfn = half ? tc_select_kernel<512> : tc_select_kernel<kSelThreads>;
+  ensure_dyn_smem(reinterpret_cast<const void*>(kfn), smem);
   const FastTable f = ft ? *ft : FastTable{};
   static const bool probe = std::getenv("LAIVG_TC_PROBE") != nullptr;
-  tc_select_kernel<<<nq, kSelThreads, smem, st>>>(approx, splits, Q, d, centroids, cnorm, nc, metric,
+  kfn<<<nq, half ? 512 : kSelThreads, smem, st>>>(approx, splits, Q, d, centroids, cnorm, nc, metric,
                                            n_out,
                                            cap, order, res_off, list_off, f, ft != nullptr,
                                            scan_sorted, probe);
