@@ -5,7 +5,8 @@ infrastructure: the oracle is the checker). Each trial draws an index shape
 exact ties), a metric, a residency, a miss mode, nprobe and k (incl. k above
 the candidate count), and checks single-query hybrid_search, the batch path
 and the scan-only search_clusters against the oracle with the §8c rule,
-batch == single bit for bit, and the prefetch planner and coverage exactly.
+batch == single == staged single bit for bit, and the prefetch planner and
+coverage exactly.
 
     python tools/fuzz_parity.py --trials 200 --seed 1
 """
@@ -64,11 +65,16 @@ def main():
                 if rng.random() < frac and sizes[c] > 0:
                     dev.store.insert(c)
             res, _ = laiv.hybrid_search_batch(dev, Q, L, k)
+            dev.stage_queries(Q)
             for q in range(nq):
                 single, _ = laiv.hybrid_search(dev, Q[q], L, k)
                 got = res.topk(q)
                 assert np.array_equal(got.ids, single.topk.ids), "batch != single ids"
                 assert np.array_equal(got.scores, single.topk.scores), "batch != single scores"
+                # the staged-row entry (single-query kernel reading HBM rows)
+                si, ss, _, _ = dev.hybrid_search_staged(q, L, k)
+                assert np.array_equal(si, single.topk.ids), "staged != host ids"
+                assert np.array_equal(ss, single.topk.scores), "staged != host scores"
                 want = orc.ivf_search(cen, vecs, ids, off, metric, Q[q], L, k)
                 assert_topk_parity(metric, got.ids, got.scores, *want)
                 probe = laiv.coarse_probe(dev, Q[q], L).reshape(-1)
