@@ -193,6 +193,7 @@ struct Ctx {
   bool tc_ok = false;
   float* d_approx = nullptr; // [max_batch][nc] tf32 scores
   float* d_cnorm = nullptr;  // [nc] ||c|| rounded up
+  TcSelectScratch tcs{};     // three-kernel exact selection scratch
   float* d_Q = nullptr;
   double* d_scores = nullptr;
   uint32_t* d_order = nullptr;
@@ -776,6 +777,7 @@ Ctx::~Ctx() {
                   (void*)so.part_s, (void*)so.part_id, (void*)so.part_vi, (void*)so.ticket,
                   (void*)so.gpart_s, (void*)so.gpart_id, (void*)so.gpart_vi,
                   (void*)d_staged, (void*)d_approx, (void*)d_cnorm, (void*)d_keys,
+                  (void*)tcs.cand, (void*)tcs.key, (void*)tcs.ncand,
                   (void*)d_ctl, (void*)d_wbuf, (void*)d_wsink, (void*)d_wread}) {
     if (p) cudaFree(p);
   }
@@ -918,6 +920,13 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
     }
     d_cnorm = dev_alloc<float>(nc);
     CK(cudaMemcpy(d_cnorm, cn.data(), nc * sizeof(float), cudaMemcpyHostToDevice));
+    if (!std::getenv("LAIVG_TC_SELECT1")) { // (A/B: the single-kernel selection)
+      uint32_t cap = 2;
+      while (cap < nc) cap <<= 1;
+      tcs.cand = dev_alloc<uint32_t>(size_t(max_batch) * cap);
+      tcs.key = dev_alloc<uint64_t>(size_t(max_batch) * cap);
+      tcs.ncand = dev_alloc<uint32_t>(max_batch);
+    }
   }
   d_scores = dev_alloc<double>(size_t(max_batch) * nc);
   d_order = dev_alloc<uint32_t>(size_t(max_batch) * std::max(nc, 1u));
@@ -1327,7 +1336,7 @@ void Ctx::coarse(const float* dQ, uint32_t nq, uint32_t n_out, cudaStream_t st, 
     const uint32_t S = launch_coarse_tc(dQ, nq, d_cen, ix->nc, ix->d, d_approx, sms, st);
     launch_tc_select(d_approx, S, dQ, nq, ix->d, d_cen, d_cnorm, ix->nc, ix->metric, n_out,
                      d_order, part ? d_res : nullptr, part ? d_list_off : nullptr, f, st,
-                     /*scan_sorted=*/part && nq > 1);
+                     /*scan_sorted=*/part && nq > 1, &tcs);
     return;
   }
   launch_coarse_scores(dQ, nq, d_cen, ix->nc, ix->d, ix->metric, d_scores, st);

@@ -497,7 +497,8 @@ __device__ void block_bitonic_sort(uint64_t (&k)[E], uint32_t (&v)[E], uint64_t*
         if (j == 1) inthread_stage<E, 1>(k, v, kk);
         else if (j == 2) inthread_stage<E, 2>(k, v, kk);
         else if (j == 4) inthread_stage<E, 4>(k, v, kk);
-        else inthread_stage<E, 8>(k, v, kk);
+        else if (j == 8) inthread_stage<E, 8>(k, v, kk);
+        else inthread_stage<E, 16>(k, v, kk);
       } else if (j < 32u * E) {
         const int lm = static_cast<int>(j / E);
 #pragma unroll
@@ -1016,6 +1017,361 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1)
   }
   if (dbg) g_tc_dbg[6] = globaltimer();
 }
+
+// ---- batched exact selection, three kernels ------------------------------
+// tc_filter_kernel   per query: the bounds pass, radix select and candidate
+//                    collection of tc_select_kernel; candidates to global
+// tc_rescore_stream  one CTA per SM over the flattened (query, candidate)
+//                    pairs: a producer warp gathers candidate centroid rows
+//                    with bulk copies into a two-stage ring (the scan's
+//                    design), eight consumer warps score them with
+//                    warp_coarse_score's arithmetic (same lane-strided fp64
+//                    terms, same butterfly) -> exact order keys
+// tc_sort_kernel     per query: register/shuffle bitonic sort on (key, id),
+//                    first n_out, fused residency split
+template <int NT>
+__global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1)
+    tc_filter_kernel(const float* __restrict__ approx, uint32_t splits,
+                     const float* __restrict__ Q, uint32_t d, const float* __restrict__ cnorm,
+                     uint32_t nc, int metric, uint32_t n_out, uint32_t cap,
+                     uint32_t* __restrict__ cand, uint32_t* __restrict__ ncand) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  uint32_t* lok = reinterpret_cast<uint32_t*>(sm);
+  float* hik = reinterpret_cast<float*>(sm + ((static_cast<size_t>(nc) * 4 + 15) & ~size_t(15)));
+  __shared__ uint32_t hist[256];
+  __shared__ double red[32];
+  __shared__ uint32_t s_prefix, s_rank, s_count;
+  const uint32_t q = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* qv = Q + static_cast<uint64_t>(q) * d;
+  const float* aq = approx + static_cast<uint64_t>(q) * nc;
+  const uint64_t plane = static_cast<uint64_t>(gridDim.x) * nc;
+  double part = 0.0;
+  for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) {
+    const float x = qv[i];
+    part += static_cast<double>(x) * x;
+  }
+  part = warp_sum(part);
+  if (lane == 0) red[warp] = part;
+  if (threadIdx.x == 0) {
+    s_prefix = 0;
+    s_rank = n_out - 1;
+    s_count = 0;
+  }
+  __syncthreads();
+  double qn2 = 0.0;
+  for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) qn2 += red[w];
+  const double qn = sqrt(qn2) * (1.0 + 1e-12);
+  for (uint32_t c0 = threadIdx.x; c0 < nc; c0 += 4 * blockDim.x) {
+    double a[4];
+    float cn[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t c = c0 + u * blockDim.x;
+      a[u] = 0.0;
+      cn[u] = 0.0f;
+      if (c < nc) {
+        cn[u] = cnorm[c];
+        for (uint32_t z = 0; z < splits; ++z) a[u] += aq[z * plane + c];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t c = c0 + u * blockDim.x;
+      if (c < nc) {
+        float lo, hi;
+        tc_bounds(metric, a[u], qn, qn2, cn[u], lo, hi);
+        lok[c] = ~float_order(lo);
+        hik[c] = hi;
+      }
+    }
+  }
+  uint32_t mask = 0;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const uint32_t prefix = s_prefix;
+    for (uint32_t c0 = 0; c0 < nc; c0 += blockDim.x) {
+      const uint32_t c = c0 + threadIdx.x;
+      const bool in = c < nc && (lok[c] & mask) == prefix;
+      const uint32_t bin = in ? (lok[c] >> shift) & 255u : 256u;
+      const unsigned peers = __match_any_sync(kFull, bin);
+      if (in && (__ffs(peers) - 1) == lane) atomicAdd(&hist[bin], __popc(peers));
+    }
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t h[8], tot = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        h[i] = hist[lane * 8 + i];
+        tot += h[i];
+      }
+      uint32_t inc = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += t;
+      }
+      const uint32_t rank = s_rank, excl = inc - tot;
+      if (rank >= excl && rank < inc) {
+        uint32_t r = rank - excl, b = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (r >= h[i] && b == static_cast<uint32_t>(i)) {
+            r -= h[i];
+            ++b;
+          }
+        }
+        s_rank = r;
+        s_prefix = prefix | ((lane * 8u + b) << shift);
+      }
+    }
+    mask |= 255u << shift;
+    __syncthreads();
+  }
+  const float T = order_float(~s_prefix);
+  uint32_t* out = cand + static_cast<uint64_t>(q) * cap;
+  for (uint32_t c0 = 0; c0 < nc; c0 += blockDim.x) {
+    const uint32_t c = c0 + threadIdx.x;
+    const bool take = c < nc && hik[c] >= T;
+    const unsigned m = __ballot_sync(kFull, take);
+    uint32_t base = 0;
+    if (lane == 0 && m) base = atomicAdd(&s_count, static_cast<uint32_t>(__popc(m)));
+    base = __shfl_sync(kFull, base, 0);
+    if (take) out[base + __popc(m & ((1u << lane) - 1u))] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) ncand[q] = s_count;
+}
+
+constexpr int kRsConsumers = 8;
+constexpr int kRsThreads = 32 * (kRsConsumers + 1);
+constexpr uint32_t kRsTile = 32; // rows per ring stage
+constexpr uint32_t kRsMaxPairs = 2048; // pairs one CTA resolves up front (grid sized to fit)
+template <int NCH>
+__global__ void __launch_bounds__(kRsThreads, 1)
+    tc_rescore_stream_kernel(const float* __restrict__ Q, uint32_t d,
+                             const float* __restrict__ cen, int metric, uint32_t nq, uint32_t cap,
+                             const uint32_t* __restrict__ cand, const uint32_t* __restrict__ ncand,
+                             uint64_t* __restrict__ ckey) {
+  extern __shared__ __align__(128) unsigned char smr[];
+  constexpr uint32_t S = 2;
+  const size_t row_f = d;
+  float* ring = reinterpret_cast<float*>(smr);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smr + S * kRsTile * row_f * 4);
+  uint64_t* empty = full + S;
+  uint32_t* mq = reinterpret_cast<uint32_t*>(empty + S);  // [S][T] query of the row
+  uint32_t* mi = mq + S * kRsTile;                         // [S][T] candidate index
+  uint32_t* mn = mi + S * kRsTile;                         // [S] rows in the stage
+  uint32_t* pref = mn + S;                                 // [nq + 1]
+  uint32_t* rq = pref + nq + 1;                            // this CTA's pairs: query,
+  uint32_t* ri = rq + kRsMaxPairs;                         //   candidate index,
+  uint32_t* rc = ri + kRsMaxPairs;                         //   centroid
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // exclusive prefix of the candidate counts (every CTA, in shared memory)
+  if (warp == 0) {
+    uint32_t run = 0;
+    for (uint32_t b = 0; b < nq; b += 32) {
+      const uint32_t q = b + lane;
+      const uint32_t v = q < nq ? ncand[q] : 0u;
+      uint32_t inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += t;
+      }
+      if (q < nq) pref[q] = run + inc - v;
+      run += __shfl_sync(kFull, inc, 31);
+    }
+    if (lane == 0) pref[nq] = run;
+  }
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kRsConsumers);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t P = pref[nq];
+  const uint64_t p0 = P * blockIdx.x / gridDim.x, p1 = P * (blockIdx.x + 1) / gridDim.x;
+  uint32_t tg = 0; // ring tiles issued / consumed so far (stage parity)
+  uint32_t cur_q = 0xffffffffu;
+  double qd[NCH * 4];
+  for (uint64_t c0 = p0; c0 < p1; c0 += kRsMaxPairs) {
+    const uint32_t np = static_cast<uint32_t>(min(static_cast<uint64_t>(kRsMaxPairs), p1 - c0));
+    // resolve this chunk's pairs once, every thread, all candidate loads in flight
+    for (uint32_t x = threadIdx.x; x < np; x += blockDim.x) {
+      const uint64_t p = c0 + x;
+      uint32_t lo = 0, hi = nq - 1; // last q with pref[q] <= p
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (pref[mid] <= p) lo = mid;
+        else hi = mid - 1;
+      }
+      const uint32_t i = static_cast<uint32_t>(p - pref[lo]);
+      rq[x] = lo;
+      ri[x] = i;
+      rc[x] = cand[static_cast<uint64_t>(lo) * cap + i];
+    }
+    __syncthreads();
+    const uint32_t ntiles = (np + kRsTile - 1) / kRsTile;
+    if (warp == 0) {
+      // producer: one lane issues the row copies, the others publish metadata
+      for (uint32_t t = 0; t < ntiles; ++t) {
+        const uint32_t tt = tg + t, s = tt % S;
+        mbar_wait(empty + s, ((tt / S) & 1u) ^ 1u);
+        const uint32_t x0 = t * kRsTile;
+        const uint32_t n = min(kRsTile, np - x0);
+        if (static_cast<uint32_t>(lane) < n) {
+          mq[s * kRsTile + lane] = rq[x0 + lane];
+          mi[s * kRsTile + lane] = ri[x0 + lane];
+        }
+        if (lane == 0) mn[s] = n;
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive_expect_tx(full + s, n * d * 4u);
+          for (uint32_t j = 0; j < n; ++j) {
+            bulk_g2s(ring + (static_cast<size_t>(s) * kRsTile + j) * row_f,
+                     cen + static_cast<uint64_t>(rc[x0 + j]) * d, d * 4u, full + s);
+          }
+        }
+        __syncwarp();
+      }
+    } else {
+      const int cw = warp - 1;
+      for (uint32_t t = 0; t < ntiles; ++t) {
+        const uint32_t tt = tg + t, s = tt % S;
+        mbar_wait(full + s, (tt / S) & 1u);
+        const uint32_t n = mn[s];
+        auto stage_query = [&](uint32_t q) { // this query's terms in registers (fp64)
+          const float4* q4 = reinterpret_cast<const float4*>(Q + static_cast<uint64_t>(q) * d);
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) {
+            const uint32_t jj = lane + 32u * c;
+            const float4 v = jj < d / 4 ? __ldg(q4 + jj) : make_float4(0.f, 0.f, 0.f, 0.f);
+            qd[4 * c + 0] = v.x;
+            qd[4 * c + 1] = v.y;
+            qd[4 * c + 2] = v.z;
+            qd[4 * c + 3] = v.w;
+          }
+          cur_q = q;
+        };
+        // rows cw, cw + 8, cw + 16, cw + 24 of the stage: four independent
+        // accumulator chains when they share a query (the usual case)
+        constexpr int kR = static_cast<int>(kRsTile) / kRsConsumers;
+        const uint32_t j0 = cw;
+        bool same = j0 + (kR - 1) * kRsConsumers < n;
+        const uint32_t q0 = j0 < n ? mq[s * kRsTile + j0] : 0u;
+#pragma unroll
+        for (int u = 1; u < kR; ++u) {
+          same = same && mq[s * kRsTile + j0 + u * kRsConsumers] == q0;
+        }
+        if (same) {
+          if (q0 != cur_q) stage_query(q0);
+          double acc[kR];
+          const float4* r4[kR];
+#pragma unroll
+          for (int u = 0; u < kR; ++u) {
+            acc[u] = 0.0;
+            r4[u] = reinterpret_cast<const float4*>(
+                ring + (static_cast<size_t>(s) * kRsTile + j0 + u * kRsConsumers) * row_f);
+          }
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) {
+            const uint32_t jj = lane + 32u * c;
+            if (jj < d / 4) {
+#pragma unroll
+              for (int u = 0; u < kR; ++u) Acc4<true>::run(metric, qd + 4 * c, r4[u][jj], acc[u]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kR; ++u) acc[u] = warp_sum(acc[u]);
+          if (lane == 0) {
+#pragma unroll
+            for (int u = 0; u < kR; ++u) {
+              ckey[static_cast<uint64_t>(q0) * cap + mi[s * kRsTile + j0 + u * kRsConsumers]] =
+                  order_key(acc[u], metric);
+            }
+          }
+        } else {
+          for (uint32_t j = j0; j < n; j += kRsConsumers) {
+            const uint32_t q = mq[s * kRsTile + j];
+            if (q != cur_q) stage_query(q);
+            const float4* r4 = reinterpret_cast<const float4*>(
+                ring + (static_cast<size_t>(s) * kRsTile + j) * row_f);
+            double acc = 0.0;
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+              const uint32_t jj = lane + 32u * c;
+              if (jj < d / 4) Acc4<true>::run(metric, qd + 4 * c, r4[jj], acc);
+            }
+            acc = warp_sum(acc);
+            if (lane == 0) {
+              ckey[static_cast<uint64_t>(q) * cap + mi[s * kRsTile + j]] = order_key(acc, metric);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+      }
+    }
+    tg += ntiles;
+    __syncthreads(); // the chunk's metadata arrays are rewritten next
+  }
+}
+
+constexpr int kSortThreads = 256;
+template <int E>
+__device__ void tc_sort_run(const uint64_t* kq, const uint32_t* cq, uint32_t n, uint64_t* sk,
+                            uint32_t* sv) {
+  uint64_t k[E];
+  uint32_t v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t i = threadIdx.x * E + e;
+    k[e] = i < n ? kq[i] : ~0ull;
+    v[e] = i < n ? cq[i] : ~0u;
+  }
+  block_bitonic_sort<E>(k, v, sk, sv, static_cast<uint32_t>(kSortThreads) * E);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    sk[threadIdx.x * E + e] = k[e];
+    sv[threadIdx.x * E + e] = v[e];
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSortThreads)
+    tc_sort_kernel(uint32_t cap, const uint32_t* __restrict__ cand,
+                   const uint32_t* __restrict__ ncand, const uint64_t* __restrict__ ckey,
+                   uint32_t n_out, uint32_t* __restrict__ order, const int64_t* res_off,
+                   const uint64_t* list_off, FastTable ft, bool do_partition, bool scan_sorted) {
+  extern __shared__ __align__(16) unsigned char smx[];
+  const uint32_t q = blockIdx.x, n = ncand[q];
+  uint32_t m = kSortThreads;
+  while (m < n) m <<= 1;
+  uint64_t* sk = reinterpret_cast<uint64_t*>(smx);
+  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + m);
+  const uint64_t* kq = ckey + static_cast<uint64_t>(q) * cap;
+  const uint32_t* cq = cand + static_cast<uint64_t>(q) * cap;
+  switch (m / kSortThreads) {
+    case 1: tc_sort_run<1>(kq, cq, n, sk, sv); break;
+    case 2: tc_sort_run<2>(kq, cq, n, sk, sv); break;
+    case 4: tc_sort_run<4>(kq, cq, n, sk, sv); break;
+    case 8: tc_sort_run<8>(kq, cq, n, sk, sv); break;
+    case 16: tc_sort_run<16>(kq, cq, n, sk, sv); break;
+    default: tc_sort_run<32>(kq, cq, n, sk, sv); break;
+  }
+  uint32_t* out = order + static_cast<uint64_t>(q) * n_out;
+  for (uint32_t i = threadIdx.x; i < n_out; i += blockDim.x) out[i] = sv[i];
+  if (do_partition) {
+    __syncthreads();
+    if (scan_sorted) sort_ids_block(sv, n_out);
+    partition_block(sv, n_out, res_off, list_off, ft, q);
+  }
+}
+
 
 // --------------------------------------------------------------------------
 // shared scan epilogue: CTA merge, grid merge, exact re-score of survivors
@@ -2594,12 +2950,11 @@ void launch_tc_select(const float* approx, uint32_t splits, const float* Q, uint
                       uint32_t d, const float* centroids, const float* cnorm, uint32_t nc, int metric,
                       uint32_t n_out, uint32_t* order, const int64_t* res_off,
                       const uint64_t* list_off, const FastTable* ft, cudaStream_t st,
-                      bool scan_sorted) {
+                      bool scan_sorted, const TcSelectScratch* sc) {
   if (nq == 0 || n_out == 0) return;
   uint32_t cap = 2;
   while (cap < nc) cap <<= 1;
-  const size_t smem = tc_select_smem(nc, d);
-  if (smem > 227 * 1024) throw CudaError("tc_select: shared memory exceeds 227 KB");
+  const FastTable f = ft ? *ft : FastTable{};
   int nsm = 148;
   {
     int dv = 0;
@@ -2607,9 +2962,32 @@ void launch_tc_select(const float* approx, uint32_t splits, const float* Q, uint
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dv);
   }
   const bool half = nq > uint32_t(nsm);
+  if (sc != nullptr && sc->cand != nullptr && cap <= 8192 && (d % 4) == 0 && d <= 1024) {
+    // filter (per query) -> streamed exact re-score (one CTA per SM) -> sort
+    const size_t fs = 2 * ((size_t(nc) * 4 + 15) & ~size_t(15));
+    auto ffn = half ? tc_filter_kernel<512> : tc_filter_kernel<kSelThreads>;
+    ensure_dyn_smem(reinterpret_cast<const void*>(ffn), fs);
+    ffn<<<nq, half ? 512 : kSelThreads, fs, st>>>(approx, splits, Q, d, cnorm, nc, metric, n_out,
+                                                 cap, sc->cand, sc->ncand);
+    after_launch();
+    const size_t rs = 2 * size_t(kRsTile) * d * 4 + 2 * 16 + 2 * kRsTile * 8 + 16 +
+                      (size_t(nq) + 1) * 4 + size_t(kRsMaxPairs) * 12 + 64;
+    auto rfn = d <= 768 ? tc_rescore_stream_kernel<6> : tc_rescore_stream_kernel<8>;
+    ensure_dyn_smem(reinterpret_cast<const void*>(rfn), rs);
+    rfn<<<nsm, kRsThreads, rs, st>>>(Q, d, centroids, metric, nq, cap, sc->cand, sc->ncand,
+                                      sc->key);
+    after_launch();
+    const size_t ss = size_t(std::max<uint32_t>(cap, kSortThreads)) * 12 + 16;
+    ensure_dyn_smem(reinterpret_cast<const void*>(tc_sort_kernel), ss);
+    tc_sort_kernel<<<nq, kSortThreads, ss, st>>>(cap, sc->cand, sc->ncand, sc->key, n_out, order,
+                                                 res_off, list_off, f, ft != nullptr, scan_sorted);
+    after_launch();
+    return;
+  }
+  const size_t smem = tc_select_smem(nc, d);
+  if (smem > 227 * 1024) throw CudaError("tc_select: shared memory exceeds 227 KB");
   auto kfn = half ? tc_select_kernel<512> : tc_select_kernel<kSelThreads>;
   ensure_dyn_smem(reinterpret_cast<const void*>(kfn), smem);
-  const FastTable f = ft ? *ft : FastTable{};
   static const bool probe = std::getenv("LAIVG_TC_PROBE") != nullptr;
   kfn<<<nq, half ? 512 : kSelThreads, smem, st>>>(approx, splits, Q, d, centroids, cnorm, nc, metric,
                                            n_out,

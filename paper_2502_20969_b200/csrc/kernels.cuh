@@ -167,12 +167,19 @@ uint32_t launch_coarse_tc(const float* Q, uint32_t nq, const float* centroids, u
 // re-scored with the fp64 arithmetic of launch_coarse_scores and sorted on
 // (score, cluster id). With `ft`, also splits the probe by residency.
 // cnorm[c] = ||c|| rounded up.
+// Device scratch of the three-kernel batched selection: candidates and
+// their exact keys [nq][cap] (cap = pow2 >= nc), counts [nq].
+struct TcSelectScratch {
+  uint32_t* cand = nullptr;
+  uint64_t* key = nullptr;
+  uint32_t* ncand = nullptr;
+};
 void launch_tc_select(const float* approx, uint32_t splits, const float* Q, uint32_t nq,
                       uint32_t d,
                       const float* centroids, const float* cnorm, uint32_t nc, int metric,
                       uint32_t n_out, uint32_t* order, const int64_t* res_off,
                       const uint64_t* list_off, const FastTable* ft, cudaStream_t st,
-                      bool scan_sorted = false);
+                      bool scan_sorted = false, const TcSelectScratch* sc = nullptr);
 // ---- schedulers on the GPU (sched.cu) ----
 // dist[i * n + j] (j > i) = serial fp64 L2^2 of queries i and j (the
 // reference's l2_sq_d order: bit-identical to the CPU).
