@@ -717,9 +717,48 @@ struct Ctx {
     const bool staged = src != h_Q;
     last_fused = use_fused(lp, k, G);
     if (last_fused) {
-      // one kernel: a direct launch costs less host time than a graph launch
       ++fused_seq; // this call executes one fused launch
-      enqueue_coarse_path(lp, k, G, src, tr);
+      // host row (fixed arguments): a captured graph of event + kernel +
+      // event; a staged row is a per-call argument: direct launch
+      static const bool fgraph =
+          std::getenv("LAIVG_FUSED_GRAPH") ? std::atoi(std::getenv("LAIVG_FUSED_GRAPH")) != 0 : true;
+      if (!fgraph || staged || !use_graphs) {
+        enqueue_coarse_path(lp, k, G, src, tr);
+        return;
+      }
+      const uint64_t key = (1ull << 63) | (uint64_t(lp) << 33) | (uint64_t(uint32_t(k)) << 1);
+      auto it = graph_tab.find(key);
+      if (it != graph_tab.end()) {
+        CK(cudaGraphLaunch(it->second.ge, comp));
+        launch_counter() += it->second.kernels;
+        if (tr) tr->mark("kernel");
+        return;
+      }
+      enqueue_coarse_path(lp, k, G, src, tr); // runs this call, sets attributes
+      GraphEntry e;
+      const uint64_t launched = launch_counter().load();
+      bool ok = cudaStreamBeginCapture(comp, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+      if (ok) {
+        capturing = true;
+        try {
+          enqueue_coarse_path(lp, k, G, src);
+        } catch (...) {
+          ok = false;
+        }
+        capturing = false;
+        ok = (cudaStreamEndCapture(comp, &e.g) == cudaSuccess) && ok && e.g != nullptr;
+      }
+      e.kernels = launch_counter().load() - launched;
+      launch_counter() = launched; // captured launches did not run
+      ok = ok && cudaGraphInstantiate(&e.ge, e.g, 0) == cudaSuccess;
+      ok = ok && cudaGraphUpload(e.ge, comp) == cudaSuccess;
+      cudaGetLastError();
+      if (ok) {
+        graph_tab[key] = e;
+      } else {
+        if (e.g) cudaGraphDestroy(e.g);
+        use_graphs = false; // capture unsupported here: stay eager
+      }
       return;
     }
     if (staged) *h_qslot = src; // read by the chain's first kernel
