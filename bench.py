@@ -314,6 +314,18 @@ def reference_index(cen, vecs, ids, off, metric):
     return ri
 
 
+def host_cpu_model():
+    """lscpu-style model string of the host cores (state them)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(ri, q_out, L, k, threads, sample):
     """The reference laiv::ivf_search on `threads` host threads over `sample`
     queries; returns q/s, p50 latency and the results."""
@@ -359,7 +371,8 @@ def run_reference(args, cfg):
         "p50_latency_ms": float(np.median(lats) * 1e3),
         "config": config_block(cfg, args, sigma),
         "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads,
-                         "kind": "reference",
+                         "kind": "reference", "cpu_model": host_cpu_model(),
+                         "single_thread_latency_ms": float(np.median(lats) * 1e3),
                          "sample": f"{per_step} queries per step (one per host thread), "
                                    f"laiv::ivf_search from oracle/_ref/libref.so"},
         "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0,
@@ -548,6 +561,7 @@ def run_ours(args, cfg):
         "roofline": {"kernel": kname, "bound": "hbm", "achieved": achieved,
                      "peak": peak, "peak_kind": f"{peak_kind} copy (MEASURED_PEAKS.json hbm_gbs)",
                      "unit": "GB/s", "frac": achieved / peak,
+                     "frac_vs_8tbps": achieved / 8000.0,
                      "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": bytes_kernel / max(len(rec), 1),
                      "avg_launch_ms": t_dom / max(len(rec), 1) * 1e3,
@@ -602,7 +616,8 @@ def run_ours(args, cfg):
             eq += bool(np.array_equal(got_ids, cb["ids"][j]) and
                        np.array_equal(got_sc, cb["scores"][j]))
         line["cpu_baseline"] = {"value": cb["qps"], "unit": "queries/s", "cores": threads,
-                                "kind": "reference",
+                                "kind": "reference", "cpu_model": host_cpu_model(),
+                                "single_thread_latency_ms": cb["p50_ms"],
                                 "p50_latency_ms": cb["p50_ms"], "wall_s": cb["wall_s"],
                                 "cpu_seconds": cb["wall_s"] * threads,
                                 "sample": f"{sample} q_out queries of the bench generator (the "
