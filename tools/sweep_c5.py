@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--nprobe", default="32,64,128,256,512,1024")
     ap.add_argument("--cache", default="0.05,0.10,0.25,0.50")
     ap.add_argument("--peers", action="store_true")
+    ap.add_argument("--acc", default="fp64", choices=["fp64", "fp32"])
     a = ap.parse_args()
     sys.path.insert(0, ROOT)
     import bench
@@ -35,8 +36,9 @@ def main():
             bench.CONFIGS["_sweep"] = cfg
             args = argparse.Namespace(gpus=1, steps=a.steps, warmup=a.warmup, impl="ours",
                                       config="_sweep", metric="ip", window=a.window, sigma=None,
-                                      cpu_sample=0, no_cpu_baseline=True, acc="fp64", scan="tma",
-                                      workers=a.workers, peers=a.peers)
+                                      cpu_sample=0, no_cpu_baseline=True, acc=a.acc, scan="tma",
+                                      workers=a.workers, peers=a.peers, single="fused",
+                                      window_load=0.0, window_buffer_gb=16.0, budget_scale=1.0)
             import io
             from contextlib import redirect_stdout
 
@@ -53,6 +55,8 @@ def main():
                               "peer_lists_mean": r.get("peer_lists_mean", 0.0), "peers": a.peers,
                               "host_scan_ms_mean": r["host_scan_ms_max_mean"],
                               "schedule_ms_mean": r["schedule_ms_mean"],
+                              "acc": a.acc,
+                              "gpu_scan_ms_per_step": line.get("roofline", {}).get("avg_launch_ms"),
                               "results_identical": line["value_e2e_results_identical"]}),
                   flush=True)
 
