@@ -1987,7 +1987,7 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
     const unsigned old = atomicAdd(bar, add);
     const uint64_t t0 = globaltimer();
     while (((old ^ ld_acquire_gpu(bar)) & 0x80000000u) == 0u) {
-      if (globaltimer() - t0 > 4000000000ull) __trap();
+      if (globaltimer() - t0 > 20000000000ull) __trap(); // 20 s: far beyond any time slice
     }
     __threadfence();
   }
