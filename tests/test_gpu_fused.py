@@ -214,3 +214,28 @@ def test_plain_call_without_timing(laiv):
         assert np.array_equal(res.topk.scores, e_sc[: cnt.value])
         assert res.fast_clusters == fast[: nf.value].tolist()
         assert tm.t_kernel > 0.0
+
+
+@pytest.mark.parametrize("metric", [IP, L2])
+def test_fused_odd_shapes(orc, laiv, metric):
+    # odd nc (the key loader's tail), d = 764 (the generic consumer path, not
+    # the d = 768 specialisation), k across the register top-k widths, a
+    # probe capped by max_probe
+    rng = np.random.default_rng(17 + metric)
+    nc, d = 77, 764
+    sizes = rng.integers(1, 90, nc)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.uint64)
+    n = int(off[-1])
+    vecs = rng.standard_normal((n, d)).astype(np.float32)
+    ids = rng.permutation(3 * n)[:n].astype(np.uint64)
+    cen = rng.standard_normal((nc, d)).astype(np.float32)
+    ix, fused, chain = pair(laiv, cen, vecs, ids, off, metric, max_probe=40)
+    set_res((fused, chain), (rng.random(nc) < 0.6).astype(np.uint8))
+    for t in range(10):
+        q = rng.standard_normal(d).astype(np.float32)
+        L = int(rng.choice([1, 9, 40]))
+        k = int(rng.choice([1, 31, 33, 64, 65, 128, 129, 256]))
+        a = laiv.hybrid_search(fused, q, L, k)
+        same(a, laiv.hybrid_search(chain, q, L, k))
+        want = orc.ivf_search(cen, vecs, ids, off, metric, q, L, k)
+        assert_topk_parity(metric, a[0].topk.ids, a[0].topk.scores, *want)
