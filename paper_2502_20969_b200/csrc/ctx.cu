@@ -915,7 +915,7 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
   d_cen = dev_alloc<float>(size_t(nc) * d);
   CK(cudaMemcpy(d_cen, ix->centroids.data(), size_t(nc) * d * sizeof(float),
                 cudaMemcpyHostToDevice));
-  d_list_off = dev_alloc<uint64_t>(nc + 1);
+  d_list_off = dev_alloc<uint64_t>(nc + 3); // padded: the fused kernel bulk-copies 16 B multiples
   CK(cudaMemcpy(d_list_off, ix->list_off.data(), (nc + 1) * sizeof(uint64_t),
                 cudaMemcpyHostToDevice));
   d_ids = dev_alloc<uint64_t>(ix->total());
@@ -925,7 +925,7 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
 
   capacity = o.capacity_bytes;
   h_res.assign(nc, -1);
-  d_res = dev_alloc<int64_t>(nc);
+  d_res = dev_alloc<int64_t>(nc + 2); // padded (see d_list_off)
   res_stage[0] = pin_alloc<int64_t>(nc);
   res_stage[1] = pin_alloc<int64_t>(nc);
   slab_vecs = capacity / ix->member_bytes();

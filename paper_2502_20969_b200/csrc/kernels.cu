@@ -2011,6 +2011,7 @@ struct FusedArgs {
   unsigned* ctl;                // [0] grid barrier word, [1] call sequence, [2] done ticket
   unsigned long long* stamps;   // [32] phase stamps of CTA 0 (mapped), nullable
   unsigned long long* cta_stamps; // [G][4] entry, query ready, keys ready, done; nullable
+  int tables;                   // residency + list offsets bulk-copied into shared memory
   int qdirect;                  // every CTA reads a host row itself (diagnostics)
   const float* slab;
   const uint64_t* ids;
@@ -2028,6 +2029,17 @@ __host__ __device__ inline size_t fused_tables_bytes(uint32_t L, uint32_t G) {
 // Selection scratch, aliased onto the ring before the scan starts.
 __host__ __device__ inline size_t fused_select_bytes(uint32_t nc, uint32_t L) {
   return 2 * (static_cast<size_t>(nc) * 12 + 16) + static_cast<size_t>(L) * (8 + 4 + 4) + 64;
+}
+// Bytes of the residency table and list offsets as bulk-copied (16-byte
+// multiples; the device arrays are padded for it).
+__host__ __device__ inline size_t fused_res_bytes(uint32_t nc) {
+  return (static_cast<size_t>(nc) * 8 + 15) & ~size_t(15);
+}
+__host__ __device__ inline size_t fused_off_bytes(uint32_t nc) {
+  return (static_cast<size_t>(nc + 1) * 8 + 15) & ~size_t(15);
+}
+__host__ __device__ inline size_t fused_tables_at(uint32_t nc, uint32_t L) {
+  return (fused_select_bytes(nc, L) + 127) & ~size_t(127);
 }
 
 template <int R, int NCHC>
@@ -2464,6 +2476,25 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_query_kernel(FusedArgs
     }
     __syncthreads();
   }
+  // the residency table and list offsets stream into shared memory while the
+  // coarse phase and the selection run (the split needs them after)
+  __shared__ __align__(8) uint64_t tbar;
+  const int64_t* res_tab = a.res_off;
+  const uint64_t* off_tab = a.list_off;
+  if (a.tables) {
+    unsigned char* tb0 = smem + fused_tables_at(a.nc, L);
+    if (threadIdx.x == 0) {
+      mbar_init(&tbar, 1);
+      fence_mbar_init();
+      const uint32_t rb = static_cast<uint32_t>(fused_res_bytes(a.nc));
+      const uint32_t ob = static_cast<uint32_t>(fused_off_bytes(a.nc));
+      mbar_arrive_expect_tx(&tbar, rb + ob);
+      bulk_g2s(tb0, a.res_off, rb, &tbar);
+      bulk_g2s(tb0 + rb, a.list_off, ob, &tbar);
+    }
+    res_tab = reinterpret_cast<const int64_t*>(tb0);
+    off_tab = reinterpret_cast<const uint64_t*>(tb0 + fused_res_bytes(a.nc));
+  }
   if (stamp) st[1] = globaltimer();
   const unsigned long long t_b1 = a.cta_stamps ? globaltimer() : 0ull;
 
@@ -2556,7 +2587,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_query_kernel(FusedArgs
                     a.stamps && blockIdx.x == 0 ? s_dbg : nullptr);
   if (stamp) st[4] = globaltimer();
   // residency split + this query's scan-CTA start table (partition step)
-  partition_block(probe, L, a.res_off, a.list_off, ft, 0);
+  if (a.tables) mbar_wait(&tbar, 0);
+  partition_block(probe, L, res_tab, off_tab, ft, 0);
   __syncthreads();
   if (blockIdx.x == 0 && warp == kFusedWarps - 1) {
     // host I/O warp: the probe and the fast count go out, then the flag
@@ -3048,6 +3080,17 @@ void launch_scan(const float* Q, uint32_t nq, uint32_t d, int metric, int k,
 #undef LAIVG_D
 }
 
+// The two tables fit in the ring region next to the selection scratch.
+bool fused_tables_fit(uint32_t nc, uint32_t d, uint32_t L, int kk, uint32_t G,
+                      const ScanTune& tune) {
+  const TmaGeom g = tma_geom(d, kk, G, tune);
+  size_t region = (size_t(g.S) * g.T * d * 4 + 127) & ~size_t(127);
+  const size_t merge = epilogue_scratch(kConsumers, kk, G);
+  if (region < merge) region = (merge + 127) & ~size_t(127);
+  return fused_tables_at(nc, L) + fused_res_bytes(nc) + fused_off_bytes(nc) <= region &&
+         !std::getenv("LAIVG_NO_TABLES");
+}
+
 size_t fused_query_smem(uint32_t nc, uint32_t d, uint32_t L, int k, bool acc_fp64, uint32_t G,
                         const ScanTune& tune) {
   if (!acc_fp64 && k + kRerankMargin > kMaxK) acc_fp64 = true;
@@ -3110,6 +3153,7 @@ void launch_fused_query(const FusedQuery& q, const ScanOut& out, bool acc_fp64,
   a.ctl = q.ctl;
   a.stamps = q.stamps;
   a.cta_stamps = q.cta_stamps;
+  a.tables = fused_tables_fit(q.nc, q.d, q.L, kk, q.grid, tune) ? 1 : 0;
   a.qdirect = q.qdirect;
   a.slab = q.slab;
   a.ids = q.ids;
