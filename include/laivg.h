@@ -300,6 +300,15 @@ int laivg_link_peak(laivg_ctx* ctx, uint64_t bytes, double* h2d_gbps, double* d2
  * callers that pass no timing struct. */
 int laivg_link_bytes(const laivg_ctx* ctx, uint64_t* h2d_bytes, uint64_t* d2h_bytes);
 
+/* Batched hit scan: how many batches ran the list-major tensor-core scan
+ * (each resident list read once per 16 queries probing it; policy env
+ * LAIVG_LIST_SCAN = 0 off / 1 on / unset auto), how many of those fell back
+ * to the per-query scan (candidate buffer overflow), and the current EMA of
+ * queries per resident probed list the auto policy reads. Extension of
+ * search_clusters (ivf.cpp:301-343) for batches; results are identical. */
+int laivg_list_scan_stats(const laivg_ctx* ctx, uint64_t* runs, uint64_t* fallbacks,
+                          double* queries_per_list);
+
 /* ---- hybrid search (tiered.cpp:148-198) ---------------------------------- */
 typedef struct {
   double bandwidth_bytes_per_s; /* budget.hpp:14 */

@@ -111,6 +111,7 @@ SIGNATURES = {
     "laivg_window_load": (i32, [vp, u64, f64]),
     "laivg_link_peak": (i32, [vp, u64, P(f64), P(f64)]),
     "laivg_link_bytes": (i32, [vp, P(u64), P(u64)]),
+    "laivg_list_scan_stats": (i32, [vp, P(u64), P(u64), P(f64)]),
     "laivg_hybrid_search": (i32, [vp, vp, i32, i32, P(CostModelC), vp, vp, P(u32), vp,
                                   P(u32), vp, P(u32), P(f64), P(HybridTimingC)]),
     "laivg_coverage": (i32, [vp, vp, vp, i32, P(f64)]),

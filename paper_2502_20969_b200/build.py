@@ -30,9 +30,9 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
 CXX_FLAGS = ["-O3", "-std=c++20", "-fPIC", "-march=x86-64-v3", "-ffp-contract=off",
              "-Wall", f"-I{ROOT}/include", "-pthread"]
 
-CU = ["kernels.cu", "coarse_tc.cu", "sched.cu", "wide.cu", "ctx.cu"]
+CU = ["kernels.cu", "coarse_tc.cu", "listscan.cu", "sched.cu", "wide.cu", "ctx.cu"]
 CPP = ["host.cpp", "laix.cpp", "synth.cpp"]
-HEADERS = ["kernels.cuh", "host.hpp", "dev_common.cuh", "synth.hpp"]
+HEADERS = ["kernels.cuh", "host.hpp", "dev_common.cuh", "umma.cuh", "synth.hpp"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:

@@ -33,6 +33,7 @@
 #include "dev_common.cuh"
 #include "host.hpp"
 #include "kernels.cuh"
+#include "umma.cuh"
 
 namespace laivg {
 using namespace dev;
@@ -42,52 +43,6 @@ constexpr uint32_t kTcM = 128;     // centroids per CTA (UMMA M)
 constexpr uint32_t kTcKB = 32;     // fp32 elements per k-block = one 128-byte swizzle row
 constexpr uint32_t kTcStages = 4;  // TMA ring depth
 constexpr uint32_t kTcThreads = 128;
-
-// UMMA shared-memory descriptor of a K-major operand tile in the canonical
-// 128-byte-swizzle layout TMA writes (8-row x 128-byte atoms, 1024 B apart).
-__device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t saddr) {
-  uint64_t desc = 0;
-  desc |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);      // start address
-  desc |= static_cast<uint64_t>(1u) << 16;                      // LBO (unused: swizzled K-major)
-  desc |= static_cast<uint64_t>(1024u >> 4) << 32;              // SBO: next 8-row atom
-  desc |= static_cast<uint64_t>(1u) << 46;                      // descriptor version (sm_100)
-  desc |= static_cast<uint64_t>(2u) << 61;                      // SWIZZLE_128B
-  return desc;
-}
-
-// Instruction descriptor: kind::tf32, fp32 accumulator, both operands K-major.
-__host__ __device__ constexpr uint32_t tf32_idesc(uint32_t M, uint32_t N) {
-  return (1u << 4)           // D format: F32
-         | (2u << 7)         // A format: TF32
-         | (2u << 10)        // B format: TF32
-         | ((N >> 3) << 17)  // N / 8
-         | ((M >> 4) << 24); // M / 16
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t x,
-                                            int32_t y, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                          uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(bar))
-      : "memory");
-}
 
 template <uint32_t N>
 __global__ void __launch_bounds__(kTcThreads, 1)
@@ -222,7 +177,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // Row-major fp32 matrix [rows][d] as a 2D tensor map with a (32 x box_rows)
 // box and 128-byte swizzle; out-of-range rows/columns read as zero.
-CUtensorMap make_map(const float* base, uint32_t rows, uint32_t d, uint32_t box_rows) {
+CUtensorMap make_map(const float* base, uint64_t rows, uint32_t d, uint32_t box_rows) {
   auto fn = encode_fn();
   if (!fn) throw CudaError("cuTensorMapEncodeTiled unavailable from the driver");
   CUtensorMap m;
@@ -255,6 +210,10 @@ void launch_tc_n(const float* Q, uint32_t nq, const float* cen, uint32_t nc, uin
 }
 
 } // namespace
+
+CUtensorMap make_row_tile_map(const float* base, uint64_t rows, uint32_t d, uint32_t box_rows) {
+  return make_map(base, rows, d, box_rows);
+}
 
 bool coarse_tc_supported(uint32_t nc, uint32_t d) {
   return (d % 4) == 0 && d >= 4 && nc <= kTcMaxNc && encode_fn() != nullptr;

@@ -194,6 +194,16 @@ struct Ctx {
   float* d_approx = nullptr; // [max_batch][nc] tf32 scores
   float* d_cnorm = nullptr;  // [nc] ||c|| rounded up
   TcSelectScratch tcs{};     // three-kernel exact selection scratch
+  // list-major tensor-core batched scan (listscan.cu), allocated on first use
+  ListScanScratch lss{};
+  unsigned* h_ls_flag = nullptr;
+  unsigned* dm_ls_flag = nullptr;
+  bool ls_result = false;    // the last batch's scan results came from the list scan
+  double ls_qpl = 0;         // EMA of queries per resident probed list (batches)
+  uint64_t ls_runs = 0, ls_fallbacks = 0;
+  bool want_list_scan(uint32_t nq, int k) const;
+  void ensure_list_scan();
+  void run_list_scan(const float* dQ, uint32_t nq, uint32_t lp, int k, cudaStream_t st);
   float* d_Q = nullptr;
   double* d_scores = nullptr;
   uint32_t* d_order = nullptr;
@@ -817,13 +827,15 @@ Ctx::~Ctx() {
                   (void*)so.gpart_s, (void*)so.gpart_id, (void*)so.gpart_vi,
                   (void*)d_staged, (void*)d_approx, (void*)d_cnorm, (void*)d_keys,
                   (void*)tcs.cand, (void*)tcs.key, (void*)tcs.ncand,
+                  (void*)lss.qcount, (void*)lss.lists, (void*)lss.lq_off, (void*)lss.item_off,
+                  (void*)lss.qidx, (void*)lss.meta, (void*)lss.gtau, (void*)lss.gcnt, lss.cand,
                   (void*)d_ctl, (void*)d_wbuf, (void*)d_wsink, (void*)d_wread}) {
     if (p) cudaFree(p);
   }
   for (void* p : {(void*)res_stage[0], (void*)res_stage[1], (void*)h_Q, (void*)h_qslot,
                   (void*)h_order, (void*)h_out_s, (void*)h_out_id,
                   (void*)h_out_cnt, (void*)h_fcount, (void*)h_flag, (void*)h_stamps,
-                  (void*)h_cta_stamps}) {
+                  (void*)h_cta_stamps, (void*)h_ls_flag}) {
     if (p) cudaFreeHost(p);
   }
   for (void* p : {(void*)fft.slab, (void*)fft.row, (void*)fft.len, (void*)fft.cluster,
@@ -1102,7 +1114,7 @@ std::vector<Scored> Ctx::scan_result(uint32_t q, uint32_t G, int k, uint64_t V) 
     return g;
   }
   const int kk = scan_kk(k, acc_fp64);
-  if (!host_final) {
+  if (!host_final || ls_result) {
     std::vector<Scored> g(h_out_cnt[q]);
     for (uint32_t i = 0; i < h_out_cnt[q]; ++i) {
       g[i] = {h_out_s[size_t(q) * k + i], h_out_id[size_t(q) * k + i]};
@@ -1610,6 +1622,63 @@ void Ctx::finish_fetch(size_t nchunks, FetchStats& st) {
   }
 }
 
+// List-major scan policy (LAIVG_LIST_SCAN): "0" off, "1" whenever the shape
+// allows, default auto: when the previous batches' queries per resident
+// probed list (EMA) reach LAIVG_LIST_SCAN_QPL (default 4).
+bool Ctx::want_list_scan(uint32_t nq, int k) const {
+  const char* em = std::getenv("LAIVG_LIST_SCAN"); // read per call (tests switch it)
+  const int mode = em ? std::atoi(em) : 2;
+  const char* eq = std::getenv("LAIVG_LIST_SCAN_QPL");
+  const double qpl_min = eq ? std::atof(eq) : 4.0;
+  if (mode == 0 || nq < 2 || !list_scan_supported(ix->d, k) || slab_vecs == 0) return false;
+  return mode == 1 || ls_qpl >= qpl_min;
+}
+
+void Ctx::ensure_list_scan() {
+  if (lss.cand) return;
+  const uint32_t nc = ix->nc;
+  lss.gcap = 16384;
+  lss.qcount = dev_alloc<uint32_t>(std::max(nc, 1u));
+  lss.lists = dev_alloc<uint32_t>(std::max(nc, 1u));
+  lss.lq_off = dev_alloc<uint32_t>(nc + 1);
+  lss.item_off = dev_alloc<uint32_t>(nc + 1);
+  lss.qidx = dev_alloc<uint32_t>(std::max<size_t>(1, size_t(max_batch) * max_probe));
+  lss.meta = dev_alloc<uint32_t>(4);
+  lss.gtau = dev_alloc<uint32_t>(max_batch);
+  lss.gcnt = dev_alloc<uint32_t>(max_batch);
+  lss.cand = dev_alloc<uint4>(size_t(max_batch) * lss.gcap);
+  h_ls_flag = pin_alloc_mapped<unsigned>(1, &dm_ls_flag);
+}
+
+void Ctx::run_list_scan(const float* dQ, uint32_t nq, uint32_t lp, int k, cudaStream_t st) {
+  ensure_list_scan();
+  *reinterpret_cast<volatile unsigned*>(h_ls_flag) = 0u;
+  ListScan p;
+  p.Q = dQ;
+  p.nq = nq;
+  p.d = ix->d;
+  p.nc = ix->nc;
+  p.lp = lp;
+  p.metric = ix->metric;
+  p.k = k;
+  p.order = d_order;
+  p.res = d_res;
+  p.list_off = d_list_off;
+  p.slab = d_slab;
+  p.slab_rows = slab_vecs;
+  p.ids = d_ids;
+  p.out_s = dm_out_s;
+  p.out_id = dm_out_id;
+  p.out_count = dm_out_cnt;
+  p.fcount_in = ft.count;
+  p.fcount_out = dm_fcount;
+  p.flag_host = dm_ls_flag;
+  p.grid = sms;
+  p.scratch = lss;
+  launch_list_scan(p, st);
+  ++ls_runs;
+}
+
 Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq, int L,
                                    int k) {
   if (k < 1) throw std::invalid_argument("k must be >= 1");
@@ -1644,9 +1713,14 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
                      cudaMemcpyDeviceToHost, aux));
   rec(ev_probe, aux);
   rec(ev_p, comp);
+  bool use_ls = !wide && want_list_scan(nq, k);
   if (!wide) {
-    launch_scan(dQ, nq, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl, tune,
-                comp);
+    if (use_ls) {
+      run_list_scan(dQ, nq, lp, k, comp);
+    } else {
+      launch_scan(dQ, nq, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl,
+                  tune, comp);
+    }
     rec(ev_s, comp);
     rec(ev_c, comp); // results are in mapped host memory
   }
@@ -1670,6 +1744,26 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
       }
     }
     r.nslow[q] = uint32_t(slow[q].size());
+  }
+  {
+    // sharing of the resident lists across the batch (list-scan policy)
+    std::vector<unsigned char> seen(ix->nc, 0);
+    uint64_t pairs = 0, lists = 0;
+    for (uint32_t q = 0; q < nq; ++q) {
+      for (uint32_t i = 0; i < lp; ++i) {
+        const uint32_t c = h_order[size_t(q) * lp + i];
+        if (h_res[c] < 0) continue;
+        ++pairs;
+        if (!seen[c]) {
+          seen[c] = 1;
+          ++lists;
+        }
+      }
+    }
+    if (lists) {
+      const double qpl = double(pairs) / double(lists);
+      ls_qpl = ls_qpl > 0 ? 0.5 * ls_qpl + 0.5 * qpl : qpl;
+    }
   }
   if (wide) { // the candidate sort is sized by the probe split
     scan_wide(dQ, nq, ft, d_slab, vfast, k, dm_fcount, comp);
@@ -1709,6 +1803,17 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
     }
   }
   CK(cudaEventSynchronize(ev_c));
+  if (use_ls && *reinterpret_cast<volatile unsigned*>(h_ls_flag)) {
+    // a candidate buffer overflowed (e.g. many equal scores): per-query scan
+    ++ls_fallbacks;
+    use_ls = false;
+    launch_scan(dQ, nq, ix->d, ix->metric, k, ft, d_slab, d_ids, so, G, acc_fp64, scan_impl, tune,
+                comp);
+    rec(ev_s, comp);
+    rec(ev_c, comp);
+    CK(cudaEventSynchronize(ev_c));
+  }
+  ls_result = use_ls;
   if (nchunks) CK(cudaEventSynchronize(ev_fdone));
   for (uint32_t q = 0; q < nq; ++q) {
     if (h_fcount[q] != r.nfast[q]) {
@@ -1727,7 +1832,10 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
   r.t_fetch = fst.t_fetch;
   r.h2d_bytes += fst.fetch_bytes;
   r.d2h_bytes += uint64_t(nq) * lp * sizeof(uint32_t) + uint64_t(nq) * sizeof(uint32_t) +
-                 result_bytes(nq, uint32_t(G), k) + fetch_result_bytes(nchunks, nq, k);
+                 (use_ls ? uint64_t(nq) * (k * (sizeof(float) + sizeof(uint64_t)) + 4)
+                         : result_bytes(nq, uint32_t(G), k)) +
+                 fetch_result_bytes(nchunks, nq, k);
+  ls_result = false;
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, ev_a, nchunks ? ev_fdone : ev_s));
   r.t_g = ms * 1e-3;
@@ -2799,6 +2907,16 @@ int laivg_link_bytes(const laivg_ctx* ctx, uint64_t* h2d_bytes, uint64_t* d2h_by
     need(ctx, "ctx");
     if (h2d_bytes) *h2d_bytes = ctx->c.link_h2d_total;
     if (d2h_bytes) *d2h_bytes = ctx->c.link_d2h_total;
+  });
+}
+
+int laivg_list_scan_stats(const laivg_ctx* ctx, uint64_t* runs, uint64_t* fallbacks,
+                          double* queries_per_list) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (runs) *runs = ctx->c.ls_runs;
+    if (fallbacks) *fallbacks = ctx->c.ls_fallbacks;
+    if (queries_per_list) *queries_per_list = ctx->c.ls_qpl;
   });
 }
 

@@ -180,6 +180,47 @@ void launch_tc_select(const float* approx, uint32_t splits, const float* Q, uint
                       uint32_t n_out, uint32_t* order, const int64_t* res_off,
                       const uint64_t* list_off, const FastTable* ft, cudaStream_t st,
                       bool scan_sorted = false, const TcSelectScratch* sc = nullptr);
+// ---- list-major batched scan on tensor cores (listscan.cu) ----
+// Device scratch: per-cluster query counts / cursors [nc], resident lists
+// with their query offsets and work-item offsets [nc + 1], query slots
+// [nq * L], per-query candidates [nq][gcap] (16 B each), counts and shared
+// thresholds [nq], meta[4].
+struct ListScanScratch {
+  uint32_t* qcount = nullptr;
+  uint32_t* lists = nullptr;
+  uint32_t* lq_off = nullptr;
+  uint32_t* item_off = nullptr;
+  uint32_t* qidx = nullptr;
+  uint32_t* meta = nullptr;
+  uint32_t* gtau = nullptr;
+  uint32_t* gcnt = nullptr;
+  void* cand = nullptr;
+  uint32_t gcap = 0;
+};
+struct ListScan {
+  const float* Q = nullptr;          // [nq][d] on the device
+  uint32_t nq = 0, d = 0, nc = 0, lp = 0;
+  int metric = 0, k = 0;
+  const uint32_t* order = nullptr;   // [nq][lp] probe
+  const int64_t* res = nullptr;      // residency (slab row of each list or -1)
+  const uint64_t* list_off = nullptr;
+  const float* slab = nullptr;
+  uint64_t slab_rows = 0;
+  const uint64_t* ids = nullptr;
+  float* out_s = nullptr;            // [nq][k]
+  uint64_t* out_id = nullptr;
+  uint32_t* out_count = nullptr;
+  const uint32_t* fcount_in = nullptr;
+  uint32_t* fcount_out = nullptr;
+  unsigned* flag_host = nullptr;     // set to 1 if a candidate buffer overflowed
+  int grid = 0;
+  ListScanScratch scratch;
+};
+bool list_scan_supported(uint32_t d, int k);
+size_t list_scan_smem(uint32_t d);
+// Exact per-query top-k of the resident probed lists (the per-query scan's
+// result) into out_*; on overflow *flag_host = 1 and the outputs are invalid.
+void launch_list_scan(const ListScan& p, cudaStream_t st);
 // ---- schedulers on the GPU (sched.cu) ----
 // dist[i * n + j] (j > i) = serial fp64 L2^2 of queries i and j (the
 // reference's l2_sq_d order: bit-identical to the CPU).

@@ -364,6 +364,13 @@ class Device:
         check(lib().laivg_link_peak(self.h, int(nbytes), C.byref(a), C.byref(b)))
         return a.value, b.value
 
+    def list_scan_stats(self) -> tuple[int, int, float]:
+        """(batches on the list-major tensor-core scan, of which fell back to
+        the per-query scan, EMA of queries per resident probed list)."""
+        r, f, q = C.c_uint64(), C.c_uint64(), C.c_double()
+        check(lib().laivg_list_scan_stats(self.h, C.byref(r), C.byref(f), C.byref(q)))
+        return r.value, f.value, q.value
+
     def stage_queries(self, Q) -> None:
         Q = _c(Q, np.float32).reshape(-1, self.ix.d)
         self._staged = Q
