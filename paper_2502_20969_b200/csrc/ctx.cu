@@ -1624,12 +1624,13 @@ void Ctx::finish_fetch(size_t nchunks, FetchStats& st) {
 
 // List-major scan policy (LAIVG_LIST_SCAN): "0" off, "1" whenever the shape
 // allows, default auto: when the previous batches' queries per resident
-// probed list (EMA) reach LAIVG_LIST_SCAN_QPL (default 4).
+// probed list (EMA) reach LAIVG_LIST_SCAN_QPL (default 1.5; measured
+// crossover ~1.3, profiles/r02/list_scan_sharing.jsonl).
 bool Ctx::want_list_scan(uint32_t nq, int k) const {
   const char* em = std::getenv("LAIVG_LIST_SCAN"); // read per call (tests switch it)
   const int mode = em ? std::atoi(em) : 2;
   const char* eq = std::getenv("LAIVG_LIST_SCAN_QPL");
-  const double qpl_min = eq ? std::atof(eq) : 4.0;
+  const double qpl_min = eq ? std::atof(eq) : 1.5;
   if (mode == 0 || nq < 2 || !list_scan_supported(ix->d, k) || slab_vecs == 0) return false;
   return mode == 1 || ls_qpl >= qpl_min;
 }

@@ -10,7 +10,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2502_20969_b200", "liblaivg.so")
-KEEP = [r"scan_tma_kernelILb1ELi1ELi6E", r"coarse_tc_kernelILj256E", r"fused_query_kernel"]
+KEEP = [r"scan_tma_kernelILb1ELi1ELi6E", r"coarse_tc_kernelILj256E", r"fused_query_kernel",
+        r"list_scan_tc_kernel"]
 PROOF = ["UTCHMMA", "UTCQMMA", "UTMALDG", "UBLKCP", "LDTM", "SYNCS", "DFMA", "FFMA"]
 
 

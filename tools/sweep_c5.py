@@ -26,13 +26,30 @@ def main():
     ap.add_argument("--cache", default="0.05,0.10,0.25,0.50")
     ap.add_argument("--peers", action="store_true")
     ap.add_argument("--acc", default="fp64", choices=["fp64", "fp32"])
+    ap.add_argument("--micro", default="",
+                    help="comma list of micro-batch sizes (default: the config's)")
+    ap.add_argument("--list-scan", default="",
+                    help="comma list of LAIVG_LIST_SCAN modes per point (0 off, 1 on, "
+                         "auto = unset); default: the environment's")
     a = ap.parse_args()
     sys.path.insert(0, ROOT)
     import bench
 
-    for cf in [float(x) for x in a.cache.split(",")]:
-        for L in [int(x) for x in a.nprobe.split(",")]:
+    micros = [int(x) for x in a.micro.split(",")] if a.micro else [None]
+    modes = a.list_scan.split(",") if a.list_scan else [None]
+    points = [(m, mode, cf, L) for m in micros for mode in modes
+              for cf in [float(x) for x in a.cache.split(",")]
+              for L in [int(x) for x in a.nprobe.split(",")]]
+    for micro, mode, cf, L in points:
+        if mode is not None:
+            if mode == "auto":
+                os.environ.pop("LAIVG_LIST_SCAN", None)
+            else:
+                os.environ["LAIVG_LIST_SCAN"] = mode
+        if True:
             cfg = dict(bench.CONFIGS[a.config], nprobe=L, cache_frac=cf)
+            if micro:
+                cfg["micro"] = micro
             bench.CONFIGS["_sweep"] = cfg
             args = argparse.Namespace(gpus=1, steps=a.steps, warmup=a.warmup, impl="ours",
                                       config="_sweep", metric="ip", window=a.window, sigma=None,
@@ -55,7 +72,8 @@ def main():
                               "peer_lists_mean": r.get("peer_lists_mean", 0.0), "peers": a.peers,
                               "host_scan_ms_mean": r["host_scan_ms_max_mean"],
                               "schedule_ms_mean": r["schedule_ms_mean"],
-                              "acc": a.acc,
+                              "acc": a.acc, "micro": cfg.get("micro"),
+                              "list_scan": mode or os.environ.get("LAIVG_LIST_SCAN", "auto"),
                               "gpu_scan_ms_per_step": line.get("roofline", {}).get("avg_launch_ms"),
                               "results_identical": line["value_e2e_results_identical"]}),
                   flush=True)
