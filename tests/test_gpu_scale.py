@@ -208,6 +208,19 @@ def test_c2_lookahead_and_batch(laiv, c2, metric):
                      f"host lists {tm.cpu_lists})", metric, got, list(zip(wi2, ws2)))
     assert exact >= 255
     assert tm.fetched_lists > 0
+    # the same batch with the hits on the list-major tensor-core scan
+    os.environ["LAIVG_LIST_SCAN"] = "1"
+    try:
+        res2, _ = laiv.hybrid_search_batch(dev, qo, 256, _C2.k)
+    finally:
+        os.environ.pop("LAIVG_LIST_SCAN", None)
+    assert dev.list_scan_stats()[0] == 1
+    got2 = [(res2.ids[q, : res2.counts[q]], res2.scores[q, : res2.counts[q]]) for q in range(256)]
+    exact2 = _compare(f"C2 {name} batch 256 x nprobe 256, list-major scan", metric, got2,
+                      list(zip(wi2, ws2)))
+    assert exact2 >= 255
+    assert all(np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+               for a, b in zip(got, got2))
     dev.close()
     ix.close()
     ri.close()

@@ -64,7 +64,15 @@ def main():
             for c in range(nc):
                 if rng.random() < frac and sizes[c] > 0:
                     dev.store.insert(c)
+            os.environ["LAIVG_LIST_SCAN"] = "1"  # list-major tensor-core scan
+            res_ls, _ = laiv.hybrid_search_batch(dev, Q, L, k)
+            os.environ["LAIVG_LIST_SCAN"] = "0"  # per-query scan
             res, _ = laiv.hybrid_search_batch(dev, Q, L, k)
+            os.environ.pop("LAIVG_LIST_SCAN", None)
+            for q in range(nq):
+                assert np.array_equal(res_ls.topk(q).ids, res.topk(q).ids), "list != query ids"
+                assert np.array_equal(res_ls.topk(q).scores, res.topk(q).scores), \
+                    "list != query scores"
             dev.stage_queries(Q)
             for q in range(nq):
                 single, _ = laiv.hybrid_search(dev, Q[q], L, k)
