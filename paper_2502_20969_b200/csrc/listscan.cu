@@ -163,14 +163,45 @@ __device__ void ls_compact(uint32_t* lo, uint32_t* hi, uint16_t* rw, uint32_t* c
   __syncwarp();
 }
 
+// Claims the next work item and decodes it into item[] (valid, cluster, r0,
+// r1, query-slot base, queries) and *s0 (slab row of the item's first row).
+__device__ void ls_claim(const LsArgs& a, uint32_t* item, long long* s0) {
+  const uint32_t t = atomicAdd(a.meta + 2, 1u);
+  const uint32_t total = a.meta[1], nl = a.meta[0];
+  if (t >= total || *reinterpret_cast<volatile uint32_t*>(a.meta + 3)) {
+    item[0] = 0;
+    return;
+  }
+  uint32_t lo = 0, hi = nl - 1; // largest u with item_off[u] <= t
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    if (a.item_off[mid] <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  const uint32_t u = lo, c = a.lists[u];
+  const uint32_t qc = a.lq_off[u + 1] - a.lq_off[u];
+  const uint32_t groups = (qc + kLsNQ - 1) / kLsNQ;
+  const uint32_t local = t - a.item_off[u];
+  const uint32_t chunk = local / groups, g = local - chunk * groups;
+  const uint64_t len = a.list_off[c + 1] - a.list_off[c];
+  const uint32_t r0 = chunk * kLsChunk;
+  item[0] = 1;
+  item[1] = c;
+  item[2] = r0;
+  item[3] = static_cast<uint32_t>(len < uint64_t(r0) + kLsChunk ? len : uint64_t(r0) + kLsChunk);
+  item[4] = a.lq_off[u] + g * kLsNQ;
+  item[5] = min(kLsNQ, qc - g * kLsNQ);
+  *s0 = a.res[c] + r0;
+}
+
 __global__ void __launch_bounds__(kLsThreads, 1)
     list_scan_tc_kernel(const __grid_constant__ CUtensorMap slab_map, LsArgs a) {
   extern __shared__ unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kLsStages], empty[kLsStages], acc_full[2], acc_empty[2],
       norm_full[2];
   __shared__ uint32_t tmem_slot;
-  __shared__ uint32_t s_item[8]; // valid, c, r0, r1, qbase, nqg
-  __shared__ long long s_s0;     // slab row of the item's first row
+  __shared__ uint32_t s_item[2][8]; // current / next: valid, c, r0, r1, qbase, nqg
+  __shared__ long long s_s0[2];     // slab row of the item's first row
   __shared__ uint32_t s_q[kLsNQ], s_tau[kLsNQ], s_cnt[kLsNQ];
   __shared__ float s_qn[kLsNQ];
   __shared__ double s_qn2[kLsNQ];
@@ -217,51 +248,29 @@ __global__ void __launch_bounds__(kLsThreads, 1)
   // role-private running counters (the ring and TMEM phases run across items)
   uint32_t it = 0, ab = 0;
 
+  // The producer claims the next item once it has issued the current one's
+  // loads; it starts loading while warps 1-11 stage the item's queries.
+  uint32_t cur = 0;
+  if (threadIdx.x == 0) ls_claim(a, s_item[0], &s_s0[0]);
+  __syncthreads();
   for (;;) {
-    if (threadIdx.x == 0) {
-      const uint32_t t = atomicAdd(a.meta + 2, 1u);
-      const uint32_t total = a.meta[1], nl = a.meta[0];
-      if (t >= total || a.meta[3]) {
-        s_item[0] = 0;
-      } else {
-        uint32_t lo = 0, hi = nl - 1; // largest u with item_off[u] <= t
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi + 1) >> 1;
-          if (a.item_off[mid] <= t) lo = mid;
-          else hi = mid - 1;
-        }
-        const uint32_t u = lo, c = a.lists[u];
-        const uint32_t qc = a.lq_off[u + 1] - a.lq_off[u];
-        const uint32_t groups = (qc + kLsNQ - 1) / kLsNQ;
-        const uint32_t local = t - a.item_off[u];
-        const uint32_t chunk = local / groups, g = local - chunk * groups;
-        const uint64_t len = a.list_off[c + 1] - a.list_off[c];
-        const uint32_t r0 = chunk * kLsChunk;
-        s_item[0] = 1;
-        s_item[1] = c;
-        s_item[2] = r0;
-        s_item[3] = static_cast<uint32_t>(len < uint64_t(r0) + kLsChunk ? len : uint64_t(r0) + kLsChunk);
-        s_item[4] = a.lq_off[u] + g * kLsNQ;
-        s_item[5] = min(kLsNQ, qc - g * kLsNQ);
-        s_s0 = a.res[c] + r0;
-      }
-    }
-    __syncthreads();
-    if (!s_item[0]) break;
-    const uint32_t c = s_item[1], r0 = s_item[2], r1 = s_item[3], nqg = s_item[5];
-    const long long s0 = s_s0;
+    if (!s_item[cur][0]) break;
+    const uint32_t c = s_item[cur][1], r0 = s_item[cur][2], r1 = s_item[cur][3];
+    const uint32_t nqg = s_item[cur][5];
+    const long long s0 = s_s0[cur];
     const uint32_t nrb = (r1 - r0 + kLsM - 1) / kLsM;
 
     // ---- stage the item's queries (B operand, K-major, 128-byte swizzle) ----
-    if (threadIdx.x < kLsNQ) {
-      const uint32_t j = threadIdx.x;
-      s_q[j] = j < nqg ? a.qidx[s_item[4] + j] : 0u;
-      s_cnt[j] = 0;
-    }
-    __syncthreads();
-    {
+    if (warp > 0) {
+      constexpr uint32_t kStg = kLsThreads - 32;
+      const uint32_t st = threadIdx.x - 32;
+      if (st < kLsNQ) {
+        s_q[st] = st < nqg ? a.qidx[s_item[cur][4] + st] : 0u;
+        s_cnt[st] = 0;
+      }
+      named_sync(2, kStg);
       const uint32_t per_q = nkb * 8; // float4 chunks per query row
-      for (uint32_t x = threadIdx.x; x < kLsNQ * per_q; x += kLsThreads) {
+      for (uint32_t x = st; x < kLsNQ * per_q; x += kStg) {
         const uint32_t j = x / per_q, r = x - j * per_q, kb = r >> 3, ch = r & 7;
         const uint32_t f = kb * kLsKB + ch * 4;
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -270,23 +279,23 @@ __global__ void __launch_bounds__(kLsThreads, 1)
         }
         *reinterpret_cast<float4*>(qB + kb * (kLsNQ * 128) + j * 128 + ((ch ^ (j & 7)) << 4)) = v;
       }
-      for (uint32_t j = warp; j < nqg; j += kLsThreads / 32) {
+      for (uint32_t j = warp - 1; j < nqg; j += kStg / 32) {
         const float* q = a.Q + uint64_t(s_q[j]) * d;
-        double s = 0.0;
+        double sq = 0.0;
         for (uint32_t i = lane; i < d; i += 32) {
           const double x = q[i];
-          s = fma(x, x, s);
+          sq = fma(x, x, sq);
         }
-        s = warp_sum(s);
+        sq = warp_sum(sq);
         if (lane == 0) {
-          s_qn2[j] = s;
-          s_qn[j] = __double2float_ru(sqrt(s) * (1.0 + 1e-6));
+          s_qn2[j] = sq;
+          s_qn[j] = __double2float_ru(sqrt(sq) * (1.0 + 1e-6));
           s_tau[j] = a.gtau[s_q[j]];
         }
       }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      named_sync(2, kStg);
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
 
     if (warp == 0) {
       if (lane == 0) { // ---- TMA producer ----
@@ -299,6 +308,7 @@ __global__ void __launch_bounds__(kLsThreads, 1)
                         static_cast<int32_t>(s0 + rb * kLsM), full + s);
           }
         }
+        ls_claim(a, s_item[cur ^ 1u], &s_s0[cur ^ 1u]);
       }
       __syncwarp();
     } else if (warp == 1) {
@@ -440,6 +450,7 @@ __global__ void __launch_bounds__(kLsThreads, 1)
       }
     }
     __syncthreads(); // the item's MMAs are complete (the epilogue saw acc_full)
+    cur ^= 1u;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
