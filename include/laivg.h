@@ -334,7 +334,8 @@ typedef struct {
   uint64_t fetched_bytes;   /* vector bytes fetched on demand */
   double t_fetch;           /* copy-stream time of all fetch copies (s) */
   uint32_t peer_lists;      /* missed lists copied from a peer GPU's cache */
-  uint32_t reserved0;
+  uint32_t list_scan;       /* batched: 1 when the hits ran on the list-major
+                               tensor-core scan (laivg_list_scan_stats) */
   uint64_t peer_bytes;
   /* bytes this call moved across the host link, counted from the copies it
      issued: h2d = query rows (host-buffer entry points) + the residency
@@ -346,6 +347,10 @@ typedef struct {
      is then its coarse + selection phase (CTA 0's globaltimer) and t_scan the
      rest. 0 when the multi-kernel chain ran. */
   double t_kernel;
+  /* batched: vector bytes (4·d·n) of the DISTINCT resident probed lists, what
+     a list-major scan reads at least once (scanned_bytes counts every
+     (query, list) pair) */
+  uint64_t distinct_bytes;
 } laivg_hybrid_timing;
 
 /* hybrid_search for one query. fast_out / slow_out (nullable, L entries)

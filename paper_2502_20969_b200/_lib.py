@@ -54,8 +54,9 @@ class HybridTimingC(C.Structure):
                 ("model_t_c", f64), ("model_t_2", f64), ("t_coarse", f64), ("t_scan", f64),
                 ("scanned_vectors", u64), ("scanned_bytes", u64), ("fetched_lists", u32),
                 ("cpu_lists", u32), ("fetched_bytes", u64), ("t_fetch", f64),
-                ("peer_lists", u32), ("reserved0", u32), ("peer_bytes", u64),
-                ("h2d_bytes", u64), ("d2h_bytes", u64), ("t_kernel", f64)]
+                ("peer_lists", u32), ("list_scan", u32), ("peer_bytes", u64),
+                ("h2d_bytes", u64), ("d2h_bytes", u64), ("t_kernel", f64),
+                ("distinct_bytes", u64)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/laivg.h

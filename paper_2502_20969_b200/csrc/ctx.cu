@@ -201,7 +201,7 @@ struct Ctx {
   bool ls_result = false;    // the last batch's scan results came from the list scan
   double ls_qpl = 0;         // EMA of queries per resident probed list (batches)
   uint64_t ls_runs = 0, ls_fallbacks = 0;
-  bool want_list_scan(uint32_t nq, int k) const;
+  bool want_list_scan(uint32_t nq, uint32_t lp, int k) const;
   void ensure_list_scan();
   void run_list_scan(const float* dQ, uint32_t nq, uint32_t lp, int k, cudaStream_t st);
   float* d_Q = nullptr;
@@ -549,6 +549,8 @@ struct Ctx {
     uint64_t fetch_bytes = 0, cpu_query_bytes = 0, peer_bytes = 0;
     double t_fetch = 0; // copy-stream time of the fetch copies
     uint64_t h2d_bytes = 0, d2h_bytes = 0; // host-link bytes of this call
+    uint32_t list_scan = 0;                // hits ran on the list-major scan
+    uint64_t distinct_bytes = 0;           // 4·d·n over distinct resident probed lists
   };
   BatchResult search_batch(const float* dQ, const float* hQ, uint32_t nq, int L, int k);
   // The GPU side of the miss path, shared by both searches: peer-resident
@@ -1625,14 +1627,17 @@ void Ctx::finish_fetch(size_t nchunks, FetchStats& st) {
 // List-major scan policy (LAIVG_LIST_SCAN): "0" off, "1" whenever the shape
 // allows, default auto: when the previous batches' queries per resident
 // probed list (EMA) reach LAIVG_LIST_SCAN_QPL (default 1.5; measured
-// crossover ~1.3, profiles/r02/list_scan_sharing.jsonl).
-bool Ctx::want_list_scan(uint32_t nq, int k) const {
+// crossover ~1.3, profiles/r02/list_scan_sharing.jsonl). Before any batch
+// the estimate is the uniform-probe prior nq * L / nc (topical batches share
+// more than that).
+bool Ctx::want_list_scan(uint32_t nq, uint32_t lp, int k) const {
   const char* em = std::getenv("LAIVG_LIST_SCAN"); // read per call (tests switch it)
   const int mode = em ? std::atoi(em) : 2;
   const char* eq = std::getenv("LAIVG_LIST_SCAN_QPL");
   const double qpl_min = eq ? std::atof(eq) : 1.5;
   if (mode == 0 || nq < 2 || !list_scan_supported(ix->d, k) || slab_vecs == 0) return false;
-  return mode == 1 || ls_qpl >= qpl_min;
+  const double est = ls_qpl > 0 ? ls_qpl : double(nq) * lp / std::max(1u, ix->nc);
+  return mode == 1 || est >= qpl_min;
 }
 
 void Ctx::ensure_list_scan() {
@@ -1714,7 +1719,7 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
                      cudaMemcpyDeviceToHost, aux));
   rec(ev_probe, aux);
   rec(ev_p, comp);
-  bool use_ls = !wide && want_list_scan(nq, k);
+  bool use_ls = !wide && want_list_scan(nq, lp, k);
   if (!wide) {
     if (use_ls) {
       run_list_scan(dQ, nq, lp, k, comp);
@@ -1758,6 +1763,7 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
         if (!seen[c]) {
           seen[c] = 1;
           ++lists;
+          r.distinct_bytes += ix->list_len(c) * uint64_t(ix->d) * 4;
         }
       }
     }
@@ -1815,6 +1821,7 @@ Ctx::BatchResult Ctx::search_batch(const float* dQ, const float* hQ, uint32_t nq
     CK(cudaEventSynchronize(ev_c));
   }
   ls_result = use_ls;
+  r.list_scan = use_ls ? 1u : 0u;
   if (nchunks) CK(cudaEventSynchronize(ev_fdone));
   for (uint32_t q = 0; q < nq; ++q) {
     if (h_fcount[q] != r.nfast[q]) {
@@ -2138,6 +2145,8 @@ void fill_timing(laivg_hybrid_timing* t, const Ctx::Result& r,
   t->t_fetch = r.t_fetch;
   t->peer_lists = r.peer_lists;
   t->peer_bytes = r.peer_bytes;
+  t->list_scan = 0;
+  t->distinct_bytes = 0;
   t->h2d_bytes = r.h2d_bytes;
   t->d2h_bytes = r.d2h_bytes;
   if (cost) { // tiered.cpp:190-196
@@ -2188,6 +2197,8 @@ void fill_batch_timing(laivg_hybrid_timing* t, const Ctx::BatchResult& r,
   t->peer_bytes = r.peer_bytes;
   t->h2d_bytes = r.h2d_bytes;
   t->d2h_bytes = r.d2h_bytes;
+  t->list_scan = r.list_scan;
+  t->distinct_bytes = r.distinct_bytes;
   if (cost) { // tiered.cpp:190-196 summed over the batch
     double miss = 0, hit = 0;
     for (size_t q = 0; q < r.nfast.size(); ++q) {

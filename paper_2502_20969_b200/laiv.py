@@ -653,6 +653,8 @@ class HybridTiming:                                               # tiered.hpp:8
     h2d_bytes: int = 0         # host-link bytes the call moved (counted by the library)
     d2h_bytes: int = 0
     t_kernel: float = 0.0      # fused single-query kernel duration (0: multi-kernel chain)
+    list_scan: int = 0         # batch hits scanned by the list-major tensor-core scan
+    distinct_bytes: int = 0    # batch: vector bytes of the distinct resident probed lists
 
 
 @dataclass
@@ -668,7 +670,7 @@ def _timing(t: HybridTimingC) -> HybridTiming:
                         t.t_coarse, t.t_scan, int(t.scanned_vectors), int(t.scanned_bytes),
                         int(t.fetched_lists), int(t.cpu_lists), int(t.fetched_bytes), t.t_fetch,
                         int(t.peer_lists), int(t.peer_bytes), int(t.h2d_bytes),
-                        int(t.d2h_bytes), t.t_kernel)
+                        int(t.d2h_bytes), t.t_kernel, int(t.list_scan), int(t.distinct_bytes))
 
 
 def plan_prefetch(dev: Device, q_in, budget_bytes: int) -> PrefetchPlan:  # tiered.hpp:100-101

@@ -149,12 +149,21 @@ def test_list_scan_auto_policy(laiv, monkeypatch):
     set_residency(dev, np.ones(64, np.uint8))
     monkeypatch.delenv("LAIVG_LIST_SCAN", raising=False)
     monkeypatch.setenv("LAIVG_LIST_SCAN_QPL", "4")
-    laiv.hybrid_search_batch(dev, qo, 32, 10)   # 40 queries x 32 of 64 lists
+    laiv.hybrid_search_batch(dev, qo[:6], 32, 10)   # prior 6 x 32 / 64 = 3 < 4
     r, f, qpl = dev.list_scan_stats()
-    assert r == 0 and qpl > 4
+    assert r == 0 and qpl > 1
+    laiv.hybrid_search_batch(dev, qo, 32, 10)       # EMA of 6 and 40 queries
+    r, f, qpl = dev.list_scan_stats()
+    assert qpl > 4
     laiv.hybrid_search_batch(dev, qo, 32, 10)
     r, f, _ = dev.list_scan_stats()
-    assert r == 1 and f == 0
+    assert r >= 1 and f == 0
     monkeypatch.setenv("LAIVG_LIST_SCAN_QPL", "1000")
     laiv.hybrid_search_batch(dev, qo, 32, 10)
-    assert dev.list_scan_stats()[0] == 1
+    assert dev.list_scan_stats()[0] == r
+    # a fresh context decides its first batch on the prior nq * L / nc
+    dev2 = laiv.Device(ix, BIG, miss_fetch="off")
+    set_residency(dev2, np.ones(64, np.uint8))
+    monkeypatch.setenv("LAIVG_LIST_SCAN_QPL", "4")
+    laiv.hybrid_search_batch(dev2, qo, 32, 10)      # prior 40 x 32 / 64 = 20
+    assert dev2.list_scan_stats()[0] == 1
