@@ -288,11 +288,14 @@ def profiled_traffic(kernel_prefix: str, config: str = "c2"):
             vals = []
             for k in doc["kernels"]:
                 if kernel_prefix in k["name"]:
-                    rd = float(k["dram__bytes_read.sum"].split()[0])
-                    wr = float(k["dram__bytes_write.sum"].split()[0])
-                    unit = k["dram__bytes_read.sum"].split()[1]
-                    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
-                    vals.append((rd + wr) * scale)
+                    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+                    def nbytes(v):
+                        x, unit = v.split()[:2]
+                        return float(x.replace(",", "")) * scale[unit]
+
+                    vals.append(nbytes(k["dram__bytes_read.sum"]) +
+                                nbytes(k["dram__bytes_write.sum"]))
             if vals:
                 return float(np.mean(vals)), os.path.relpath(path, ROOT)
         except (OSError, KeyError, ValueError, IndexError):
