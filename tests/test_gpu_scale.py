@@ -202,7 +202,12 @@ def test_c2_lookahead_and_batch(laiv, c2, metric):
     wi2, ws2, _ = ri.search_many(qo, 256, _C2.k, THREADS)
     dev.store.clear()
     laiv.prefetch_batch(dev, qi, np.full(256, cap // 256, np.uint64), chan, 0.0)
-    res, tm = laiv.hybrid_search_batch(dev, qo, 256, _C2.k)
+    os.environ["LAIVG_LIST_SCAN"] = "0"  # hits on the per-query scan
+    try:
+        res, tm = laiv.hybrid_search_batch(dev, qo, 256, _C2.k)
+    finally:
+        os.environ.pop("LAIVG_LIST_SCAN", None)
+    assert dev.list_scan_stats()[0] == 0
     got = [(res.ids[q, : res.counts[q]], res.scores[q, : res.counts[q]]) for q in range(256)]
     exact = _compare(f"C2 {name} batch 256 x nprobe 256 (fetched lists {tm.fetched_lists}, "
                      f"host lists {tm.cpu_lists})", metric, got, list(zip(wi2, ws2)))
