@@ -202,6 +202,9 @@ struct Ctx {
   double ls_qpl = 0;         // EMA of queries per resident probed list (batches)
   uint64_t ls_runs = 0, ls_fallbacks = 0;
   bool want_list_scan(uint32_t nq, uint32_t lp, int k) const;
+  double list_scan_sharing(uint32_t nq, uint32_t lp) const {
+    return ls_qpl > 0 ? ls_qpl : double(nq) * lp / std::max(1u, ix->nc);
+  }
   void ensure_list_scan();
   void run_list_scan(const float* dQ, uint32_t nq, uint32_t lp, int k, cudaStream_t st);
   float* d_Q = nullptr;
@@ -1636,8 +1639,7 @@ bool Ctx::want_list_scan(uint32_t nq, uint32_t lp, int k) const {
   const char* eq = std::getenv("LAIVG_LIST_SCAN_QPL");
   const double qpl_min = eq ? std::atof(eq) : 1.5;
   if (mode == 0 || nq < 2 || !list_scan_supported(ix->d, k) || slab_vecs == 0) return false;
-  const double est = ls_qpl > 0 ? ls_qpl : double(nq) * lp / std::max(1u, ix->nc);
-  return mode == 1 || est >= qpl_min;
+  return mode == 1 || list_scan_sharing(nq, lp) >= qpl_min;
 }
 
 void Ctx::ensure_list_scan() {
@@ -1681,6 +1683,13 @@ void Ctx::run_list_scan(const float* dQ, uint32_t nq, uint32_t lp, int k, cudaSt
   p.flag_host = dm_ls_flag;
   p.grid = sms;
   p.scratch = lss;
+  // 32-query items once lists are shared by >= 12 queries (each 16-query
+  // group streams its chunk again); LAIVG_LIST_SCAN_N forces 16 / 32
+  const char* en = std::getenv("LAIVG_LIST_SCAN_N");
+  const uint32_t forced = en ? uint32_t(std::atoi(en)) : 0u;
+  p.group = forced == 16 || forced == 32 ? forced
+            : (list_scan_sharing(nq, lp) >= 12.0 ? 32u : 16u);
+  if (!list_scan_supported(ix->d, k, p.group)) p.group = 16;
   launch_list_scan(p, st);
   ++ls_runs;
 }

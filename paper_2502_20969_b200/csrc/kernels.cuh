@@ -214,10 +214,11 @@ struct ListScan {
   uint32_t* fcount_out = nullptr;
   unsigned* flag_host = nullptr;     // set to 1 if a candidate buffer overflowed
   int grid = 0;
+  uint32_t group = 16;               // queries per work item: 16, or 32 for heavily shared lists
   ListScanScratch scratch;
 };
-bool list_scan_supported(uint32_t d, int k);
-size_t list_scan_smem(uint32_t d);
+bool list_scan_supported(uint32_t d, int k, uint32_t group = 16);
+size_t list_scan_smem(uint32_t d, uint32_t group = 16);
 // Exact per-query top-k of the resident probed lists (the per-query scan's
 // result) into out_*; on overflow *flag_host = 1 and the outputs are invalid.
 void launch_list_scan(const ListScan& p, cudaStream_t st);

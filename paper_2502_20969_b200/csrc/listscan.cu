@@ -54,10 +54,10 @@ CUtensorMap make_row_tile_map(const float* base, uint64_t rows, uint32_t d, uint
 using namespace dev;
 namespace {
 
-constexpr uint32_t kLsNQ = 16;       // queries per item (UMMA N)
+constexpr uint32_t kLsNQMax = 32;    // queries per item (UMMA N): 16, or 32 for shared lists
 constexpr uint32_t kLsM = 128;       // list rows per row-block (UMMA M)
 constexpr uint32_t kLsKB = 32;       // floats per k-block (one 128-byte swizzle row)
-constexpr uint32_t kLsStages = 6;    // ring depth (16 KB stages)
+__host__ __device__ constexpr uint32_t ls_stages(uint32_t nq) { return nq <= 16 ? 6u : 4u; } // ring (16 KB)
 constexpr uint32_t kLsStage = kLsM * kLsKB * 4;
 constexpr uint32_t kLsChunk = 1024;  // list rows per item
 constexpr uint32_t kLsSlots = 16;    // candidate slots per lane of a compacting warp
@@ -165,7 +165,7 @@ __device__ void ls_compact(uint32_t* lo, uint32_t* hi, uint16_t* rw, uint32_t* c
 
 // Claims the next work item and decodes it into item[] (valid, cluster, r0,
 // r1, query-slot base, queries) and *s0 (slab row of the item's first row).
-__device__ void ls_claim(const LsArgs& a, uint32_t* item, long long* s0) {
+__device__ void ls_claim(const LsArgs& a, uint32_t kNQ, uint32_t* item, long long* s0) {
   const uint32_t t = atomicAdd(a.meta + 2, 1u);
   const uint32_t total = a.meta[1], nl = a.meta[0];
   if (t >= total || *reinterpret_cast<volatile uint32_t*>(a.meta + 3)) {
@@ -180,7 +180,7 @@ __device__ void ls_claim(const LsArgs& a, uint32_t* item, long long* s0) {
   }
   const uint32_t u = lo, c = a.lists[u];
   const uint32_t qc = a.lq_off[u + 1] - a.lq_off[u];
-  const uint32_t groups = (qc + kLsNQ - 1) / kLsNQ;
+  const uint32_t groups = (qc + kNQ - 1) / kNQ;
   const uint32_t local = t - a.item_off[u];
   const uint32_t chunk = local / groups, g = local - chunk * groups;
   const uint64_t len = a.list_off[c + 1] - a.list_off[c];
@@ -189,13 +189,16 @@ __device__ void ls_claim(const LsArgs& a, uint32_t* item, long long* s0) {
   item[1] = c;
   item[2] = r0;
   item[3] = static_cast<uint32_t>(len < uint64_t(r0) + kLsChunk ? len : uint64_t(r0) + kLsChunk);
-  item[4] = a.lq_off[u] + g * kLsNQ;
-  item[5] = min(kLsNQ, qc - g * kLsNQ);
+  item[4] = a.lq_off[u] + g * kNQ;
+  item[5] = min(kNQ, qc - g * kNQ);
   *s0 = a.res[c] + r0;
 }
 
+template <uint32_t kLsNQ>
 __global__ void __launch_bounds__(kLsThreads, 1)
     list_scan_tc_kernel(const __grid_constant__ CUtensorMap slab_map, LsArgs a) {
+  constexpr uint32_t kLsStages = ls_stages(kLsNQ);
+  constexpr uint32_t kTmemCols = 2 * kLsNQ; // double-buffered accumulator (power of 2 >= 32)
   extern __shared__ unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kLsStages], empty[kLsStages], acc_full[2], acc_empty[2],
       norm_full[2];
@@ -212,7 +215,7 @@ __global__ void __launch_bounds__(kLsThreads, 1)
   const uint32_t d = a.d;
   const uint32_t nkb = (d + kLsKB - 1) / kLsKB;
   unsigned char* ring = smem;
-  unsigned char* qB = ring + kLsStages * kLsStage;            // nkb x (16 rows x 128 B)
+  unsigned char* qB = ring + kLsStages * kLsStage;            // nkb x (NQ rows x 128 B)
   uint32_t* c_lo = reinterpret_cast<uint32_t*>(qB + nkb * kLsNQ * 128);
   const uint32_t cap = a.cap, trig = cap - kLsM; // a row-block always fits above trig
   uint32_t* c_hi = c_lo + kLsNQ * cap;
@@ -236,7 +239,7 @@ __global__ void __launch_bounds__(kLsThreads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_slot)),
-                 "n"(32)
+                 "n"(kTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -251,7 +254,7 @@ __global__ void __launch_bounds__(kLsThreads, 1)
   // The producer claims the next item once it has issued the current one's
   // loads; it starts loading while warps 1-11 stage the item's queries.
   uint32_t cur = 0;
-  if (threadIdx.x == 0) ls_claim(a, s_item[0], &s_s0[0]);
+  if (threadIdx.x == 0) ls_claim(a, kLsNQ, s_item[0], &s_s0[0]);
   __syncthreads();
   for (;;) {
     if (!s_item[cur][0]) break;
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(kLsThreads, 1)
                         static_cast<int32_t>(s0 + rb * kLsM), full + s);
           }
         }
-        ls_claim(a, s_item[cur ^ 1u], &s_s0[cur ^ 1u]);
+        ls_claim(a, kLsNQ, s_item[cur ^ 1u], &s_s0[cur ^ 1u]);
       }
       __syncwarp();
     } else if (warp == 1) {
@@ -369,15 +372,19 @@ __global__ void __launch_bounds__(kLsThreads, 1)
         mbar_wait(acc_full + b, ph);
         mbar_wait(norm_full + b, ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        uint32_t v[16];
-        const uint32_t taddr = tmem + ((32u * quad) << 16) + b * kLsNQ;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-            "%13,%14,%15}, [%16];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-              "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
-              "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(taddr));
+        uint32_t v[kLsNQ];
+#pragma unroll
+        for (uint32_t h = 0; h < kLsNQ; h += 16) {
+          const uint32_t taddr = tmem + ((32u * quad) << 16) + b * kLsNQ + h;
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+              "%13,%14,%15}, [%16];"
+              : "=r"(v[h + 0]), "=r"(v[h + 1]), "=r"(v[h + 2]), "=r"(v[h + 3]), "=r"(v[h + 4]),
+                "=r"(v[h + 5]), "=r"(v[h + 6]), "=r"(v[h + 7]), "=r"(v[h + 8]), "=r"(v[h + 9]),
+                "=r"(v[h + 10]), "=r"(v[h + 11]), "=r"(v[h + 12]), "=r"(v[h + 13]),
+                "=r"(v[h + 14]), "=r"(v[h + 15])
+              : "r"(taddr));
+        }
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         const float vn2f = s_vn2[b][e];
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -455,7 +462,8 @@ __global__ void __launch_bounds__(kLsThreads, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(kTmemCols)
                  : "memory");
   }
 }
@@ -525,13 +533,14 @@ __device__ void block_scan3(uint32_t (&v)[3], uint32_t (&tot)[3], uint32_t* sh) 
 __global__ void __launch_bounds__(1024) ls_plan_kernel(uint32_t* qcount, uint32_t nc,
                                                        const uint64_t* __restrict__ list_off,
                                                        uint32_t* lists, uint32_t* lq_off,
-                                                       uint32_t* item_off, uint32_t* meta) {
+                                                       uint32_t* item_off, uint32_t* meta,
+                                                       uint32_t gq) {
   __shared__ uint32_t sh[96 + 96];
   const uint32_t per = (nc + 1023) / 1024;
   const uint32_t c0 = min(nc, threadIdx.x * per), c1 = min(nc, c0 + per);
   auto items = [&](uint32_t c, uint32_t qc) {
     const uint64_t len = list_off[c + 1] - list_off[c];
-    return uint32_t((qc + kLsNQ - 1) / kLsNQ) * uint32_t((len + kLsChunk - 1) / kLsChunk);
+    return uint32_t((qc + gq - 1) / gq) * uint32_t((len + kLsChunk - 1) / kLsChunk);
   };
   uint32_t v[3] = {0, 0, 0};
   for (uint32_t c = c0; c < c1; ++c) {
@@ -696,24 +705,25 @@ __global__ void __launch_bounds__(kLsFinalThreads) ls_final_kernel(LsFinal a) {
 
 // Candidate slots per query per item that fit next to the ring and the
 // staged queries (multiple of 32, <= kLsMaxCap).
-static uint32_t list_scan_cap(uint32_t d) {
+static uint32_t list_scan_cap(uint32_t d, uint32_t nq) {
   const uint32_t nkb = (d + kLsKB - 1) / kLsKB;
-  const size_t fixed = 1024 + size_t(kLsStages) * kLsStage + size_t(nkb) * kLsNQ * 128 + 4096;
+  const size_t fixed = 1024 + size_t(ls_stages(nq)) * kLsStage + size_t(nkb) * nq * 128 + 4096;
   const size_t avail = 227 * 1024 > fixed ? 227 * 1024 - fixed : 0;
-  size_t cap = avail / (kLsNQ * (4 + 4 + 2));
+  size_t cap = avail / (nq * (4 + 4 + 2));
   cap = std::min<size_t>(cap, kLsMaxCap) & ~size_t(31);
   return static_cast<uint32_t>(cap);
 }
 
-bool list_scan_supported(uint32_t d, int k) {
+bool list_scan_supported(uint32_t d, int k, uint32_t group) {
+  if (group != 16 && group != 32) return false;
   return (d % 4) == 0 && d >= 4 && d <= 1024 && k >= 1 && k <= int(kLsMaxK) &&
-         list_scan_cap(d) >= kLsM + 2 * uint32_t(k);
+         list_scan_cap(d, group) >= kLsM + 2 * uint32_t(k);
 }
 
-size_t list_scan_smem(uint32_t d) {
+size_t list_scan_smem(uint32_t d, uint32_t group) {
   const uint32_t nkb = (d + kLsKB - 1) / kLsKB;
-  return 1024 + size_t(kLsStages) * kLsStage + size_t(nkb) * kLsNQ * 128 +
-         size_t(kLsNQ) * list_scan_cap(d) * (4 + 4 + 2);
+  return 1024 + size_t(ls_stages(group)) * kLsStage + size_t(nkb) * group * 128 +
+         size_t(group) * list_scan_cap(d, group) * (4 + 4 + 2);
 }
 
 static void ls_ck(cudaError_t e, const char* what) {
@@ -733,8 +743,9 @@ void launch_list_scan(const ListScan& p, cudaStream_t st) {
     ls_count_kernel<<<nq, 128, 0, st>>>(p.order, p.lp, p.res, s.qcount);
     after_launch();
   }
+  const uint32_t gq = p.group == 32 ? 32u : 16u;
   ls_plan_kernel<<<1, 1024, 0, st>>>(s.qcount, p.nc, p.list_off, s.lists, s.lq_off, s.item_off,
-                                     s.meta);
+                                     s.meta, gq);
   after_launch();
   if (p.lp) {
     ls_fill_kernel<<<nq, 128, 0, st>>>(p.order, p.lp, p.res, s.qcount, s.qidx);
@@ -756,12 +767,13 @@ void launch_list_scan(const ListScan& p, cudaStream_t st) {
   a.gcnt = s.gcnt;
   a.cand = reinterpret_cast<uint4*>(s.cand);
   a.gcap = s.gcap;
-  a.cap = list_scan_cap(p.d);
+  a.cap = list_scan_cap(p.d, gq);
   a.flag_host = p.flag_host;
   const CUtensorMap map = make_row_tile_map(p.slab, p.slab_rows, p.d, kLsM);
-  const size_t smem = list_scan_smem(p.d);
-  ensure_dyn_smem(reinterpret_cast<const void*>(list_scan_tc_kernel), smem);
-  list_scan_tc_kernel<<<p.grid, kLsThreads, smem, st>>>(map, a);
+  const size_t smem = list_scan_smem(p.d, gq);
+  auto kern = gq == 32 ? list_scan_tc_kernel<32> : list_scan_tc_kernel<16>;
+  ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
+  kern<<<p.grid, kLsThreads, smem, st>>>(map, a);
   after_launch();
   LsFinal f;
   f.Q = p.Q;

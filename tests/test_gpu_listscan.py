@@ -43,9 +43,16 @@ def assert_same(base, got, nq):
     assert np.array_equal(base.nfast, got.nfast)
 
 
+@pytest.fixture(params=[16, 32], ids=["g16", "g32"])
+def group(request, monkeypatch):
+    """Queries per work item (UMMA N): 16, or 32 for heavily shared lists."""
+    monkeypatch.setenv("LAIVG_LIST_SCAN_N", str(request.param))
+    return request.param
+
+
 @pytest.mark.parametrize("metric", [IP, L2])
 @pytest.mark.parametrize("k", [1, 10, 32, 64])
-def test_list_scan_planted(orc, laiv, monkeypatch, metric, k):
+def test_list_scan_planted(orc, laiv, monkeypatch, group, metric, k):
     cen, vecs, ids, off, qi, qo, _ = planted_data()
     ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric(metric))
     dev = laiv.Device(ix, BIG, miss_fetch="off")
@@ -61,7 +68,7 @@ def test_list_scan_planted(orc, laiv, monkeypatch, metric, k):
 
 
 @pytest.mark.parametrize("metric", [IP, L2])
-def test_list_scan_shapes(orc, laiv, monkeypatch, metric):
+def test_list_scan_shapes(orc, laiv, monkeypatch, group, metric):
     # ragged lists: empty, shorter than one row-block, multi-chunk (> 1024
     # rows); d = 100 (the last k-block is partial); 200 queries on 24 lists
     # (many 16-query groups per list)
@@ -94,7 +101,7 @@ def test_list_scan_shapes(orc, laiv, monkeypatch, metric):
             assert_topk_parity(metric, got.topk(t).ids, got.topk(t).scores, *want)
 
 
-def test_list_scan_ties_fall_back(orc, laiv, monkeypatch):
+def test_list_scan_ties_fall_back(orc, laiv, monkeypatch, group):
     # every member of a list equal: all scores tie, the candidate buffers
     # overflow, the batch is re-run on the per-query scan (same answer)
     d, nc, per = 64, 8, 700
