@@ -831,7 +831,7 @@ Ctx::~Ctx() {
                   (void*)so.part_s, (void*)so.part_id, (void*)so.part_vi, (void*)so.ticket,
                   (void*)so.gpart_s, (void*)so.gpart_id, (void*)so.gpart_vi,
                   (void*)d_staged, (void*)d_approx, (void*)d_cnorm, (void*)d_keys,
-                  (void*)tcs.cand, (void*)tcs.key, (void*)tcs.ncand,
+                  (void*)tcs.cand, (void*)tcs.key, (void*)tcs.ncand, (void*)tcs.qmask,
                   (void*)lss.qcount, (void*)lss.lists, (void*)lss.lq_off, (void*)lss.item_off,
                   (void*)lss.qidx, (void*)lss.meta, (void*)lss.gtau, (void*)lss.gcnt, lss.cand,
                   (void*)d_ctl, (void*)d_wbuf, (void*)d_wsink, (void*)d_wread}) {
@@ -982,6 +982,7 @@ void Ctx::init(const Index* index, const laivg_opts& o) {
       tcs.cand = dev_alloc<uint32_t>(size_t(max_batch) * cap);
       tcs.key = dev_alloc<uint64_t>(size_t(max_batch) * cap);
       tcs.ncand = dev_alloc<uint32_t>(max_batch);
+      tcs.qmask = dev_alloc<uint32_t>(size_t((max_batch + 31) / 32) * nc);
     }
   }
   d_scores = dev_alloc<double>(size_t(max_batch) * nc);

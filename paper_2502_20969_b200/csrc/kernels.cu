@@ -1034,7 +1034,8 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1)
     tc_filter_kernel(const float* __restrict__ approx, uint32_t splits,
                      const float* __restrict__ Q, uint32_t d, const float* __restrict__ cnorm,
                      uint32_t nc, int metric, uint32_t n_out, uint32_t cap,
-                     uint32_t* __restrict__ cand, uint32_t* __restrict__ ncand) {
+                     uint32_t* __restrict__ cand, uint32_t* __restrict__ ncand,
+                     uint32_t* __restrict__ qmask) {
   extern __shared__ __align__(16) unsigned char sm[];
   uint32_t* lok = reinterpret_cast<uint32_t*>(sm);
   float* hik = reinterpret_cast<float*>(sm + ((static_cast<size_t>(nc) * 4 + 15) & ~size_t(15)));
@@ -1138,10 +1139,102 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1)
     uint32_t base = 0;
     if (lane == 0 && m) base = atomicAdd(&s_count, static_cast<uint32_t>(__popc(m)));
     base = __shfl_sync(kFull, base, 0);
-    if (take) out[base + __popc(m & ((1u << lane) - 1u))] = c;
+    if (take) {
+      out[base + __popc(m & ((1u << lane) - 1u))] = c;
+      if (qmask) atomicOr(qmask + static_cast<uint64_t>(q >> 5) * nc + c, 1u << (q & 31));
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) ncand[q] = s_count;
+}
+
+// List-major exact re-score: CTA (x, y) holds the 32 queries of block y in
+// shared memory and walks centroids [x * chunk, (x + 1) * chunk); each warp
+// loads a centroid row once into registers (the next one in flight) and
+// scores it for every block query that kept it as a candidate (qmask), two
+// queries at a time, with warp_coarse_score's exact sequence (lane-strided
+// float4 terms, Acc4, butterfly), so the keys are the ones the per-pair
+// re-score computes. Centroid rows leave L2 once per 32-query block instead
+// of once per (query, candidate) pair.
+template <int NCH>
+__global__ void __launch_bounds__(256, 2)
+    tc_rescore_lm_kernel(const float* __restrict__ Q, uint32_t d, const float* __restrict__ cen,
+                         int metric, uint32_t nq, uint32_t nc, uint32_t cap, uint32_t chunk,
+                         const uint32_t* __restrict__ qmask, uint64_t* __restrict__ key) {
+  extern __shared__ __align__(16) unsigned char smq[];
+  float4* sq4 = reinterpret_cast<float4*>(smq);
+  const uint32_t qb = blockIdx.y, q0 = qb * 32, nb = min(32u, nq - q0);
+  const uint32_t d4 = d >> 2;
+  const uint32_t c0 = blockIdx.x * chunk, c1 = min(nc, c0 + chunk);
+  uint32_t* smask = reinterpret_cast<uint32_t*>(smq + static_cast<size_t>(32) * d * 4);
+  __shared__ __align__(8) uint64_t qbar;
+  // the block's query rows are contiguous: one bulk copy
+  const uint32_t qbytes = nb * d * 4;
+  if (threadIdx.x == 0) {
+    mbar_init(&qbar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(&qbar, qbytes);
+    bulk_g2s(sq4, Q + static_cast<uint64_t>(q0) * d, qbytes, &qbar);
+  }
+  for (uint32_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+    smask[c - c0] = qmask[static_cast<uint64_t>(qb) * nc + c];
+  }
+  __syncthreads();
+  mbar_wait(&qbar, 0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t W = 8; // warps per CTA
+  const float4* cen4 = reinterpret_cast<const float4*>(cen);
+  auto next = [&](uint32_t c) { // next centroid of this warp with a candidate query
+    while (c < c1 && smask[c - c0] == 0) c += W;
+    return c;
+  };
+  auto load_row = [&](uint32_t c, float4 (&r)[NCH]) {
+#pragma unroll
+    for (int t = 0; t < NCH; ++t) {
+      const uint32_t jj = lane + 32u * t;
+      r[t] = jj < d4 ? __ldg(cen4 + static_cast<uint64_t>(c) * d4 + jj)
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  float4 r[NCH], rn[NCH];
+  uint32_t c = next(c0 + warp);
+  if (c < c1) load_row(c, r);
+  while (c < c1) {
+    const uint32_t cn = next(c + W);
+    if (cn < c1) load_row(cn, rn); // in flight while this row is scored
+    uint32_t m = smask[c - c0];
+    while (m) {
+      // two block queries at a time (independent accumulation chains)
+      const uint32_t b0 = __ffs(m) - 1;
+      m &= m - 1;
+      const bool two = m != 0;
+      const uint32_t b1 = two ? __ffs(m) - 1 : b0;
+      if (two) m &= m - 1;
+      const float4* qv0 = sq4 + static_cast<size_t>(b0) * d4;
+      const float4* qv1 = sq4 + static_cast<size_t>(b1) * d4;
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int t = 0; t < NCH; ++t) {
+        const uint32_t jj = lane + 32u * t;
+        if (jj < d4) {
+          const float4 x0 = qv0[jj], x1 = qv1[jj];
+          const double qd0[4] = {x0.x, x0.y, x0.z, x0.w};
+          const double qd1[4] = {x1.x, x1.y, x1.z, x1.w};
+          Acc4<true>::run(metric, qd0, r[t], a0);
+          Acc4<true>::run(metric, qd1, r[t], a1);
+        }
+      }
+      a0 = warp_sum(a0);
+      a1 = warp_sum(a1);
+      if (lane == 0) {
+        key[static_cast<uint64_t>(q0 + b0) * cap + c] = order_key(a0, metric);
+        if (two) key[static_cast<uint64_t>(q0 + b1) * cap + c] = order_key(a1, metric);
+      }
+    }
+    c = cn;
+#pragma unroll
+    for (int t = 0; t < NCH; ++t) r[t] = rn[t];
+  }
 }
 
 constexpr int kRsConsumers = 8;
@@ -1324,14 +1417,14 @@ __global__ void __launch_bounds__(kRsThreads, 1)
 constexpr int kSortThreads = 256;
 template <int E>
 __device__ void tc_sort_run(const uint64_t* kq, const uint32_t* cq, uint32_t n, uint64_t* sk,
-                            uint32_t* sv) {
+                            uint32_t* sv, bool dense) {
   uint64_t k[E];
   uint32_t v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const uint32_t i = threadIdx.x * E + e;
-    k[e] = i < n ? kq[i] : ~0ull;
     v[e] = i < n ? cq[i] : ~0u;
+    k[e] = i < n ? kq[dense ? v[e] : i] : ~0ull; // dense: keys indexed by centroid id
   }
   block_bitonic_sort<E>(k, v, sk, sv, static_cast<uint32_t>(kSortThreads) * E);
 #pragma unroll
@@ -1346,7 +1439,8 @@ __global__ void __launch_bounds__(kSortThreads)
     tc_sort_kernel(uint32_t cap, const uint32_t* __restrict__ cand,
                    const uint32_t* __restrict__ ncand, const uint64_t* __restrict__ ckey,
                    uint32_t n_out, uint32_t* __restrict__ order, const int64_t* res_off,
-                   const uint64_t* list_off, FastTable ft, bool do_partition, bool scan_sorted) {
+                   const uint64_t* list_off, FastTable ft, bool do_partition, bool scan_sorted,
+                   bool dense) {
   extern __shared__ __align__(16) unsigned char smx[];
   const uint32_t q = blockIdx.x, n = ncand[q];
   uint32_t m = kSortThreads;
@@ -1356,12 +1450,12 @@ __global__ void __launch_bounds__(kSortThreads)
   const uint64_t* kq = ckey + static_cast<uint64_t>(q) * cap;
   const uint32_t* cq = cand + static_cast<uint64_t>(q) * cap;
   switch (m / kSortThreads) {
-    case 1: tc_sort_run<1>(kq, cq, n, sk, sv); break;
-    case 2: tc_sort_run<2>(kq, cq, n, sk, sv); break;
-    case 4: tc_sort_run<4>(kq, cq, n, sk, sv); break;
-    case 8: tc_sort_run<8>(kq, cq, n, sk, sv); break;
-    case 16: tc_sort_run<16>(kq, cq, n, sk, sv); break;
-    default: tc_sort_run<32>(kq, cq, n, sk, sv); break;
+    case 1: tc_sort_run<1>(kq, cq, n, sk, sv, dense); break;
+    case 2: tc_sort_run<2>(kq, cq, n, sk, sv, dense); break;
+    case 4: tc_sort_run<4>(kq, cq, n, sk, sv, dense); break;
+    case 8: tc_sort_run<8>(kq, cq, n, sk, sv, dense); break;
+    case 16: tc_sort_run<16>(kq, cq, n, sk, sv, dense); break;
+    default: tc_sort_run<32>(kq, cq, n, sk, sv, dense); break;
   }
   uint32_t* out = order + static_cast<uint64_t>(q) * n_out;
   for (uint32_t i = threadIdx.x; i < n_out; i += blockDim.x) out[i] = sv[i];
@@ -2999,20 +3093,46 @@ void launch_tc_select(const float* approx, uint32_t splits, const float* Q, uint
     const size_t fs = 2 * ((size_t(nc) * 4 + 15) & ~size_t(15));
     auto ffn = half ? tc_filter_kernel<512> : tc_filter_kernel<kSelThreads>;
     ensure_dyn_smem(reinterpret_cast<const void*>(ffn), fs);
+    // per-pair streamed re-score by default; LAIVG_TC_RESCORE=lm selects the
+    // list-major re-score (measured: 13.4 vs ~11-23 us at nq 32, 46.8 vs ~54
+    // us at nq 256, whole call no faster: profiles/r02/tc_rescore_lm.jsonl)
+    const char* lm_env = std::getenv("LAIVG_TC_RESCORE"); // read per call (tests switch it)
+    const bool lm_on = lm_env && std::string(lm_env) == "lm";
+    const bool lm = lm_on && sc->qmask != nullptr;
+    if (lm) {
+      if (cudaMemsetAsync(sc->qmask, 0, size_t((nq + 31) / 32) * nc * sizeof(uint32_t), st) !=
+          cudaSuccess) {
+        throw CudaError("tc_select: qmask reset failed");
+      }
+    }
     ffn<<<nq, half ? 512 : kSelThreads, fs, st>>>(approx, splits, Q, d, cnorm, nc, metric, n_out,
-                                                 cap, sc->cand, sc->ncand);
+                                                 cap, sc->cand, sc->ncand,
+                                                 lm ? sc->qmask : nullptr);
     after_launch();
-    const size_t rs = 2 * size_t(kRsTile) * d * 4 + 2 * 16 + 2 * kRsTile * 8 + 16 +
-                      (size_t(nq) + 1) * 4 + size_t(kRsMaxPairs) * 12 + 64;
-    auto rfn = d <= 768 ? tc_rescore_stream_kernel<6> : tc_rescore_stream_kernel<8>;
-    ensure_dyn_smem(reinterpret_cast<const void*>(rfn), rs);
-    rfn<<<nsm, kRsThreads, rs, st>>>(Q, d, centroids, metric, nq, cap, sc->cand, sc->ncand,
-                                      sc->key);
-    after_launch();
+    if (lm) {
+      const uint32_t nqb = (nq + 31) / 32;
+      const uint32_t chunks = std::max<uint32_t>(1, (2u * uint32_t(nsm) + nqb - 1) / nqb);
+      const uint32_t chunk = (nc + chunks - 1) / chunks;
+      const size_t qs = size_t(32) * d * 4 + size_t(chunk) * 4;
+      auto lfn = d <= 768 ? tc_rescore_lm_kernel<6> : tc_rescore_lm_kernel<8>;
+      ensure_dyn_smem(reinterpret_cast<const void*>(lfn), qs);
+      lfn<<<dim3((nc + chunk - 1) / chunk, nqb), 256, qs, st>>>(Q, d, centroids, metric, nq, nc,
+                                                                cap, chunk, sc->qmask, sc->key);
+      after_launch();
+    } else {
+      const size_t rs = 2 * size_t(kRsTile) * d * 4 + 2 * 16 + 2 * kRsTile * 8 + 16 +
+                        (size_t(nq) + 1) * 4 + size_t(kRsMaxPairs) * 12 + 64;
+      auto rfn = d <= 768 ? tc_rescore_stream_kernel<6> : tc_rescore_stream_kernel<8>;
+      ensure_dyn_smem(reinterpret_cast<const void*>(rfn), rs);
+      rfn<<<nsm, kRsThreads, rs, st>>>(Q, d, centroids, metric, nq, cap, sc->cand, sc->ncand,
+                                        sc->key);
+      after_launch();
+    }
     const size_t ss = size_t(std::max<uint32_t>(cap, kSortThreads)) * 12 + 16;
     ensure_dyn_smem(reinterpret_cast<const void*>(tc_sort_kernel), ss);
     tc_sort_kernel<<<nq, kSortThreads, ss, st>>>(cap, sc->cand, sc->ncand, sc->key, n_out, order,
-                                                 res_off, list_off, f, ft != nullptr, scan_sorted);
+                                                 res_off, list_off, f, ft != nullptr, scan_sorted,
+                                                 lm);
     after_launch();
     return;
   }

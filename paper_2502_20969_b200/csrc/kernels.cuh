@@ -173,6 +173,10 @@ struct TcSelectScratch {
   uint32_t* cand = nullptr;
   uint64_t* key = nullptr;
   uint32_t* ncand = nullptr;
+  // list-major re-score: per 32-query block and centroid, the bit set of
+  // block queries that hold the centroid as a candidate [ceil(nq/32)][nc];
+  // key is then indexed by centroid id ([nq][cap], cap >= nc)
+  uint32_t* qmask = nullptr;
 };
 void launch_tc_select(const float* approx, uint32_t splits, const float* Q, uint32_t nq,
                       uint32_t d,

@@ -57,9 +57,17 @@ def test_tc_coarse_error_bound(laiv, nc, d):
         assert ratio.max() < 0.75 * TC_ERR, ratio.max()
 
 
+@pytest.fixture(params=["stream", "lm"])
+def rescore(request, monkeypatch):
+    """The batched selection's exact re-score: per (query, candidate) pair
+    (default) or list-major (LAIVG_TC_RESCORE=lm)."""
+    monkeypatch.setenv("LAIVG_TC_RESCORE", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("metric", [IP, L2])
 @pytest.mark.parametrize("nc,d", [(300, 768), (4096, 768), (1000, 100)])
-def test_tc_probe_bit_exact(orc, laiv, metric, nc, d):
+def test_tc_probe_bit_exact(orc, laiv, rescore, metric, nc, d):
     cen, vecs, ids, off, qi, qo, ix = synth_index(laiv, nc, 4, d, metric, nq=48)
     dev_tc = laiv.Device(ix, 1 << 20, coarse_impl="tensor")
     dev_64 = laiv.Device(ix, 1 << 20, coarse_impl="fp64")
@@ -81,7 +89,7 @@ def test_tc_probe_bit_exact(orc, laiv, metric, nc, d):
                               laiv.coarse_probe(dev_64, Q[t], 64))
 
 
-def test_tc_probe_exact_ties(laiv):
+def test_tc_probe_exact_ties(laiv, rescore):
     # duplicated centroids: exact score ties ordered by ascending cluster id
     rng = np.random.default_rng(9)
     base = rng.standard_normal((50, 64)).astype(np.float32)
