@@ -174,3 +174,19 @@ def test_list_scan_auto_policy(laiv, monkeypatch):
     monkeypatch.setenv("LAIVG_LIST_SCAN_QPL", "4")
     laiv.hybrid_search_batch(dev2, qo, 32, 10)      # prior 40 x 32 / 64 = 20
     assert dev2.list_scan_stats()[0] == 1
+
+
+def test_list_scan_in_fp32_accumulation_contexts(orc, laiv, monkeypatch):
+    # a context in fp32 + re-score mode: the list scan's exact answer equals
+    # the per-query scan's (whose survivors are re-scored in fp64)
+    cen, vecs, ids, off, qi, qo, _ = planted_data()
+    for metric in (IP, L2):
+        ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric(metric))
+        dev = laiv.Device(ix, BIG, miss_fetch="off", acc_fp64=False)
+        set_residency(dev, np.ones(64, np.uint8))
+        base, got, _, runs, fb = both_paths(laiv, dev, qo, 16, 10, monkeypatch)
+        assert runs == 1 and fb == 0
+        assert_same(base, got, len(qo))
+        for t in range(0, len(qo), 8):
+            want = orc.ivf_search(cen, vecs, ids, off, metric, qo[t], 16, 10)
+            assert_topk_parity(metric, got.topk(t).ids, got.topk(t).scores, *want)
