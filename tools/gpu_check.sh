@@ -1,5 +1,5 @@
 #!/bin/bash
-# One GPU session: gpu tests, smoke, bench (C2 and C1), launch lists, full ncu
+# One GPU session: gpu tests, smoke, bench (C2, C1, c2b), launch lists, full ncu
 # of the dominant kernel (fused_query_kernel on the single-query path).
 # usage (from repo root, under gpurun): bash tools/gpu_check.sh [tag]
 set -x
@@ -13,6 +13,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>
 fi
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
 timeout 900 python bench.py --config c1 > $O/bench_c1.json 2> $O/bench_c1.err
+timeout 900 python bench.py --config c2b --steps 5 --warmup 3 > $O/bench_c2b.json 2> $O/bench_c2b.err
 if [ "${NCU:-1}" = 1 ]; then
 for cfg in c2 c1; do
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
