@@ -139,9 +139,12 @@ def test_c1_batched(laiv, c1, metric):
         laiv.prefetch_batch(dev, qi[sel], np.full(n, cap // n, np.uint64), chan, 0.0)
         res, _ = laiv.hybrid_search_batch(dev, qo[sel], _C1.L, _C1.k)
         got += [(res.ids[q, : res.counts[q]], res.scores[q, : res.counts[q]]) for q in range(n)]
-    exact = _compare(f"C1 {'ip' if metric == 0 else 'l2'} batched (64/call, 25% cache)", metric,
-                     got, want[metric])
+    runs, fallbacks, qpl = dev.list_scan_stats()
+    exact = _compare(f"C1 {'ip' if metric == 0 else 'l2'} batched (64/call, 25% cache; hits on "
+                     f"the list-major scan in {runs} of {(_C1.nq + 63) // 64} batches, "
+                     f"{qpl:.1f} queries per list)", metric, got, want[metric])
     assert exact >= _C1.nq - 2
+    assert runs > 0 and fallbacks == 0
     dev.close()
     ix.close()
 
