@@ -219,6 +219,7 @@ struct ListScan {
   unsigned* flag_host = nullptr;     // set to 1 if a candidate buffer overflowed
   int grid = 0;
   uint32_t group = 16;               // queries per work item: 16, or 32 for heavily shared lists
+  uint32_t chunk = 1024;             // list rows per work item (multiple of 128, <= 65536)
   ListScanScratch scratch;
 };
 bool list_scan_supported(uint32_t d, int k, uint32_t group = 16);

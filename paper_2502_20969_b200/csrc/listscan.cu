@@ -59,7 +59,7 @@ constexpr uint32_t kLsM = 128;       // list rows per row-block (UMMA M)
 constexpr uint32_t kLsKB = 32;       // floats per k-block (one 128-byte swizzle row)
 __host__ __device__ constexpr uint32_t ls_stages(uint32_t nq) { return nq <= 16 ? 6u : 4u; } // ring (16 KB)
 constexpr uint32_t kLsStage = kLsM * kLsKB * 4;
-constexpr uint32_t kLsChunk = 1024;  // list rows per item
+constexpr uint32_t kLsChunk = 1024;  // list rows per item unless the caller sets ListScan::chunk
 constexpr uint32_t kLsSlots = 16;    // candidate slots per lane of a compacting warp
 constexpr uint32_t kLsMaxCap = 32 * kLsSlots; // candidate slots per query per item (<=)
 constexpr uint32_t kLsMaxK = 64;
@@ -94,6 +94,7 @@ struct LsArgs {
   uint4* cand;         // [nq][gcap] (lo key, hi key, cluster, slab row)
   uint32_t gcap;
   uint32_t cap;        // candidate slots per query per item (<= kLsMaxCap)
+  uint32_t chunk;      // list rows per item (multiple of 128, <= 65536: u16 row index)
   unsigned* flag_host; // overflow, mapped host memory
 };
 
@@ -184,11 +185,11 @@ __device__ void ls_claim(const LsArgs& a, uint32_t kNQ, uint32_t* item, long lon
   const uint32_t local = t - a.item_off[u];
   const uint32_t chunk = local / groups, g = local - chunk * groups;
   const uint64_t len = a.list_off[c + 1] - a.list_off[c];
-  const uint32_t r0 = chunk * kLsChunk;
+  const uint32_t r0 = chunk * a.chunk;
   item[0] = 1;
   item[1] = c;
   item[2] = r0;
-  item[3] = static_cast<uint32_t>(len < uint64_t(r0) + kLsChunk ? len : uint64_t(r0) + kLsChunk);
+  item[3] = static_cast<uint32_t>(len < uint64_t(r0) + a.chunk ? len : uint64_t(r0) + a.chunk);
   item[4] = a.lq_off[u] + g * kNQ;
   item[5] = min(kNQ, qc - g * kNQ);
   *s0 = a.res[c] + r0;
@@ -553,13 +554,13 @@ __global__ void __launch_bounds__(1024) ls_plan_kernel(uint32_t* qcount, uint32_
                                                        const uint64_t* __restrict__ list_off,
                                                        uint32_t* lists, uint32_t* lq_off,
                                                        uint32_t* item_off, uint32_t* meta,
-                                                       uint32_t gq) {
+                                                       uint32_t gq, uint32_t rows) {
   __shared__ uint32_t sh[96 + 96];
   const uint32_t per = (nc + 1023) / 1024;
   const uint32_t c0 = min(nc, threadIdx.x * per), c1 = min(nc, c0 + per);
   auto items = [&](uint32_t c, uint32_t qc) {
     const uint64_t len = list_off[c + 1] - list_off[c];
-    return uint32_t((qc + gq - 1) / gq) * uint32_t((len + kLsChunk - 1) / kLsChunk);
+    return uint32_t((qc + gq - 1) / gq) * uint32_t((len + rows - 1) / rows);
   };
   uint32_t v[3] = {0, 0, 0};
   for (uint32_t c = c0; c < c1; ++c) {
@@ -763,8 +764,10 @@ void launch_list_scan(const ListScan& p, cudaStream_t st) {
     after_launch();
   }
   const uint32_t gq = p.group == 32 ? 32u : 16u;
+  uint32_t rows = p.chunk >= kLsM && p.chunk <= 65536 && p.chunk % kLsM == 0 ? p.chunk
+                                                                            : kLsChunk;
   ls_plan_kernel<<<1, 1024, 0, st>>>(s.qcount, p.nc, p.list_off, s.lists, s.lq_off, s.item_off,
-                                     s.meta, gq);
+                                     s.meta, gq, rows);
   after_launch();
   if (p.lp) {
     ls_fill_kernel<<<nq, 128, 0, st>>>(p.order, p.lp, p.res, s.qcount, s.qidx);
@@ -787,6 +790,7 @@ void launch_list_scan(const ListScan& p, cudaStream_t st) {
   a.cand = reinterpret_cast<uint4*>(s.cand);
   a.gcap = s.gcap;
   a.cap = list_scan_cap(p.d, gq);
+  a.chunk = rows;
   a.flag_host = p.flag_host;
   const CUtensorMap map = make_row_tile_map(p.slab, p.slab_rows, p.d, kLsM);
   const CUtensorMap tail = make_row_tile_map(p.slab, p.slab_rows, p.d, 16);

@@ -190,3 +190,31 @@ def test_list_scan_in_fp32_accumulation_contexts(orc, laiv, monkeypatch):
         for t in range(0, len(qo), 8):
             want = orc.ivf_search(cen, vecs, ids, off, metric, qo[t], 16, 10)
             assert_topk_parity(metric, got.topk(t).ids, got.topk(t).scores, *want)
+
+
+@pytest.mark.parametrize("chunk", [128, 384, 4096])
+def test_list_scan_chunk_lengths(orc, laiv, monkeypatch, chunk):
+    # rows per work item from one row-block to whole lists: same answers
+    rng = np.random.default_rng(23)
+    d, nc = 64, 12
+    lens = rng.integers(0, 3000, nc)
+    lens[2] = 0
+    lens[4] = 129
+    off = np.zeros(nc + 1, np.uint64)
+    off[1:] = np.cumsum(lens)
+    n = int(off[-1])
+    cen = rng.standard_normal((nc, d)).astype(np.float32)
+    vecs = (cen[np.repeat(np.arange(nc), lens)] +
+            0.3 * rng.standard_normal((n, d))).astype(np.float32)
+    ids = rng.permutation(n).astype(np.uint64)
+    ix = laiv.IvfIndex(cen, vecs, ids, off, laiv.Metric.InnerProduct)
+    dev = laiv.Device(ix, BIG, miss_fetch="off")
+    set_residency(dev, np.ones(nc, np.uint8))
+    Q = (cen[rng.integers(0, nc, 60)] + 0.3 * rng.standard_normal((60, d))).astype(np.float32)
+    monkeypatch.setenv("LAIVG_LIST_SCAN_CHUNK", str(chunk))
+    base, got, _, runs, fb = both_paths(laiv, dev, Q, 5, 10, monkeypatch)
+    assert runs == 1 and fb == 0
+    assert_same(base, got, len(Q))
+    for t in range(0, len(Q), 10):
+        want = orc.ivf_search(cen, vecs, ids, off, IP, Q[t], 5, 10)
+        assert_topk_parity(IP, got.topk(t).ids, got.topk(t).scores, *want)
