@@ -57,7 +57,7 @@ namespace {
 constexpr uint32_t kLsNQMax = 32;    // queries per item (UMMA N): 16, or 32 for shared lists
 constexpr uint32_t kLsM = 128;       // list rows per row-block (UMMA M)
 constexpr uint32_t kLsKB = 32;       // floats per k-block (one 128-byte swizzle row)
-__host__ __device__ constexpr uint32_t ls_stages(uint32_t nq) { return nq <= 16 ? 6u : 4u; } // ring (16 KB)
+__host__ __device__ constexpr uint32_t ls_stages(uint32_t nq) { return nq <= 16 ? 8u : 4u; } // ring (16 KB)
 constexpr uint32_t kLsStage = kLsM * kLsKB * 4;
 constexpr uint32_t kLsChunk = 1024;  // list rows per item unless the caller sets ListScan::chunk
 constexpr uint32_t kLsSlots = 16;    // candidate slots per lane of a compacting warp
